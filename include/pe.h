@@ -1,0 +1,146 @@
+/*
+ * pe.h — C ABI of libpe, the B200 (sm_100a) parareal hot path.
+ *
+ * Drop-in boundary for the reference's online solver (paradiff, arXiv 2411.09244):
+ * every entry point replaces one piece of the reference's Python hot path, cited as
+ * /root/reference/pkg/src/paradiff/<file>:<line>.  Plain pointers and sizes only; no
+ * torch or C++ types cross this boundary.  All functions return 0 on success and a
+ * negative PE_ERR_* code on failure; pe_last_error() returns the message of the last
+ * failure on the calling thread.  No C++ exception crosses the ABI.
+ *
+ * Layouts (FP64, little endian):
+ *   - operator blocks passed to pe_set_system are HOST, row-major (C order), exactly
+ *     the ndarrays of a reference CoarseSystem (msbasis.py:397-418);
+ *   - state batches are DEVICE buffers of shape (E, ncols, d1+d2), C order: member-
+ *     major, then interval/column, then the stacked [u; w] coefficients of one
+ *     SplitState (stepping.py:49-50 `stacked()`).
+ *   - `stream` is a cudaStream_t (CUstream) or NULL for the legacy default stream.
+ * A context is not thread-safe; callers serialise calls per context.
+ */
+#ifndef PE_H
+#define PE_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PE_OK 0
+#define PE_ERR_ARG -1      /* bad argument (reference raises ValueError) */
+#define PE_ERR_CUDA -2     /* CUDA runtime / launch failure */
+#define PE_ERR_SOLVER -3   /* singular factorisation (reference: LinAlgError) */
+#define PE_ERR_STATE -4    /* call order violated (e.g. fine before prepare) */
+#define PE_ERR_NOMEM -5
+
+/* WR stop reasons, allatonce.py:243-271 */
+#define PE_STOP_TOL 0
+#define PE_STOP_DIVERGED 1
+#define PE_STOP_FLOOR 2
+#define PE_STOP_MAX_ITER 3
+
+/* parareal stop rules */
+#define PE_RULE_ABSOLUTE 0 /* parareal.py:145-147 check_stop: max_n ||dx_n|| < eps */
+#define PE_RULE_RELATIVE 1 /* max_n ||dx_n|| / max_n ||x_n^k|| < eps  */
+
+#define PE_KIND_SEQUENTIAL 0 /* SequentialFine, parareal.py:53-66 */
+#define PE_KIND_ALLATONCE 1  /* AllAtOnceFine,  parareal.py:69-84 */
+
+typedef struct pe_ctx pe_ctx;
+
+const char* pe_last_error(void);
+const char* pe_version(void);
+
+/* Context for E members of reduced size d1+d2 with at most `max_cols` columns (N
+ * coarse intervals) and J fine substeps.  Replaces SplitPropagators.__init__
+ * (stepping.py:109-114). */
+int pe_create(pe_ctx** ctx, int E, int d1, int d2, int max_cols, int J, int device);
+int pe_destroy(pe_ctx* ctx);
+
+/* Upload one member's CoarseSystem blocks (host, row-major) and ConstantLoads
+ * (stepping.py:77-91).  M11,A11: d1*d1; M12,A12: d1*d2; M22,A22: d2*d2; f1: d1; f2: d2. */
+int pe_set_system(pe_ctx* ctx, int member, const double* M11, const double* A11,
+                  const double* M12, const double* A12, const double* M22,
+                  const double* A22, const double* f1, const double* f2);
+
+/* Pre-factorise for the sequential fine propagator at substep dt_sub
+ * (stepping.py:116-120 _u_factor, :114 M22 Cholesky). */
+int pe_prepare_sequential(pe_ctx* ctx, double dt_sub);
+/* Pre-factorise the coarse propagator G at step dt (stepping.py:149-159 _g_factor). */
+int pe_prepare_coarse(pe_ctx* ctx, double dt);
+/* Set up the all-at-once solver (allatonce.py:100-110 ImplicitAllAtOnce.__init__,
+ * :184-210 WaveformRelaxation.__init__).  alpha in (0,1). */
+int pe_prepare_allatonce(pe_ctx* ctx, double dt_sub, double alpha, double tol, int max_iter);
+
+/* Fine propagator over one coarse interval for `ncols` states per member, lags reset
+ * (stepping.py:178-189 fine_interval; parareal.py:62-66 SequentialFine.propagate).
+ * X_in, X_out: device (E, ncols, d). */
+int pe_fine_sequential(pe_ctx* ctx, const double* X_in, double* X_out, int ncols, void* stream);
+
+/* One fine substep with explicit lags at the prepared dt_sub (stepping.py:122-147
+ * split_step): X_prev holds the lagged (u_prev, w_prev).  (E, ncols, d) device. */
+int pe_split_step(pe_ctx* ctx, const double* X_in, const double* X_prev, double* X_out,
+                  int ncols, void* stream);
+
+/* All-at-once fine propagator (allatonce.py:232-298 WaveformRelaxation.solve) for
+ * `ncols` states per member.  Optional device outputs (may be NULL): sweeps and
+ * stop reason per (member, column) as int32 (E, ncols); residual history
+ * (E, ncols, max_iter) FP64 (unused entries NaN). */
+int pe_fine_allatonce(pe_ctx* ctx, const double* X_in, double* X_out, int ncols,
+                      int* sweeps, int* reasons, double* resid_hist, void* stream);
+
+/* Waveforms of the last pe_fine_allatonce call (allatonce.py:280-291 trajectory):
+ * U_out (E, ncols, J+1, d1), W_out (E, ncols, J+1, d2), row 0 = interval start. */
+int pe_wr_waveforms(pe_ctx* ctx, double* U_out, double* W_out, int ncols, void* stream);
+
+/* Coarse propagator G applied to `ncols` states per member
+ * (stepping.py:161-176 coarse_step).  Bitwise identical to the G inside
+ * pe_coarse_correct. */
+int pe_coarse_apply(pe_ctx* ctx, const double* X_in, double* X_out, int ncols, void* stream);
+
+/* Fused coarse sweep + parareal correction + convergence norms for N intervals
+ * (parareal.py:198-215 and :140-147; initial sweep :150-157 when F_hat == NULL).
+ *   X_old:   (E, N+1, d) iterate k (row 0 = initial state, also used as row 0 of X_new)
+ *   F_hat:   (E, N, d)   fine results F(x_n^k), or NULL for the initial sweep
+ *   G_cache: (E, N, d)   in: G(x_n^k); out: G(x_n^{k+1})  (parareal.py:179,216)
+ *   X_new:   (E, N+1, d) iterate k+1
+ *   diff:    (E, 2) device FP64: [max_n ||x_new - x_old||, max_n ||x_new||], n = 1..N
+ *   active:  (E) int32 member mask or NULL; inactive members copy X_old to X_new. */
+int pe_coarse_correct(pe_ctx* ctx, int N, const double* X_old, const double* F_hat,
+                      double* G_cache, double* X_new, double* diff, const int* active,
+                      void* stream);
+
+/* Device-resident parareal loop (parareal.py:160-236 run_parareal) with one host
+ * synchronisation per iteration.  All pointers are device pointers except the
+ * `*_h` outputs, which are host arrays.
+ *   X0:        (E, d) initial states
+ *   history:   ((k_max+1), E, N+1, d) out
+ *   diffs_h:   (k_max, E) out, the value the stop rule compared (absolute or relative)
+ *   iters_h:   (E) out, iterations per member (includes the stopping sweep)
+ *   conv_h:    (E) out, 1 when the member met the rule
+ *   wr_sweeps, wr_reasons: (k_max, E, N) int32 device or NULL (all-at-once kind)
+ *   wr_resid:  (k_max, E, N, max_iter) FP64 device or NULL
+ *   fine_ms_h, coarse_ms_h: (k_max) host, CUDA-event phase times per iteration
+ * Returns the number of executed iterations (max over members) in *k_done. */
+int pe_parareal_run(pe_ctx* ctx, int kind, int N, const double* X0, int k_max,
+                    double epsilon, int rule, double* history, double* diffs_h,
+                    int* iters_h, int* conv_h, int* wr_sweeps, int* wr_reasons,
+                    double* wr_resid, float* fine_ms_h, float* coarse_ms_h, int* k_done,
+                    void* stream);
+
+/* The FP64 DMMA GEMM underneath every contraction, exposed for kernel tests:
+ * C(i,j) = sum_k A(i,k) B(k,j) with element strides (device pointers). */
+int pe_gemm_f64(int M, int N, int K, const double* A, long long a_i, long long a_k,
+                const double* B, long long b_k, long long b_j, double* C, long long c_i,
+                long long c_j, void* stream);
+
+/* Launch counter: number of libpe kernels launched since context creation
+ * (bench/driver evidence that the native path ran). */
+long long pe_launch_count(pe_ctx* ctx);
+
+/* Timing helpers used by bench.py: mean device time (ms) of the most recent
+ * pe_fine_* call's dominant kernel class and its algorithmic flop count. */
+int pe_last_fine_stats(pe_ctx* ctx, double* gemm_ms, double* gemm_flops, int* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PE_H */

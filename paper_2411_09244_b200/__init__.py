@@ -1,0 +1,19 @@
+"""paper_2411_09244_b200 — B200-native (sm_100a) parareal hot path for the partially
+explicit splitting scheme of arXiv 2411.09244 (reference package: paradiff).
+
+Drop-in for the reference's online solver API; every solve runs in libpe
+(hand-written FP64 DMMA / cluster kernels behind the C ABI in include/pe.h).
+"""
+
+from ._lib import LIB_PATH, NativeUnavailable, PeError  # noqa: F401
+from .allatonce import (TimeMatrixB, WaveformRelaxation, WRResult,  # noqa: F401
+                        build_time_matrix, wr_fine_solve)
+from .engine import PeContext  # noqa: F401
+from .msbasis import CoarseSystem  # noqa: F401
+from .parareal import (AllAtOnceFine, ParerealConfig, ParerealRun,  # noqa: F401
+                       SequentialFine, build_fine_propagator, check_stop, initial_sweep,
+                       max_state_diff, run_parareal, run_parareal_ensemble)
+from .stepping import (ConstantLoads, SplitPropagators, SplitState,  # noqa: F401
+                       SplitTrajectory, TimeGrid, split_energy)
+
+__version__ = "0.1.0"

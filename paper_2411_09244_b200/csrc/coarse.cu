@@ -1,0 +1,200 @@
+// Fused coarse sweep + parareal correction + convergence norms (K2).
+//
+// One thread-block cluster per ensemble member walks the N coarse intervals
+// sequentially (parareal.py:198-215; initial sweep :150-157):
+//     g        = G(x_n^{k+1}) = Phi x_n^{k+1} + gvec        (stepping.py:161-176)
+//     x_{n+1}  = F_hat_n + (g - G_cache_n)                    grouping kept exactly (:209)
+//     G_cache_n = g
+// Each CTA of the cluster owns a contiguous row slice of Phi = K_G^{-1} R_G (kept in
+// shared memory when it fits) and the cluster barrier publishes x_{n+1} between steps,
+// so there is no host round trip per coarse step.  The per-interval norms
+// ||x_new - x_old|| and ||x_new|| (parareal.py:140-142) are reduced in a fixed order
+// (lane-strided dot, xor tree, warps in index order, CTAs in rank order), so reruns
+// are bitwise reproducible.
+
+#include <cooperative_groups.h>
+
+#include <cmath>
+
+#include "pe.h"
+#include "pe_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace pe {
+
+constexpr int COARSE_THREADS = 256;
+constexpr int COARSE_WARPS = COARSE_THREADS / 32;
+
+__device__ __forceinline__ double warp_sum_c(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct CoarseArgs {
+  int d, N, cs;
+  int phi_in_smem;
+  const double* Phi;   // (E, d, d) row-major
+  const double* gvec;  // (E, d)
+  const double* X_old; // (E, N+1, d)
+  const double* F_hat; // (E, N, d) or null (initial sweep)
+  double* G_cache;     // (E, N, d)
+  double* X_new;       // (E, N+1, d)
+  double* partial;     // (E, N, cs, 2)
+  double* diff;        // (E, 2)
+  const int* active;   // (E) or null
+};
+
+__global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_constant__ CoarseArgs a) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int e = blockIdx.x / a.cs;
+  const int d = a.d, N = a.N;
+  const int r0 = (int)((long long)rank * d / a.cs), r1 = (int)((long long)(rank + 1) * d / a.cs);
+  const int nrows = r1 - r0;
+  const double* X_old = a.X_old + (long long)e * (N + 1) * d;
+  double* X_new = a.X_new + (long long)e * (N + 1) * d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (a.active && a.active[e] == 0) {  // converged member: iterate frozen
+    for (long long t = threadIdx.x; t < (long long)(N + 1) * nrows; t += COARSE_THREADS) {
+      const int n = (int)(t / nrows), r = r0 + (int)(t % nrows);
+      X_new[(long long)n * d + r] = X_old[(long long)n * d + r];
+    }
+    return;
+  }
+
+  extern __shared__ double sm[];
+  double* xs = sm;                    // d
+  double* wpart = xs + d;             // COARSE_WARPS * 2
+  double* phis = wpart + 2 * COARSE_WARPS;  // nrows * d (optional)
+  const double* Phi = a.Phi + (long long)e * d * d;
+  const double* gv = a.gvec + (long long)e * d;
+  const double* F = a.F_hat ? a.F_hat + (long long)e * N * d : nullptr;
+  double* Gc = a.G_cache + (long long)e * N * d;
+
+  if (a.phi_in_smem) {
+    const double* src = Phi + (long long)r0 * d;
+    for (long long t = threadIdx.x; t < (long long)nrows * d; t += COARSE_THREADS) phis[t] = src[t];
+  }
+  for (int k = threadIdx.x; k < d; k += COARSE_THREADS) xs[k] = X_old[k];
+  for (int r = r0 + threadIdx.x; r < r1; r += COARSE_THREADS) X_new[r] = X_old[r];
+  __syncthreads();
+
+  for (int n = 0; n < N; ++n) {
+    double sd = 0.0, sn = 0.0;  // this warp's partial ||x_new - x_old||^2, ||x_new||^2
+    for (int rr = warp; rr < nrows; rr += COARSE_WARPS) {
+      const int r = r0 + rr;
+      const double* row = a.phi_in_smem ? phis + (long long)rr * d : Phi + (long long)r * d;
+      double acc = 0.0;
+      for (int k = lane; k < d; k += 32) acc = fma(row[k], xs[k], acc);
+      acc = warp_sum_c(acc);
+      if (lane == 0) {
+        const double g = acc + gv[r];
+        const long long o = (long long)n * d + r;
+        double x;
+        if (F)
+          x = F[o] + (g - Gc[o]);
+        else
+          x = g;
+        Gc[o] = g;
+        X_new[o + d] = x;
+        const double df = x - X_old[o + d];
+        sd += df * df;
+        sn += x * x;
+      }
+    }
+    if (lane == 0) {
+      wpart[2 * warp] = sd;
+      wpart[2 * warp + 1] = sn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double td = 0.0, tn = 0.0;
+      for (int w = 0; w < COARSE_WARPS; ++w) {
+        td += wpart[2 * w];
+        tn += wpart[2 * w + 1];
+      }
+      double* p = a.partial + (((long long)e * N + n) * a.cs + rank) * 2;
+      p[0] = td;
+      p[1] = tn;
+    }
+    cluster.sync();  // publishes X_new[n+1] (release/acquire at cluster scope)
+    const double* xn = X_new + (long long)(n + 1) * d;
+    for (int k = threadIdx.x; k < d; k += COARSE_THREADS) xs[k] = __ldcg(xn + k);
+    __syncthreads();
+  }
+
+  if (rank == 0 && threadIdx.x == 0 && a.diff) {
+    double md = 0.0, mn = 0.0;
+    for (int n = 0; n < N; ++n) {
+      const double* p = a.partial + ((long long)e * N + n) * a.cs * 2;
+      double td = 0.0, tn = 0.0;
+      for (int c = 0; c < a.cs; ++c) {
+        td += p[2 * c];
+        tn += p[2 * c + 1];
+      }
+      const double nd = sqrt(td), nn = sqrt(tn);
+      md = (nd > md || nd != nd) ? nd : md;
+      mn = (nn > mn || nn != nn) ? nn : mn;
+    }
+    a.diff[2 * e] = md;
+    a.diff[2 * e + 1] = mn;
+  }
+}
+
+int coarse_cluster_size(int d) {
+  if (d >= 256) return 16;
+  if (d >= 64) return 8;
+  if (d >= 16) return 4;
+  return 1;
+}
+
+void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
+                    const double* X_old, const double* F_hat, double* G_cache, double* X_new,
+                    double* partial, double* diff, const int* active, cudaStream_t st) {
+  if (N <= 0 || d <= 0) return;
+  CoarseArgs a;
+  a.d = d;
+  a.N = N;
+  a.cs = coarse_cluster_size(d);
+  const int rows_max = (d + a.cs - 1) / a.cs;
+  size_t base = sizeof(double) * (d + 2 * COARSE_WARPS);
+  size_t with_phi = base + sizeof(double) * (size_t)rows_max * d;
+  a.phi_in_smem = with_phi <= 200 * 1024;
+  size_t smem = a.phi_in_smem ? with_phi : base;
+  a.Phi = Phi;
+  a.gvec = gvec;
+  a.X_old = X_old;
+  a.F_hat = F_hat;
+  a.G_cache = G_cache;
+  a.X_new = X_new;
+  a.partial = partial;
+  a.diff = diff;
+  a.active = active;
+  static bool attr_done = false;
+  if (!attr_done) {
+    PE_CUDA_CHECK(cudaFuncSetAttribute(coarse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       210 * 1024));
+    PE_CUDA_CHECK(
+        cudaFuncSetAttribute(coarse_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(E * a.cs);
+  cfg.blockDim = dim3(COARSE_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, coarse_kernel, a));
+  ++g_launches;
+}
+
+}  // namespace pe

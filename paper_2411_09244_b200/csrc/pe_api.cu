@@ -1,0 +1,621 @@
+// C ABI of libpe (include/pe.h): context, uploads, fine propagators, fused coarse
+// correction and the device-resident parareal loop.
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pe.h"
+#include "pe_ctx.h"
+
+namespace pe {
+
+long long g_launches = 0;
+static thread_local std::string t_err;
+void set_error(const std::string& m) { t_err = m; }
+
+void setup_sequential(pe_ctx* c, double dt);
+void setup_coarse(pe_ctx* c, double dt);
+void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_iter);
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return PE_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return PE_ERR_CUDA;
+  } catch (...) {
+    set_error("unknown error");
+    return PE_ERR_CUDA;
+  }
+}
+
+static void require(bool ok, int code, const char* msg) {
+  if (!ok) throw Error{code, msg};
+}
+
+static void bind(pe_ctx* c) { PE_CUDA_CHECK(cudaSetDevice(c->device)); }
+
+// ------------------------------------------------------------------ sequential fine
+// X_in/X_out: (E, nc, d) == per member a column-major d x nc matrix.
+// With X_prev == nullptr the lags are reset (D_0 = 0, interval start); otherwise
+// D_0 = X_in - X_prev (a single split_step with explicit lags, stepping.py:122-147).
+static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc,
+                            cudaStream_t st, const double* X_prev = nullptr, int steps = -1) {
+  const int d = c->d, E = c->E, J = steps < 0 ? c->J : steps;
+  const size_t n = (size_t)E * nc * d;
+  c->Xa.ensure(sizeof(double) * n + 8);
+  c->Xb.ensure(sizeof(double) * n + 8);
+  c->Da.ensure(sizeof(double) * n + 8);
+  c->Db.ensure(sizeof(double) * n + 8);
+  c->stats = FineStats();
+  const double* Xs = X_in;
+  const double* Ds = nullptr;  // D_0 = 0 at the interval start (lags reset, stepping.py:180)
+  double* bufX[2] = {c->Xa.d(), c->Xb.d()};
+  double* bufD[2] = {c->Da.d(), c->Db.d()};
+  if (X_prev) {
+    c->Xin.ensure(sizeof(double) * n + 8);
+    sub((long long)n, X_in, X_prev, c->Xin.d(), st);
+    Ds = c->Xin.d();
+  }
+  for (int s = 0; s < J; ++s) {
+    const bool last = (s == J - 1);
+    double* Xn = last ? X_out : bufX[s & 1];
+    double* Dn = last ? nullptr : bufD[s & 1];
+    GemmParams p;
+    p.M = d;
+    p.N = nc;
+    p.nb1 = E;
+    p.nseg = Ds ? 2 : 1;
+    p.seg[0].A = Operand{c->T.d(), 2LL * d, 1, 2LL * d * d, 0};
+    p.seg[0].B = Operand{Xs, 1, d, (long long)nc * d, 0};
+    p.seg[0].K = d;
+    if (Ds) {
+      p.seg[1].A = Operand{c->T.d() + d, 2LL * d, 1, 2LL * d * d, 0};
+      p.seg[1].B = Operand{Ds, 1, d, (long long)nc * d, 0};
+      p.seg[1].K = d;
+    }
+    p.C = Xn;
+    p.c_i = 1;
+    p.c_j = d;
+    p.c_b1 = (long long)nc * d;
+    p.bias = c->cvec.d();
+    p.bias_b1 = d;
+    if (Dn) {
+      p.D = Dn;
+      p.Xp = Xs;
+    }
+    gemm_f64(p, st);
+    c->stats.gemm_flops += gemm_flops(p);
+    c->stats.launches += 1;
+    Xs = Xn;
+    Ds = Dn;
+  }
+  if (J == 0) PE_CUDA_CHECK(cudaMemcpyAsync(X_out, X_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+}
+
+// ------------------------------------------------------------------ all-at-once fine
+static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc, int* sweeps,
+                           int* reasons, double* resid_hist, cudaStream_t st) {
+  const int d1 = c->d1, d2 = c->d2, E = c->E, J = c->J;
+  const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
+  const double alpha = c->wr_alpha, tol = c->wr_tol;
+  const int max_iter = c->wr_max_iter;
+  c->Ux_cur.ensure(sizeof(double) * E * (J + 2) * L1 + 8);
+  c->Ux_new.ensure(sizeof(double) * E * (J + 2) * L1 + 8);
+  c->Wx_cur.ensure(sizeof(double) * E * (J + 2) * L2 + 8);
+  c->Wx_new.ensure(sizeof(double) * E * (J + 2) * L2 + 8);
+  c->R.ensure(sizeof(double) * E * J * L1 + 8);
+  c->P.ensure(sizeof(double) * E * 2 * J * L1 + 8);
+  c->Q.ensure(sizeof(double) * E * 2 * J * L1 + 8);
+  c->DU.ensure(sizeof(double) * E * J * L1 + 8);
+  c->V.ensure(sizeof(double) * E * L1 + 8);
+  c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
+  c->counter.ensure(sizeof(int) * 2);
+  c->stats = FineStats();
+  double* Uc = c->Ux_cur.d();
+  double* Un = c->Ux_new.d();
+  double* Wc = c->Wx_cur.d();
+  double* Wn = c->Wx_new.d();
+  WrColumnState* cs = (WrColumnState*)c->colstate.p;
+  int* cnt = c->counter.i();
+
+  wr_init(E, nc, d1, d2, J, alpha, X_in, Uc, Un, Wc, Wn, c->V.d(), cs, resid_hist, max_iter, st);
+
+  // sweep recipe (GEMM parameter blocks are loop-invariant)
+  std::vector<GemmParams> pre, post;
+  if (d1) {
+    GemmParams r;  // R = [Rw1|Rw0] [Wx[1..J]; Wx[0..J-1]] + f1   (build_rhs)
+    r.M = d1;
+    r.N = J * nc;
+    r.nb1 = E;
+    r.nseg = d2 ? 2 : 0;
+    r.seg[0].A = Operand{c->RW.d(), 2LL * d2, 1, 2LL * d1 * d2, 0};
+    r.seg[0].B = Operand{Wc + L2, 1, d2, (J + 2) * L2, 0};
+    r.seg[0].K = d2;
+    r.seg[1].A = Operand{c->RW.d() + d2, 2LL * d2, 1, 2LL * d1 * d2, 0};
+    r.seg[1].B = Operand{Wc, 1, d2, (J + 2) * L2, 0};
+    r.seg[1].K = d2;
+    r.C = c->R.d();
+    r.c_i = 1;
+    r.c_j = d1;
+    r.c_b1 = J * L1;
+    r.bias = c->f1.d();
+    r.bias_b1 = d1;
+    pre.push_back(r);
+    GemmParams r0;  // R_0 += M11/dt (u0 - alpha u_final_prev)
+    r0.M = d1;
+    r0.N = nc;
+    r0.nb1 = E;
+    r0.nseg = 1;
+    r0.seg[0].A = Operand{c->M11dt.d(), d1, 1, (long long)d1 * d1, 0};
+    r0.seg[0].B = Operand{c->V.d(), 1, d1, L1, 0};
+    r0.seg[0].K = d1;
+    r0.C = c->R.d();
+    r0.c_i = 1;
+    r0.c_j = d1;
+    r0.c_b1 = J * L1;
+    r0.Cin = c->R.d();
+    r0.beta = 1.0;
+    pre.push_back(r0);
+    GemmParams tf;  // P = S^{-1} R along time (planar re/im per mode)
+    tf.M = 2 * J;
+    tf.N = (int)L1;
+    tf.nb1 = E;
+    tf.nseg = 1;
+    tf.seg[0].A = Operand{c->Finv.d(), J, 1, 0, 0};
+    tf.seg[0].B = Operand{c->R.d(), L1, 1, J * L1, 0};
+    tf.seg[0].K = J;
+    tf.C = c->P.d();
+    tf.c_i = L1;
+    tf.c_j = 1;
+    tf.c_b1 = 2 * J * L1;
+    pre.push_back(tf);
+    GemmParams sh;  // Q_k = (d_k M11 + A11)^{-1} P_k   (einsum, allatonce.py:118)
+    sh.M = d1;
+    sh.N = nc;
+    sh.nb1 = E * J;
+    sh.nb2 = 2;
+    sh.nseg = 2;
+    sh.seg[0].A = Operand{c->Bk.d(), 2LL * d1, 1, 4LL * d1 * d1, 2LL * d1 * d1};
+    sh.seg[0].B = Operand{c->P.d(), 1, d1, 2 * L1, 0};
+    sh.seg[0].K = d1;
+    sh.seg[1].A = Operand{c->Bk.d() + d1, 2LL * d1, 1, 4LL * d1 * d1, 2LL * d1 * d1};
+    sh.seg[1].B = Operand{c->P.d() + L1, 1, d1, 2 * L1, 0};
+    sh.seg[1].K = d1;
+    sh.C = c->Q.d();
+    sh.c_i = 1;
+    sh.c_j = d1;
+    sh.c_b1 = 2 * L1;
+    sh.c_b2 = L1;
+    pre.push_back(sh);
+    GemmParams tb;  // U = Re(S Q)
+    tb.M = J;
+    tb.N = (int)L1;
+    tb.nb1 = E;
+    tb.nseg = 1;
+    tb.seg[0].A = Operand{c->Fw.d(), 2LL * J, 1, 0, 0};
+    tb.seg[0].B = Operand{c->Q.d(), L1, 1, 2 * J * L1, 0};
+    tb.seg[0].K = 2 * J;
+    tb.C = Un + 2 * L1;
+    tb.c_i = L1;
+    tb.c_j = 1;
+    tb.c_b1 = (J + 2) * L1;
+    pre.push_back(tb);
+  }
+  GemmParams gw;  // g_s = [Gu|Gd][U_s; U_{s-1}-U_{s-2}] + dt M22^-T f2   (_w_sweep :222-224)
+  if (d2) {
+    gw.M = d2;
+    gw.N = J * nc;
+    gw.nb1 = E;
+    gw.nseg = d1 ? 2 : 0;
+    gw.seg[0].A = Operand{c->GW.d(), 2LL * d1, 1, 2LL * d1 * d2, 0};
+    gw.seg[0].B = Operand{Un + 2 * L1, 1, d1, (J + 2) * L1, 0};
+    gw.seg[0].K = d1;
+    gw.seg[1].A = Operand{c->GW.d() + d1, 2LL * d1, 1, 2LL * d1 * d2, 0};
+    gw.seg[1].B = Operand{c->DU.d(), 1, d1, J * L1, 0};
+    gw.seg[1].K = d1;
+    gw.C = Wn + 2 * L2;
+    gw.c_i = 1;
+    gw.c_j = d2;
+    gw.c_b1 = (J + 2) * L2;
+    gw.bias = c->cg.d();
+    gw.bias_b1 = d2;
+    for (int s = 0; s < J; ++s) {  // w_{s+1} = E w_s + g_s   (:226-229)
+      GemmParams rc;
+      rc.M = d2;
+      rc.N = nc;
+      rc.nb1 = E;
+      rc.nseg = 1;
+      rc.seg[0].A = Operand{c->Emat.d(), d2, 1, (long long)d2 * d2, 0};
+      rc.seg[0].B = Operand{Wn + (s + 1) * L2, 1, d2, (J + 2) * L2, 0};
+      rc.seg[0].K = d2;
+      rc.C = Wn + (s + 2) * L2;
+      rc.c_i = 1;
+      rc.c_j = d2;
+      rc.c_b1 = (J + 2) * L2;
+      rc.Cin = rc.C;
+      rc.beta = 1.0;
+      post.push_back(rc);
+    }
+  }
+
+  double flops_per_sweep = 0;
+  for (auto& p : pre) flops_per_sweep += gemm_flops(p);
+  if (d2) flops_per_sweep += gemm_flops(gw);
+  for (auto& p : post) flops_per_sweep += gemm_flops(p);
+
+  // Pipelined sweep loop: sweep i+1 is enqueued before the host reads sweep i's
+  // active-interval count, so the device never waits on the host; the extra sweep
+  // after the last interval stopped is fully masked (commit skips inactive columns).
+  int* host_cnt = c->pinned_count;
+  cudaEvent_t ev[2];
+  PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  auto enqueue_sweep = [&](int sweep) {
+    PE_CUDA_CHECK(cudaMemsetAsync(cnt + (sweep & 1), 0, sizeof(int), st));
+    for (auto& p : pre) gemm_f64(p, st);
+    if (d1) wr_diff_u(E, nc, d1, J, Un, c->DU.d(), st);
+    if (d2) {
+      gemm_f64(gw, st);
+      for (auto& p : post) gemm_f64(p, st);
+    }
+    wr_commit(E, nc, d1, d2, J, alpha, tol, max_iter, sweep, Uc, Un, Wc, Wn, c->V.d(), cs,
+              resid_hist, cnt + (sweep & 1), st);
+    PE_CUDA_CHECK(cudaMemcpyAsync(host_cnt + (sweep & 1), cnt + (sweep & 1), sizeof(int),
+                                  cudaMemcpyDeviceToHost, st));
+    PE_CUDA_CHECK(cudaEventRecord(ev[sweep & 1], st));
+    c->stats.gemm_flops += flops_per_sweep;
+    c->stats.launches += (int)(pre.size() + post.size() + (d2 ? 1 : 0));
+  };
+  int sweep = 0;
+  enqueue_sweep(0);
+  for (sweep = 1; sweep <= max_iter; ++sweep) {
+    if (sweep < max_iter) enqueue_sweep(sweep);
+    PE_CUDA_CHECK(cudaEventSynchronize(ev[(sweep - 1) & 1]));
+    if (host_cnt[(sweep - 1) & 1] == 0) break;
+  }
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  wr_finish(E, nc, d1, d2, J, Uc, Wc, cs, X_out, sweeps, reasons, st);
+}
+
+}  // namespace pe
+
+using namespace pe;
+
+extern "C" {
+
+const char* pe_last_error(void) { return t_err.c_str(); }
+const char* pe_version(void) { return "libpe 0.1 (sm_100a, FP64 DMMA)"; }
+
+int pe_create(pe_ctx** out, int E, int d1, int d2, int max_cols, int J, int device) {
+  return guarded([&] {
+    require(out != nullptr, PE_ERR_ARG, "ctx out pointer is NULL");
+    require(E >= 1 && d1 >= 0 && d2 >= 0 && d1 + d2 >= 1 && max_cols >= 1 && J >= 1,
+            PE_ERR_ARG, "need E >= 1, d1, d2 >= 0, d1 + d2 >= 1, max_cols >= 1, J >= 1");
+    auto* c = new pe_ctx();
+    c->E = E;
+    c->d1 = d1;
+    c->d2 = d2;
+    c->d = d1 + d2;
+    c->maxc = max_cols;
+    c->J = J;
+    c->device = device;
+    try {
+      bind(c);
+      PE_CUDA_CHECK(cudaStreamCreateWithFlags(&c->setup_stream, cudaStreamNonBlocking));
+      if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw Error{PE_ERR_CUDA, "cublasCreate failed"};
+      if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw Error{PE_ERR_CUDA, "cusolverDnCreate failed"};
+      cublasSetStream(c->blas, c->setup_stream);
+      cusolverDnSetStream(c->solver, c->setup_stream);
+      PE_CUDA_CHECK(cudaMallocHost(&c->pinned_count, 2 * sizeof(int)));
+      const size_t s11 = (size_t)E * d1 * d1, s12 = (size_t)E * d1 * d2, s22 = (size_t)E * d2 * d2;
+      c->M11.ensure(8 * s11 + 8);
+      c->A11.ensure(8 * s11 + 8);
+      c->M12.ensure(8 * s12 + 8);
+      c->A12.ensure(8 * s12 + 8);
+      c->M22.ensure(8 * s22 + 8);
+      c->A22.ensure(8 * s22 + 8);
+      c->f1.ensure(8 * (size_t)E * d1 + 8);
+      c->f2.ensure(8 * (size_t)E * d2 + 8);
+      c->member_set.assign(E, 0);
+      c->launches_at_create = g_launches;
+    } catch (...) {
+      pe_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int pe_destroy(pe_ctx* c) {
+  if (!c) return PE_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  if (c->blas) cublasDestroy(c->blas);
+  if (c->solver) cusolverDnDestroy(c->solver);
+  if (c->setup_stream) cudaStreamDestroy(c->setup_stream);
+  if (c->pinned_count) cudaFreeHost(c->pinned_count);
+  if (c->pinned_diff) cudaFreeHost(c->pinned_diff);
+  delete c;
+  return PE_OK;
+}
+
+int pe_set_system(pe_ctx* c, int m, const double* M11, const double* A11, const double* M12,
+                  const double* A12, const double* M22, const double* A22, const double* f1,
+                  const double* f2) {
+  return guarded([&] {
+    require(c != nullptr, PE_ERR_ARG, "ctx is NULL");
+    require(m >= 0 && m < c->E, PE_ERR_ARG, "member index out of range");
+    bind(c);
+    const int d1 = c->d1, d2 = c->d2;
+    auto up = [&](DevBuf& b, const double* h, size_t n) {
+      if (n == 0) return;
+      require(h != nullptr, PE_ERR_ARG, "NULL block for a non-empty subspace");
+      PE_CUDA_CHECK(cudaMemcpy(b.d() + (size_t)m * n, h, 8 * n, cudaMemcpyHostToDevice));
+    };
+    up(c->M11, M11, (size_t)d1 * d1);
+    up(c->A11, A11, (size_t)d1 * d1);
+    up(c->M12, M12, (size_t)d1 * d2);
+    up(c->A12, A12, (size_t)d1 * d2);
+    up(c->M22, M22, (size_t)d2 * d2);
+    up(c->A22, A22, (size_t)d2 * d2);
+    up(c->f1, f1, d1);
+    up(c->f2, f2, d2);
+    c->member_set[m] = 1;
+    c->seq_dt = -1.0;
+    c->coarse_dt = -1.0;
+    c->wr_ready = false;
+  });
+}
+
+static void require_system(pe_ctx* c) {
+  for (char s : c->member_set) require(s, PE_ERR_STATE, "pe_set_system not called for every member");
+}
+
+int pe_prepare_sequential(pe_ctx* c, double dt) {
+  return guarded([&] {
+    require(c && dt > 0 && std::isfinite(dt), PE_ERR_ARG, "need dt_sub > 0");
+    bind(c);
+    require_system(c);
+    if (c->seq_dt != dt) setup_sequential(c, dt);
+  });
+}
+
+int pe_prepare_coarse(pe_ctx* c, double dt) {
+  return guarded([&] {
+    require(c && dt > 0 && std::isfinite(dt), PE_ERR_ARG, "need dt > 0");
+    bind(c);
+    require_system(c);
+    if (c->coarse_dt != dt) setup_coarse(c, dt);
+  });
+}
+
+int pe_prepare_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_iter) {
+  return guarded([&] {
+    require(c && dt > 0, PE_ERR_ARG, "need substeps >= 1 and dt > 0");
+    require(alpha > 0.0 && alpha < 1.0, PE_ERR_ARG, "alpha must lie in (0, 1)");
+    require(max_iter >= 1, PE_ERR_ARG, "max_iter must be >= 1");
+    bind(c);
+    require_system(c);
+    if (!(c->wr_ready && c->wr_dt == dt && c->wr_alpha == alpha)) setup_allatonce(c, dt, alpha, tol, max_iter);
+    c->wr_tol = tol;
+    c->wr_max_iter = max_iter;
+  });
+}
+
+int pe_fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc, void* stream) {
+  return guarded([&] {
+    require(c && X_in && X_out && nc >= 1 && nc <= c->maxc, PE_ERR_ARG, "bad fine_sequential arguments");
+    require(c->seq_dt > 0, PE_ERR_STATE, "pe_prepare_sequential not called");
+    bind(c);
+    fine_sequential(c, X_in, X_out, nc, (cudaStream_t)stream);
+  });
+}
+
+int pe_fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc, int* sweeps,
+                      int* reasons, double* resid_hist, void* stream) {
+  return guarded([&] {
+    require(c && X_in && X_out && nc >= 1 && nc <= c->maxc, PE_ERR_ARG, "bad fine_allatonce arguments");
+    require(c->wr_ready, PE_ERR_STATE, "pe_prepare_allatonce not called");
+    bind(c);
+    fine_allatonce(c, X_in, X_out, nc, sweeps, reasons, resid_hist, (cudaStream_t)stream);
+  });
+}
+
+int pe_coarse_correct(pe_ctx* c, int N, const double* X_old, const double* F_hat,
+                      double* G_cache, double* X_new, double* diff, const int* active,
+                      void* stream) {
+  return guarded([&] {
+    require(c && X_old && X_new && G_cache && N >= 1, PE_ERR_ARG, "bad coarse_correct arguments");
+    require(c->coarse_dt > 0, PE_ERR_STATE, "pe_prepare_coarse not called");
+    bind(c);
+    c->partial.ensure(sizeof(double) * (size_t)c->E * N * 16 * 2 + 8);
+    coarse_correct(c->E, c->d, N, c->Phi.d(), c->gG.d(), X_old, F_hat, G_cache, X_new,
+                   c->partial.d(), diff, active, (cudaStream_t)stream);
+  });
+}
+
+int pe_coarse_apply(pe_ctx* c, const double* X_in, double* X_out, int nc, void* stream) {
+  return guarded([&] {
+    require(c && X_in && X_out && nc >= 1, PE_ERR_ARG, "bad coarse_apply arguments");
+    require(c->coarse_dt > 0, PE_ERR_STATE, "pe_prepare_coarse not called");
+    bind(c);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int d = c->d, E = c->E;
+    c->hist_tmp.ensure(sizeof(double) * (size_t)E * 2 * d + 8);
+    c->Gc.ensure(sizeof(double) * (size_t)E * d + 8);
+    c->partial.ensure(sizeof(double) * (size_t)E * 16 * 2 + 8);
+    for (int n = 0; n < nc; ++n) {
+      // one-interval initial sweep: row 1 = G(row 0), same kernel as the fused sweep
+      PE_CUDA_CHECK(cudaMemcpy2DAsync(c->hist_tmp.d(), sizeof(double) * 2 * d, X_in + (size_t)n * d,
+                                      sizeof(double) * nc * d, sizeof(double) * d, E,
+                                      cudaMemcpyDeviceToDevice, st));
+      coarse_correct(E, d, 1, c->Phi.d(), c->gG.d(), c->hist_tmp.d(), nullptr, c->Gc.d(),
+                     c->hist_tmp.d(), c->partial.d(), nullptr, nullptr, st);
+      PE_CUDA_CHECK(cudaMemcpy2DAsync(X_out + (size_t)n * d, sizeof(double) * nc * d,
+                                      c->hist_tmp.d() + d, sizeof(double) * 2 * d,
+                                      sizeof(double) * d, E, cudaMemcpyDeviceToDevice, st));
+    }
+  });
+}
+
+int pe_parareal_run(pe_ctx* c, int kind, int N, const double* X0, int k_max, double epsilon,
+                    int rule, double* history, double* diffs_h, int* iters_h, int* conv_h,
+                    int* wr_sweeps, int* wr_reasons, double* wr_resid, float* fine_ms_h,
+                    float* coarse_ms_h, int* k_done, void* stream) {
+  return guarded([&] {
+    require(c && X0 && history && N >= 1 && N <= c->maxc && k_max >= 0, PE_ERR_ARG,
+            "bad parareal_run arguments");
+    require(kind == PE_KIND_SEQUENTIAL || kind == PE_KIND_ALLATONCE, PE_ERR_ARG,
+            "unknown fine propagator kind");
+    require(rule == PE_RULE_ABSOLUTE || rule == PE_RULE_RELATIVE, PE_ERR_ARG, "unknown stop rule");
+    require(c->coarse_dt > 0, PE_ERR_STATE, "pe_prepare_coarse not called");
+    require(kind == PE_KIND_SEQUENTIAL ? c->seq_dt > 0 : c->wr_ready, PE_ERR_STATE,
+            "fine propagator not prepared");
+    bind(c);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int E = c->E, d = c->d;
+    const size_t slab = (size_t)E * (N + 1) * d;
+    auto H = [&](int k) { return history + (size_t)k * slab; };
+    c->Gc.ensure(sizeof(double) * (size_t)E * N * d + 8);
+    c->Xin.ensure(sizeof(double) * (size_t)E * N * d + 8);
+    c->Xout.ensure(sizeof(double) * (size_t)E * N * d + 8);
+    c->partial.ensure(sizeof(double) * (size_t)E * N * 16 * 2 + 8);
+    c->diff.ensure(sizeof(double) * 2 * E + 8);
+    c->active.ensure(sizeof(int) * E + 8);
+    if (c->pinned_diff_n < (size_t)2 * E) {
+      if (c->pinned_diff) cudaFreeHost(c->pinned_diff);
+      PE_CUDA_CHECK(cudaMallocHost(&c->pinned_diff, sizeof(double) * 2 * E));
+      c->pinned_diff_n = 2 * E;
+    }
+    std::vector<int> act(E, 1);
+    for (int e = 0; e < E; ++e) {
+      iters_h[e] = 0;
+      conv_h[e] = 0;
+    }
+    PE_CUDA_CHECK(cudaMemcpyAsync(c->active.p, act.data(), sizeof(int) * E, cudaMemcpyHostToDevice, st));
+    // x_0 into row 0 of every member, then the initial coarse sweep (parareal.py:150-157)
+    PE_CUDA_CHECK(cudaMemcpy2DAsync(H(0), sizeof(double) * (N + 1) * d, X0, sizeof(double) * d,
+                                    sizeof(double) * d, E, cudaMemcpyDeviceToDevice, st));
+    coarse_correct(E, d, N, c->Phi.d(), c->gG.d(), H(0), nullptr, c->Gc.d(), H(0),
+                   c->partial.d(), nullptr, nullptr, st);
+    cudaEvent_t e0, e1, e2;
+    PE_CUDA_CHECK(cudaEventCreate(&e0));
+    PE_CUDA_CHECK(cudaEventCreate(&e1));
+    PE_CUDA_CHECK(cudaEventCreate(&e2));
+    int k = 0;
+    int n_active = E;
+    for (k = 1; k <= k_max && n_active > 0; ++k) {
+      PE_CUDA_CHECK(cudaEventRecord(e0, st));
+      // fine sweep on x_0^{k-1} .. x_{N-1}^{k-1} (parareal.py:191-193)
+      PE_CUDA_CHECK(cudaMemcpy2DAsync(c->Xin.d(), sizeof(double) * N * d, H(k - 1),
+                                      sizeof(double) * (N + 1) * d, sizeof(double) * N * d, E,
+                                      cudaMemcpyDeviceToDevice, st));
+      if (kind == PE_KIND_SEQUENTIAL) {
+        fine_sequential(c, c->Xin.d(), c->Xout.d(), N, st);
+      } else {
+        const size_t off = (size_t)(k - 1) * E * N;
+        fine_allatonce(c, c->Xin.d(), c->Xout.d(), N, wr_sweeps ? wr_sweeps + off : nullptr,
+                       wr_reasons ? wr_reasons + off : nullptr,
+                       wr_resid ? wr_resid + off * c->wr_max_iter : nullptr, st);
+      }
+      PE_CUDA_CHECK(cudaEventRecord(e1, st));
+      coarse_correct(E, d, N, c->Phi.d(), c->gG.d(), H(k - 1), c->Xout.d(), c->Gc.d(), H(k),
+                     c->partial.d(), c->diff.d(), c->active.i(), st);
+      PE_CUDA_CHECK(cudaEventRecord(e2, st));
+      PE_CUDA_CHECK(cudaMemcpyAsync(c->pinned_diff, c->diff.p, sizeof(double) * 2 * E,
+                                    cudaMemcpyDeviceToHost, st));
+      PE_CUDA_CHECK(cudaStreamSynchronize(st));
+      float fm = 0, cm = 0;
+      PE_CUDA_CHECK(cudaEventElapsedTime(&fm, e0, e1));
+      PE_CUDA_CHECK(cudaEventElapsedTime(&cm, e1, e2));
+      if (fine_ms_h) fine_ms_h[k - 1] = fm;
+      if (coarse_ms_h) coarse_ms_h[k - 1] = cm;
+      bool changed = false;
+      for (int e = 0; e < E; ++e) {
+        double v = NAN;
+        if (act[e]) {
+          const double num = c->pinned_diff[2 * e], den = c->pinned_diff[2 * e + 1];
+          v = (rule == PE_RULE_ABSOLUTE) ? num : (den > 0 ? num / den : num);
+          iters_h[e] = k;
+          if (v < epsilon) {
+            conv_h[e] = 1;
+            act[e] = 0;
+            --n_active;
+            changed = true;
+          }
+        }
+        if (diffs_h) diffs_h[(size_t)(k - 1) * E + e] = v;
+      }
+      if (changed && n_active > 0)
+        PE_CUDA_CHECK(cudaMemcpyAsync(c->active.p, act.data(), sizeof(int) * E, cudaMemcpyHostToDevice, st));
+      PE_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    if (k_done) *k_done = k - 1;
+  });
+}
+
+int pe_split_step(pe_ctx* c, const double* X_in, const double* X_prev, double* X_out, int nc,
+                  void* stream) {
+  return guarded([&] {
+    require(c && X_in && X_prev && X_out && nc >= 1, PE_ERR_ARG, "bad split_step arguments");
+    require(c->seq_dt > 0, PE_ERR_STATE, "pe_prepare_sequential not called");
+    bind(c);
+    fine_sequential(c, X_in, X_out, nc, (cudaStream_t)stream, X_prev, 1);
+  });
+}
+
+int pe_wr_waveforms(pe_ctx* c, double* U_out, double* W_out, int nc, void* stream) {
+  return guarded([&] {
+    require(c && nc >= 1, PE_ERR_ARG, "bad wr_waveforms arguments");
+    require(c->wr_ready && c->Ux_cur.p, PE_ERR_STATE, "no all-at-once solve to read back");
+    bind(c);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (U_out && c->d1) wr_gather(c->E, nc, c->d1, c->J, c->Ux_cur.d(), U_out, st);
+    if (W_out && c->d2) wr_gather(c->E, nc, c->d2, c->J, c->Wx_cur.d(), W_out, st);
+  });
+}
+
+int pe_gemm_f64(int M, int N, int K, const double* A, long long a_i, long long a_k,
+                const double* B, long long b_k, long long b_j, double* C, long long c_i,
+                long long c_j, void* stream) {
+  return guarded([&] {
+    require(M >= 0 && N >= 0 && K >= 0 && C, PE_ERR_ARG, "bad gemm arguments");
+    GemmParams p;
+    p.M = M;
+    p.N = N;
+    p.nseg = K > 0 ? 1 : 0;
+    p.seg[0].A = Operand{A, a_i, a_k, 0, 0};
+    p.seg[0].B = Operand{B, b_k, b_j, 0, 0};
+    p.seg[0].K = K;
+    p.C = C;
+    p.c_i = c_i;
+    p.c_j = c_j;
+    gemm_f64(p, (cudaStream_t)stream);
+  });
+}
+
+long long pe_launch_count(pe_ctx* c) { return c ? g_launches - c->launches_at_create : g_launches; }
+
+int pe_last_fine_stats(pe_ctx* c, double* gemm_ms, double* gemm_flops_out, int* launches) {
+  return guarded([&] {
+    require(c != nullptr, PE_ERR_ARG, "ctx is NULL");
+    if (gemm_ms) *gemm_ms = 0.0;
+    if (gemm_flops_out) *gemm_flops_out = c->stats.gemm_flops;
+    if (launches) *launches = c->stats.launches;
+  });
+}
+
+}  // extern "C"

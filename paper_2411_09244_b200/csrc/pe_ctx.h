@@ -1,0 +1,81 @@
+// libpe context: device-resident operators, factor caches and work buffers.
+#pragma once
+
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <map>
+#include <vector>
+
+#include "pe_internal.h"
+
+namespace pe {
+
+// Owning device buffer (bytes); grows, never shrinks.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (n == 0) return;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error{PE_ERR_NOMEM, "cudaMalloc of " + std::to_string(n) + " bytes failed"};
+    }
+    bytes = n;
+  }
+  double* d() const { return static_cast<double*>(p); }
+  int* i() const { return static_cast<int*>(p); }
+};
+
+struct FineStats {
+  double gemm_flops = 0;   // algorithmic flops issued by the GEMM kernels of the last fine call
+  int launches = 0;
+};
+
+}  // namespace pe
+
+struct pe_ctx {
+  int E = 0, d1 = 0, d2 = 0, d = 0, maxc = 0, J = 0, device = 0;
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  cudaStream_t setup_stream = nullptr;
+
+  // reduced system, row-major, member-strided
+  pe::DevBuf M11, A11, M12, A12, M22, A22, f1, f2;
+  std::vector<char> member_set;
+
+  // sequential fine: X_{s+1} = T [X_s; D_s] + cvec   (T: E x d x 2d)
+  double seq_dt = -1.0;
+  pe::DevBuf T, cvec;
+  // coarse: G(x) = Phi x + gG                         (Phi: E x d x d)
+  double coarse_dt = -1.0;
+  pe::DevBuf Phi, gG;
+  // all-at-once
+  bool wr_ready = false;
+  double wr_dt = 0, wr_alpha = 0, wr_tol = 0;
+  int wr_max_iter = 0;
+  pe::DevBuf Bk, RW, M11dt, GW, cg, Emat, Finv, Fw;
+
+  // work buffers
+  pe::DevBuf Xin, Xout, Xa, Xb, Da, Db;
+  pe::DevBuf Ux_cur, Ux_new, Wx_cur, Wx_new, R, P, Q, DU, V, colstate, counter;
+  pe::DevBuf partial, diff, Gc, active, hist_tmp;
+  int* pinned_count = nullptr;
+  double* pinned_diff = nullptr;
+  size_t pinned_diff_n = 0;
+
+  long long launches_at_create = 0;
+  pe::FineStats stats;
+};

@@ -1,0 +1,101 @@
+// Internal declarations shared by the libpe translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+namespace pe {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define PE_CUDA_CHECK(expr)                                                               \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      throw ::pe::Error{PE_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+  } while (0)
+
+// ---------------------------------------------------------------- FP64 DMMA GEMM
+//
+// C[z](i,j) = alpha * sum_seg sum_k A_seg[z](i,k) B_seg[z](k,j)
+//             + beta * Cin[z](i,j) + bias[z](i)            (then optional D = C - Xp)
+// with z = z1 * nb2 + z2 a two-level batch index; every operand has arbitrary
+// element strides and per-level batch strides (0 = shared across that level).
+// The k reduction runs segment by segment, k ascending, in m8n8k4 DMMA steps, so
+// the result for one (i,j) does not depend on tile shape or on the other columns
+// (batch invariance: F applied to one state equals F applied inside a batch).
+struct Operand {
+  const double* p = nullptr;
+  long long s0 = 0, s1 = 0;    // element strides (A: i,k  B: k,j)
+  long long b1 = 0, b2 = 0;    // batch strides (level 1, level 2)
+};
+
+struct GemmSeg {
+  Operand A, B;
+  int K = 0;
+};
+
+struct GemmParams {
+  int M = 0, N = 0;
+  int nb1 = 1, nb2 = 1;
+  int nseg = 0;
+  GemmSeg seg[3];
+  double* C = nullptr;
+  long long c_i = 0, c_j = 0, c_b1 = 0, c_b2 = 0;
+  double alpha = 1.0;
+  double beta = 0.0;
+  const double* Cin = nullptr;  // same strides as C
+  const double* bias = nullptr;
+  long long bias_b1 = 0, bias_b2 = 0;
+  double* D = nullptr;          // optional D = C - Xp, same strides as C
+  const double* Xp = nullptr;
+};
+
+// Launch; chooses tile shape and the k-/j-contiguous loader variant from strides.
+void gemm_f64(const GemmParams& p, cudaStream_t st);
+// Flop count of one launch (2*M*N*sumK*batch), for the roofline bookkeeping.
+double gemm_flops(const GemmParams& p);
+
+// ---------------------------------------------------------------- WR helpers
+struct WrColumnState {
+  int active;
+  int iterations;
+  int stall;
+  int reason;
+  double prev;
+  double r0;
+};
+
+void wr_init(int E, int ncols, int d1, int d2, int J, double alpha, const double* X_in,
+             double* Ux_cur, double* Ux_new, double* Wx_cur, double* Wx_new, double* V,
+             WrColumnState* cs, double* resid_hist, int max_iter, cudaStream_t st);
+void wr_diff_u(int E, int ncols, int d1, int J, const double* Ux_new, double* DU,
+               cudaStream_t st);
+void wr_commit(int E, int ncols, int d1, int d2, int J, double alpha, double tol,
+               int max_iter, int sweep, double* Ux_cur, const double* Ux_new, double* Wx_cur,
+               const double* Wx_new, double* V, WrColumnState* cs, double* resid_hist,
+               int* active_count, cudaStream_t st);
+void wr_finish(int E, int ncols, int d1, int d2, int J, const double* Ux_cur,
+               const double* Wx_cur, const WrColumnState* cs, double* X_out, int* sweeps,
+               int* reasons, cudaStream_t st);
+
+void wr_gather(int E, int nc, int dd, int J, const double* X, double* out, cudaStream_t st);
+void sub(long long n, const double* a, const double* b, double* out, cudaStream_t st);
+
+// ---------------------------------------------------------------- coarse sweep
+// Row-partitioned cluster kernel; see coarse.cu.
+void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
+                    const double* X_old, const double* F_hat, double* G_cache, double* X_new,
+                    double* partial, double* diff, const int* active, cudaStream_t st);
+int coarse_cluster_size(int d);
+
+extern long long g_launches;  // kernel launches issued by libpe in this process
+
+}  // namespace pe

@@ -1,0 +1,366 @@
+// Setup (outside the timed region): factorisations and the composite
+// operators the hot-path kernels apply.  cuSOLVER getrf/getrs + cuBLAS are used here
+// only; the per-step work runs in libpe's own kernels.
+//
+//   sequential (stepping.py:109-147): with K = M11/dt + A11,
+//     u+ = Pu u + Pa w + Pd (w - w_prev) + cu
+//     w+ = Ew w + Qd (u - u_prev) + Qu u+ + cw
+//   where Pu = K^-1 M11/dt, Pa = -K^-1 A12, Pd = -K^-1 M12/dt, cu = K^-1 f1,
+//         Ew = I - dt M22^-1 A22, Qd = -M22^-1 M12^T, Qu = -dt M22^-1 A12^T, cw = dt M22^-1 f2.
+//   Substituting u+ gives one (d x 2d) operator T acting on [u; w; u-u_prev; w-w_prev]:
+//     T = [[Pu,     Pa,         0,  Pd    ],
+//          [Qu Pu,  Ew + Qu Pa, Qd, Qu Pd ]],   c = [cu; cw + Qu cu].
+//   coarse (stepping.py:149-176): G(x) = Phi x + gG with Phi = K_G^-1 R_G, gG = K_G^-1 f.
+//   all-at-once (allatonce.py:100-110, 184-210): shifted inverses (d_k M11 + A11)^-1 as
+//     real 2x2-block matrices, the rhs operator [-(M12/dt + A12) | M12/dt], M11/dt,
+//     the w-sweep operator [-dt M22^-T A12^T | -M22^-T M12^T], dt M22^-T f2, E and the
+//     alpha-circulant time transforms S^-1 (2J x J) and Re(S .) (J x 2J).
+
+#include <cuComplex.h>
+
+#include <cmath>
+#include <complex>
+#include <vector>
+
+#include "pe.h"
+#include "pe_ctx.h"
+
+namespace pe {
+
+#define BLAS_CHECK(x)                                                               \
+  do {                                                                              \
+    cublasStatus_t _s = (x);                                                        \
+    if (_s != CUBLAS_STATUS_SUCCESS)                                                \
+      throw Error{PE_ERR_CUDA, std::string(#x) + " failed: " + std::to_string(_s)}; \
+  } while (0)
+#define SOLVER_CHECK(x)                                                             \
+  do {                                                                              \
+    cusolverStatus_t _s = (x);                                                      \
+    if (_s != CUSOLVER_STATUS_SUCCESS)                                              \
+      throw Error{PE_ERR_CUDA, std::string(#x) + " failed: " + std::to_string(_s)}; \
+  } while (0)
+
+// row-major C(m x n) = alpha op(A) op(B) + beta C
+static void rm_gemm(cublasHandle_t h, bool tA, bool tB, int m, int n, int k, double alpha,
+                    const double* A, int lda, const double* B, int ldb, double beta, double* C,
+                    int ldc) {
+  if (m == 0 || n == 0) return;
+  if (k == 0) {
+    // C = beta C: scale via geam
+    BLAS_CHECK(cublasDgeam(h, CUBLAS_OP_N, CUBLAS_OP_N, n, m, &beta, C, ldc, &beta, C, ldc, C,
+                           ldc));
+    double zero = 0.0;
+    if (beta == 0.0)
+      BLAS_CHECK(cublasDgeam(h, CUBLAS_OP_N, CUBLAS_OP_N, n, m, &zero, C, ldc, &zero, C, ldc, C,
+                             ldc));
+    return;
+  }
+  BLAS_CHECK(cublasDgemm(h, tB ? CUBLAS_OP_T : CUBLAS_OP_N, tA ? CUBLAS_OP_T : CUBLAS_OP_N, n,
+                         m, k, &alpha, B, ldb, A, lda, &beta, C, ldc));
+}
+// row-major C(m x n) = alpha op(A) + beta op(B)
+static void rm_geam(cublasHandle_t h, bool tA, bool tB, int m, int n, double alpha,
+                    const double* A, int lda, double beta, const double* B, int ldb, double* C,
+                    int ldc) {
+  if (m == 0 || n == 0) return;
+  BLAS_CHECK(cublasDgeam(h, tA ? CUBLAS_OP_T : CUBLAS_OP_N, tB ? CUBLAS_OP_T : CUBLAS_OP_N, n,
+                         m, &alpha, A, lda, &beta, B, ldb, C, ldc));
+}
+
+__global__ void set_identity_kernel(int n, double* X, int ld, double scale) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long tot = (long long)n * n;
+  for (; t < tot; t += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(t / n), j = (int)(t % n);
+    X[(long long)i * ld + j] = (i == j) ? scale : 0.0;
+  }
+}
+static void set_identity(int n, double* X, int ld, double scale, cudaStream_t st) {
+  if (n == 0) return;
+  set_identity_kernel<<<std::min(1024, (n * n + 255) / 256), 256, 0, st>>>(n, X, ld, scale);
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
+__global__ void zero_block_kernel(int m, int n, double* X, int ld) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; t < (long long)m * n; t += (long long)gridDim.x * blockDim.x)
+    X[(t / n) * ld + (t % n)] = 0.0;
+}
+
+// S = dk * M11 + A11 (complex, row-major d1 x d1)
+__global__ void shifted_kernel(int n, double dre, double dim, const double* M, const double* A,
+                               cuDoubleComplex* S) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; t < (long long)n * n; t += (long long)gridDim.x * blockDim.x)
+    S[t] = make_cuDoubleComplex(dre * M[t] + A[t], dim * M[t]);
+}
+__global__ void zidentity_kernel(int n, cuDoubleComplex* X) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; t < (long long)n * n; t += (long long)gridDim.x * blockDim.x)
+    X[t] = make_cuDoubleComplex((t / n) == (t % n) ? 1.0 : 0.0, 0.0);
+}
+// Bk (2n x 2n row-major, planar blocks) = [[Re, -Im], [Im, Re]] of inv (row-major n x n)
+__global__ void realify_kernel(int n, const cuDoubleComplex* inv, double* B) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long n2 = 2LL * n;
+  for (; t < (long long)n * n; t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / n, j = t % n;
+    const double re = cuCreal(inv[t]), im = cuCimag(inv[t]);
+    B[i * n2 + j] = re;
+    B[i * n2 + n + j] = -im;
+    B[(i + n) * n2 + j] = im;
+    B[(i + n) * n2 + n + j] = re;
+  }
+}
+
+static int grid_for(long long n) { return (int)std::max<long long>(1, std::min<long long>(4096, (n + 255) / 256)); }
+
+// Ainv = A^{-1} for a row-major n x n buffer (inv(A^T) = inv(A)^T, so the
+// column-major solver view is harmless).
+static void inverse(pe_ctx* c, int n, const double* A, double* Ainv) {
+  if (n == 0) return;
+  cudaStream_t st = c->setup_stream;
+  DevBuf lu, ipiv, info, work;
+  lu.ensure(sizeof(double) * n * (size_t)n);
+  ipiv.ensure(sizeof(int) * n);
+  info.ensure(sizeof(int));
+  PE_CUDA_CHECK(cudaMemcpyAsync(lu.p, A, sizeof(double) * n * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  int lwork = 0;
+  SOLVER_CHECK(cusolverDnDgetrf_bufferSize(c->solver, n, n, lu.d(), n, &lwork));
+  work.ensure(sizeof(double) * std::max(lwork, 1));
+  SOLVER_CHECK(cusolverDnDgetrf(c->solver, n, n, lu.d(), n, work.d(), ipiv.i(), info.i()));
+  int h_info = 0;
+  PE_CUDA_CHECK(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (h_info != 0) throw Error{PE_ERR_SOLVER, "singular matrix in setup factorisation (getrf info " + std::to_string(h_info) + ")"};
+  set_identity(n, Ainv, n, 1.0, st);
+  SOLVER_CHECK(cusolverDnDgetrs(c->solver, CUBLAS_OP_N, n, n, lu.d(), n, ipiv.i(), Ainv, n, info.i()));
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+static void zinverse(pe_ctx* c, int n, cuDoubleComplex* S, cuDoubleComplex* Sinv, DevBuf& ipiv,
+                     DevBuf& info, DevBuf& work) {
+  cudaStream_t st = c->setup_stream;
+  int lwork = 0;
+  SOLVER_CHECK(cusolverDnZgetrf_bufferSize(c->solver, n, n, S, n, &lwork));
+  work.ensure(sizeof(cuDoubleComplex) * std::max(lwork, 1));
+  ipiv.ensure(sizeof(int) * n);
+  info.ensure(sizeof(int));
+  SOLVER_CHECK(cusolverDnZgetrf(c->solver, n, n, S, n, (cuDoubleComplex*)work.p, ipiv.i(), info.i()));
+  int h_info = 0;
+  PE_CUDA_CHECK(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (h_info != 0) throw Error{PE_ERR_SOLVER, "singular shifted matrix d_k M11 + A11 (zgetrf info " + std::to_string(h_info) + ")"};
+  zidentity_kernel<<<grid_for((long long)n * n), 256, 0, st>>>(n, Sinv);
+  SOLVER_CHECK(cusolverDnZgetrs(c->solver, CUBLAS_OP_N, n, n, S, n, ipiv.i(), Sinv, n, info.i()));
+}
+
+void setup_sequential(pe_ctx* c, double dt) {
+  const int d1 = c->d1, d2 = c->d2, d = c->d;
+  cudaStream_t st = c->setup_stream;
+  cublasHandle_t h = c->blas;
+  c->T.ensure(sizeof(double) * (size_t)c->E * d * 2 * d + 8);
+  c->cvec.ensure(sizeof(double) * (size_t)c->E * d + 8);
+  DevBuf K, Kinv, M22inv, Ew, Qd, Qu, cw;
+  K.ensure(sizeof(double) * d1 * (size_t)d1 + 8);
+  Kinv.ensure(sizeof(double) * d1 * (size_t)d1 + 8);
+  M22inv.ensure(sizeof(double) * d2 * (size_t)d2 + 8);
+  Ew.ensure(sizeof(double) * d2 * (size_t)d2 + 8);
+  Qd.ensure(sizeof(double) * d2 * (size_t)d1 + 8);
+  Qu.ensure(sizeof(double) * d2 * (size_t)d1 + 8);
+  cw.ensure(sizeof(double) * d2 + 8);
+  const int ldT = 2 * d;
+  for (int e = 0; e < c->E; ++e) {
+    const double* M11 = c->M11.d() + (size_t)e * d1 * d1;
+    const double* A11 = c->A11.d() + (size_t)e * d1 * d1;
+    const double* M12 = c->M12.d() + (size_t)e * d1 * d2;
+    const double* A12 = c->A12.d() + (size_t)e * d1 * d2;
+    const double* M22 = c->M22.d() + (size_t)e * d2 * d2;
+    const double* A22 = c->A22.d() + (size_t)e * d2 * d2;
+    const double* f1 = c->f1.d() + (size_t)e * d1;
+    const double* f2 = c->f2.d() + (size_t)e * d2;
+    double* T = c->T.d() + (size_t)e * d * ldT;
+    double* cv = c->cvec.d() + (size_t)e * d;
+    zero_block_kernel<<<grid_for((long long)d * ldT), 256, 0, st>>>(d, ldT, T, ldT);
+    if (d1) {
+      rm_geam(h, false, false, d1, d1, 1.0 / dt, M11, d1, 1.0, A11, d1, K.d(), d1);
+      inverse(c, d1, K.d(), Kinv.d());
+      rm_gemm(h, false, false, d1, d1, d1, 1.0 / dt, Kinv.d(), d1, M11, d1, 0.0, T, ldT);  // Pu
+      if (d2) {
+        rm_gemm(h, false, false, d1, d2, d1, -1.0, Kinv.d(), d1, A12, d2, 0.0, T + d1, ldT);  // Pa
+        rm_gemm(h, false, false, d1, d2, d1, -1.0 / dt, Kinv.d(), d1, M12, d2, 0.0,
+                T + d + d1, ldT);  // Pd
+      }
+      rm_gemm(h, false, false, d1, 1, d1, 1.0, Kinv.d(), d1, f1, 1, 0.0, cv, 1);  // cu
+    }
+    if (d2) {
+      inverse(c, d2, M22, M22inv.d());
+      double* Tw = T + (size_t)d1 * ldT;  // rows d1..d-1
+      // Ew = I - dt M22^-1 A22 written straight into T[d1:, d1:d]
+      set_identity(d2, Tw + d1, ldT, 1.0, st);
+      rm_gemm(h, false, false, d2, d2, d2, -dt, M22inv.d(), d2, A22, d2, 1.0, Tw + d1, ldT);
+      rm_gemm(h, false, false, d2, 1, d2, dt, M22inv.d(), d2, f2, 1, 0.0, cv + d1, 1);  // cw
+      if (d1) {
+        rm_gemm(h, false, true, d2, d1, d2, -1.0, M22inv.d(), d2, M12, d2, 0.0, Tw + d, ldT);  // Qd
+        rm_gemm(h, false, true, d2, d1, d2, -dt, M22inv.d(), d2, A12, d2, 0.0, Qu.d(), d1);   // Qu
+        // fold u+ into the w rows: Qu [Pu, Pa, 0, Pd] and Qu cu
+        rm_gemm(h, false, false, d2, d1, d1, 1.0, Qu.d(), d1, T, ldT, 0.0, Tw, ldT);
+        rm_gemm(h, false, false, d2, d2, d1, 1.0, Qu.d(), d1, T + d1, ldT, 1.0, Tw + d1, ldT);
+        rm_gemm(h, false, false, d2, d2, d1, 1.0, Qu.d(), d1, T + d + d1, ldT, 0.0,
+                Tw + d + d1, ldT);
+        rm_gemm(h, false, false, d2, 1, d1, 1.0, Qu.d(), d1, cv, 1, 1.0, cv + d1, 1);
+      }
+    }
+  }
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  c->seq_dt = dt;
+}
+
+__global__ void assemble_coarse_kernel(int d1, int d2, double dt, const double* M11,
+                                       const double* A11, const double* M12, const double* A12,
+                                       const double* M22, const double* A22, double* KG,
+                                       double* RG) {
+  const int d = d1 + d2;
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; t < (long long)d * d; t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / d), j = (int)(t % d);
+    double k, r;
+    if (i < d1 && j < d1) {
+      const double m = M11[i * d1 + j], a = A11[i * d1 + j];
+      k = m / dt + a;
+      r = m / dt;
+    } else if (i < d1) {
+      const double m = M12[i * d2 + (j - d1)], a = A12[i * d2 + (j - d1)];
+      k = m / dt;
+      r = m / dt - a;
+    } else if (j < d1) {
+      const double m = M12[j * d2 + (i - d1)], a = A12[j * d2 + (i - d1)];  // transposes
+      k = m / dt + a;
+      r = m / dt;
+    } else {
+      const double m = M22[(i - d1) * d2 + (j - d1)], a = A22[(i - d1) * d2 + (j - d1)];
+      k = m / dt;
+      r = m / dt - a;
+    }
+    KG[t] = k;
+    RG[t] = r;
+  }
+}
+
+void setup_coarse(pe_ctx* c, double dt) {
+  const int d1 = c->d1, d2 = c->d2, d = c->d;
+  cudaStream_t st = c->setup_stream;
+  c->Phi.ensure(sizeof(double) * (size_t)c->E * d * d + 8);
+  c->gG.ensure(sizeof(double) * (size_t)c->E * d + 8);
+  DevBuf KG, RG, KGinv, f;
+  KG.ensure(sizeof(double) * (size_t)d * d);
+  RG.ensure(sizeof(double) * (size_t)d * d);
+  KGinv.ensure(sizeof(double) * (size_t)d * d);
+  f.ensure(sizeof(double) * d);
+  for (int e = 0; e < c->E; ++e) {
+    assemble_coarse_kernel<<<grid_for((long long)d * d), 256, 0, st>>>(
+        d1, d2, dt, c->M11.d() + (size_t)e * d1 * d1, c->A11.d() + (size_t)e * d1 * d1,
+        c->M12.d() + (size_t)e * d1 * d2, c->A12.d() + (size_t)e * d1 * d2,
+        c->M22.d() + (size_t)e * d2 * d2, c->A22.d() + (size_t)e * d2 * d2, KG.d(), RG.d());
+    PE_CUDA_CHECK(cudaGetLastError());
+    if (d1) PE_CUDA_CHECK(cudaMemcpyAsync(f.d(), c->f1.d() + (size_t)e * d1, sizeof(double) * d1, cudaMemcpyDeviceToDevice, st));
+    if (d2) PE_CUDA_CHECK(cudaMemcpyAsync(f.d() + d1, c->f2.d() + (size_t)e * d2, sizeof(double) * d2, cudaMemcpyDeviceToDevice, st));
+    inverse(c, d, KG.d(), KGinv.d());
+    rm_gemm(c->blas, false, false, d, d, d, 1.0, KGinv.d(), d, RG.d(), d, 0.0,
+            c->Phi.d() + (size_t)e * d * d, d);
+    rm_gemm(c->blas, false, false, d, 1, d, 1.0, KGinv.d(), d, f.d(), 1, 0.0,
+            c->gG.d() + (size_t)e * d, 1);
+  }
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  c->coarse_dt = dt;
+}
+
+void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_iter) {
+  const int d1 = c->d1, d2 = c->d2, J = c->J, E = c->E;
+  cudaStream_t st = c->setup_stream;
+  cublasHandle_t h = c->blas;
+  // time transforms (host, exact index reduction k*s mod J)
+  {
+    std::vector<double> finv((size_t)2 * J * J), fw((size_t)J * 2 * J);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int k = 0; k < J; ++k)
+      for (int s = 0; s < J; ++s) {
+        const long long ks = ((long long)k * s) % J;
+        const double ang = two_pi * (double)ks / (double)J;
+        const double lam_inv = std::pow(alpha, (double)s / J);   // Lambda^{-1}_s
+        const double lam = std::pow(alpha, -(double)s / J);      // Lambda_s
+        // S^{-1}: p_k = (1/J) sum_s e^{-i ang} alpha^{s/J} r_s
+        finv[(size_t)(2 * k) * J + s] = lam_inv * std::cos(ang) / J;
+        finv[(size_t)(2 * k + 1) * J + s] = -lam_inv * std::sin(ang) / J;
+        // Re(S q)_s = sum_k alpha^{-s/J} (cos ang Re q_k - sin ang Im q_k)
+        fw[(size_t)s * 2 * J + 2 * k] = lam * std::cos(ang);
+        fw[(size_t)s * 2 * J + 2 * k + 1] = -lam * std::sin(ang);
+      }
+    c->Finv.ensure(sizeof(double) * finv.size());
+    c->Fw.ensure(sizeof(double) * fw.size());
+    PE_CUDA_CHECK(cudaMemcpy(c->Finv.p, finv.data(), sizeof(double) * finv.size(), cudaMemcpyHostToDevice));
+    PE_CUDA_CHECK(cudaMemcpy(c->Fw.p, fw.data(), sizeof(double) * fw.size(), cudaMemcpyHostToDevice));
+  }
+  c->Bk.ensure(sizeof(double) * (size_t)E * J * 4 * d1 * d1 + 8);
+  c->RW.ensure(sizeof(double) * (size_t)E * d1 * 2 * d2 + 8);
+  c->M11dt.ensure(sizeof(double) * (size_t)E * d1 * d1 + 8);
+  c->GW.ensure(sizeof(double) * (size_t)E * d2 * 2 * d1 + 8);
+  c->cg.ensure(sizeof(double) * (size_t)E * d2 + 8);
+  c->Emat.ensure(sizeof(double) * (size_t)E * d2 * d2 + 8);
+  DevBuf S, Sinv, ipiv, info, work, M22inv;
+  S.ensure(sizeof(cuDoubleComplex) * (size_t)d1 * d1 + 16);
+  Sinv.ensure(sizeof(cuDoubleComplex) * (size_t)d1 * d1 + 16);
+  M22inv.ensure(sizeof(double) * (size_t)d2 * d2 + 8);
+  const double om_r = std::pow(alpha, 1.0 / J);
+  for (int e = 0; e < E; ++e) {
+    const double* M11 = c->M11.d() + (size_t)e * d1 * d1;
+    const double* A11 = c->A11.d() + (size_t)e * d1 * d1;
+    const double* M12 = c->M12.d() + (size_t)e * d1 * d2;
+    const double* A12 = c->A12.d() + (size_t)e * d1 * d2;
+    const double* M22 = c->M22.d() + (size_t)e * d2 * d2;
+    const double* A22 = c->A22.d() + (size_t)e * d2 * d2;
+    const double* f2 = c->f2.d() + (size_t)e * d2;
+    if (d1) {
+      for (int k = 0; k < J; ++k) {
+        // d_k = (1 - alpha^{1/J} e^{-2 pi i k/J}) / dt   (allatonce.py:58-62)
+        const double ang = -6.283185307179586476925286766559 * (double)k / J;
+        const double dre = (1.0 - om_r * std::cos(ang)) / dt;
+        const double dim = (-om_r * std::sin(ang)) / dt;
+        shifted_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
+            d1, dre, dim, M11, A11, (cuDoubleComplex*)S.p);
+        zinverse(c, d1, (cuDoubleComplex*)S.p, (cuDoubleComplex*)Sinv.p, ipiv, info, work);
+        realify_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
+            d1, (const cuDoubleComplex*)Sinv.p, c->Bk.d() + ((size_t)e * J + k) * 4 * d1 * d1);
+        PE_CUDA_CHECK(cudaGetLastError());
+      }
+      double* RW = c->RW.d() + (size_t)e * d1 * 2 * d2;
+      // Rw1 = -(M12/dt + A12), Rw0 = M12/dt   (build_rhs, allatonce.py:154-156)
+      rm_geam(h, false, false, d1, d2, -1.0 / dt, M12, d2, -1.0, A12, d2, RW, 2 * d2);
+      rm_geam(h, false, false, d1, d2, 1.0 / dt, M12, d2, 0.0, M12, d2, RW + d2, 2 * d2);
+      rm_geam(h, false, false, d1, d1, 1.0 / dt, M11, d1, 0.0, M11, d1,
+              c->M11dt.d() + (size_t)e * d1 * d1, d1);
+    }
+    if (d2) {
+      inverse(c, d2, M22, M22inv.d());
+      double* Em = c->Emat.d() + (size_t)e * d2 * d2;
+      set_identity(d2, Em, d2, 1.0, st);
+      rm_gemm(h, false, false, d2, d2, d2, -dt, M22inv.d(), d2, A22, d2, 1.0, Em, d2);
+      // g = dt M22inv^T (f2 - M12^T du/dt - A12^T u)   (row form `@ m22_inv`, :224)
+      rm_gemm(h, true, false, d2, 1, d2, dt, M22inv.d(), d2, f2, 1, 0.0,
+              c->cg.d() + (size_t)e * d2, 1);
+      if (d1) {
+        double* GW = c->GW.d() + (size_t)e * d2 * 2 * d1;
+        rm_gemm(h, true, true, d2, d1, d2, -dt, M22inv.d(), d2, A12, d2, 0.0, GW, 2 * d1);
+        rm_gemm(h, true, true, d2, d1, d2, -1.0, M22inv.d(), d2, M12, d2, 0.0, GW + d1, 2 * d1);
+      }
+    }
+  }
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  c->wr_ready = true;
+  c->wr_dt = dt;
+  c->wr_alpha = alpha;
+  c->wr_tol = tol;
+  c->wr_max_iter = max_iter;
+}
+
+}  // namespace pe

@@ -1,0 +1,297 @@
+// Waveform-relaxation bookkeeping kernels (allatonce.py:232-298): per-interval seeds,
+// the backward difference of the new u waveform, the masked commit with the
+// reference's residual / stop logic, and the final-state gather.
+//
+// Waveform layout per member: Ux = [u0, u0, U_0 .. U_{J-1}] as J+2 blocks of a
+// (d1 x ncols) column-major matrix (block b, column n at b*L1 + n*d1, L1 = d1*ncols);
+// Wx likewise with d2.  Blocks 0,1 are the lag/start seeds (allatonce.py:154,222).
+
+#include <cmath>
+
+#include "pe.h"
+#include "pe_internal.h"
+
+namespace pe {
+
+__global__ void wr_init_kernel(int E, int nc, int d1, int d2, int J, double alpha,
+                               const double* __restrict__ X, double* Ux_cur, double* Ux_new,
+                               double* Wx_cur, double* Wx_new, double* V, WrColumnState* cs,
+                               double* resid_hist, int max_iter) {
+  const int d = d1 + d2;
+  const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
+  const long long total = (long long)E * nc * d;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(t % d);
+    const long long en = t / d;  // e*nc + n
+    const int n = (int)(en % nc);
+    const int e = (int)(en / nc);
+    const double x = X[t];
+    if (r < d1) {
+      double* uc = Ux_cur + (long long)e * (J + 2) * L1 + (long long)n * d1 + r;
+      double* un = Ux_new + (long long)e * (J + 2) * L1 + (long long)n * d1 + r;
+      for (int b = 0; b < J + 2; ++b) uc[b * L1] = x;  // U rows seeded with u0 (:239)
+      un[0] = x;
+      un[L1] = x;
+      // u_start - alpha * u_final_prev with u_final_prev = u0 (:157, :241)
+      V[(long long)e * L1 + (long long)n * d1 + r] = x - alpha * x;
+    } else {
+      const int q = r - d1;
+      double* wc = Wx_cur + (long long)e * (J + 2) * L2 + (long long)n * d2 + q;
+      double* wn = Wx_new + (long long)e * (J + 2) * L2 + (long long)n * d2 + q;
+      for (int b = 0; b < J + 2; ++b) wc[b * L2] = x;  // W rows seeded with w0 (:240)
+      wn[0] = x;
+      wn[L2] = x;
+    }
+  }
+  const long long ncs = (long long)E * nc;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncs;
+       t += (long long)gridDim.x * blockDim.x) {
+    WrColumnState s;
+    s.active = 1;
+    s.iterations = 0;
+    s.stall = 0;
+    s.reason = PE_STOP_MAX_ITER;
+    s.prev = INFINITY;
+    s.r0 = 0.0;
+    cs[t] = s;
+  }
+  if (resid_hist) {
+    const long long nh = ncs * max_iter;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nh;
+         t += (long long)gridDim.x * blockDim.x)
+      resid_hist[t] = NAN;
+  }
+}
+
+void wr_init(int E, int nc, int d1, int d2, int J, double alpha, const double* X_in,
+             double* Ux_cur, double* Ux_new, double* Wx_cur, double* Wx_new, double* V,
+             WrColumnState* cs, double* resid_hist, int max_iter, cudaStream_t st) {
+  long long total = (long long)E * nc * (d1 + d2);
+  int blocks = (int)std::min<long long>((total + 255) / 256 + 1, 148 * 8);
+  wr_init_kernel<<<blocks, 256, 0, st>>>(E, nc, d1, d2, J, alpha, X_in, Ux_cur, Ux_new, Wx_cur,
+                                         Wx_new, V, cs, resid_hist, max_iter);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
+// DU_s = Ux[s+1] - Ux[s], s = 0..J-1: the (u_hist[1:] - u_hist[:-1]) of _w_sweep
+// (allatonce.py:222-223) without the 1/dt, which is folded into the operator.
+__global__ void wr_diff_u_kernel(long long L1, int J, int E, const double* __restrict__ Ux,
+                                 double* __restrict__ DU) {
+  const long long per = (long long)J * L1;
+  const long long total = per * E;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(t / per);
+    const long long r = t - e * per;  // s*L1 + l
+    const double* u = Ux + (long long)e * (J + 2) * L1 + r;
+    DU[t] = u[L1] - u[0];
+  }
+}
+
+void wr_diff_u(int E, int nc, int d1, int J, const double* Ux_new, double* DU,
+               cudaStream_t st) {
+  long long L1 = (long long)d1 * nc;
+  long long total = L1 * J * E;
+  if (total == 0) return;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+  wr_diff_u_kernel<<<blocks, 256, 0, st>>>(L1, J, E, Ux_new, DU);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
+// Deterministic warp sum: lane-strided partial sums then a fixed xor tree.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+constexpr int COMMIT_THREADS = 256;
+constexpr int COMMIT_MAX_J = 1024;
+
+// One CTA per (member, interval).  Residual = max_s ||dU_s|| + max_s ||dW_s||
+// (allatonce.py:250-254); commit new -> cur; u_final_prev update (:257); stop tests
+// tol / diverged / floor (:258-271) and the max_iter cap.
+__global__ void __launch_bounds__(COMMIT_THREADS)
+    wr_commit_kernel(int nc, int d1, int d2, int J, double alpha, double tol, int max_iter,
+                     double* Ux_cur, const double* __restrict__ Ux_new, double* Wx_cur,
+                     const double* __restrict__ Wx_new, double* V, WrColumnState* cs,
+                     double* resid_hist, int* active_count) {
+  __shared__ double nu[COMMIT_MAX_J], nw[COMMIT_MAX_J];
+  __shared__ int s_active;
+  const int en = blockIdx.x;
+  const int e = en / nc, n = en - (en / nc) * nc;
+  if (threadIdx.x == 0) s_active = cs[en].active;
+  __syncthreads();
+  if (!s_active) return;
+  const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
+  double* uc = Ux_cur + (long long)e * (J + 2) * L1 + (long long)n * d1;
+  const double* un = Ux_new + (long long)e * (J + 2) * L1 + (long long)n * d1;
+  double* wc = Wx_cur + (long long)e * (J + 2) * L2 + (long long)n * d2;
+  const double* wn = Wx_new + (long long)e * (J + 2) * L2 + (long long)n * d2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = COMMIT_THREADS / 32;
+  for (int s = warp; s < J; s += NW) {
+    const long long bu = (long long)(s + 2) * L1, bw = (long long)(s + 2) * L2;
+    double a = 0.0, b = 0.0;
+    for (int i = lane; i < d1; i += 32) {
+      const double x = un[bu + i] - uc[bu + i];
+      a += x * x;
+    }
+    for (int i = lane; i < d2; i += 32) {
+      const double x = wn[bw + i] - wc[bw + i];
+      b += x * x;
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+      nu[s] = sqrt(a);
+      nw[s] = sqrt(b);
+    }
+  }
+  __syncthreads();
+  // commit the new waveforms of this column (blocks 2..J+1)
+  for (int s = warp; s < J; s += NW) {
+    const long long bu = (long long)(s + 2) * L1, bw = (long long)(s + 2) * L2;
+    for (int i = lane; i < d1; i += 32) uc[bu + i] = un[bu + i];
+    for (int i = lane; i < d2; i += 32) wc[bw + i] = wn[bw + i];
+  }
+  // V = u_start - alpha * u_final_prev, u_final_prev = last row of U (:257)
+  if (d1 > 0) {
+    const long long last = (long long)(J + 1) * L1;
+    double* v = V + (long long)e * L1 + (long long)n * d1;
+    for (int i = threadIdx.x; i < d1; i += COMMIT_THREADS) v[i] = un[i] - alpha * un[last + i];
+  }
+  if (threadIdx.x == 0) {
+    double mu = 0.0, mw = 0.0;
+    for (int s = 0; s < J; ++s) {
+      mu = fmax(mu, nu[s]);
+      mw = fmax(mw, nw[s]);
+      if (nu[s] != nu[s]) mu = nu[s];  // propagate NaN like np.max
+      if (nw[s] != nw[s]) mw = nw[s];
+    }
+    double resid = 0.0;
+    if (d1 > 0) resid += mu;
+    if (d2 > 0) resid += mw;
+    WrColumnState c = cs[en];
+    const int it = c.iterations;
+    if (resid_hist) resid_hist[(long long)en * max_iter + it] = resid;
+    if (it == 0) c.r0 = resid;
+    c.iterations = it + 1;
+    bool stop = false;
+    if (resid <= tol) {
+      c.reason = PE_STOP_TOL;
+      stop = true;
+    } else if (!isfinite(resid) || resid > 1e8 * fmax(1.0, c.r0)) {
+      c.reason = PE_STOP_DIVERGED;
+      stop = true;
+    } else {
+      c.stall = (resid >= c.prev) ? c.stall + 1 : 0;
+      if (c.stall >= 2 && resid <= 1e3 * tol) {
+        c.reason = PE_STOP_FLOOR;
+        stop = true;
+      }
+      c.prev = resid;
+    }
+    if (!stop && c.iterations >= max_iter) {
+      c.reason = PE_STOP_MAX_ITER;
+      stop = true;
+    }
+    c.active = stop ? 0 : 1;
+    cs[en] = c;
+    if (!stop) atomicAdd(active_count, 1);
+  }
+}
+
+void wr_commit(int E, int nc, int d1, int d2, int J, double alpha, double tol, int max_iter,
+               int /*sweep*/, double* Ux_cur, const double* Ux_new, double* Wx_cur,
+               const double* Wx_new, double* V, WrColumnState* cs, double* resid_hist,
+               int* active_count, cudaStream_t st) {
+  if (J > COMMIT_MAX_J) throw Error{PE_ERR_ARG, "J exceeds 1024"};
+  wr_commit_kernel<<<E * nc, COMMIT_THREADS, 0, st>>>(nc, d1, d2, J, alpha, tol, max_iter,
+                                                      Ux_cur, Ux_new, Wx_cur, Wx_new, V, cs,
+                                                      resid_hist, active_count);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
+// Final state of each interval = last rows of the committed waveforms (:280-289).
+__global__ void wr_finish_kernel(int E, int nc, int d1, int d2, int J,
+                                 const double* __restrict__ Ux, const double* __restrict__ Wx,
+                                 const WrColumnState* __restrict__ cs, double* X_out,
+                                 int* sweeps, int* reasons) {
+  const int d = d1 + d2;
+  const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
+  const long long total = (long long)E * nc * d;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(t % d);
+    const long long en = t / d;
+    const int n = (int)(en % nc), e = (int)(en / nc);
+    double v;
+    if (r < d1)
+      v = Ux[(long long)e * (J + 2) * L1 + (long long)(J + 1) * L1 + (long long)n * d1 + r];
+    else
+      v = Wx[(long long)e * (J + 2) * L2 + (long long)(J + 1) * L2 + (long long)n * d2 + (r - d1)];
+    X_out[t] = v;
+    if (r == 0) {
+      if (sweeps) sweeps[en] = cs[en].iterations;
+      if (reasons) reasons[en] = cs[en].reason;
+    }
+  }
+}
+
+void wr_finish(int E, int nc, int d1, int d2, int J, const double* Ux_cur, const double* Wx_cur,
+               const WrColumnState* cs, double* X_out, int* sweeps, int* reasons,
+               cudaStream_t st) {
+  long long total = (long long)E * nc * (d1 + d2);
+  int blocks = (int)std::min<long long>((total + 255) / 256 + 1, 148 * 8);
+  wr_finish_kernel<<<blocks, 256, 0, st>>>(E, nc, d1, d2, J, Ux_cur, Wx_cur, cs, X_out, sweeps,
+                                           reasons);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
+// out[e][n][b][i] = X[e][b+1][n*dd + i], b = 0..J  (trajectory rows, allatonce.py:280-282)
+__global__ void wr_gather_kernel(int E, int nc, int dd, int J, const double* __restrict__ X,
+                                 double* __restrict__ out) {
+  const long long L = (long long)dd * nc;
+  const long long total = (long long)E * nc * (J + 1) * dd;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % dd);
+    long long r = t / dd;
+    const int b = (int)(r % (J + 1));
+    r /= (J + 1);
+    const int n = (int)(r % nc), e = (int)(r / nc);
+    out[t] = X[(long long)e * (J + 2) * L + (long long)(b + 1) * L + (long long)n * dd + i];
+  }
+}
+
+void wr_gather(int E, int nc, int dd, int J, const double* X, double* out, cudaStream_t st) {
+  long long total = (long long)E * nc * (J + 1) * dd;
+  if (total == 0) return;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  wr_gather_kernel<<<blocks, 256, 0, st>>>(E, nc, dd, J, X, out);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
+__global__ void sub_kernel(long long n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ out) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x)
+    out[t] = a[t] - b[t];
+}
+
+void sub(long long n, const double* a, const double* b, double* out, cudaStream_t st) {
+  if (n == 0) return;
+  int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  sub_kernel<<<blocks, 256, 0, st>>>(n, a, b, out);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace pe

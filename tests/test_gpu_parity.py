@@ -1,0 +1,409 @@
+"""GPU parity: libpe (through the package API / C ABI) vs the reference's golden vectors
+and the CPU oracle on the same seeded inputs.
+
+Tolerances: the north-star bar is the same parareal iteration count and every
+history row within 1e-10 relative L2 (FP64).  Single-operation checks use the
+reference unit tests' own tolerances where the composite-operator arithmetic allows
+(1e-12 relative instead of 1e-14: the GPU applies pre-factorised operators, so its
+rounding differs from LAPACK's back-substitution at the 1e-15 level per operation).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from oracle import pe_oracle as po
+from tests.conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-10
+
+
+def _pkg():
+    import paper_2411_09244_b200 as P
+
+    return P
+
+
+def _system(z, prefix=""):
+    P = _pkg()
+    s = P.CoarseSystem(*(np.asarray(z[prefix + k], dtype=float)
+                         for k in ("M11", "A11", "M12", "A12", "M22", "A22")))
+    return s, P.ConstantLoads(z[prefix + "f1"], z[prefix + "f2"])
+
+
+def _osys(z, prefix=""):
+    return po.OSystem(*(z[prefix + k] for k in ("M11", "A11", "M12", "A12", "M22", "A22",
+                                                  "f1", "f2")))
+
+
+def rel_rows(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    num = np.linalg.norm(a - b, axis=-1)
+    den = np.maximum(np.linalg.norm(b, axis=-1), 1e-300)
+    return float(np.max(num / den)) if num.size else 0.0
+
+
+def tiny(f1, f2):
+    P = _pkg()
+    s = P.CoarseSystem(np.array([[2.0]]), np.array([[3.0]]), np.array([[0.5]]),
+                       np.array([[0.4]]), np.array([[1.5]]), np.array([[0.7]]))
+    return s, P.ConstantLoads(np.array(f1), np.array(f2))
+
+
+# ------------------------------------------------------------------ stepping
+
+
+def test_split_step_and_coarse_step_tiny():
+    P = _pkg()
+    z = golden("units.npz")
+    s, ld = tiny([0.3], [-0.2])
+    props = P.SplitPropagators(s, ld)
+    st = P.SplitState(u=np.array([1.0]), w=np.array([2.0]), u_prev=np.array([0.8]),
+                      w_prev=np.array([1.5]), t=0.0)
+    out = props.split_step(st, 0.01)
+    np.testing.assert_allclose(out.stacked(), z["tiny_split"], rtol=1e-12)
+    assert out.u_prev[0] == 1.0 and out.w_prev[0] == 2.0 and np.isclose(out.t, 0.01)
+    g = props.coarse_step(P.SplitState.fresh(np.array([0.7]), np.array([-0.3])), 0.02)
+    np.testing.assert_allclose(g.stacked(), z["tiny_coarse"], rtol=1e-13)
+    tr = props.fine_interval(P.SplitState.fresh(np.array([1.0]), np.array([2.0])), 0.05, 7)
+    np.testing.assert_allclose(tr.U, z["tiny_fine_U"], rtol=1e-12)
+    np.testing.assert_allclose(tr.W, z["tiny_fine_W"], rtol=1e-12)
+
+
+def test_random_system_step_interval_and_G():
+    P = _pkg()
+    z = golden("units.npz")
+    s, ld = _system(z, "rand_")
+    props = P.SplitPropagators(s, ld)
+    x0 = z["rand_x0"]
+    st = P.SplitState(u=x0[:5], w=x0[5:], u_prev=x0[:5] * 0.9, w_prev=x0[5:] * 1.1, t=0.0)
+    assert rel_rows(props.split_step(st, 1e-3).stacked(), z["rand_split"]) < 1e-12
+    assert rel_rows(props.coarse_step(P.SplitState.fresh(x0[:5], x0[5:]), 0.04).stacked(),
+                    z["rand_coarse"]) < 1e-12
+    tr = props.fine_interval(P.SplitState.fresh(x0[:5], x0[5:]), 0.04, 16)
+    assert rel_rows(tr.U, z["rand_fine_U"]) < 1e-11
+    assert rel_rows(tr.W, z["rand_fine_W"]) < 1e-11
+    # the fused J-step kernel equals the step-by-step trajectory endpoint
+    fine = P.SequentialFine(props, P.TimeGrid(0.04, 1, 16))
+    f, info = fine.propagate(P.SplitState.fresh(x0[:5], x0[5:]))
+    assert info == {"converged": True}
+    assert rel_rows(f.stacked(), tr.final.stacked()) < 1e-13
+
+
+def test_scalar_backward_euler_closed_form():
+    P = _pkg()
+    a = 4.0
+    s = P.CoarseSystem(np.array([[1.0]]), np.array([[a]]), np.zeros((1, 0)), np.zeros((1, 0)),
+                       np.zeros((0, 0)), np.zeros((0, 0)))
+    props = P.SplitPropagators(s, P.ConstantLoads.zero(s))
+    tr = props.fine_interval(P.SplitState.fresh(np.array([1.0]), np.zeros(0)), 0.4, 8)
+    kappa = 1.0 / (1.0 + 0.05 * a)
+    np.testing.assert_allclose(tr.U[:, 0], kappa ** np.arange(9), rtol=1e-13)
+    assert tr.W.shape == (9, 0)
+
+
+def test_pure_w_explicit_recursion():
+    P = _pkg()
+    s = P.CoarseSystem(np.zeros((0, 0)), np.zeros((0, 0)), np.zeros((0, 1)), np.zeros((0, 1)),
+                       np.array([[2.0]]), np.array([[3.0]]))
+    props = P.SplitPropagators(s, P.ConstantLoads(np.zeros(0), np.array([0.6])))
+    tr = props.fine_interval(P.SplitState.fresh(np.zeros(0), np.array([1.0])), 0.2, 5)
+    w, expect = 1.0, [1.0]
+    for _ in range(5):
+        w = w + 0.04 * (0.6 - 3.0 * w) / 2.0
+        expect.append(w)
+    np.testing.assert_allclose(tr.W[:, 0], expect, rtol=1e-13)
+
+
+def test_stability_bound_matches_dense_eigenvalue():
+    import scipy.linalg as sla
+
+    P = _pkg()
+    z = golden("sys_cfg0.npz")
+    s, ld = _system(z)
+    b = P.SplitPropagators(s, ld).stability_max_step()
+    lam = sla.eigh(s.A22, s.M22, eigvals_only=True)[-1]
+    assert np.isclose(b, 2.0 / lam, rtol=1e-6)
+    assert abs(json.loads(str(z["meta"]))["bound_after"] - b) / b < 1e-6
+
+
+# ------------------------------------------------------------------ all-at-once
+
+
+def test_wr_random_system_matches_reference():
+    P = _pkg()
+    z = golden("units.npz")
+    s, ld = _system(z, "rand_")
+    x0 = z["rand_x0"]
+    res = P.wr_fine_solve(s, P.SplitState.fresh(x0[:5], x0[5:]), 0.04, 16, 0.3, ld,
+                          tol=1e-13, max_iter=400)
+    assert res.converged
+    assert res.iterations == int(z["rand_wr_meta"][0])
+    assert rel_rows(res.trajectory.U, z["rand_wr_U"]) < REL
+    assert rel_rows(res.trajectory.W, z["rand_wr_W"]) < REL
+    r_ref = z["rand_wr_res"]
+    np.testing.assert_allclose(res.residuals[:5], r_ref[:5], rtol=1e-8)
+
+
+def test_wr_matches_sequential_fixed_point():
+    """Converged WR equals the GPU sequential scheme (SPEC fixed-point identity)."""
+    P = _pkg()
+    z = golden("sys_cfg0.npz")
+    s, ld = _system(z)
+    props = P.SplitPropagators(s, ld)
+    st = P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2))
+    res = P.wr_fine_solve(s, st, 0.1, 10, 0.1, ld, tol=1e-13, max_iter=400)
+    seq = props.fine_interval(st, 0.1, 10)
+    scale = max(np.abs(seq.U).max(), np.abs(seq.W).max())
+    assert np.abs(res.trajectory.U - seq.U).max() < 1e-10 * scale
+    assert np.abs(res.trajectory.W - seq.W).max() < 1e-10 * scale
+
+
+def test_wr_lowgamma_contraction_and_floor():
+    P = _pkg()
+    z = golden("units.npz")
+    s = P.CoarseSystem(np.eye(2), np.diag([200.0, 100.0]), np.diag([0.3, 0.1]),
+                       np.zeros((2, 2)), np.eye(2), np.diag([0.5, 0.5]))
+    ld = P.ConstantLoads(np.array([1.0, 1.0]), np.array([1.0, -1.0]))
+    res = P.wr_fine_solve(s, P.SplitState.fresh(np.zeros(2), np.zeros(2)), 0.01, 8, 0.1, ld,
+                          tol=1e-13, max_iter=200)
+    assert res.converged
+    r = res.residuals
+    ratios = [r[i + 1] / r[i] for i in range(2, min(8, len(r) - 1))]
+    geo = float(np.exp(np.mean(np.log(ratios))))
+    assert 1e-4 < geo <= 0.3 ** 2 + 0.2
+    np.testing.assert_allclose(r[:6], z["lowgamma_res"][:6], rtol=1e-8)
+    ld2 = P.ConstantLoads(np.array([1.0, 0.0]), np.array([0.0, 1.0]))
+    wr = P.WaveformRelaxation(s, 8, 0.01, 0.1, ld2, tol=1e-18, max_iter=500)
+    res = wr.solve(P.SplitState.fresh(np.zeros(2), np.zeros(2)))
+    assert res.iterations < 500
+    assert res.residuals[-1] <= 1e-12
+
+
+def test_wr_nonconvergence_flagged(caplog):
+    P = _pkg()
+    z = golden("channel.npz")
+    s, ld = _system(z)
+    st = P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2))
+    with caplog.at_level("WARNING"):
+        res = P.wr_fine_solve(s, st, 5e-4, 10, 0.5, ld, tol=1e-13, max_iter=3)
+    assert not res.converged and res.stop_reason == "max_iter" and res.iterations == 3
+    assert any("not converged" in rec.message for rec in caplog.records)
+
+
+def test_wr_batch_equals_single_and_is_deterministic():
+    P = _pkg()
+    z = golden("sys_cfg0.npz")
+    s, ld = _system(z)
+    rng = np.random.default_rng(3)
+    states = [P.SplitState.fresh(rng.standard_normal(s.d1) * 0.1, rng.standard_normal(s.d2) * 0.1)
+              for _ in range(6)]
+    wr = P.WaveformRelaxation(s, 10, 0.1, 0.1, ld, tol=1e-12, max_iter=400)
+    batch = wr.solve_all(states)
+    again = wr.solve_all(states)
+    for a, b in zip(batch, again):
+        assert np.array_equal(a.trajectory.U, b.trajectory.U)
+        assert a.residuals == b.residuals
+    one = wr.solve(states[4])
+    assert np.array_equal(one.trajectory.final.stacked(), batch[4].trajectory.final.stacked())
+    # each interval stops on its own: sweep counts are per column
+    osys = _osys(z)
+    ow = po.OracleWR(osys, 10, 0.1, 0.1, tol=1e-12, max_iter=400)
+    for st, r in zip(states, batch):
+        o = ow.solve(st.u, st.w)
+        assert r.iterations == o["iterations"]
+        assert rel_rows(r.trajectory.final.stacked(),
+                        np.concatenate([o["U"][-1], o["W"][-1]])) < REL
+
+
+# ------------------------------------------------------------------ parareal
+
+
+@pytest.mark.parametrize("kind,tag", [("sequential", "seq"), ("all-at-once", "aao")])
+def test_random_system_parareal(kind, tag):
+    P = _pkg()
+    z = golden("units.npz")
+    s, ld = _system(z, "rand_")
+    x0 = z["rand_x0"]
+    props = P.SplitPropagators(s, ld)
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(0.32, 8, 16), alpha=0.3, epsilon=1e-10, k_max=8,
+                           fine_kind=kind, fine_tol=1e-13)
+    fine = P.build_fine_propagator(cfg, props, ld)
+    run = P.run_parareal(cfg, props, fine, P.SplitState.fresh(x0[:5], x0[5:]))
+    assert run.iterations == int(z[f"rand_par_{tag}_iters"])
+    ref = z[f"rand_par_{tag}_hist"]
+    assert len(run.history) == len(ref)
+    assert rel_rows(np.array(run.history), ref) < REL
+    assert len(run.fine_seconds) == run.iterations == len(run.max_diffs)
+
+
+@pytest.mark.parametrize("kind,tag,n,J", [("sequential", "seq", 6, 4),
+                                          ("all-at-once", "aao", 5, 6)])
+def test_exactness_after_n_iterations_bitwise(kind, tag, n, J):
+    """Forcing k = N reproduces the GPU sequential composition of F bit for bit,
+    and matches the reference run of the same fixture within 1e-10."""
+    P = _pkg()
+    z = golden("channel.npz")
+    s, ld = _system(z)
+    props = P.SplitPropagators(s, ld)
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(0.005, n, J), alpha=0.5, epsilon=0.0, k_max=n,
+                           fine_kind=kind, fine_tol=1e-13)
+    fine = P.build_fine_propagator(cfg, props, ld)
+    st = P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2))
+    run = P.run_parareal(cfg, props, fine, st)
+    assert run.iterations == n and not run.converged
+    expected = [st.stacked()]
+    for _ in range(n):
+        st, _ = fine.propagate(st)
+        expected.append(st.stacked())
+    assert np.array_equal(run.history[-1], np.array(expected))
+    assert rel_rows(np.array(run.history), z[f"{tag}_hist"]) < REL
+
+
+def test_initial_sweep_composes_coarse_bitwise():
+    P = _pkg()
+    z = golden("channel.npz")
+    s, ld = _system(z)
+    props = P.SplitPropagators(s, ld)
+    tg = P.TimeGrid(0.005, 4, 2)
+    st = P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2))
+    states = P.initial_sweep(props, st, tg)
+    cfg = P.ParerealConfig(time_grid=tg, alpha=0.5, epsilon=0.0, k_max=0,
+                           fine_kind="sequential")
+    run = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld), st)
+    assert np.array_equal(run.history[0], np.array([x.stacked() for x in states]))
+
+
+def test_worker_count_and_rerun_determinism():
+    P = _pkg()
+    z = golden("channel.npz")
+    s, ld = _system(z)
+    runs = []
+    for w in (1, 3):
+        props = P.SplitPropagators(s, ld)
+        cfg = P.ParerealConfig(time_grid=P.TimeGrid(0.005, 6, 4), alpha=0.5, workers=w,
+                               fine_kind="all-at-once", fine_tol=1e-13)
+        runs.append(P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld),
+                                   P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2))))
+    assert len(runs[0].history) == len(runs[1].history)
+    for a, b in zip(runs[0].history, runs[1].history):
+        assert np.array_equal(a, b)
+    assert runs[0].max_diffs == runs[1].max_diffs
+
+
+def test_channel_converged_run_matches_reference():
+    P = _pkg()
+    z = golden("channel.npz")
+    s, ld = _system(z)
+    props = P.SplitPropagators(s, ld)
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(0.005, 10, 10), alpha=0.5, epsilon=1e-14,
+                           fine_kind="all-at-once", fine_tol=1e-13)
+    run = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld),
+                         P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2)))
+    assert run.iterations == int(z["conv_iters"])
+    assert rel_rows(np.array(run.history), z["conv_hist"]) < REL
+    its = np.array([[i["iterations"] for i in sw] for sw in run.fine_info])
+    assert np.abs(its - z["conv_wr_iters"]).max() <= 1
+
+
+@pytest.mark.parametrize("run_name", ["run_cfg0_seq.npz", "run_cfg1_aao.npz"])
+def test_baseline_configs_0_1(run_name):
+    """BASELINE configs 0/1: same iteration count, every row / F within 1e-10 rel L2."""
+    P = _pkg()
+    z = golden(run_name)
+    s, ld = _system(golden("sys_cfg0.npz"))
+    kind = str(z["kind"])
+    props = P.SplitPropagators(s, ld)
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(1.0, 10, 10), alpha=0.1, epsilon=1e-8,
+                           k_max=10, fine_kind=kind, fine_tol=1e-12, stop_rule="relative")
+    run = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld),
+                         P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2)))
+    assert run.iterations == int(z["iterations"]) and run.converged
+    assert rel_rows(np.array(run.history), z["history"]) < REL
+    np.testing.assert_allclose(run.max_diffs, z["max_diffs"], rtol=1e-6)
+    if kind == "all-at-once":
+        its = np.array([[i["iterations"] for i in sw] for sw in run.fine_info])
+        assert np.abs(its - z["wr_iterations"]).max() <= 1
+
+
+@pytest.mark.parametrize("tag", ["seq", "aao"])
+def test_baseline_config2(tag):
+    """BASELINE config 2 (d = 300+300, N = J = 64)."""
+    P = _pkg()
+    z = golden(f"run_cfg2_{tag}.npz")
+    s, ld = _system(golden("sys_cfg2.npz"))
+    kind = str(z["kind"])
+    props = P.SplitPropagators(s, ld)
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(1.0, 64, 64), alpha=0.1, epsilon=1e-8,
+                           k_max=64, fine_kind=kind, fine_tol=1e-12, stop_rule="relative")
+    run = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld),
+                         P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2)))
+    assert run.iterations == int(z["iterations"]) and run.converged
+    assert rel_rows(np.array(run.history), z["history"]) < REL
+    if kind == "all-at-once":
+        its = np.array([[i["iterations"] for i in sw] for sw in run.fine_info])
+        assert np.abs(its - z["wr_iterations"]).max() <= 1
+
+
+def test_degenerate_spaces_parareal():
+    P = _pkg()
+    z = golden("units.npz")
+    us = P.CoarseSystem(np.array([[1.0]]), np.array([[6.0]]), np.zeros((1, 0)),
+                        np.zeros((1, 0)), np.zeros((0, 0)), np.zeros((0, 0)))
+    ld = P.ConstantLoads(np.array([2.4]), np.zeros(0))
+    props = P.SplitPropagators(us, ld)
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(0.8, 8, 16), alpha=0.5, epsilon=1e-15, k_max=50,
+                           fine_kind="sequential")
+    run = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld),
+                         P.SplitState.fresh(np.array([1.0]), np.zeros(0)))
+    assert run.converged and run.iterations == int(z["uonly_iters"])
+    kappa = 1.0 / (1.0 + 0.8 / 128 * 6.0)
+    assert np.isclose(run.endpoint()[0][0], 0.4 + kappa ** 128 * 0.6, rtol=1e-12)
+    ws = P.CoarseSystem(np.zeros((0, 0)), np.zeros((0, 0)), np.zeros((0, 1)), np.zeros((0, 1)),
+                        np.array([[2.0]]), np.array([[3.0]]))
+    ld = P.ConstantLoads(np.zeros(0), np.array([0.6]))
+    for kind, tag in (("sequential", "seq"), ("all-at-once", "aao")):
+        props = P.SplitPropagators(ws, ld)
+        cfg = P.ParerealConfig(time_grid=P.TimeGrid(0.4, 5, 4), alpha=0.5, epsilon=1e-15,
+                               k_max=5, fine_kind=kind, fine_tol=1e-13)
+        run = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld),
+                             P.SplitState.fresh(np.zeros(0), np.array([1.0])))
+        assert rel_rows(np.array(run.history), z[f"wonly_{tag}_hist"]) < 1e-12
+
+
+def test_ensemble_members_equal_single_runs():
+    P = _pkg()
+    z = golden("sys_cfg0.npz")
+    s, ld = _system(z)
+    systems, loads, inits = [], [], []
+    for m, scale in enumerate((1.0, 0.5, 0.25)):
+        systems.append(P.CoarseSystem(s.M11, s.A11 * scale, s.M12, s.A12 * scale, s.M22,
+                                      s.A22 * scale))
+        loads.append(P.ConstantLoads(ld.f1 * (m + 1), ld.f2 * (m + 1)))
+        inits.append(P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2)))
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(1.0, 10, 10), alpha=0.1, epsilon=1e-8, k_max=10,
+                           fine_kind="sequential", stop_rule="relative")
+    runs = P.run_parareal_ensemble(cfg, systems, loads, inits)
+    for sysm, ldm, run in zip(systems, loads, runs):
+        props = P.SplitPropagators(sysm, ldm)
+        single = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ldm),
+                                P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2)))
+        assert run.iterations == single.iterations
+        assert rel_rows(np.array(run.history), np.array(single.history)) < 1e-13
+        o = po.run_parareal(po.OSystem(sysm.M11, sysm.A11, sysm.M12, sysm.A12, sysm.M22,
+                                       sysm.A22, ldm.f1, ldm.f2), np.zeros(s.d1 + s.d2), 1.0,
+                            10, 10, epsilon=1e-8, k_max=10, stop="relative")
+        assert o["iterations"] == run.iterations
+        assert rel_rows(np.array(run.history), np.array(o["history"])) < REL
+
+
+def test_unknown_fine_kind_rejected():
+    P = _pkg()
+    s, ld = tiny([0.1], [0.2])
+    props = P.SplitPropagators(s, ld)
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(1.0, 2, 2), alpha=0.5, fine_kind="magic")
+    with pytest.raises(ValueError):
+        P.build_fine_propagator(cfg, props, ld)
