@@ -108,6 +108,14 @@ int pe_coarse_correct(pe_ctx* ctx, int N, const double* X_old, const double* F_h
                       double* G_cache, double* X_new, double* diff, const int* active,
                       void* stream);
 
+/* One parareal iteration (parareal.py:188-215): the fine sweep on rows 0..N-1 of
+ * X_old (E, N+1, d), then the fused coarse sweep / correction / norms into X_new.
+ * G_cache as in pe_coarse_correct (initialise it with an initial sweep).  This is the
+ * "step" bench.py times. */
+int pe_parareal_iterate(pe_ctx* ctx, int kind, int N, const double* X_old, double* X_new,
+                        double* G_cache, double* diff, const int* active, int* wr_sweeps,
+                        int* wr_reasons, double* wr_resid, void* stream);
+
 /* Device-resident parareal loop (parareal.py:160-236 run_parareal) with one host
  * synchronisation per iteration.  All pointers are device pointers except the
  * `*_h` outputs, which are host arrays.
@@ -136,8 +144,11 @@ int pe_gemm_f64(int M, int N, int K, const double* A, long long a_i, long long a
  * (bench/driver evidence that the native path ran). */
 long long pe_launch_count(pe_ctx* ctx);
 
-/* Timing helpers used by bench.py: mean device time (ms) of the most recent
- * pe_fine_* call's dominant kernel class and its algorithmic flop count. */
+/* Roofline bookkeeping for bench.py.  With profiling on, every GEMM launch of the
+ * fine propagators is bracketed by CUDA events on its stream; pe_last_fine_stats
+ * returns, for the most recent fine sweep, the summed GEMM time (ms, 0 when profiling
+ * is off), their algorithmic flops and the number of GEMM launches. */
+int pe_set_profiling(pe_ctx* ctx, int on);
 int pe_last_fine_stats(pe_ctx* ctx, double* gemm_ms, double* gemm_flops, int* launches);
 
 #ifdef __cplusplus

@@ -42,6 +42,38 @@ static void require(bool ok, int code, const char* msg) {
 
 static void bind(pe_ctx* c) { PE_CUDA_CHECK(cudaSetDevice(c->device)); }
 
+// GEMM launch with optional per-launch CUDA-event timing (bench roofline pass).
+static void run_gemm(pe_ctx* c, const GemmParams& p, cudaStream_t st) {
+  if (c->profiling) {
+    if ((int)c->prof_events.size() < 2 * (c->prof_used + 1)) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        PE_CUDA_CHECK(cudaEventCreate(&e));
+        c->prof_events.push_back(e);
+      }
+    }
+    PE_CUDA_CHECK(cudaEventRecord(c->prof_events[2 * c->prof_used], st));
+    gemm_f64(p, st);
+    PE_CUDA_CHECK(cudaEventRecord(c->prof_events[2 * c->prof_used + 1], st));
+    ++c->prof_used;
+  } else {
+    gemm_f64(p, st);
+  }
+  c->stats.gemm_flops += gemm_flops(p);
+  c->stats.launches += 1;
+}
+
+static void collect_profile(pe_ctx* c, cudaStream_t st) {
+  if (!c->profiling || c->prof_used == 0) return;
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  for (int i = 0; i < c->prof_used; ++i) {
+    float ms = 0;
+    PE_CUDA_CHECK(cudaEventElapsedTime(&ms, c->prof_events[2 * i], c->prof_events[2 * i + 1]));
+    c->stats.gemm_ms += ms;
+  }
+  c->prof_used = 0;
+}
+
 // ------------------------------------------------------------------ sequential fine
 // X_in/X_out: (E, nc, d) == per member a column-major d x nc matrix.
 // With X_prev == nullptr the lags are reset (D_0 = 0, interval start); otherwise
@@ -91,13 +123,12 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
       p.D = Dn;
       p.Xp = Xs;
     }
-    gemm_f64(p, st);
-    c->stats.gemm_flops += gemm_flops(p);
-    c->stats.launches += 1;
+    run_gemm(c, p, st);
     Xs = Xn;
     Ds = Dn;
   }
   if (J == 0) PE_CUDA_CHECK(cudaMemcpyAsync(X_out, X_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  collect_profile(c, st);
 }
 
 // ------------------------------------------------------------------ all-at-once fine
@@ -246,10 +277,6 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     }
   }
 
-  double flops_per_sweep = 0;
-  for (auto& p : pre) flops_per_sweep += gemm_flops(p);
-  if (d2) flops_per_sweep += gemm_flops(gw);
-  for (auto& p : post) flops_per_sweep += gemm_flops(p);
 
   // Pipelined sweep loop: sweep i+1 is enqueued before the host reads sweep i's
   // active-interval count, so the device never waits on the host; the extra sweep
@@ -260,19 +287,18 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   auto enqueue_sweep = [&](int sweep) {
     PE_CUDA_CHECK(cudaMemsetAsync(cnt + (sweep & 1), 0, sizeof(int), st));
-    for (auto& p : pre) gemm_f64(p, st);
+    for (auto& p : pre) run_gemm(c, p, st);
     if (d1) wr_diff_u(E, nc, d1, J, Un, c->DU.d(), st);
     if (d2) {
-      gemm_f64(gw, st);
-      for (auto& p : post) gemm_f64(p, st);
+      run_gemm(c, gw, st);
+      for (auto& p : post) run_gemm(c, p, st);
     }
     wr_commit(E, nc, d1, d2, J, alpha, tol, max_iter, sweep, Uc, Un, Wc, Wn, c->V.d(), cs,
               resid_hist, cnt + (sweep & 1), st);
     PE_CUDA_CHECK(cudaMemcpyAsync(host_cnt + (sweep & 1), cnt + (sweep & 1), sizeof(int),
                                   cudaMemcpyDeviceToHost, st));
     PE_CUDA_CHECK(cudaEventRecord(ev[sweep & 1], st));
-    c->stats.gemm_flops += flops_per_sweep;
-    c->stats.launches += (int)(pre.size() + post.size() + (d2 ? 1 : 0));
+    collect_profile(c, st);
   };
   int sweep = 0;
   enqueue_sweep(0);
@@ -285,6 +311,27 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
   wr_finish(E, nc, d1, d2, J, Uc, Wc, cs, X_out, sweeps, reasons, st);
+}
+
+// One parareal iteration (parareal.py:188-215): fine sweep on x_0..x_{N-1} of X_old,
+// then the fused coarse sweep / correction / norms into X_new.
+static void parareal_iterate(pe_ctx* c, int kind, int N, const double* X_old, double* X_new,
+                             double* G_cache, double* diff, const int* active, int* wr_sweeps,
+                             int* wr_reasons, double* wr_resid, cudaStream_t st) {
+  const int E = c->E, d = c->d;
+  c->Xin.ensure(sizeof(double) * (size_t)E * N * d + 8);
+  c->Xout.ensure(sizeof(double) * (size_t)E * N * d + 8);
+  c->partial.ensure(sizeof(double) * (size_t)E * N * 16 * 2 + 8);
+  PE_CUDA_CHECK(cudaMemcpy2DAsync(c->Xin.d(), sizeof(double) * N * d, X_old,
+                                  sizeof(double) * (N + 1) * d, sizeof(double) * N * d, E,
+                                  cudaMemcpyDeviceToDevice, st));
+  if (kind == PE_KIND_SEQUENTIAL)
+    fine_sequential(c, c->Xin.d(), c->Xout.d(), N, st);
+  else
+    fine_allatonce(c, c->Xin.d(), c->Xout.d(), N, wr_sweeps, wr_reasons, wr_resid, st);
+  if (c->ev_mid) PE_CUDA_CHECK(cudaEventRecord(c->ev_mid, st));
+  coarse_correct(E, d, N, c->Phi.d(), c->gG.d(), X_old, c->Xout.d(), G_cache, X_new,
+                 c->partial.d(), diff, active, st);
 }
 
 }  // namespace pe
@@ -345,6 +392,7 @@ int pe_destroy(pe_ctx* c) {
   if (c->setup_stream) cudaStreamDestroy(c->setup_stream);
   if (c->pinned_count) cudaFreeHost(c->pinned_count);
   if (c->pinned_diff) cudaFreeHost(c->pinned_diff);
+  for (auto e : c->prof_events) cudaEventDestroy(e);
   delete c;
   return PE_OK;
 }
@@ -487,8 +535,6 @@ int pe_parareal_run(pe_ctx* c, int kind, int N, const double* X0, int k_max, dou
     const size_t slab = (size_t)E * (N + 1) * d;
     auto H = [&](int k) { return history + (size_t)k * slab; };
     c->Gc.ensure(sizeof(double) * (size_t)E * N * d + 8);
-    c->Xin.ensure(sizeof(double) * (size_t)E * N * d + 8);
-    c->Xout.ensure(sizeof(double) * (size_t)E * N * d + 8);
     c->partial.ensure(sizeof(double) * (size_t)E * N * 16 * 2 + 8);
     c->diff.ensure(sizeof(double) * 2 * E + 8);
     c->active.ensure(sizeof(int) * E + 8);
@@ -516,21 +562,13 @@ int pe_parareal_run(pe_ctx* c, int kind, int N, const double* X0, int k_max, dou
     int n_active = E;
     for (k = 1; k <= k_max && n_active > 0; ++k) {
       PE_CUDA_CHECK(cudaEventRecord(e0, st));
-      // fine sweep on x_0^{k-1} .. x_{N-1}^{k-1} (parareal.py:191-193)
-      PE_CUDA_CHECK(cudaMemcpy2DAsync(c->Xin.d(), sizeof(double) * N * d, H(k - 1),
-                                      sizeof(double) * (N + 1) * d, sizeof(double) * N * d, E,
-                                      cudaMemcpyDeviceToDevice, st));
-      if (kind == PE_KIND_SEQUENTIAL) {
-        fine_sequential(c, c->Xin.d(), c->Xout.d(), N, st);
-      } else {
-        const size_t off = (size_t)(k - 1) * E * N;
-        fine_allatonce(c, c->Xin.d(), c->Xout.d(), N, wr_sweeps ? wr_sweeps + off : nullptr,
+      const size_t off = (size_t)(k - 1) * E * N;
+      c->ev_mid = e1;
+      parareal_iterate(c, kind, N, H(k - 1), H(k), c->Gc.d(), c->diff.d(), c->active.i(),
+                       wr_sweeps ? wr_sweeps + off : nullptr,
                        wr_reasons ? wr_reasons + off : nullptr,
                        wr_resid ? wr_resid + off * c->wr_max_iter : nullptr, st);
-      }
-      PE_CUDA_CHECK(cudaEventRecord(e1, st));
-      coarse_correct(E, d, N, c->Phi.d(), c->gG.d(), H(k - 1), c->Xout.d(), c->Gc.d(), H(k),
-                     c->partial.d(), c->diff.d(), c->active.i(), st);
+      c->ev_mid = nullptr;
       PE_CUDA_CHECK(cudaEventRecord(e2, st));
       PE_CUDA_CHECK(cudaMemcpyAsync(c->pinned_diff, c->diff.p, sizeof(double) * 2 * E,
                                     cudaMemcpyDeviceToHost, st));
@@ -588,6 +626,31 @@ int pe_wr_waveforms(pe_ctx* c, double* U_out, double* W_out, int nc, void* strea
   });
 }
 
+int pe_parareal_iterate(pe_ctx* c, int kind, int N, const double* X_old, double* X_new,
+                        double* G_cache, double* diff, const int* active, int* wr_sweeps,
+                        int* wr_reasons, double* wr_resid, void* stream) {
+  return guarded([&] {
+    require(c && X_old && X_new && G_cache && N >= 1 && N <= c->maxc, PE_ERR_ARG,
+            "bad parareal_iterate arguments");
+    require(kind == PE_KIND_SEQUENTIAL || kind == PE_KIND_ALLATONCE, PE_ERR_ARG,
+            "unknown fine propagator kind");
+    require(c->coarse_dt > 0, PE_ERR_STATE, "pe_prepare_coarse not called");
+    require(kind == PE_KIND_SEQUENTIAL ? c->seq_dt > 0 : c->wr_ready, PE_ERR_STATE,
+            "fine propagator not prepared");
+    bind(c);
+    parareal_iterate(c, kind, N, X_old, X_new, G_cache, diff, active, wr_sweeps, wr_reasons,
+                     wr_resid, (cudaStream_t)stream);
+  });
+}
+
+int pe_set_profiling(pe_ctx* c, int on) {
+  return guarded([&] {
+    require(c != nullptr, PE_ERR_ARG, "ctx is NULL");
+    c->profiling = on != 0;
+    c->prof_used = 0;
+  });
+}
+
 int pe_gemm_f64(int M, int N, int K, const double* A, long long a_i, long long a_k,
                 const double* B, long long b_k, long long b_j, double* C, long long c_i,
                 long long c_j, void* stream) {
@@ -612,7 +675,7 @@ long long pe_launch_count(pe_ctx* c) { return c ? g_launches - c->launches_at_cr
 int pe_last_fine_stats(pe_ctx* c, double* gemm_ms, double* gemm_flops_out, int* launches) {
   return guarded([&] {
     require(c != nullptr, PE_ERR_ARG, "ctx is NULL");
-    if (gemm_ms) *gemm_ms = 0.0;
+    if (gemm_ms) *gemm_ms = c->stats.gemm_ms;
     if (gemm_flops_out) *gemm_flops_out = c->stats.gemm_flops;
     if (launches) *launches = c->stats.launches;
   });

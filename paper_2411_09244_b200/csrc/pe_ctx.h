@@ -41,6 +41,7 @@ struct DevBuf {
 
 struct FineStats {
   double gemm_flops = 0;   // algorithmic flops issued by the GEMM kernels of the last fine call
+  double gemm_ms = 0;      // summed CUDA-event time of those launches (profiling mode only)
   int launches = 0;
 };
 
@@ -77,5 +78,9 @@ struct pe_ctx {
   size_t pinned_diff_n = 0;
 
   long long launches_at_create = 0;
+  cudaEvent_t ev_mid = nullptr;  // fine/coarse boundary inside pe_parareal_run
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_events;
+  int prof_used = 0;
   pe::FineStats stats;
 };

@@ -161,13 +161,23 @@ class PeContext:
             out["wr_resid"] = wrh[:K].cpu().numpy() if wrh is not None else None
         return out
 
+    def iterate(self, kind: str, N: int, X_old, X_new, G_cache, diff, active=None,
+                wr_sweeps=None, wr_reasons=None, wr_resid=None):
+        """One parareal iteration X_old -> X_new (the bench "step")."""
+        check(self.lib.pe_parareal_iterate(
+            self.ptr, PE_KIND[kind], N, _ptr(X_old), _ptr(X_new), _ptr(G_cache), _ptr(diff),
+            _ptr(active), _ptr(wr_sweeps), _ptr(wr_reasons), _ptr(wr_resid), self.stream()))
+
+    def set_profiling(self, on: bool):
+        check(self.lib.pe_set_profiling(self.ptr, 1 if on else 0))
+
     def launch_count(self) -> int:
         return int(self.lib.pe_launch_count(self.ptr))
 
     def fine_stats(self):
         ms, fl, n = C.c_double(), C.c_double(), C.c_int()
         check(self.lib.pe_last_fine_stats(self.ptr, C.byref(ms), C.byref(fl), C.byref(n)))
-        return dict(gemm_flops=fl.value, launches=n.value)
+        return dict(gemm_ms=ms.value, gemm_flops=fl.value, launches=n.value)
 
 
 def stop_reason_name(code: int) -> str:
