@@ -149,6 +149,9 @@ long long pe_launch_count(pe_ctx* ctx);
  * returns, for the most recent fine sweep, the summed GEMM time (ms, 0 when profiling
  * is off), their algorithmic flops and the number of GEMM launches. */
 int pe_set_profiling(pe_ctx* ctx, int on);
+/* Select the persistent cluster-resident recurrence kernels for the sequential-in-time
+ * chains (default on) or one DMMA GEMM launch per step (reference-like structure). */
+int pe_set_recurrence(pe_ctx* ctx, int on);
 int pe_last_fine_stats(pe_ctx* ctx, double* gemm_ms, double* gemm_flops, int* launches);
 
 #ifdef __cplusplus

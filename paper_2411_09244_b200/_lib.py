@@ -55,6 +55,7 @@ SIGNATURES = {
     "pe_parareal_iterate": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P,
                                       _P]),
     "pe_set_profiling": (C.c_int, [_P, C.c_int]),
+    "pe_set_recurrence": (C.c_int, [_P, C.c_int]),
     "pe_launch_count": (C.c_longlong, [_P]),
     "pe_last_fine_stats": (C.c_int, [_P, _D, _D, _I]),
 }

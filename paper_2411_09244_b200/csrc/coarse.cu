@@ -84,23 +84,50 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
 
   for (int n = 0; n < N; ++n) {
     double sd = 0.0, sn = 0.0;  // this warp's partial ||x_new - x_old||^2, ||x_new||^2
-    for (int rr = warp; rr < nrows; rr += COARSE_WARPS) {
+    // prefetch this warp's per-row operands across lanes (lane i <-> i-th row of the warp)
+    double pf_f = 0.0, pf_g = 0.0, pf_b = 0.0, pf_o = 0.0;
+    {
+      const int rr = warp + COARSE_WARPS * lane;
+      if (rr < nrows) {
+        const long long o = (long long)n * d + r0 + rr;
+        pf_b = gv[r0 + rr];
+        pf_o = X_old[o + d];
+        if (F) {
+          pf_f = F[o];
+          pf_g = Gc[o];
+        }
+      }
+    }
+    int i = 0;
+    for (int rr = warp; rr < nrows; rr += COARSE_WARPS, ++i) {
       const int r = r0 + rr;
       const double* row = a.phi_in_smem ? phis + (long long)rr * d : Phi + (long long)r * d;
       double acc = 0.0;
       for (int k = lane; k < d; k += 32) acc = fma(row[k], xs[k], acc);
       acc = warp_sum_c(acc);
+      const long long o = (long long)n * d + r;
+      double fb = __shfl_sync(0xffffffffu, pf_b, i & 31);
+      double ff = __shfl_sync(0xffffffffu, pf_f, i & 31);
+      double fg = __shfl_sync(0xffffffffu, pf_g, i & 31);
+      double xo = __shfl_sync(0xffffffffu, pf_o, i & 31);
+      if (i >= 32) {  // more rows per warp than lanes: plain loads
+        fb = gv[r];
+        xo = X_old[o + d];
+        if (F) {
+          ff = F[o];
+          fg = Gc[o];
+        }
+      }
       if (lane == 0) {
-        const double g = acc + gv[r];
-        const long long o = (long long)n * d + r;
+        const double g = acc + fb;
         double x;
         if (F)
-          x = F[o] + (g - Gc[o]);
+          x = ff + (g - fg);
         else
           x = g;
         Gc[o] = g;
         X_new[o + d] = x;
-        const double df = x - X_old[o + d];
+        const double df = x - xo;
         sd += df * df;
         sn += x * x;
       }

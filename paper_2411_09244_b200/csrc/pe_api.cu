@@ -42,8 +42,10 @@ static void require(bool ok, int code, const char* msg) {
 
 static void bind(pe_ctx* c) { PE_CUDA_CHECK(cudaSetDevice(c->device)); }
 
-// GEMM launch with optional per-launch CUDA-event timing (bench roofline pass).
-static void run_gemm(pe_ctx* c, const GemmParams& p, cudaStream_t st) {
+// Launch `fn` (one DMMA-class kernel doing `flops` algorithmic flops) with optional
+// per-launch CUDA-event timing (bench roofline pass).
+template <class F>
+static void profiled(pe_ctx* c, double flops, cudaStream_t st, F&& fn) {
   if (c->profiling) {
     if ((int)c->prof_events.size() < 2 * (c->prof_used + 1)) {
       for (int i = 0; i < 64; ++i) {
@@ -53,14 +55,18 @@ static void run_gemm(pe_ctx* c, const GemmParams& p, cudaStream_t st) {
       }
     }
     PE_CUDA_CHECK(cudaEventRecord(c->prof_events[2 * c->prof_used], st));
-    gemm_f64(p, st);
+    fn();
     PE_CUDA_CHECK(cudaEventRecord(c->prof_events[2 * c->prof_used + 1], st));
     ++c->prof_used;
   } else {
-    gemm_f64(p, st);
+    fn();
   }
-  c->stats.gemm_flops += gemm_flops(p);
+  c->stats.gemm_flops += flops;
   c->stats.launches += 1;
+}
+
+static void run_gemm(pe_ctx* c, const GemmParams& p, cudaStream_t st) {
+  profiled(c, gemm_flops(p), st, [&] { gemm_f64(p, st); });
 }
 
 static void collect_profile(pe_ctx* c, cudaStream_t st) {
@@ -95,6 +101,18 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
     c->Xin.ensure(sizeof(double) * n + 8);
     sub((long long)n, X_in, X_prev, c->Xin.d(), st);
     Ds = c->Xin.d();
+  } else {
+    int rpc_, cs_;
+    size_t sm_;
+    if (J > 0 && c->use_recur && recur_plan(d, 2 * d, &rpc_, &cs_, &sm_)) {
+      // all J substeps in one persistent cluster launch (T's row slices fit in smem)
+      c->Xs.ensure(sizeof(double) * 4 * n + 8);
+      profiled(c, 2.0 * d * (2.0 * d) * nc * E * J, st, [&] {
+        recur_seq(E, d, nc, J, c->T.d(), c->cvec.d(), X_in, X_out, c->Xs.d(), st);
+      });
+      collect_profile(c, st);
+      return;
+    }
   }
   for (int s = 0; s < J; ++s) {
     const bool last = (s == J - 1);
@@ -146,6 +164,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   c->P.ensure(sizeof(double) * E * 2 * J * L1 + 8);
   c->Q.ensure(sizeof(double) * E * 2 * J * L1 + 8);
   c->DU.ensure(sizeof(double) * E * J * L1 + 8);
+  c->DW.ensure(sizeof(double) * E * J * L2 + 8);
   c->V.ensure(sizeof(double) * E * L1 + 8);
   c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
   c->counter.ensure(sizeof(int) * 2);
@@ -162,7 +181,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   // sweep recipe (GEMM parameter blocks are loop-invariant)
   std::vector<GemmParams> pre, post;
   if (d1) {
-    GemmParams r;  // R = [Rw1|Rw0] [Wx[1..J]; Wx[0..J-1]] + f1   (build_rhs)
+    GemmParams r;  // R = [-A12 | -M12/dt] [Wx[1..J]; DW] + f1   (build_rhs)
     r.M = d1;
     r.N = J * nc;
     r.nb1 = E;
@@ -171,7 +190,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     r.seg[0].B = Operand{Wc + L2, 1, d2, (J + 2) * L2, 0};
     r.seg[0].K = d2;
     r.seg[1].A = Operand{c->RW.d() + d2, 2LL * d2, 1, 2LL * d1 * d2, 0};
-    r.seg[1].B = Operand{Wc, 1, d2, (J + 2) * L2, 0};
+    r.seg[1].B = Operand{c->DW.d(), 1, d2, J * L2, 0};
     r.seg[1].K = d2;
     r.C = c->R.d();
     r.c_i = 1;
@@ -240,6 +259,9 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     tb.c_b1 = (J + 2) * L1;
     pre.push_back(tb);
   }
+  int rpc_, cs_;
+  size_t sm_;
+  const bool use_rw = c->use_recur && d2 > 0 && recur_plan(d2, d2, &rpc_, &cs_, &sm_);
   GemmParams gw;  // g_s = [Gu|Gd][U_s; U_{s-1}-U_{s-2}] + dt M22^-T f2   (_w_sweep :222-224)
   if (d2) {
     gw.M = d2;
@@ -258,7 +280,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     gw.c_b1 = (J + 2) * L2;
     gw.bias = c->cg.d();
     gw.bias_b1 = d2;
-    for (int s = 0; s < J; ++s) {  // w_{s+1} = E w_s + g_s   (:226-229)
+    for (int s = 0; s < J && !use_rw; ++s) {  // w_{s+1} = E w_s + g_s   (:226-229)
       GemmParams rc;
       rc.M = d2;
       rc.N = nc;
@@ -287,11 +309,15 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   auto enqueue_sweep = [&](int sweep) {
     PE_CUDA_CHECK(cudaMemsetAsync(cnt + (sweep & 1), 0, sizeof(int), st));
+    if (d1 && d2) wr_diff_u(E, nc, d2, J, Wc, c->DW.d(), st);  // DW_s = Wx[s+1] - Wx[s]
     for (auto& p : pre) run_gemm(c, p, st);
     if (d1) wr_diff_u(E, nc, d1, J, Un, c->DU.d(), st);
     if (d2) {
       run_gemm(c, gw, st);
       for (auto& p : post) run_gemm(c, p, st);
+      if (use_rw)  // all J steps of the w recursion in one cluster-resident launch
+        profiled(c, 2.0 * d2 * d2 * nc * E * J, st,
+                 [&] { recur_wr(E, d2, nc, J, c->Emat.d(), Wn, st); });
     }
     wr_commit(E, nc, d1, d2, J, alpha, tol, max_iter, sweep, Uc, Un, Wc, Wn, c->V.d(), cs,
               resid_hist, cnt + (sweep & 1), st);
@@ -640,6 +666,13 @@ int pe_parareal_iterate(pe_ctx* c, int kind, int N, const double* X_old, double*
     bind(c);
     parareal_iterate(c, kind, N, X_old, X_new, G_cache, diff, active, wr_sweeps, wr_reasons,
                      wr_resid, (cudaStream_t)stream);
+  });
+}
+
+int pe_set_recurrence(pe_ctx* c, int on) {
+  return guarded([&] {
+    require(c != nullptr, PE_ERR_ARG, "ctx is NULL");
+    c->use_recur = on != 0;
   });
 }
 

@@ -70,8 +70,8 @@ struct pe_ctx {
   pe::DevBuf Bk, RW, M11dt, GW, cg, Emat, Finv, Fw;
 
   // work buffers
-  pe::DevBuf Xin, Xout, Xa, Xb, Da, Db;
-  pe::DevBuf Ux_cur, Ux_new, Wx_cur, Wx_new, R, P, Q, DU, V, colstate, counter;
+  pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs;
+  pe::DevBuf Ux_cur, Ux_new, Wx_cur, Wx_new, R, P, Q, DU, DW, V, colstate, counter;
   pe::DevBuf partial, diff, Gc, active, hist_tmp;
   int* pinned_count = nullptr;
   double* pinned_diff = nullptr;
@@ -80,6 +80,7 @@ struct pe_ctx {
   long long launches_at_create = 0;
   cudaEvent_t ev_mid = nullptr;  // fine/coarse boundary inside pe_parareal_run
   bool profiling = false;
+  bool use_recur = true;  // persistent cluster recurrences (else one GEMM per step)
   std::vector<cudaEvent_t> prof_events;
   int prof_used = 0;
   pe::FineStats stats;

@@ -89,6 +89,12 @@ void wr_finish(int E, int ncols, int d1, int d2, int J, const double* Ux_cur,
 void wr_gather(int E, int nc, int dd, int J, const double* X, double* out, cudaStream_t st);
 void sub(long long n, const double* a, const double* b, double* out, cudaStream_t st);
 
+// ---------------------------------------------------------------- recurrences (recur.cu)
+bool recur_plan(int M, int KT, int* rpc, int* cs, size_t* smem);
+bool recur_wr(int E, int d2, int nc, int J, const double* Emat, double* Wx, cudaStream_t st);
+bool recur_seq(int E, int d, int nc, int S, const double* T, const double* c, const double* Xin,
+               double* Xout, double* scratch, cudaStream_t st);
+
 // ---------------------------------------------------------------- coarse sweep
 // Row-partitioned cluster kernel; see coarse.cu.
 void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,

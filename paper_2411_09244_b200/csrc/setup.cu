@@ -12,7 +12,8 @@
 //          [Qu Pu,  Ew + Qu Pa, Qd, Qu Pd ]],   c = [cu; cw + Qu cu].
 //   coarse (stepping.py:149-176): G(x) = Phi x + gG with Phi = K_G^-1 R_G, gG = K_G^-1 f.
 //   all-at-once (allatonce.py:100-110, 184-210): shifted inverses (d_k M11 + A11)^-1 as
-//     real 2x2-block matrices, the rhs operator [-(M12/dt + A12) | M12/dt], M11/dt,
+//     real 2x2-block matrices, the rhs operator [-A12 | -M12/dt] on [w_s; w_s - w_{s-1}]
+//     (difference first, as build_rhs does), M11/dt,
 //     the w-sweep operator [-dt M22^-T A12^T | -M22^-T M12^T], dt M22^-T f2, E and the
 //     alpha-circulant time transforms S^-1 (2J x J) and Re(S .) (J x 2J).
 
@@ -334,9 +335,10 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
         PE_CUDA_CHECK(cudaGetLastError());
       }
       double* RW = c->RW.d() + (size_t)e * d1 * 2 * d2;
-      // Rw1 = -(M12/dt + A12), Rw0 = M12/dt   (build_rhs, allatonce.py:154-156)
-      rm_geam(h, false, false, d1, d2, -1.0 / dt, M12, d2, -1.0, A12, d2, RW, 2 * d2);
-      rm_geam(h, false, false, d1, d2, 1.0 / dt, M12, d2, 0.0, M12, d2, RW + d2, 2 * d2);
+      // [-A12 | -M12/dt] acting on [w_{s}; w_{s} - w_{s-1}]: difference first, like
+      // build_rhs's dw = (w_hist[1:] - w_hist[:-1]) / dt (allatonce.py:154-156)
+      rm_geam(h, false, false, d1, d2, -1.0, A12, d2, 0.0, A12, d2, RW, 2 * d2);
+      rm_geam(h, false, false, d1, d2, -1.0 / dt, M12, d2, 0.0, M12, d2, RW + d2, 2 * d2);
       rm_geam(h, false, false, d1, d1, 1.0 / dt, M11, d1, 0.0, M11, d1,
               c->M11dt.d() + (size_t)e * d1 * d1, d1);
     }

@@ -168,6 +168,9 @@ class PeContext:
             self.ptr, PE_KIND[kind], N, _ptr(X_old), _ptr(X_new), _ptr(G_cache), _ptr(diff),
             _ptr(active), _ptr(wr_sweeps), _ptr(wr_reasons), _ptr(wr_resid), self.stream()))
 
+    def set_recurrence(self, on: bool):
+        check(self.lib.pe_set_recurrence(self.ptr, 1 if on else 0))
+
     def set_profiling(self, on: bool):
         check(self.lib.pe_set_profiling(self.ptr, 1 if on else 0))
 

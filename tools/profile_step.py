@@ -1,0 +1,44 @@
+"""Run setup + one warm parareal iteration, then ONE profiled iteration inside a
+cudaProfilerStart/Stop range (ncu --profile-from-start off captures exactly one step)."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+import paper_2411_09244_b200 as P  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="cfg2-aao")
+ap.add_argument("--steps", type=int, default=1)
+args = ap.parse_args()
+wl = bench.WORKLOADS[args.workload]
+blocks, f1, f2, meta = bench.load_system(wl["sys"])
+s = P.CoarseSystem(**blocks)
+ctx = P.PeContext([s], [P.ConstantLoads(f1, f2)], wl["J"])
+N, J, T, kind = wl["N"], wl["J"], wl["T"], wl["kind"]
+ctx.prepare_coarse(T / N)
+if kind == "sequential":
+    ctx.prepare_sequential(T / N / J)
+else:
+    ctx.prepare_allatonce(T / N / J, wl["alpha"], bench.FINE_TOL, bench.MAX_ITER)
+d = s.d1 + s.d2
+A = torch.zeros(1, N + 1, d, dtype=torch.float64, device="cuda")
+B = torch.zeros_like(A)
+Gc = torch.zeros(1, N, d, dtype=torch.float64, device="cuda")
+diff = torch.zeros(1, 2, dtype=torch.float64, device="cuda")
+ctx.coarse_correct(N, A, None, Gc, A)
+ctx.iterate(kind, N, A, B, Gc, diff)
+A, B = B, A
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
+for _ in range(args.steps):
+    ctx.iterate(kind, N, A, B, Gc, diff)
+    A, B = B, A
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
+print("profiled", args.workload, "launches", ctx.launch_count())
