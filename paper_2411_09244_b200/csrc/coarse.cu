@@ -149,7 +149,19 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
     }
     cluster.sync();  // publishes X_new[n+1] (release/acquire at cluster scope)
     const double* xn = X_new + (long long)(n + 1) * d;
-    for (int k = threadIdx.x; k < d; k += COARSE_THREADS) xs[k] = __ldcg(xn + k);
+    for (int base = 0; base < d; base += 4 * COARSE_THREADS) {  // 4 loads in flight per thread
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = base + u * COARSE_THREADS + threadIdx.x;
+        v[u] = k < d ? __ldcg(xn + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = base + u * COARSE_THREADS + threadIdx.x;
+        if (k < d) xs[k] = v[u];
+      }
+    }
     __syncthreads();
   }
 

@@ -167,6 +167,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   c->DW.ensure(sizeof(double) * E * J * L2 + 8);
   c->V.ensure(sizeof(double) * E * L1 + 8);
   c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
+  c->nrm.ensure(sizeof(double) * 2 * E * nc * J + 8);
   c->counter.ensure(sizeof(int) * 2);
   c->stats = FineStats();
   double* Uc = c->Ux_cur.d();
@@ -320,7 +321,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
                  [&] { recur_wr(E, d2, nc, J, c->Emat.d(), Wn, st); });
     }
     wr_commit(E, nc, d1, d2, J, alpha, tol, max_iter, sweep, Uc, Un, Wc, Wn, c->V.d(), cs,
-              resid_hist, cnt + (sweep & 1), st);
+              resid_hist, cnt + (sweep & 1), c->nrm.d(), st);
     PE_CUDA_CHECK(cudaMemcpyAsync(host_cnt + (sweep & 1), cnt + (sweep & 1), sizeof(int),
                                   cudaMemcpyDeviceToHost, st));
     PE_CUDA_CHECK(cudaEventRecord(ev[sweep & 1], st));

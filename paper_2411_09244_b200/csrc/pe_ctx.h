@@ -72,7 +72,7 @@ struct pe_ctx {
   // work buffers
   pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs;
   pe::DevBuf Ux_cur, Ux_new, Wx_cur, Wx_new, R, P, Q, DU, DW, V, colstate, counter;
-  pe::DevBuf partial, diff, Gc, active, hist_tmp;
+  pe::DevBuf partial, diff, Gc, active, hist_tmp, nrm;
   int* pinned_count = nullptr;
   double* pinned_diff = nullptr;
   size_t pinned_diff_n = 0;

@@ -5,14 +5,21 @@
 //              (stepping.py:122-147 x J, lags reset at the interval start :180)
 //
 // Interval columns are independent, so one thread-block cluster owns one (member,
-// column group of 8 intervals) and walks all steps in a single launch.  Each CTA of the
-// cluster keeps its 8-row-aligned slice of the stationary operator in shared memory
-// for the whole launch; per step it computes its rows with FP64 DMMA (m8n8k4, K split
-// across warps, partials reduced in a fixed order), publishes them through L2 and the
-// cluster barrier orders the step.  No host round trip, no per-step launch.
+// column group of 8 intervals) and walks all steps in a single launch.  Each CTA keeps its
+// 8-row-aligned slice of the stationary operator in shared memory for the whole launch
+// and computes its rows with FP64 DMMA (m8n8k4, K split across warps, partials reduced in
+// a fixed order).  The new rows go point to point: 16-byte `st.async` remote stores into
+// every peer's double-buffered x tile, each signalling the *receiver's* mbarrier
+// (complete_tx).  A CTA waits only on its own mbarrier for the bytes of the step it
+// consumes, so there is no cluster-wide barrier per step (B200 measurements:
+// cluster.sync ~0.21 us; 13-way 8-byte DSMEM push + sync ~1.6 us per step).
 // Column results do not depend on the column group they land in (batch invariance).
 
 #include <cooperative_groups.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "pe.h"
 #include "pe_internal.h"
@@ -23,12 +30,14 @@ namespace pe {
 
 constexpr int RC_THREADS = 256;
 constexpr int RC_WARPS = RC_THREADS / 32;
-constexpr int RC_CG = 8;  // interval columns per cluster (one n8 DMMA tile)
+constexpr int RC_CG = 8;    // interval columns per cluster (one n8 DMMA tile)
+constexpr int RC_CGP = 12;  // padded x row: 8 columns + 4 (conflict-free B fragments)
 
 struct RecurArgs {
   int mode;        // 0 = WR, 1 = SEQ
   int M;           // output rows (d2 for WR, d for SEQ)
   int KT;          // operator columns (d2 for WR, 2d for SEQ)
+  int KTP;         // KT padded to a multiple of 4 * RC_WARPS
   int nc;          // interval columns per member
   int S;           // steps
   int rpc;         // rows per CTA (multiple of 8)
@@ -39,18 +48,61 @@ struct RecurArgs {
   // WR: W (J+2 blocks of M x nc per member), block 1 = w0, block s+2 = g_s -> W_s
   double* W;
   long long w_b, L;
-  // SEQ: X_in / X_out (E, nc, M), scratch Xs (2 x E x nc x 2M) for [X; D] exchange
+  // SEQ: X_in / X_out (E, nc, M)
   const double* Xin;
   double* Xout;
-  double* Xs;
   const double* bias;
   long long bias_b;
+  unsigned long long* trace;  // optional phase timestamps (CTA 0, thread 0), debug only
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot) \
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[slot] = gtimer();
 
 __device__ __forceinline__ void dmma_rc(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned map_rank(unsigned local_smem, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v2(unsigned remote_addr, double x, double y,
+                                            unsigned remote_bar) {
+  asm volatile(
+      "st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+      ::"r"(remote_addr), "l"(__double_as_longlong(x)), "l"(__double_as_longlong(y)),
+      "r"(remote_bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
 }
 
 template <int MT>  // m8 tiles per CTA (rpc = 8 * MT)
@@ -62,60 +114,110 @@ __global__ void __launch_bounds__(RC_THREADS) recur_kernel(const __grid_constant
   const int e = cid / ngroups, grp = cid - (cid / ngroups) * ngroups;
   const int r0 = rank * a.rpc;
   const int c0 = grp * RC_CG;
-  const int KT = a.KT, M = a.M;
-  const int SKO = KT + 4;  // padded row stride (doubles) of the operator slice / x columns
-  extern __shared__ double sm[];
-  double* opS = sm;                        // rpc x SKO
-  double* xs = opS + (size_t)a.rpc * SKO;  // RC_CG x SKO  (x column-major by column)
-  double* red = xs + (size_t)RC_CG * SKO;  // RC_WARPS x rpc x RC_CG
+  const int KT = a.KT, KTP = a.KTP, M = a.M;
+  const int SKO = KTP + 4;  // operator row stride (doubles); +4 keeps A fragments conflict-free
+  extern __shared__ __align__(16) double sm[];
+  double* opS = sm;                                 // rpc x SKO
+  double* xs2 = opS + (size_t)a.rpc * SKO;          // 2 x KTP x RC_CGP  (x[k][c], 2 buffers)
+  double* red = xs2 + (size_t)2 * KTP * RC_CGP;     // RC_WARPS x rpc x RC_CG
+  double* ybuf = red + (size_t)RC_WARPS * a.rpc * RC_CG;  // rpc x RC_CG (x part)
+  double* dbuf = ybuf + (size_t)a.rpc * RC_CG;            // rpc x RC_CG (SEQ d part)
+  __shared__ __align__(8) unsigned long long mbar[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
+  TRACE(0)
 
-  // operator slice -> smem (rows past M are zero)
+  // operator slice -> smem (rows past M and columns past KT are zero), loads batched
   const double* Op = a.Op + (long long)e * a.op_b;
-  for (int idx = tid; idx < a.rpc * KT; idx += RC_THREADS) {
-    const int r = idx / KT, k = idx - (idx / KT) * KT;
-    opS[r * SKO + k] = (r0 + r < M) ? Op[(long long)(r0 + r) * a.ldo + k] : 0.0;
+  for (int r = 0; r < a.rpc; r += 4) {
+    double v[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = tid + h * RC_THREADS;
+        const bool ok = (r + u < a.rpc) && (r0 + r + u < M) && (k < KT);
+        v[u][h] = ok ? __ldg(Op + (long long)(r0 + r + u) * a.ldo + k) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = tid + h * RC_THREADS;
+        if (r + u < a.rpc && k < KTP) opS[(r + u) * SKO + k] = v[u][h];
+      }
+    for (int k = tid + 2 * RC_THREADS; k < KTP; k += RC_THREADS)  // KT > 512: plain loop
+      for (int u = 0; u < 4 && r + u < a.rpc; ++u)
+        opS[(r + u) * SKO + k] =
+            (r0 + r + u < M && k < KT) ? __ldg(Op + (long long)(r0 + r + u) * a.ldo + k) : 0.0;
   }
-  // step-0 input: WR x = w0 (block 1 of W); SEQ [x; d] = [X_in; 0]
-  double* Wm = nullptr;
-  if (a.mode == 0) {
-    Wm = a.W + (long long)e * a.w_b;
-    const double* src = Wm + a.L;
-    for (int idx = tid; idx < RC_CG * KT; idx += RC_THREADS) {
-      const int c = idx / KT, k = idx - (idx / KT) * KT;
-      xs[c * SKO + k] = (c0 + c < a.nc) ? __ldcg(src + (long long)(c0 + c) * M + k) : 0.0;
+  // step-0 input into buffer 0 (x[k][c]); buffer 1 zeroed (padding columns / k past KT)
+  double* Wm = (a.mode == 0) ? a.W + (long long)e * a.w_b : nullptr;
+  for (int idx = tid; idx < KTP * RC_CGP; idx += RC_THREADS) {
+    const int k = idx / RC_CGP, c = idx - (idx / RC_CGP) * RC_CGP;
+    double v = 0.0;
+    if (c < RC_CG && c0 + c < a.nc && k < KT) {
+      if (a.mode == 0)
+        v = __ldcg(Wm + a.L + (long long)(c0 + c) * M + k);  // W_{-1} = w0 (block 1)
+      else if (k < M)
+        v = a.Xin[((long long)e * a.nc + c0 + c) * M + k];  // [X_0; D_0 = 0]
     }
-  } else {
-    const double* X0 = a.Xin + (long long)e * a.nc * M;
-    for (int idx = tid; idx < RC_CG * KT; idx += RC_THREADS) {
-      const int c = idx / KT, k = idx - (idx / KT) * KT;
-      xs[c * SKO + k] = (c0 + c < a.nc && k < M) ? X0[(long long)(c0 + c) * M + k] : 0.0;
-    }
+    xs2[idx] = v;
+    xs2[(size_t)KTP * RC_CGP + idx] = 0.0;
   }
-  const int Etot = gridDim.x / (a.cs * ngroups);
-  __syncthreads();
+  // one mbarrier per x buffer; bytes per phase = all M rows x 8 columns (x, and d for SEQ)
+  const unsigned bytes = (unsigned)(M * RC_CG * 8 * (a.mode == 1 ? 2 : 1));
+  if (tid == 0) {
+    mbar_init(smem_u32(&mbar[0]), 1);
+    mbar_init(smem_u32(&mbar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster.sync();  // barriers initialised and buffers zeroed before any peer pushes
+  if (tid == 0) {  // arm: buffer 1 <- step-0 rows, buffer 0 <- step-1 rows
+    mbar_expect_tx(smem_u32(&mbar[1]), bytes);
+    if (a.S > 2) mbar_expect_tx(smem_u32(&mbar[0]), bytes);
+  }
+  TRACE(1)
 
-  // split-K over warps, in multiples of 4
-  const int kq = (KT + 3) / 4;
-  const int kper = (kq + RC_WARPS - 1) / RC_WARPS;
-  const int kb = warp * kper * 4, ke = min(KT, (warp + 1) * kper * 4);
+  // split-K over warps (KTP is a multiple of 4 * RC_WARPS: no predicates in the loop)
+  const int kper = KTP / RC_WARPS;
+  const int kb = warp * kper;
   const double* bias = (a.mode == 1) ? a.bias + (long long)e * a.bias_b : nullptr;
+  constexpr int OUT_PER_T = (8 * MT * RC_CG + RC_THREADS - 1) / RC_THREADS;
+  const unsigned xs_base = smem_u32(xs2);
+  const unsigned bar_base = smem_u32(&mbar[0]);
 
   for (int s = 0; s < a.S; ++s) {
+    const int cur = s & 1;
+    const double* xs = xs2 + (size_t)cur * KTP * RC_CGP;
+    if (s > 0) {
+      mbar_wait(bar_base + 8 * cur, ((s - 1) >> 1) & 1);
+      // re-arm this buffer for the rows of step s+1 (consumed at step s+2)
+      if (tid == 0 && s + 2 < a.S) mbar_expect_tx(bar_base + 8 * cur, bytes);
+    }
+    TRACE(2 + 4 * s)
+    double gpre[OUT_PER_T];
+    if (a.mode == 0) {  // g_s for this thread's outputs, fetched under the DMMA work
+#pragma unroll
+      for (int u = 0; u < OUT_PER_T; ++u) {
+        const int idx = tid + u * RC_THREADS;
+        const int r = idx >> 3, c = idx & 7;
+        gpre[u] = (idx < a.rpc * RC_CG && r0 + r < M && c0 + c < a.nc)
+                      ? __ldcg(Wm + (long long)(s + 2) * a.L + (long long)(c0 + c) * M + r0 + r)
+                      : 0.0;
+      }
+    }
     double acc[MT][2];
 #pragma unroll
     for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = 0.0;
-    for (int k = kb; k < ke; k += 4) {
-      const int kk = k + t4;
-      const double b = (kk < KT) ? xs[g * SKO + kk] : 0.0;
+    const double* xb = xs + (size_t)(kb + t4) * RC_CGP + g;
+    const double* ob = opS + (size_t)g * SKO + kb + t4;
+#pragma unroll 4
+    for (int k = 0; k < kper; k += 4) {
+      const double b = xb[(size_t)k * RC_CGP];
 #pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        const double av = (kk < KT) ? opS[(m * 8 + g) * SKO + kk] : 0.0;
-        dmma_rc(acc[m][0], acc[m][1], av, b);
-      }
+      for (int m = 0; m < MT; ++m) dmma_rc(acc[m][0], acc[m][1], ob[(size_t)m * 8 * SKO + k], b);
     }
-    // partial tile (row m*8+g, cols 2*t4, 2*t4+1) -> red[warp]
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
       double* rw = red + ((size_t)warp * a.rpc + m * 8 + g) * RC_CG + 2 * t4;
@@ -123,64 +225,78 @@ __global__ void __launch_bounds__(RC_THREADS) recur_kernel(const __grid_constant
       rw[1] = acc[m][1];
     }
     __syncthreads();
+    TRACE(3 + 4 * s)
     const bool last = (s == a.S - 1);
-    for (int idx = tid; idx < a.rpc * RC_CG; idx += RC_THREADS) {
-      const int r = idx / RC_CG, c = idx - (idx / RC_CG) * RC_CG;
+    // fixed-order reduction over warps + epilogue, one (row, column) per thread
+#pragma unroll
+    for (int u = 0; u < OUT_PER_T; ++u) {
+      const int idx = tid + u * RC_THREADS;
+      if (idx >= a.rpc * RC_CG) continue;
+      const int r = idx >> 3, c = idx & 7;
       const int gr = r0 + r, gc = c0 + c;
-      if (gr >= M || gc >= a.nc) continue;
       double v = 0.0;
       for (int w = 0; w < RC_WARPS; ++w) v += red[((size_t)w * a.rpc + r) * RC_CG + c];
-      if (a.mode == 0) {
-        double* dst = Wm + (long long)(s + 2) * a.L + (long long)gc * M + gr;
-        v = __dadd_rn(v, *dst);  // + g_s  (w = E w + g, allatonce.py:228)
-        *dst = v;
-      } else {
-        v = __dadd_rn(v, bias[gr]);
-        const double xprev = xs[c * SKO + gr];
-        if (last) {
-          a.Xout[((long long)e * a.nc + gc) * M + gr] = v;
+      double dv = 0.0;
+      if (gr < M) {
+        if (a.mode == 0) {
+          v = __dadd_rn(v, gpre[u]);  // + g_s  (w = E w + g, allatonce.py:228)
+          if (gc < a.nc) Wm[(long long)(s + 2) * a.L + (long long)gc * M + gr] = v;
         } else {
-          // exchange buffer: (2, E, nc, 2M), parity s&1; [X_{s+1}; D_{s+1}]
-          double* xb = a.Xs + (((long long)(s & 1) * Etot + e) * a.nc + gc) * 2 * M;
-          xb[gr] = v;
-          xb[M + gr] = __dsub_rn(v, xprev);
+          v = __dadd_rn(v, bias[gr]);
+          dv = __dsub_rn(v, xs[(size_t)gr * RC_CGP + c]);  // D_{s+1} = X_{s+1} - X_s
+          if (last && gc < a.nc) a.Xout[((long long)e * a.nc + gc) * M + gr] = v;
         }
+        if (gc >= a.nc) v = dv = 0.0;  // padding columns stay zero
       }
+      ybuf[idx] = v;
+      dbuf[idx] = dv;
     }
-    cluster.sync();  // rows of step s published (release/acquire, cluster scope)
     if (!last) {
-      if (a.mode == 0) {
-        const double* src = Wm + (long long)(s + 2) * a.L;
-        for (int idx = tid; idx < RC_CG * KT; idx += RC_THREADS) {
-          const int c = idx / KT, k = idx - (idx / KT) * KT;
-          xs[c * SKO + k] = (c0 + c < a.nc) ? __ldcg(src + (long long)(c0 + c) * M + k) : 0.0;
-        }
-      } else {
-        const double* src = a.Xs + ((long long)(s & 1) * Etot + e) * a.nc * 2 * M;
-        for (int idx = tid; idx < RC_CG * KT; idx += RC_THREADS) {
-          const int c = idx / KT, k = idx - (idx / KT) * KT;
-          xs[c * SKO + k] = (c0 + c < a.nc) ? __ldcg(src + (long long)(c0 + c) * 2 * M + k) : 0.0;
+      __syncthreads();
+      // push: (row, peer) pairs; 4 x 16-byte st.async per row (8 columns), + d rows for SEQ
+      const int nrow = min(a.rpc, M - r0);
+      const unsigned nbuf = xs_base + (unsigned)(((s + 1) & 1) * KTP * RC_CGP * 8);
+      const unsigned nbar = bar_base + 8 * ((s + 1) & 1);
+      const int pairs = nrow * a.cs;
+      for (int p = tid; p < pairs; p += RC_THREADS) {
+        const int r = p / a.cs, q = p - (p / a.cs) * a.cs;
+        const unsigned rbar = map_rank(nbar, q);
+        const unsigned dst = map_rank(nbuf + (unsigned)((r0 + r) * RC_CGP * 8), q);
+        const double* y = ybuf + r * RC_CG;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) st_async_v2(dst + 16 * h, y[2 * h], y[2 * h + 1], rbar);
+        if (a.mode == 1) {
+          const unsigned dd = map_rank(nbuf + (unsigned)((M + r0 + r) * RC_CGP * 8), q);
+          const double* dy = dbuf + r * RC_CG;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) st_async_v2(dd + 16 * h, dy[2 * h], dy[2 * h + 1], rbar);
         }
       }
-      __syncthreads();
     }
+    TRACE(4 + 4 * s)
+    TRACE(5 + 4 * s)
   }
+  cluster.sync();  // no CTA leaves while peers' stores to it may be in flight
 }
 
-// Plan: the largest cluster (<= 16 CTAs) whose 8-row-aligned operator slices cover M,
-// provided a slice (plus x and the split-K scratch) fits in shared memory.
+static size_t recur_smem(int r, int KTP) {
+  return sizeof(double) * ((size_t)r * (KTP + 4) + 2 * (size_t)KTP * RC_CGP +
+                           (size_t)RC_WARPS * r * RC_CG + 2 * (size_t)r * RC_CG);
+}
+
+static int pad_k(int KT) { return (KT + 4 * RC_WARPS - 1) / (4 * RC_WARPS) * (4 * RC_WARPS); }
+
+// Plan: the smallest 8-row-aligned slice over <= 16 CTAs whose operator slice, x double
+// buffer and split-K scratch fit in shared memory.
 bool recur_plan(int M, int KT, int* rpc, int* cs, size_t* smem) {
-  for (int c = 16; c >= 1; --c) {
-    const int r = ((M + c - 1) / c + 7) / 8 * 8;
-    const size_t bytes = sizeof(double) * ((size_t)r * (KT + 4) + (size_t)RC_CG * (KT + 4) +
-                                           (size_t)RC_WARPS * r * RC_CG);
-    if (r > 64 || bytes > 200 * 1024) return false;  // larger c only shrinks r
-    *rpc = r;
-    *cs = (M + r - 1) / r;
-    *smem = bytes;
-    return true;
-  }
-  return false;
+  const int KTP = pad_k(KT);
+  const int r = ((M + 15) / 16 + 7) / 8 * 8;
+  const size_t bytes = recur_smem(r, KTP);
+  if (r > 64 || bytes > 200 * 1024) return false;
+  *rpc = r;
+  *cs = (M + r - 1) / r;
+  *smem = bytes;
+  return true;
 }
 
 template <int MT>
@@ -224,6 +340,35 @@ static void dispatch(const RecurArgs& a, int E, size_t smem, cudaStream_t st) {
   }
 }
 
+static void run_traced(RecurArgs& a, int E, size_t smem, cudaStream_t st, const char* tag) {
+  static const bool trace = getenv("PE_RECUR_TRACE") != nullptr;
+  unsigned long long* tb = nullptr;
+  const int n = 2 + 4 * a.S + 8;
+  if (trace) {
+    PE_CUDA_CHECK(cudaMalloc(&tb, sizeof(unsigned long long) * n));
+    PE_CUDA_CHECK(cudaMemset(tb, 0, sizeof(unsigned long long) * n));
+  }
+  a.trace = tb;
+  dispatch(a, E, smem, st);
+  if (trace) {
+    std::vector<unsigned long long> h(n);
+    PE_CUDA_CHECK(cudaStreamSynchronize(st));
+    PE_CUDA_CHECK(cudaMemcpy(h.data(), tb, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
+    double wait = 0, mma = 0, epi = 0;
+    for (int s = 0; s < a.S; ++s) {
+      if (s > 0) wait += (h[2 + 4 * s] - h[4 + 4 * (s - 1)]) * 1e-3;
+      mma += (h[3 + 4 * s] - h[2 + 4 * s]) * 1e-3;
+      epi += (h[4 + 4 * s] - h[3 + 4 * s]) * 1e-3;
+    }
+    fprintf(stderr,
+            "recur %s trace (cs=%d rpc=%d): setup %.2f us, per step: wait %.3f mma %.3f "
+            "epi+push %.3f us, total %.2f us\n",
+            tag, a.cs, a.rpc, (h[1] - h[0]) * 1e-3, wait / a.S, mma / a.S, epi / a.S,
+            (h[5 + 4 * (a.S - 1)] - h[0]) * 1e-3);
+    cudaFree(tb);
+  }
+}
+
 bool recur_wr(int E, int d2, int nc, int J, const double* Emat, double* Wx, cudaStream_t st) {
   RecurArgs a{};
   size_t smem;
@@ -231,6 +376,7 @@ bool recur_wr(int E, int d2, int nc, int J, const double* Emat, double* Wx, cuda
   a.mode = 0;
   a.M = d2;
   a.KT = d2;
+  a.KTP = pad_k(d2);
   a.ldo = d2;
   a.nc = nc;
   a.S = J;
@@ -239,18 +385,19 @@ bool recur_wr(int E, int d2, int nc, int J, const double* Emat, double* Wx, cuda
   a.L = (long long)d2 * nc;
   a.W = Wx;
   a.w_b = (long long)(J + 2) * a.L;
-  dispatch(a, E, smem, st);
+  run_traced(a, E, smem, st, "wr");
   return true;
 }
 
 bool recur_seq(int E, int d, int nc, int S, const double* T, const double* c, const double* Xin,
-               double* Xout, double* scratch, cudaStream_t st) {
+               double* Xout, double* /*scratch*/, cudaStream_t st) {
   RecurArgs a{};
   size_t smem;
   if (!recur_plan(d, 2 * d, &a.rpc, &a.cs, &smem)) return false;
   a.mode = 1;
   a.M = d;
   a.KT = 2 * d;
+  a.KTP = pad_k(2 * d);
   a.ldo = 2 * d;
   a.nc = nc;
   a.S = S;
@@ -258,10 +405,9 @@ bool recur_seq(int E, int d, int nc, int S, const double* T, const double* c, co
   a.op_b = 2LL * d * d;
   a.Xin = Xin;
   a.Xout = Xout;
-  a.Xs = scratch;  // 2 * E * nc * 2d doubles
   a.bias = c;
   a.bias_b = d;
-  dispatch(a, E, smem, st);
+  run_traced(a, E, smem, st, "seq");
   return true;
 }
 

@@ -109,69 +109,76 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 constexpr int COMMIT_THREADS = 256;
-constexpr int COMMIT_MAX_J = 1024;
+constexpr int COMMIT_WARPS = COMMIT_THREADS / 32;
 
-// One CTA per (member, interval).  Residual = max_s ||dU_s|| + max_s ||dW_s||
-// (allatonce.py:250-254); commit new -> cur; u_final_prev update (:257); stop tests
-// tol / diverged / floor (:258-271) and the max_iter cap.
+// Phase 1 (wide): one warp per (member, interval, substep) row: ||dU_s||, ||dW_s|| into
+// nrm[en][s][2] and, for intervals still iterating, commit new -> cur (allatonce.py:256).
 __global__ void __launch_bounds__(COMMIT_THREADS)
-    wr_commit_kernel(int nc, int d1, int d2, int J, double alpha, double tol, int max_iter,
-                     double* Ux_cur, const double* __restrict__ Ux_new, double* Wx_cur,
-                     const double* __restrict__ Wx_new, double* V, WrColumnState* cs,
-                     double* resid_hist, int* active_count) {
-  __shared__ double nu[COMMIT_MAX_J], nw[COMMIT_MAX_J];
-  __shared__ int s_active;
+    wr_commit_norms_kernel(int nc, int d1, int d2, int J, double* Ux_cur,
+                           const double* __restrict__ Ux_new, double* Wx_cur,
+                           const double* __restrict__ Wx_new, const WrColumnState* cs,
+                           double* nrm) {
   const int en = blockIdx.x;
+  const int s = blockIdx.y * COMMIT_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= J || !cs[en].active) return;
   const int e = en / nc, n = en - (en / nc) * nc;
-  if (threadIdx.x == 0) s_active = cs[en].active;
-  __syncthreads();
-  if (!s_active) return;
   const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
-  double* uc = Ux_cur + (long long)e * (J + 2) * L1 + (long long)n * d1;
-  const double* un = Ux_new + (long long)e * (J + 2) * L1 + (long long)n * d1;
-  double* wc = Wx_cur + (long long)e * (J + 2) * L2 + (long long)n * d2;
-  const double* wn = Wx_new + (long long)e * (J + 2) * L2 + (long long)n * d2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NW = COMMIT_THREADS / 32;
-  for (int s = warp; s < J; s += NW) {
-    const long long bu = (long long)(s + 2) * L1, bw = (long long)(s + 2) * L2;
-    double a = 0.0, b = 0.0;
-    for (int i = lane; i < d1; i += 32) {
-      const double x = un[bu + i] - uc[bu + i];
-      a += x * x;
-    }
-    for (int i = lane; i < d2; i += 32) {
-      const double x = wn[bw + i] - wc[bw + i];
-      b += x * x;
-    }
-    a = warp_sum(a);
-    b = warp_sum(b);
-    if (lane == 0) {
-      nu[s] = sqrt(a);
-      nw[s] = sqrt(b);
-    }
+  const long long bu = (long long)e * (J + 2) * L1 + (long long)(s + 2) * L1 + (long long)n * d1;
+  const long long bw = (long long)e * (J + 2) * L2 + (long long)(s + 2) * L2 + (long long)n * d2;
+  double a = 0.0, b = 0.0;
+  for (int i = lane; i < d1; i += 32) {
+    const double un = Ux_new[bu + i];
+    const double x = un - Ux_cur[bu + i];
+    a += x * x;
+    Ux_cur[bu + i] = un;
   }
-  __syncthreads();
-  // commit the new waveforms of this column (blocks 2..J+1)
-  for (int s = warp; s < J; s += NW) {
-    const long long bu = (long long)(s + 2) * L1, bw = (long long)(s + 2) * L2;
-    for (int i = lane; i < d1; i += 32) uc[bu + i] = un[bu + i];
-    for (int i = lane; i < d2; i += 32) wc[bw + i] = wn[bw + i];
+  for (int i = lane; i < d2; i += 32) {
+    const double wn = Wx_new[bw + i];
+    const double x = wn - Wx_cur[bw + i];
+    b += x * x;
+    Wx_cur[bw + i] = wn;
   }
-  // V = u_start - alpha * u_final_prev, u_final_prev = last row of U (:257)
-  if (d1 > 0) {
-    const long long last = (long long)(J + 1) * L1;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) {
+    nrm[((long long)en * J + s) * 2] = sqrt(a);
+    nrm[((long long)en * J + s) * 2 + 1] = sqrt(b);
+  }
+}
+
+// Phase 2: one warp per interval.  Residual = max_s ||dU_s|| + max_s ||dW_s||
+// (:250-254), u_final_prev update (:257), stop tests tol / diverged / floor (:258-271)
+// and the max_iter cap.
+__global__ void __launch_bounds__(COMMIT_THREADS)
+    wr_commit_decide_kernel(int ncols_total, int nc, int d1, int d2, int J, double alpha,
+                            double tol, int max_iter, const double* __restrict__ Ux_new,
+                            double* V, WrColumnState* cs, const double* __restrict__ nrm,
+                            double* resid_hist, int* active_count) {
+  const int en = blockIdx.x * COMMIT_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (en >= ncols_total || !cs[en].active) return;
+  double mu = 0.0, mw = 0.0;
+  for (int s = lane; s < J; s += 32) {
+    const double a = nrm[((long long)en * J + s) * 2], b = nrm[((long long)en * J + s) * 2 + 1];
+    mu = (a > mu || a != a) ? a : mu;
+    mw = (b > mw || b != b) ? b : mw;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double a = __shfl_xor_sync(0xffffffffu, mu, o), b = __shfl_xor_sync(0xffffffffu, mw, o);
+    mu = (a > mu || a != a) ? a : mu;
+    mw = (b > mw || b != b) ? b : mw;
+  }
+  if (d1 > 0) {  // V = u_start - alpha * u_final_prev with the new last row
+    const int e = en / nc, n = en - (en / nc) * nc;
+    const long long L1 = (long long)d1 * nc;
+    const double* un = Ux_new + (long long)e * (J + 2) * L1 + (long long)n * d1;
     double* v = V + (long long)e * L1 + (long long)n * d1;
-    for (int i = threadIdx.x; i < d1; i += COMMIT_THREADS) v[i] = un[i] - alpha * un[last + i];
+    const long long last = (long long)(J + 1) * L1;
+    for (int i = lane; i < d1; i += 32) v[i] = un[i] - alpha * un[last + i];
   }
-  if (threadIdx.x == 0) {
-    double mu = 0.0, mw = 0.0;
-    for (int s = 0; s < J; ++s) {
-      mu = fmax(mu, nu[s]);
-      mw = fmax(mw, nw[s]);
-      if (nu[s] != nu[s]) mu = nu[s];  // propagate NaN like np.max
-      if (nw[s] != nw[s]) mw = nw[s];
-    }
+  if (lane == 0) {
     double resid = 0.0;
     if (d1 > 0) resid += mu;
     if (d2 > 0) resid += mw;
@@ -208,11 +215,15 @@ __global__ void __launch_bounds__(COMMIT_THREADS)
 void wr_commit(int E, int nc, int d1, int d2, int J, double alpha, double tol, int max_iter,
                int /*sweep*/, double* Ux_cur, const double* Ux_new, double* Wx_cur,
                const double* Wx_new, double* V, WrColumnState* cs, double* resid_hist,
-               int* active_count, cudaStream_t st) {
-  if (J > COMMIT_MAX_J) throw Error{PE_ERR_ARG, "J exceeds 1024"};
-  wr_commit_kernel<<<E * nc, COMMIT_THREADS, 0, st>>>(nc, d1, d2, J, alpha, tol, max_iter,
-                                                      Ux_cur, Ux_new, Wx_cur, Wx_new, V, cs,
-                                                      resid_hist, active_count);
+               int* active_count, double* nrm, cudaStream_t st) {
+  dim3 g1(E * nc, (J + COMMIT_WARPS - 1) / COMMIT_WARPS);
+  wr_commit_norms_kernel<<<g1, COMMIT_THREADS, 0, st>>>(nc, d1, d2, J, Ux_cur, Ux_new, Wx_cur,
+                                                        Wx_new, cs, nrm);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+  const int cols = E * nc;
+  wr_commit_decide_kernel<<<(cols + COMMIT_WARPS - 1) / COMMIT_WARPS, COMMIT_THREADS, 0, st>>>(
+      cols, nc, d1, d2, J, alpha, tol, max_iter, Ux_new, V, cs, nrm, resid_hist, active_count);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
 }
