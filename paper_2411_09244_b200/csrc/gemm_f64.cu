@@ -10,6 +10,9 @@
 // cp.async (LDGSTS) double buffering.
 
 #include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "pe.h"
@@ -172,6 +175,236 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   }
 }
 
+
+// ----------------------------------------------------------------------------------------
+// Fast path: A k-contiguous (row-major operators), B k-contiguous (BJC = false, the state /
+// waveform columns) or j-contiguous (BJC = true, the time-transform operand).  16-byte
+// cp.async.cg with per-thread precomputed offsets, a STAGES-deep pipeline with one CTA
+// barrier per k-tile, 32x32 warp tiles (4x4 DMMA m8n8k4 accumulators per warp).  The k
+// reduction order is the generic kernel's (k ascending in DMMA steps of 4 per segment), so
+// both paths give bitwise identical results and may be mixed freely.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
+template <int BM, int BN, int BK, int STAGES, bool BJC>
+struct FastCfg {
+  static constexpr int NT = (BM / 32) * (BN / 32) * 32;
+  static constexpr int SA = BK + 4;
+  static constexpr int SB = BJC ? (BN + 4) : (BK + 4);
+  static constexpr int A_TILE = BM * SA;
+  static constexpr int B_TILE = BJC ? BK * SB : BN * SB;
+  static constexpr size_t SMEM = sizeof(double) * (size_t)STAGES * (A_TILE + B_TILE);
+};
+
+template <int BM, int BN, int BK, int STAGES, bool BJC>
+__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
+    gemm_fast_kernel(const __grid_constant__ GemmParams p) {
+  using Cfg = FastCfg<BM, BN, BK, STAGES, BJC>;
+  constexpr int NT = Cfg::NT, SA = Cfg::SA, SB = Cfg::SB;
+  constexpr int WARPS_M = BM / 32;
+  extern __shared__ __align__(16) double smf[];
+  double* As = smf;
+  double* Bs = smf + STAGES * Cfg::A_TILE;
+
+  const int z = blockIdx.z;
+  const int z1 = z / p.nb2, z2 = z - (z / p.nb2) * p.nb2;
+  const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
+  const int tid = threadIdx.x;
+
+  int kt0 = 0, kt1 = 0, kt2 = 0;
+  if (p.nseg > 0) kt0 = (p.seg[0].K + BK - 1) / BK;
+  if (p.nseg > 1) kt1 = (p.seg[1].K + BK - 1) / BK;
+  if (p.nseg > 2) kt2 = (p.seg[2].K + BK - 1) / BK;
+  const int ntile = kt0 + kt1 + kt2;
+
+  // fixed per-thread chunk coordinates
+  constexpr int ACPR = BK / 2;                 // 16-byte chunks per A row
+  constexpr int AROWS = NT / ACPR;             // rows covered per pass
+  constexpr int APASS = BM / AROWS;
+  const int akc = tid % ACPR, ar = tid / ACPR;
+  constexpr int BCPR = BJC ? BN / 2 : BK / 2;
+  constexpr int BROWS = NT / BCPR;
+  constexpr int BPASS = (BJC ? BK : BN) / BROWS;
+  const int bkc = tid % BCPR, br = tid / BCPR;
+
+  auto load_tile = [&](int t, int slot) {
+    int s = 0, tt = t;
+    if (tt >= kt0) { tt -= kt0; s = 1; if (tt >= kt1) { tt -= kt1; s = 2; } }
+    const GemmSeg& sg = p.seg[s];
+    const int k0 = tt * BK, K = sg.K;
+    const double* A = sg.A.p + z1 * sg.A.b1 + z2 * sg.A.b2;
+    const double* B = sg.B.p + z1 * sg.B.b1 + z2 * sg.B.b2;
+    double* as = As + slot * Cfg::A_TILE;
+    double* bs = Bs + slot * Cfg::B_TILE;
+    {
+      const int kk = k0 + 2 * akc;
+      const int kv = max(0, min(2, K - kk));
+#pragma unroll
+      for (int i = 0; i < APASS; ++i) {
+        const int r = ar + i * AROWS, gi = i0 + r;
+        const int bytes = (gi < p.M) ? 8 * kv : 0;
+        const double* src = bytes ? A + (long long)gi * sg.A.s0 + kk : A;
+        cp_async16(as + r * SA + 2 * akc, src, bytes);
+      }
+    }
+    if (!BJC) {
+      const int kk = k0 + 2 * bkc;
+      const int kv = max(0, min(2, K - kk));
+#pragma unroll
+      for (int i = 0; i < BPASS; ++i) {
+        const int r = br + i * BROWS, gj = j0 + r;
+        const int bytes = (gj < p.N) ? 8 * kv : 0;
+        const double* src = bytes ? B + (long long)gj * sg.B.s1 + kk : B;
+        cp_async16(bs + r * SB + 2 * bkc, src, bytes);
+      }
+    } else {
+      const int jj = j0 + 2 * bkc;
+      const int jv = max(0, min(2, p.N - jj));
+#pragma unroll
+      for (int i = 0; i < BPASS; ++i) {
+        const int r = br + i * BROWS, gk = k0 + r;
+        const int bytes = (gk < K) ? 8 * jv : 0;
+        const double* src = bytes ? B + (long long)gk * sg.B.s0 + jj : B;
+        cp_async16(bs + r * SB + 2 * bkc, src, bytes);
+      }
+    }
+  };
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < ntile) load_tile(st, st);
+    cp_async_commit();
+  }
+  for (int t = 0; t < ntile; ++t) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    if (t + STAGES - 1 < ntile) load_tile(t + STAGES - 1, (t + STAGES - 1) % STAGES);
+    cp_async_commit();
+    const int slot = t % STAGES;
+    const double* as = As + slot * Cfg::A_TILE + (wm * 32 + g) * SA + t4;
+    const double* bs;
+    if (!BJC)
+      bs = Bs + slot * Cfg::B_TILE + (wn * 32 + g) * SB + t4;
+    else
+      bs = Bs + slot * Cfg::B_TILE + t4 * SB + wn * 32 + g;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) af[a] = as[a * 8 * SA + kk];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = BJC ? bs[kk * SB + b * 8] : bs[b * 8 * SB + kk];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+  }
+  cp_async_wait<0>();
+
+  const long long cb = z1 * p.c_b1 + z2 * p.c_b2;
+  double* C = p.C + cb;
+  const double* Cin = p.Cin ? p.Cin + cb : nullptr;
+  double* D = p.D ? p.D + cb : nullptr;
+  const double* Xp = p.Xp ? p.Xp + cb : nullptr;
+  const double* bias = p.bias ? p.bias + z1 * p.bias_b1 + z2 * p.bias_b2 : nullptr;
+  const bool alpha1 = (p.alpha == 1.0), beta1 = (p.beta == 1.0);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int gi = i0 + wm * 32 + a * 8 + g;
+    if (gi >= p.M) continue;
+    const double bv = bias ? bias[gi] : 0.0;
+    const long long ro = gi * p.c_i;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gj = j0 + wn * 32 + b * 8 + 2 * t4 + h;
+        if (gj >= p.N) continue;
+        const long long off = ro + gj * p.c_j;
+        double v = alpha1 ? acc[a][b][h] : __dmul_rn(p.alpha, acc[a][b][h]);
+        if (Cin) v = __dadd_rn(v, beta1 ? Cin[off] : __dmul_rn(p.beta, Cin[off]));
+        if (bias) v = __dadd_rn(v, bv);
+        C[off] = v;
+        if (D) D[off] = __dsub_rn(v, Xp[off]);
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int BK, int STAGES, bool BJC>
+static int fast_occupancy() {
+  static int occ = -1;
+  if (occ < 0) {
+    using Cfg = FastCfg<BM, BN, BK, STAGES, BJC>;
+    PE_CUDA_CHECK(cudaFuncSetAttribute(gemm_fast_kernel<BM, BN, BK, STAGES, BJC>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+    int n = 0;
+    PE_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &n, gemm_fast_kernel<BM, BN, BK, STAGES, BJC>, Cfg::NT, Cfg::SMEM));
+    occ = n;
+  }
+  return occ;
+}
+
+template <int BM, int BN, int BK, int STAGES, bool BJC>
+static void launch_fast(const GemmParams& p, cudaStream_t st) {
+  using Cfg = FastCfg<BM, BN, BK, STAGES, BJC>;
+  fast_occupancy<BM, BN, BK, STAGES, BJC>();
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.nb1 * p.nb2);
+  gemm_fast_kernel<BM, BN, BK, STAGES, BJC><<<grid, Cfg::NT, Cfg::SMEM, st>>>(p);
+  ++g_launches;
+}
+
+static bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
+
+// Fast-path eligibility: 16-byte chunks along the contiguous dimension of A and B.
+static int fast_layout(const GemmParams& p) {
+  if (p.nseg == 0) return -1;
+  int bjc = -1;
+  for (int s = 0; s < p.nseg; ++s) {
+    const Operand& A = p.seg[s].A;
+    const Operand& B = p.seg[s].B;
+    if (A.s1 != 1 || (A.s0 & 1) || (A.b1 & 1) || (A.b2 & 1) || !aligned16(A.p)) return -1;
+    int lay;
+    if (B.s0 == 1 && !(B.s1 & 1)) lay = 0;
+    else if (B.s1 == 1 && !(B.s0 & 1)) lay = 1;
+    else return -1;
+    if ((B.b1 & 1) || (B.b2 & 1) || !aligned16(B.p)) return -1;
+    if (bjc >= 0 && lay != bjc) return -1;
+    bjc = lay;
+  }
+  return bjc;
+}
+
+struct FastChoice {
+  int id;
+  double cost;
+};
+
+template <int BM, int BN, int BK, int STAGES, bool BJC>
+static double fast_cost(const GemmParams& p, double tile_eff) {
+  const int occ = fast_occupancy<BM, BN, BK, STAGES, BJC>();
+  if (occ <= 0) return 1e300;
+  const double ctas = (double)((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN) * p.nb1 * p.nb2;
+  const double slots = 148.0 * occ;
+  const double rounds = std::ceil(ctas / slots);
+  // per-round time ~ one CTA's tile work at the SM's share of DMMA throughput
+  const double per_sm = std::min(ctas, slots) / 148.0;  // CTAs sharing an SM in a round
+  return rounds * (double)BM * BN * std::max(1.0, per_sm) / tile_eff;
+}
+
 template <int BM, int BN, int BK, int WM, int WN>
 static void launch_cfg(const GemmParams& p, bool ak, bool bk, cudaStream_t st) {
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.nb1 * p.nb2);
@@ -207,10 +440,37 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
   }
   const long long batch = (long long)p.nb1 * p.nb2;
   const long long tiles64 = (long long)((p.M + 63) / 64) * ((p.N + 63) / 64) * batch;
-  if (tiles64 >= 2 * 148)
+  static const bool no_fast = getenv("PE_GEMM_GENERIC") != nullptr;
+  const int lay = no_fast ? -1 : fast_layout(p);
+  if (lay >= 0 && tiles64 >= 148) {
+    // pick the tile / pipeline variant with the best wave-quantised cost
+    double c[3];
+    if (lay == 0) {
+      c[0] = fast_cost<64, 64, 32, 3, false>(p, 1.0);
+      c[1] = fast_cost<64, 64, 16, 3, false>(p, 0.9);
+      c[2] = fast_cost<128, 64, 16, 3, false>(p, 1.05);
+    } else {
+      c[0] = fast_cost<64, 64, 32, 3, true>(p, 1.0);
+      c[1] = fast_cost<64, 64, 16, 3, true>(p, 0.9);
+      c[2] = fast_cost<128, 64, 16, 3, true>(p, 1.05);
+    }
+    int best = 0;
+    for (int i = 1; i < 3; ++i)
+      if (c[i] < c[best]) best = i;
+    if (lay == 0) {
+      if (best == 0) launch_fast<64, 64, 32, 3, false>(p, st);
+      else if (best == 1) launch_fast<64, 64, 16, 3, false>(p, st);
+      else launch_fast<128, 64, 16, 3, false>(p, st);
+    } else {
+      if (best == 0) launch_fast<64, 64, 32, 3, true>(p, st);
+      else if (best == 1) launch_fast<64, 64, 16, 3, true>(p, st);
+      else launch_fast<128, 64, 16, 3, true>(p, st);
+    }
+  } else if (tiles64 >= 2 * 148) {
     launch_cfg<64, 64, 16, 32, 32>(p, ak, bk, st);
-  else
+  } else {
     launch_cfg<32, 32, 16, 16, 16>(p, ak, bk, st);
+  }
   PE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -90,7 +90,7 @@ void wr_gather(int E, int nc, int dd, int J, const double* X, double* out, cudaS
 void sub(long long n, const double* a, const double* b, double* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- recurrences (recur.cu)
-bool recur_plan(int M, int KT, int* rpc, int* cs, size_t* smem);
+bool recur_plan(int M, int KT, int* rpc, int* cs, size_t* smem, int nclusters = 0);
 bool recur_wr(int E, int d2, int nc, int J, const double* Emat, double* Wx, cudaStream_t st);
 bool recur_seq(int E, int d, int nc, int S, const double* T, const double* c, const double* Xin,
                double* Xout, double* scratch, cudaStream_t st);

@@ -286,29 +286,87 @@ static size_t recur_smem(int r, int KTP) {
 
 static int pad_k(int KT) { return (KT + 4 * RC_WARPS - 1) / (4 * RC_WARPS) * (4 * RC_WARPS); }
 
-// Plan: the smallest 8-row-aligned slice over <= 16 CTAs whose operator slice, x double
-// buffer and split-K scratch fit in shared memory.
-bool recur_plan(int M, int KT, int* rpc, int* cs, size_t* smem) {
+template <int MT>
+static void set_attrs() {
+  static bool done = false;
+  if (!done) {
+    PE_CUDA_CHECK(cudaFuncSetAttribute(recur_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       210 * 1024));
+    PE_CUDA_CHECK(cudaFuncSetAttribute(recur_kernel<MT>,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    done = true;
+  }
+}
+
+template <int MT>
+static int max_active_clusters(int cs, size_t smem) {
+  set_attrs<MT>();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs * 64);
+  cfg.blockDim = dim3(RC_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, recur_kernel<MT>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+static int active_clusters(int rpc, int cs, size_t smem) {
+  switch (rpc / 8) {
+    case 1: return max_active_clusters<1>(cs, smem);
+    case 2: return max_active_clusters<2>(cs, smem);
+    case 3: return max_active_clusters<3>(cs, smem);
+    case 4: return max_active_clusters<4>(cs, smem);
+    case 5: return max_active_clusters<5>(cs, smem);
+    case 6: return max_active_clusters<6>(cs, smem);
+    case 7: return max_active_clusters<7>(cs, smem);
+    case 8: return max_active_clusters<8>(cs, smem);
+  }
+  return 0;
+}
+
+// Plan: 8-row-aligned slices over <= 16 CTAs whose operator slice, x double buffer and
+// split-K scratch fit in shared memory.  Clusters must fit inside a GPC, so the number of
+// co-resident clusters depends on (cluster size, smem); pick the plan with the fewest
+// waves of `nclusters`, then the thinnest slice (least DMMA work per step).
+bool recur_plan(int M, int KT, int* rpc, int* cs, size_t* smem, int nclusters) {
   const int KTP = pad_k(KT);
-  const int r = ((M + 15) / 16 + 7) / 8 * 8;
-  const size_t bytes = recur_smem(r, KTP);
-  if (r > 64 || bytes > 200 * 1024) return false;
-  *rpc = r;
-  *cs = (M + r - 1) / r;
-  *smem = bytes;
+  int best_w = 1 << 30, best_r = 0;
+  for (int r = ((M + 15) / 16 + 7) / 8 * 8; r <= 64; r += 8) {
+    const size_t bytes = recur_smem(r, KTP);
+    if (bytes > 200 * 1024) break;
+    const int c = (M + r - 1) / r;
+    int act = 1;
+    if (nclusters > 0) {
+      act = active_clusters(r, c, bytes);
+      if (act <= 0) continue;
+    }
+    const int waves = nclusters > 0 ? (nclusters + act - 1) / act : 1;
+    if (waves < best_w) {
+      best_w = waves;
+      best_r = r;
+    }
+    if (nclusters <= 0 || waves == 1) break;
+  }
+  if (best_r == 0) return false;
+  *rpc = best_r;
+  *cs = (M + best_r - 1) / best_r;
+  *smem = recur_smem(best_r, KTP);
   return true;
 }
 
 template <int MT>
 static void launch_recur(const RecurArgs& a, int E, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    PE_CUDA_CHECK(cudaFuncSetAttribute(recur_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       210 * 1024));
-    PE_CUDA_CHECK(cudaFuncSetAttribute(recur_kernel<MT>,
-                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+  set_attrs<MT>();
   const int ngroups = (a.nc + RC_CG - 1) / RC_CG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(E * ngroups * a.cs);
@@ -372,7 +430,7 @@ static void run_traced(RecurArgs& a, int E, size_t smem, cudaStream_t st, const 
 bool recur_wr(int E, int d2, int nc, int J, const double* Emat, double* Wx, cudaStream_t st) {
   RecurArgs a{};
   size_t smem;
-  if (!recur_plan(d2, d2, &a.rpc, &a.cs, &smem)) return false;
+  if (!recur_plan(d2, d2, &a.rpc, &a.cs, &smem, E * ((nc + RC_CG - 1) / RC_CG))) return false;
   a.mode = 0;
   a.M = d2;
   a.KT = d2;
@@ -393,7 +451,7 @@ bool recur_seq(int E, int d, int nc, int S, const double* T, const double* c, co
                double* Xout, double* /*scratch*/, cudaStream_t st) {
   RecurArgs a{};
   size_t smem;
-  if (!recur_plan(d, 2 * d, &a.rpc, &a.cs, &smem)) return false;
+  if (!recur_plan(d, 2 * d, &a.rpc, &a.cs, &smem, E * ((nc + RC_CG - 1) / RC_CG))) return false;
   a.mode = 1;
   a.M = d;
   a.KT = 2 * d;

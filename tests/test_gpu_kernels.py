@@ -62,3 +62,24 @@ def test_gemm_zero_k_and_batch_invariance():
         assert np.array_equal(one[:, 0], full[:, j])
     z = _gemm(A, Bc, (K, 1), (1, K), M, 3, 0)
     assert np.array_equal(z, np.zeros((M, 3)))
+
+
+def test_fast_and_generic_gemm_paths_bitwise_equal():
+    """The 16-byte cp.async fast GEMM (large launches) and the generic kernel (small
+    launches) share the k reduction order: a column computed alone (generic) equals the
+    same column inside a fast-path batch, bit for bit, for both B layouts."""
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    M, K, N = 300, 600, 2048
+    A = torch.randn(M, K, dtype=torch.float64, device="cuda", generator=g)
+    Bt = torch.randn(N, K, dtype=torch.float64, device="cuda", generator=g)  # k-contiguous
+    full = _gemm(A, Bt, (K, 1), (1, K), M, N, K)
+    ref = (A @ Bt.T).cpu().numpy()
+    assert np.abs(full - ref).max() / np.abs(ref).max() < 1e-13
+    for j in (0, 777, N - 1):
+        one = _gemm(A, Bt[j:j + 1].contiguous(), (K, 1), (1, K), M, 1, K)
+        assert np.array_equal(one[:, 0], full[:, j])
+    Bj = Bt.T.contiguous()  # j-contiguous (time-transform layout), row-major C
+    full2 = _gemm(A, Bj, (K, 1), (N, 1), M, N, K, "row")
+    assert np.array_equal(full2, full)
