@@ -38,6 +38,10 @@ WORKLOADS = {
     "cfg2-seq": dict(sys="sys_cfg2.npz", T=1.0, N=64, J=64, kind="sequential", alpha=0.1),
     "cfg0-seq": dict(sys="sys_cfg0.npz", T=1.0, N=10, J=10, kind="sequential", alpha=0.1),
     "cfg1-aao": dict(sys="sys_cfg0.npz", T=1.0, N=10, J=10, kind="all-at-once", alpha=0.1),
+    # config 3 (d = 4096+4096, N = 128, J = 100): operators from oracle/build_cfg3.py
+    # (0.8 GB, not committed; data/ travels to the GPU box with the repo snapshot)
+    "cfg3-aao": dict(sys="../../data/sys_cfg3.npz", T=2.0, N=128, J=100, kind="all-at-once",
+                     alpha=0.1),
 }
 FINE_TOL, MAX_ITER = 1e-12, 400
 
@@ -121,7 +125,60 @@ def fp64_peak_tflops(torch):
 
 # ---------------------------------------------------------------------- CPU arms
 
-def cpu_sample(wl, blocks, f1, f2, budget_s=20.0):
+def cpu_sample_large(wl, s, sweeps_hint, cores):
+    """Config 3 (d1 = d2 = 4096, J = 100): a full reference iteration needs 26.8 GB of
+    complex inverses and hours, so time the reference's per-sweep operations
+    on a bounded subset and extrapolate: the `einsum("kij,kj->ki")` shifted apply on 2
+    modes per thread of a `cores`-thread pool (the dominant, memory-bound term), plus
+    build_rhs + both FFTs + the w-sweep of one interval once, times J modes, the sweep
+    count the GPU measured on the same iteration, and N intervals."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from threadpoolctl import threadpool_limits
+
+    from oracle import pe_oracle as po
+
+    N, J, T = wl["N"], wl["J"], wl["T"]
+    dt = T / N / J
+    d1, d2 = s.d1, s.d2
+    lam = po.time_eigenvalues(J, dt, wl["alpha"])
+    rng = np.random.default_rng(0)
+    with threadpool_limits(cores):
+        invs = [np.linalg.inv(lam[k] * s.M11 + s.A11.astype(complex)) for k in (1, 2)]
+        m22_inv = np.linalg.inv(s.M22)
+        e_mat = np.eye(d2) - dt * m22_inv @ s.A22
+    p = (rng.standard_normal((1, d1)) + 1j * rng.standard_normal((1, d1)))
+    with threadpool_limits(1):
+        def apply(i):
+            t0 = time.perf_counter()
+            for inv in invs:
+                np.einsum("kij,kj->ki", inv[None], p)
+            return time.perf_counter() - t0
+        with ThreadPoolExecutor(max_workers=cores) as pool:
+            times = list(pool.map(apply, range(cores)))
+        t_mode_pool = max(times) / (2 * cores)  # seconds per mode-apply, pool aggregate
+        u0 = np.zeros(d1)
+        w0 = np.zeros(d2)
+        W = rng.standard_normal((J, d2)) * 1e-3
+        t0 = time.perf_counter()
+        rhs = po.build_rhs(s, np.tile(s.f1, (J, 1)), u0, w0, w0, W, u0, dt, wl["alpha"])
+        q = po.apply_S(po.apply_S_inverse(rhs, wl["alpha"]), wl["alpha"]).real
+        uh = np.vstack([u0, u0, q[:-1]])
+        g = dt * (np.tile(s.f2, (J, 1)) - (uh[1:] - uh[:-1]) / dt @ s.M12 - q @ s.A12) @ m22_inv
+        w = w0
+        for i in range(J):
+            w = e_mat @ w + g[i]
+        t_rest = time.perf_counter() - t0
+    t_sweep = J * t_mode_pool + t_rest / cores
+    t_iter = N * sweeps_hint * t_sweep
+    return t_iter, dict(cores=cores, extrapolated=True, sample=(
+        f"extrapolated: einsum shifted apply timed on 2 modes x {cores} threads "
+        f"({t_mode_pool * 1e3:.1f} ms per mode-apply, pool aggregate) + one build_rhs/FFT/"
+        f"w-sweep ({t_rest:.2f} s); x J={J} modes x {sweeps_hint:.1f} sweeps (GPU-measured "
+        f"mean on the same iteration) x N={N} intervals; setup (26.8 GB inverses) excluded"))
+
+
+def cpu_sample(wl, blocks, f1, f2, budget_s=20.0, sweeps_hint=None):
     """Time the CPU oracle port (restatement of the reference, same LAPACK calls) on a
     bounded sample of one parareal iteration; returns (seconds_per_iteration, info)."""
     from threadpoolctl import threadpool_limits
@@ -130,6 +187,8 @@ def cpu_sample(wl, blocks, f1, f2, budget_s=20.0):
 
     cores = len(os.sched_getaffinity(0))
     s = po.OSystem(*(blocks[k] for k in ("M11", "A11", "M12", "A12", "M22", "A22")), f1, f2)
+    if s.d1 > 2048:
+        return cpu_sample_large(wl, s, sweeps_hint or 200.0, cores)
     N, J, T = wl["N"], wl["J"], wl["T"]
     dt = T / N
     sp = po.OracleSplit(s)
@@ -247,8 +306,11 @@ def gpu_arm(args, wl, units_member):
     ctx.coarse_correct(N, A, None, Gc, A)  # initial coarse sweep (x_0 = 0, u0 = 0 projection)
     flush = torch.empty(320 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 
+    sweeps_buf = (torch.zeros(E, N, dtype=torch.int32, device="cuda")
+                  if kind == "all-at-once" else None)
+
     def step(x_old, x_new):
-        ctx.iterate(kind, N, x_old, x_new, Gc, diff)
+        ctx.iterate(kind, N, x_old, x_new, Gc, diff, wr_sweeps=sweeps_buf)
 
     for _ in range(args.warmup):
         step(A, B)
@@ -317,7 +379,8 @@ def gpu_arm(args, wl, units_member):
                "path": "paper_2411_09244_b200.run_parareal (host arrays in/out, 1 member)"}
         cpu = None
         if world == 1 and not args.no_cpu:
-            t_iter, info = cpu_sample(wl, blocks, f1, f2)
+            hint = float(sweeps_buf.float().mean()) if sweeps_buf is not None else None
+            t_iter, info = cpu_sample(wl, blocks, f1, f2, sweeps_hint=hint)
             cpu = dict(value=units_member / t_iter, unit=UNIT, cores=info["cores"], kind="port",
                        sample=info["sample"])
         line = {

@@ -14,6 +14,7 @@
 
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "pe.h"
@@ -183,6 +184,138 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
   }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Large-d path (Phi slice does not fit in a cluster's shared memory, e.g. config 3 with
+// d = 8192 and a 537 MB Phi): one launch per coarse step across all SMs so that the
+// step streams Phi at HBM bandwidth (HBM-bound at cfg3), warp per row, four
+// independent lane-strided accumulators (fixed combination order), per-block norm
+// partials reduced in block order by a final kernel.
+constexpr int CS_THREADS = 256;
+constexpr int CS_WARPS = CS_THREADS / 32;
+
+__global__ void __launch_bounds__(CS_THREADS)
+    coarse_step_stream_kernel(int d, int n, int N, const double* __restrict__ Phi,
+                              const double* __restrict__ gvec, const double* X_old,
+                              const double* F_hat, double* G_cache, double* X_new,
+                              double* partial, const int* active) {
+  const int e = blockIdx.y;
+  if (active && active[e] == 0) {
+    if (n == 0) {  // frozen member: copy the whole iterate once
+      const double* xo = X_old + (long long)e * (N + 1) * d;
+      double* xn = X_new + (long long)e * (N + 1) * d;
+      for (long long t = blockIdx.x * (long long)CS_THREADS + threadIdx.x; t < (long long)(N + 1) * d;
+           t += (long long)gridDim.x * CS_THREADS)
+        xn[t] = xo[t];
+    }
+    return;
+  }
+  extern __shared__ double xs[];
+  const double* Xo = X_old + (long long)e * (N + 1) * d;
+  double* Xn = X_new + (long long)e * (N + 1) * d;
+  const double* xcur = (n == 0) ? Xo : Xn + (long long)n * d;  // x_n^{k+1} (row 0 = x_0)
+  for (int k = threadIdx.x; k < d; k += CS_THREADS) xs[k] = __ldcg(xcur + k);
+  if (n == 0)
+    for (int r = blockIdx.x * CS_THREADS + threadIdx.x; r < d; r += gridDim.x * CS_THREADS)
+      Xn[r] = Xo[r];
+  __syncthreads();
+  const double* Pm = Phi + (long long)e * d * d;
+  const double* gv = gvec + (long long)e * d;
+  const double* F = F_hat ? F_hat + (long long)e * N * d : nullptr;
+  double* Gc = G_cache + (long long)e * N * d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double sd = 0.0, sn = 0.0;
+  for (int r = blockIdx.x * CS_WARPS + warp; r < d; r += gridDim.x * CS_WARPS) {
+    const double* row = Pm + (long long)r * d;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int k = lane;
+    for (; k + 96 < d; k += 128) {
+      a0 = fma(__ldcs(row + k), xs[k], a0);
+      a1 = fma(__ldcs(row + k + 32), xs[k + 32], a1);
+      a2 = fma(__ldcs(row + k + 64), xs[k + 64], a2);
+      a3 = fma(__ldcs(row + k + 96), xs[k + 96], a3);
+    }
+    for (; k < d; k += 32) a0 = fma(__ldcs(row + k), xs[k], a0);
+    double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const long long o = (long long)n * d + r;
+      const double g = acc + gv[r];
+      const double x = F ? F[o] + (g - Gc[o]) : g;
+      Gc[o] = g;
+      Xn[o + d] = x;
+      const double df = x - Xo[o + d];
+      sd += df * df;
+      sn += x * x;
+    }
+  }
+  __shared__ double wp[2 * CS_WARPS];
+  if (lane == 0) {
+    wp[2 * warp] = sd;
+    wp[2 * warp + 1] = sn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && partial) {
+    double td = 0.0, tn = 0.0;
+    for (int w = 0; w < CS_WARPS; ++w) {
+      td += wp[2 * w];
+      tn += wp[2 * w + 1];
+    }
+    double* p = partial + (((long long)e * N + n) * gridDim.x + blockIdx.x) * 2;
+    p[0] = td;
+    p[1] = tn;
+  }
+}
+
+__global__ void coarse_norm_reduce_kernel(int N, int nblocks, const double* partial,
+                                          double* diff, const int* active) {
+  const int e = blockIdx.x;
+  if (threadIdx.x != 0 || (active && active[e] == 0)) return;
+  double md = 0.0, mn = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double* p = partial + ((long long)e * N + n) * nblocks * 2;
+    double td = 0.0, tn = 0.0;
+    for (int b = 0; b < nblocks; ++b) {
+      td += p[2 * b];
+      tn += p[2 * b + 1];
+    }
+    const double nd = sqrt(td), nn = sqrt(tn);
+    md = (nd > md || nd != nd) ? nd : md;
+    mn = (nn > mn || nn != nn) ? nn : mn;
+  }
+  diff[2 * e] = md;
+  diff[2 * e + 1] = mn;
+}
+
+int coarse_stream_blocks(int d) { return std::min(296, (d + CS_WARPS - 1) / CS_WARPS); }
+
+static void coarse_correct_stream(int E, int d, int N, const double* Phi, const double* gvec,
+                                  const double* X_old, const double* F_hat, double* G_cache,
+                                  double* X_new, double* partial, double* diff,
+                                  const int* active, cudaStream_t st) {
+  const int nb = coarse_stream_blocks(d);
+  const size_t smem = sizeof(double) * d;
+  static bool attr = false;
+  if (!attr) {
+    PE_CUDA_CHECK(cudaFuncSetAttribute(coarse_step_stream_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  if (smem > 200 * 1024) throw Error{PE_ERR_ARG, "coarse state too large for one SM"};
+  for (int n = 0; n < N; ++n) {
+    coarse_step_stream_kernel<<<dim3(nb, E), CS_THREADS, smem, st>>>(
+        d, n, N, Phi, gvec, X_old, F_hat, G_cache, X_new, partial, active);
+    ++g_launches;
+    PE_CUDA_CHECK(cudaGetLastError());
+  }
+  if (diff) {
+    coarse_norm_reduce_kernel<<<E, 32, 0, st>>>(N, nb, partial, diff, active);
+    ++g_launches;
+    PE_CUDA_CHECK(cudaGetLastError());
+  }
+}
+
 int coarse_cluster_size(int d) {
   if (d >= 256) return 16;
   if (d >= 64) return 8;
@@ -202,6 +335,11 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   size_t base = sizeof(double) * (d + 2 * COARSE_WARPS);
   size_t with_phi = base + sizeof(double) * (size_t)rows_max * d;
   a.phi_in_smem = with_phi <= 200 * 1024;
+  if (!a.phi_in_smem) {  // Phi streamed from HBM every step: use all SMs per step
+    coarse_correct_stream(E, d, N, Phi, gvec, X_old, F_hat, G_cache, X_new, partial, diff,
+                          active, st);
+    return;
+  }
   size_t smem = a.phi_in_smem ? with_phi : base;
   a.Phi = Phi;
   a.gvec = gvec;

@@ -442,7 +442,7 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
   const long long tiles64 = (long long)((p.M + 63) / 64) * ((p.N + 63) / 64) * batch;
   static const bool no_fast = getenv("PE_GEMM_GENERIC") != nullptr;
   const int lay = no_fast ? -1 : fast_layout(p);
-  if (lay >= 0 && tiles64 >= 148) {
+  if (lay >= 0 && tiles64 >= 96) {
     // pick the tile / pipeline variant with the best wave-quantised cost
     double c[3];
     if (lay == 0) {

@@ -2,6 +2,8 @@
 // correction and the device-resident parareal loop.
 
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -168,6 +170,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   c->V.ensure(sizeof(double) * E * L1 + 8);
   c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
   c->nrm.ensure(sizeof(double) * 2 * E * nc * J + 8);
+  c->rhist.ensure(sizeof(double) * (size_t)E * nc * max_iter + 8);
   c->counter.ensure(sizeof(int) * 2);
   c->stats = FineStats();
   double* Uc = c->Ux_cur.d();
@@ -177,7 +180,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   WrColumnState* cs = (WrColumnState*)c->colstate.p;
   int* cnt = c->counter.i();
 
-  wr_init(E, nc, d1, d2, J, alpha, X_in, Uc, Un, Wc, Wn, c->V.d(), cs, resid_hist, max_iter, st);
+  wr_init(E, nc, d1, d2, J, alpha, X_in, Uc, Un, Wc, Wn, c->V.d(), cs, c->rhist.d(), max_iter, st);
 
   // sweep recipe (GEMM parameter blocks are loop-invariant)
   std::vector<GemmParams> pre, post;
@@ -301,32 +304,81 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   }
 
 
+  // One sweep = ~10 launches (+ J GEMMs when the w recursion does not fit a cluster).
+  int* host_cnt = c->pinned_count;
+  auto body = [&](int par, cudaStream_t s) {
+    PE_CUDA_CHECK(cudaMemsetAsync(cnt + par, 0, sizeof(int), s));
+    if (d1 && d2) wr_diff_u(E, nc, d2, J, Wc, c->DW.d(), s);  // DW_s = Wx[s+1] - Wx[s]
+    for (auto& p : pre) run_gemm(c, p, s);
+    if (d1) wr_diff_u(E, nc, d1, J, Un, c->DU.d(), s);
+    if (d2) {
+      run_gemm(c, gw, s);
+      for (auto& p : post) run_gemm(c, p, s);
+      if (use_rw)  // all J steps of the w recursion in one cluster-resident launch
+        profiled(c, 2.0 * d2 * d2 * nc * E * J, s,
+                 [&] { recur_wr(E, d2, nc, J, c->Emat.d(), Wn, s); });
+    }
+    wr_commit(E, nc, d1, d2, J, alpha, tol, max_iter, 0, Uc, Un, Wc, Wn, c->V.d(), cs,
+              c->rhist.d(), cnt + par, c->nrm.d(), s);
+    PE_CUDA_CHECK(cudaMemcpyAsync(host_cnt + par, cnt + par, sizeof(int), cudaMemcpyDeviceToHost, s));
+  };
+  // CUDA graphs (one per counter parity) replace the per-sweep host launch sequence when
+  // not profiling; the graphs are captured on the context's stream and replayed on `st`.
+  static const bool no_graphs = getenv("PE_NO_GRAPHS") != nullptr;
+  const bool graphs = c->use_graphs && !c->profiling && !no_graphs &&
+                      getenv("PE_RECUR_TRACE") == nullptr;
+  SweepGraphs* sg = nullptr;
+  if (graphs) {
+    const std::vector<const void*> key = {
+        Uc, Un, Wc, Wn, c->R.p, c->P.p, c->Q.p, c->DU.p, c->DW.p, c->V.p, cs, c->nrm.p,
+        c->rhist.p, cnt, host_cnt, c->Bk.p, c->RW.p, c->GW.p, c->Emat.p, c->Finv.p, c->Fw.p,
+        c->M11dt.p, c->cg.p, c->f1.p, (const void*)(intptr_t)max_iter,
+        (const void*)(intptr_t)(c->use_recur ? 1 : 0),
+        (const void*)(intptr_t)(alpha * 1e6), (const void*)(intptr_t)(tol * 1e18)};
+    sg = &c->sweep_graphs[nc];
+    if (sg->key != key) {
+      for (auto& ex : sg->exec)
+        if (ex) {
+          cudaGraphExecDestroy(ex);
+          ex = nullptr;
+        }
+      const long long launches_before = g_launches;  // capture launches nothing
+      for (int par = 0; par < 2; ++par) {
+        cudaGraph_t g;
+        PE_CUDA_CHECK(cudaStreamBeginCapture(c->work, cudaStreamCaptureModeThreadLocal));
+        try {
+          body(par, c->work);
+        } catch (...) {
+          cudaStreamEndCapture(c->work, &g);
+          throw;
+        }
+        PE_CUDA_CHECK(cudaStreamEndCapture(c->work, &g));
+        PE_CUDA_CHECK(cudaGraphInstantiate(&sg->exec[par], g, 0));
+        PE_CUDA_CHECK(cudaGraphDestroy(g));
+      }
+      sg->key = key;
+      g_launches = launches_before;
+    }
+  }
   // Pipelined sweep loop: sweep i+1 is enqueued before the host reads sweep i's
   // active-interval count, so the device never waits on the host; the extra sweep
   // after the last interval stopped is fully masked (commit skips inactive columns).
-  int* host_cnt = c->pinned_count;
   cudaEvent_t ev[2];
   PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
   PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   auto enqueue_sweep = [&](int sweep) {
-    PE_CUDA_CHECK(cudaMemsetAsync(cnt + (sweep & 1), 0, sizeof(int), st));
-    if (d1 && d2) wr_diff_u(E, nc, d2, J, Wc, c->DW.d(), st);  // DW_s = Wx[s+1] - Wx[s]
-    for (auto& p : pre) run_gemm(c, p, st);
-    if (d1) wr_diff_u(E, nc, d1, J, Un, c->DU.d(), st);
-    if (d2) {
-      run_gemm(c, gw, st);
-      for (auto& p : post) run_gemm(c, p, st);
-      if (use_rw)  // all J steps of the w recursion in one cluster-resident launch
-        profiled(c, 2.0 * d2 * d2 * nc * E * J, st,
-                 [&] { recur_wr(E, d2, nc, J, c->Emat.d(), Wn, st); });
+    if (sg) {
+      PE_CUDA_CHECK(cudaGraphLaunch(sg->exec[sweep & 1], st));
+      g_launches += c->graph_kernels;
+    } else {
+      body(sweep & 1, st);
     }
-    wr_commit(E, nc, d1, d2, J, alpha, tol, max_iter, sweep, Uc, Un, Wc, Wn, c->V.d(), cs,
-              resid_hist, cnt + (sweep & 1), c->nrm.d(), st);
-    PE_CUDA_CHECK(cudaMemcpyAsync(host_cnt + (sweep & 1), cnt + (sweep & 1), sizeof(int),
-                                  cudaMemcpyDeviceToHost, st));
     PE_CUDA_CHECK(cudaEventRecord(ev[sweep & 1], st));
     collect_profile(c, st);
   };
+  if (sg)  // kernels per graph replay, for the native-launch evidence counter
+    c->graph_kernels = (int)(pre.size() + (d2 ? 1 + post.size() + (use_rw ? 1 : 0) : 0) +
+                             (d1 && d2 ? 1 : 0) + (d1 ? 1 : 0) + 2);
   int sweep = 0;
   enqueue_sweep(0);
   for (sweep = 1; sweep <= max_iter; ++sweep) {
@@ -338,6 +390,9 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
   wr_finish(E, nc, d1, d2, J, Uc, Wc, cs, X_out, sweeps, reasons, st);
+  if (resid_hist)
+    PE_CUDA_CHECK(cudaMemcpyAsync(resid_hist, c->rhist.p, sizeof(double) * (size_t)E * nc * max_iter,
+                                  cudaMemcpyDeviceToDevice, st));
 }
 
 // One parareal iteration (parareal.py:188-215): fine sweep on x_0..x_{N-1} of X_old,
@@ -348,7 +403,7 @@ static void parareal_iterate(pe_ctx* c, int kind, int N, const double* X_old, do
   const int E = c->E, d = c->d;
   c->Xin.ensure(sizeof(double) * (size_t)E * N * d + 8);
   c->Xout.ensure(sizeof(double) * (size_t)E * N * d + 8);
-  c->partial.ensure(sizeof(double) * (size_t)E * N * 16 * 2 + 8);
+  c->partial.ensure(sizeof(double) * (size_t)E * N * 296 * 2 + 8);
   PE_CUDA_CHECK(cudaMemcpy2DAsync(c->Xin.d(), sizeof(double) * N * d, X_old,
                                   sizeof(double) * (N + 1) * d, sizeof(double) * N * d, E,
                                   cudaMemcpyDeviceToDevice, st));
@@ -386,6 +441,7 @@ int pe_create(pe_ctx** out, int E, int d1, int d2, int max_cols, int J, int devi
     try {
       bind(c);
       PE_CUDA_CHECK(cudaStreamCreateWithFlags(&c->setup_stream, cudaStreamNonBlocking));
+      PE_CUDA_CHECK(cudaStreamCreateWithFlags(&c->work, cudaStreamNonBlocking));
       if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw Error{PE_ERR_CUDA, "cublasCreate failed"};
       if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw Error{PE_ERR_CUDA, "cusolverDnCreate failed"};
       cublasSetStream(c->blas, c->setup_stream);
@@ -417,6 +473,10 @@ int pe_destroy(pe_ctx* c) {
   if (c->blas) cublasDestroy(c->blas);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->setup_stream) cudaStreamDestroy(c->setup_stream);
+  for (auto& kv : c->sweep_graphs)
+    for (auto ex : kv.second.exec)
+      if (ex) cudaGraphExecDestroy(ex);
+  if (c->work) cudaStreamDestroy(c->work);
   if (c->pinned_count) cudaFreeHost(c->pinned_count);
   if (c->pinned_diff) cudaFreeHost(c->pinned_diff);
   for (auto e : c->prof_events) cudaEventDestroy(e);
@@ -513,7 +573,7 @@ int pe_coarse_correct(pe_ctx* c, int N, const double* X_old, const double* F_hat
     require(c && X_old && X_new && G_cache && N >= 1, PE_ERR_ARG, "bad coarse_correct arguments");
     require(c->coarse_dt > 0, PE_ERR_STATE, "pe_prepare_coarse not called");
     bind(c);
-    c->partial.ensure(sizeof(double) * (size_t)c->E * N * 16 * 2 + 8);
+    c->partial.ensure(sizeof(double) * (size_t)c->E * N * 296 * 2 + 8);
     coarse_correct(c->E, c->d, N, c->Phi.d(), c->gG.d(), X_old, F_hat, G_cache, X_new,
                    c->partial.d(), diff, active, (cudaStream_t)stream);
   });
@@ -528,7 +588,7 @@ int pe_coarse_apply(pe_ctx* c, const double* X_in, double* X_out, int nc, void* 
     const int d = c->d, E = c->E;
     c->hist_tmp.ensure(sizeof(double) * (size_t)E * 2 * d + 8);
     c->Gc.ensure(sizeof(double) * (size_t)E * d + 8);
-    c->partial.ensure(sizeof(double) * (size_t)E * 16 * 2 + 8);
+    c->partial.ensure(sizeof(double) * (size_t)E * 296 * 2 + 8);
     for (int n = 0; n < nc; ++n) {
       // one-interval initial sweep: row 1 = G(row 0), same kernel as the fused sweep
       PE_CUDA_CHECK(cudaMemcpy2DAsync(c->hist_tmp.d(), sizeof(double) * 2 * d, X_in + (size_t)n * d,
@@ -562,7 +622,7 @@ int pe_parareal_run(pe_ctx* c, int kind, int N, const double* X0, int k_max, dou
     const size_t slab = (size_t)E * (N + 1) * d;
     auto H = [&](int k) { return history + (size_t)k * slab; };
     c->Gc.ensure(sizeof(double) * (size_t)E * N * d + 8);
-    c->partial.ensure(sizeof(double) * (size_t)E * N * 16 * 2 + 8);
+    c->partial.ensure(sizeof(double) * (size_t)E * N * 296 * 2 + 8);
     c->diff.ensure(sizeof(double) * 2 * E + 8);
     c->active.ensure(sizeof(int) * E + 8);
     if (c->pinned_diff_n < (size_t)2 * E) {

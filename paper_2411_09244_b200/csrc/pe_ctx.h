@@ -39,6 +39,13 @@ struct DevBuf {
   int* i() const { return static_cast<int*>(p); }
 };
 
+// One WR sweep captured as a CUDA graph per counter parity; `key` records every pointer
+// and size baked into the nodes, so any reallocation or re-setup forces a recapture.
+struct SweepGraphs {
+  std::vector<const void*> key;
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+};
+
 struct FineStats {
   double gemm_flops = 0;   // algorithmic flops issued by the GEMM kernels of the last fine call
   double gemm_ms = 0;      // summed CUDA-event time of those launches (profiling mode only)
@@ -72,7 +79,11 @@ struct pe_ctx {
   // work buffers
   pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs;
   pe::DevBuf Ux_cur, Ux_new, Wx_cur, Wx_new, R, P, Q, DU, DW, V, colstate, counter;
-  pe::DevBuf partial, diff, Gc, active, hist_tmp, nrm;
+  pe::DevBuf partial, diff, Gc, active, hist_tmp, nrm, rhist;
+  cudaStream_t work = nullptr;           // capture stream for the sweep graphs
+  bool use_graphs = true;
+  int graph_kernels = 0;   // kernels per captured sweep (launch accounting)
+  std::map<int, pe::SweepGraphs> sweep_graphs;  // keyed by interval count
   int* pinned_count = nullptr;
   double* pinned_diff = nullptr;
   size_t pinned_diff_n = 0;

@@ -440,3 +440,40 @@ def test_unknown_fine_kind_rejected():
     cfg = P.ParerealConfig(time_grid=P.TimeGrid(1.0, 2, 2), alpha=0.5, fine_kind="magic")
     with pytest.raises(ValueError):
         P.build_fine_propagator(cfg, props, ld)
+
+
+def _random_coupled(d1, d2, seed):
+    rng = np.random.default_rng(seed)
+    n = d1 + d2
+    q = rng.standard_normal((2 * n, n))
+    mass = q.T @ q / (2 * n) + 0.5 * np.eye(n)
+    r = rng.standard_normal((2 * n, n))
+    stiff = r.T @ r / (2 * n) + 0.1 * np.eye(n)
+    return mass, stiff, rng.standard_normal(n)
+
+
+def test_large_d_streaming_coarse_and_parareal():
+    """d = 800: the coarse sweep takes the all-SM streaming path (Phi not smem-resident)
+    and the fine sweep the per-step GEMMs; both kinds match the CPU oracle."""
+    P = _pkg()
+    d1 = d2 = 400
+    mass, stiff, f = _random_coupled(d1, d2, 5)
+    blocks = dict(M11=mass[:d1, :d1], A11=stiff[:d1, :d1], M12=mass[:d1, d1:],
+                  A12=stiff[:d1, d1:], M22=mass[d1:, d1:], A22=stiff[d1:, d1:])
+    s = P.CoarseSystem(**blocks)
+    ld = P.ConstantLoads(f[:d1], f[d1:])
+    osys = po.OSystem(*(blocks[k] for k in ("M11", "A11", "M12", "A12", "M22", "A22")),
+                      f[:d1], f[d1:])
+    x0 = np.random.default_rng(6).standard_normal(d1 + d2) * 0.1
+    props = P.SplitPropagators(s, ld)
+    g = props.coarse_step(P.SplitState.fresh(x0[:d1], x0[d1:]), 0.05).stacked()
+    assert rel_rows(g, po.OracleSplit(osys).coarse_step(x0, 0.05)) < 1e-12
+    for kind in ("sequential", "all-at-once"):
+        cfg = P.ParerealConfig(time_grid=P.TimeGrid(0.3, 6, 4), alpha=0.2, epsilon=1e-10,
+                               k_max=6, fine_kind=kind, fine_tol=1e-12)
+        run = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld),
+                             P.SplitState.fresh(x0[:d1], x0[d1:]))
+        ref = po.run_parareal(osys, x0, 0.3, 6, 4, kind=kind, alpha=0.2, epsilon=1e-10, k_max=6,
+                              fine_tol=1e-12)
+        assert run.iterations == ref["iterations"]
+        assert rel_rows(np.array(run.history), np.array(ref["history"])) < REL
