@@ -42,14 +42,38 @@ WORKLOADS = {
     # (0.8 GB, not committed; data/ travels to the GPU box with the repo snapshot)
     "cfg3-aao": dict(sys="../../data/sys_cfg3.npz", T=2.0, N=128, J=100, kind="all-at-once",
                      alpha=0.1),
+    # config 4: 64 seeded members (own contrast 10^U(2,8), own kappa rescaling), one batch;
+    # operators from oracle/build_cfg4.py (data/, travels with the repo snapshot)
+    "cfg4-seq": dict(members="../../data/cfg4_members.npz", T=1.0, N=32, J=32,
+                     kind="sequential", alpha=0.1),
 }
 FINE_TOL, MAX_ITER = 1e-12, 400
 
 
+BLOCKS = ("M11", "A11", "M12", "A12", "M22", "A22")
+
+
 def load_system(name):
     z = np.load(os.path.join(GOLDEN, name))
-    blocks = {k: np.ascontiguousarray(z[k]) for k in ("M11", "A11", "M12", "A12", "M22", "A22")}
+    blocks = {k: np.ascontiguousarray(z[k]) for k in BLOCKS}
     return blocks, z["f1"], z["f2"], json.loads(str(z["meta"]))
+
+
+def load_workload(wl, n_replicas=1):
+    """[(blocks, f1, f2)] per member and a representative meta dict."""
+    if "members" in wl:
+        z = np.load(os.path.join(GOLDEN, wl["members"]))
+        metas = json.loads(str(z["meta"]))
+        mem = [({k: np.ascontiguousarray(z[k][m]) for k in BLOCKS}, z["f1"][m], z["f2"][m])
+               for m in range(z["f1"].shape[0])]
+        meta = dict(metas[0])
+        meta["members"] = len(mem)
+        meta["contrast_range"] = [min(x["contrast"] for x in metas),
+                                  max(x["contrast"] for x in metas)]
+        meta["kappa_scale"] = [x["kappa_scale"] for x in metas]
+        return mem, meta
+    blocks, f1, f2, meta = load_system(wl["sys"])
+    return [(blocks, f1, f2)] * n_replicas, meta
 
 
 class ClockSampler:
@@ -249,7 +273,8 @@ def cpu_sample(wl, blocks, f1, f2, budget_s=20.0, sweeps_hint=None):
 
 
 def reference_arm(args, wl, units):
-    blocks, f1, f2, meta = load_system(wl["sys"])
+    mem, meta = load_workload(wl)
+    blocks, f1, f2 = mem[0]
     vals = []
     for i in range(args.warmup + args.steps):
         t_iter, info = cpu_sample(wl, blocks, f1, f2, budget_s=5.0)
@@ -285,14 +310,16 @@ def gpu_arm(args, wl, units_member):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2411_09244_b200 as P
 
-    blocks, f1, f2, meta = load_system(wl["sys"])
-    system = P.CoarseSystem(**blocks)
-    loads = P.ConstantLoads(f1, f2)
-    E = args.members
+    mem, meta = load_workload(wl, args.members)
+    blocks, f1, f2 = mem[0]
+    systems = [P.CoarseSystem(**b) for b, _, _ in mem]
+    loads_l = [P.ConstantLoads(a, b) for _, a, b in mem]
+    system, loads = systems[0], loads_l[0]
+    E = len(mem)
     N, J, T, kind = wl["N"], wl["J"], wl["T"], wl["kind"]
     d = system.d1 + system.d2
     units = units_member * E
-    ctx = P.PeContext([system] * E, [loads] * E, J, local)
+    ctx = P.PeContext(systems, loads_l, J, local)
     ctx.prepare_coarse(T / N)
     if kind == "sequential":
         ctx.prepare_sequential(T / N / J)
@@ -357,26 +384,38 @@ def gpu_arm(args, wl, units_member):
     if rank == 0:
         # end to end through the public API: run_parareal with host initial state in and
         # the full history (host numpy) out, K iterations, epsilon = 0 (no early stop)
-        props = P.SplitPropagators(system, loads)
         cfg = P.ParerealConfig(time_grid=P.TimeGrid(T, N, J), alpha=wl["alpha"], epsilon=0.0,
                                k_max=args.steps, fine_kind=kind, fine_tol=FINE_TOL,
                                fine_max_iter=MAX_ITER)
-        fine = P.build_fine_propagator(cfg, props, loads)
-        init = P.SplitState.fresh(np.zeros(system.d1), np.zeros(system.d2))
         warm = P.ParerealConfig(time_grid=cfg.time_grid, alpha=cfg.alpha, epsilon=0.0, k_max=1,
                                 fine_kind=kind, fine_tol=FINE_TOL, fine_max_iter=MAX_ITER)
-        P.run_parareal(warm, props, fine, init)  # setup (factorisations) stays out of e2e
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        run = P.run_parareal(cfg, props, fine, init)
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-        K = run.iterations
+        if E == 1:
+            props = P.SplitPropagators(system, loads)
+            fine = P.build_fine_propagator(cfg, props, loads)
+            init = P.SplitState.fresh(np.zeros(system.d1), np.zeros(system.d2))
+            P.run_parareal(warm, props, fine, init)  # setup (factorisations) stays out of e2e
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            run = P.run_parareal(cfg, props, fine, init)
+            torch.cuda.synchronize()
+            e2e_s = time.perf_counter() - t0
+            K = run.iterations
+            path = "paper_2411_09244_b200.run_parareal (host arrays in/out, 1 member)"
+        else:
+            inits = [P.SplitState.fresh(np.zeros(system.d1), np.zeros(system.d2))] * E
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()  # run_parareal_ensemble builds its context: setup inside
+            runs = P.run_parareal_ensemble(cfg, systems, loads_l, inits)
+            torch.cuda.synchronize()
+            e2e_s = time.perf_counter() - t0
+            K = runs[0].iterations
+            path = (f"paper_2411_09244_b200.run_parareal_ensemble ({E} members, host arrays "
+                    "in/out; includes the ensemble's setup factorisations)")
         wr_bytes = K * N * (4 + 4 + 8 * MAX_ITER) if kind == "all-at-once" else 0
-        e2e = {"value": units_member * K / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": d * 8 / K,
-               "d2h_bytes_per_step": ((K + 1) * (N + 1) * d * 8 + wr_bytes) / K,
-               "path": "paper_2411_09244_b200.run_parareal (host arrays in/out, 1 member)"}
+        e2e = {"value": units_member * E * K / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": E * d * 8 / K,
+               "d2h_bytes_per_step": E * ((K + 1) * (N + 1) * d * 8 + wr_bytes) / K,
+               "path": path}
         cpu = None
         if world == 1 and not args.no_cpu:
             hint = float(sweeps_buf.float().mean()) if sweeps_buf is not None else None
@@ -389,10 +428,12 @@ def gpu_arm(args, wl, units_member):
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded kappa field per BASELINE config; reduced operators built "
-                    "by the reference's offline CEM code, tests/golden/" + wl["sys"] + ")",
+                    "by the reference's offline CEM code, " + (wl.get("sys") or wl["members"]) +
+                    ")",
             "config": dict(workload=args.workload, d1=system.d1, d2=system.d2, N=N, J=J,
                            E_per_gpu=E, kind=kind, alpha=wl["alpha"], fine_tol=FINE_TOL,
                            kappa_scale=meta["kappa_scale"],
+                           contrast=meta.get("contrast_range", meta.get("contrast")),
                            l2="L2 flushed (320 MB write) before every timed step",
                            step="one parareal iteration: fine sweep over N intervals + fused "
                                 "coarse sweep/correction/norm"),
@@ -429,8 +470,13 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
-    _, _, _, meta = load_system(wl["sys"])
-    units = (meta["d1"] + meta["d2"]) * wl["N"] * wl["J"]
+    if "members" in wl:
+        z = np.load(os.path.join(GOLDEN, wl["members"]))
+        dd = z["M11"].shape[1] + z["M22"].shape[1]
+    else:
+        _, _, _, meta = load_system(wl["sys"])
+        dd = meta["d1"] + meta["d2"]
+    units = dd * wl["N"] * wl["J"]
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:
             return

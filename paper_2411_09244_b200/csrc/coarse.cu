@@ -335,7 +335,9 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   size_t base = sizeof(double) * (d + 2 * COARSE_WARPS);
   size_t with_phi = base + sizeof(double) * (size_t)rows_max * d;
   a.phi_in_smem = with_phi <= 200 * 1024;
-  if (!a.phi_in_smem) {  // Phi streamed from HBM every step: use all SMs per step
+  // Large d (Phi not smem-resident) or many members (more member clusters than fit at
+  // once, ~9 clusters of 16): stream Phi from HBM, all SMs per step.
+  if (!a.phi_in_smem || (long long)E * a.cs > 148) {
     coarse_correct_stream(E, d, N, Phi, gvec, X_old, F_hat, G_cache, X_new, partial, diff,
                           active, st);
     return;

@@ -208,7 +208,8 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   double* As = smf;
   double* Bs = smf + STAGES * Cfg::A_TILE;
 
-  const int z = blockIdx.z;
+  const int zt = blockIdx.z;
+  const int sp = zt % p.ksplit, z = zt / p.ksplit;
   const int z1 = z / p.nb2, z2 = z - (z / p.nb2) * p.nb2;
   const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
   const int tid = threadIdx.x;
@@ -217,7 +218,10 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   if (p.nseg > 0) kt0 = (p.seg[0].K + BK - 1) / BK;
   if (p.nseg > 1) kt1 = (p.seg[1].K + BK - 1) / BK;
   if (p.nseg > 2) kt2 = (p.seg[2].K + BK - 1) / BK;
-  const int ntile = kt0 + kt1 + kt2;
+  const int ktot = kt0 + kt1 + kt2;
+  const int kper = (ktot + p.ksplit - 1) / p.ksplit;
+  const int tbeg = min(ktot, sp * kper);
+  const int ntile = min(ktot, tbeg + kper) - tbeg;  // this split's k-tiles
 
   // fixed per-thread chunk coordinates
   constexpr int ACPR = BK / 2;                 // 16-byte chunks per A row
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   const int bkc = tid % BCPR, br = tid / BCPR;
 
   auto load_tile = [&](int t, int slot) {
-    int s = 0, tt = t;
+    int s = 0, tt = t + tbeg;
     if (tt >= kt0) { tt -= kt0; s = 1; if (tt >= kt1) { tt -= kt1; s = 2; } }
     const GemmSeg& sg = p.seg[s];
     const int k0 = tt * BK, K = sg.K;
@@ -313,6 +317,24 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   }
   cp_async_wait<0>();
 
+  if (p.ksplit > 1) {  // raw partial tile -> ws[sp][z][j][i]
+    const int batch = p.nb1 * p.nb2;
+    double* W = p.ws + ((size_t)sp * batch + z) * (size_t)p.M * p.N;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int gi = i0 + wm * 32 + a * 8 + g;
+      if (gi >= p.M) continue;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gj = j0 + wn * 32 + b * 8 + 2 * t4 + h;
+          if (gj < p.N) W[(size_t)gj * p.M + gi] = acc[a][b][h];
+        }
+    }
+    return;
+  }
+
   const long long cb = z1 * p.c_b1 + z2 * p.c_b2;
   double* C = p.C + cb;
   const double* Cin = p.Cin ? p.Cin + cb : nullptr;
@@ -343,6 +365,29 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   }
 }
 
+// Split-K reduction: C = alpha * sum_sp ws[sp] (splits in order) + epilogue.
+__global__ void splitk_reduce_kernel(const __grid_constant__ GemmParams p) {
+  const int batch = p.nb1 * p.nb2;
+  const long long per = (long long)p.M * p.N;
+  const long long total = per * batch;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int z = (int)(t / per);
+    const long long r = t - z * per;
+    const int gj = (int)(r / p.M), gi = (int)(r - (long long)gj * p.M);
+    double v = 0.0;
+    for (int sp = 0; sp < p.ksplit; ++sp) v += p.ws[(size_t)sp * total + t];
+    const int z1 = z / p.nb2, z2 = z - (z / p.nb2) * p.nb2;
+    const long long cb = z1 * p.c_b1 + z2 * p.c_b2;
+    const long long off = cb + gi * p.c_i + gj * p.c_j;
+    if (p.alpha != 1.0) v = __dmul_rn(p.alpha, v);
+    if (p.Cin) v = __dadd_rn(v, p.beta == 1.0 ? p.Cin[off] : __dmul_rn(p.beta, p.Cin[off]));
+    if (p.bias) v = __dadd_rn(v, p.bias[z1 * p.bias_b1 + z2 * p.bias_b2 + gi]);
+    p.C[off] = v;
+    if (p.D) p.D[off] = __dsub_rn(v, p.Xp[off]);
+  }
+}
+
 template <int BM, int BN, int BK, int STAGES, bool BJC>
 static int fast_occupancy() {
   static int occ = -1;
@@ -362,7 +407,7 @@ template <int BM, int BN, int BK, int STAGES, bool BJC>
 static void launch_fast(const GemmParams& p, cudaStream_t st) {
   using Cfg = FastCfg<BM, BN, BK, STAGES, BJC>;
   fast_occupancy<BM, BN, BK, STAGES, BJC>();
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.nb1 * p.nb2);
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.nb1 * p.nb2 * p.ksplit);
   gemm_fast_kernel<BM, BN, BK, STAGES, BJC><<<grid, Cfg::NT, Cfg::SMEM, st>>>(p);
   ++g_launches;
 }
@@ -398,6 +443,7 @@ static double fast_cost(const GemmParams& p, double tile_eff) {
   const int occ = fast_occupancy<BM, BN, BK, STAGES, BJC>();
   if (occ <= 0) return 1e300;
   const double ctas = (double)((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN) * p.nb1 * p.nb2;
+  if (p.N < BN / 2) return 1e300;  // mostly padding
   const double slots = 148.0 * occ;
   const double rounds = std::ceil(ctas / slots);
   // per-round time ~ one CTA's tile work at the SM's share of DMMA throughput
@@ -440,31 +486,59 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
   }
   const long long batch = (long long)p.nb1 * p.nb2;
   const long long tiles64 = (long long)((p.M + 63) / 64) * ((p.N + 63) / 64) * batch;
+  const long long tiles_n32 = (long long)((p.M + 127) / 128) * ((p.N + 31) / 32) * batch;
   static const bool no_fast = getenv("PE_GEMM_GENERIC") != nullptr;
   const int lay = no_fast ? -1 : fast_layout(p);
-  if (lay >= 0 && tiles64 >= 96) {
-    // pick the tile / pipeline variant with the best wave-quantised cost
-    double c[3];
+  // skinny launch (few row tiles x batch): split K over extra CTAs, decided from
+  // (M, K, batch) only so that any column count gives the same arithmetic
+  if (lay >= 0 && p.ws) {
+    const long long mt = (long long)((p.M + 63) / 64) * batch;
+    int ktiles = 0;
+    for (int sgi = 0; sgi < p.nseg; ++sgi) ktiles += (p.seg[sgi].K + 31) / 32;
+    int ks = (int)std::min<long long>(8, 148 / std::max<long long>(1, mt));
+    ks = std::min(ks, ktiles / 4);
+    if (ks >= 2 && (size_t)ks * batch * p.M * p.N <= p.ws_doubles) {
+      GemmParams q = p;
+      q.ksplit = ks;
+      if (lay == 0)
+        launch_fast<64, 64, 32, 3, false>(q, st);
+      else
+        launch_fast<64, 64, 32, 3, true>(q, st);
+      const long long total = (long long)batch * p.M * p.N;
+      splitk_reduce_kernel<<<(int)std::min<long long>(148 * 8, (total + 255) / 256), 256, 0, st>>>(q);
+      ++g_launches;
+      PE_CUDA_CHECK(cudaGetLastError());
+      return;
+    }
+  }
+  if (lay >= 0 && (tiles64 >= 96 || tiles_n32 >= 96)) {
+    // pick the tile / pipeline variant with the best wave-quantised cost (N <= 32:
+    // narrow 128x32 tiles, no wasted half tile)
+    double c[4];
     if (lay == 0) {
       c[0] = fast_cost<64, 64, 32, 3, false>(p, 1.0);
       c[1] = fast_cost<64, 64, 16, 3, false>(p, 0.9);
       c[2] = fast_cost<128, 64, 16, 3, false>(p, 1.05);
+      c[3] = fast_cost<128, 32, 32, 3, false>(p, 0.95);
     } else {
       c[0] = fast_cost<64, 64, 32, 3, true>(p, 1.0);
       c[1] = fast_cost<64, 64, 16, 3, true>(p, 0.9);
       c[2] = fast_cost<128, 64, 16, 3, true>(p, 1.05);
+      c[3] = fast_cost<128, 32, 32, 3, true>(p, 0.95);
     }
     int best = 0;
-    for (int i = 1; i < 3; ++i)
+    for (int i = 1; i < 4; ++i)
       if (c[i] < c[best]) best = i;
     if (lay == 0) {
       if (best == 0) launch_fast<64, 64, 32, 3, false>(p, st);
       else if (best == 1) launch_fast<64, 64, 16, 3, false>(p, st);
-      else launch_fast<128, 64, 16, 3, false>(p, st);
+      else if (best == 2) launch_fast<128, 64, 16, 3, false>(p, st);
+      else launch_fast<128, 32, 32, 3, false>(p, st);
     } else {
       if (best == 0) launch_fast<64, 64, 32, 3, true>(p, st);
       else if (best == 1) launch_fast<64, 64, 16, 3, true>(p, st);
-      else launch_fast<128, 64, 16, 3, true>(p, st);
+      else if (best == 2) launch_fast<128, 64, 16, 3, true>(p, st);
+      else launch_fast<128, 32, 32, 3, true>(p, st);
     }
   } else if (tiles64 >= 2 * 148) {
     launch_cfg<64, 64, 16, 32, 32>(p, ak, bk, st);

@@ -94,6 +94,7 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
   c->Xb.ensure(sizeof(double) * n + 8);
   c->Da.ensure(sizeof(double) * n + 8);
   c->Db.ensure(sizeof(double) * n + 8);
+  c->splitws.ensure(sizeof(double) * 8 * n + 8);
   c->stats = FineStats();
   const double* Xs = X_in;
   const double* Ds = nullptr;  // D_0 = 0 at the interval start (lags reset, stepping.py:180)
@@ -137,6 +138,8 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
     p.c_i = 1;
     p.c_j = d;
     p.c_b1 = (long long)nc * d;
+    p.ws = c->splitws.d();
+    p.ws_doubles = c->splitws.bytes / sizeof(double);
     p.bias = c->cvec.d();
     p.bias_b1 = d;
     if (Dn) {
@@ -171,6 +174,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
   c->nrm.ensure(sizeof(double) * 2 * E * nc * J + 8);
   c->rhist.ensure(sizeof(double) * (size_t)E * nc * max_iter + 8);
+  c->splitws.ensure(sizeof(double) * 8 * (size_t)E * L1 + 8);
   c->counter.ensure(sizeof(int) * 2);
   c->stats = FineStats();
   double* Uc = c->Ux_cur.d();
@@ -217,6 +221,8 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     r0.c_b1 = J * L1;
     r0.Cin = c->R.d();
     r0.beta = 1.0;
+    r0.ws = c->splitws.d();
+    r0.ws_doubles = c->splitws.bytes / sizeof(double);
     pre.push_back(r0);
     GemmParams tf;  // P = S^{-1} R along time (planar re/im per mode)
     tf.M = 2 * J;
@@ -331,7 +337,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   if (graphs) {
     const std::vector<const void*> key = {
         Uc, Un, Wc, Wn, c->R.p, c->P.p, c->Q.p, c->DU.p, c->DW.p, c->V.p, cs, c->nrm.p,
-        c->rhist.p, cnt, host_cnt, c->Bk.p, c->RW.p, c->GW.p, c->Emat.p, c->Finv.p, c->Fw.p,
+        c->rhist.p, cnt, host_cnt, c->splitws.p, c->Bk.p, c->RW.p, c->GW.p, c->Emat.p, c->Finv.p, c->Fw.p,
         c->M11dt.p, c->cg.p, c->f1.p, (const void*)(intptr_t)max_iter,
         (const void*)(intptr_t)(c->use_recur ? 1 : 0),
         (const void*)(intptr_t)(alpha * 1e6), (const void*)(intptr_t)(tol * 1e18)};

@@ -79,7 +79,7 @@ struct pe_ctx {
   // work buffers
   pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs;
   pe::DevBuf Ux_cur, Ux_new, Wx_cur, Wx_new, R, P, Q, DU, DW, V, colstate, counter;
-  pe::DevBuf partial, diff, Gc, active, hist_tmp, nrm, rhist;
+  pe::DevBuf partial, diff, Gc, active, hist_tmp, nrm, rhist, splitws;
   cudaStream_t work = nullptr;           // capture stream for the sweep graphs
   bool use_graphs = true;
   int graph_kernels = 0;   // kernels per captured sweep (launch accounting)

@@ -56,6 +56,12 @@ struct GemmParams {
   long long bias_b1 = 0, bias_b2 = 0;
   double* D = nullptr;          // optional D = C - Xp, same strides as C
   const double* Xp = nullptr;
+  // split-K for skinny launches: partial tiles go to `ws`, a reduction kernel sums the
+  // splits in order and applies the epilogue.  The split factor depends only on
+  // (M, K, batch), never on N (batch invariance).  ws == nullptr disables splitting.
+  double* ws = nullptr;
+  size_t ws_doubles = 0;
+  int ksplit = 1;  // set by gemm_f64
 };
 
 // Launch; chooses tile shape and the k-/j-contiguous loader variant from strides.

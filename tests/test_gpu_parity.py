@@ -477,3 +477,56 @@ def test_large_d_streaming_coarse_and_parareal():
                               fine_tol=1e-12)
         assert run.iterations == ref["iterations"]
         assert rel_rows(np.array(run.history), np.array(ref["history"])) < REL
+
+
+def _data(name):
+    import os
+
+    from tests.conftest import ROOT
+
+    path = os.path.join(ROOT, "data", name)
+    if not os.path.exists(path):
+        pytest.skip(f"data/{name} not built (oracle/build_cfg3.py / build_cfg4.py)")
+    return np.load(path)
+
+
+def test_config3_sampled_intervals():
+    """BASELINE config 3 (d = 4096+4096, J = 100): WR on sampled iteration-1 intervals with
+    a 3-sweep cap equals the CPU oracle (full reference runs are infeasible)."""
+    P = _pkg()
+    z = _data("sys_cfg3.npz")
+    gz = golden("cfg3_sample.npz")
+    s, ld = _system(z)
+    J, N, T = 100, 128, 2.0
+    wr = P.WaveformRelaxation(s, J, T / N, 0.1, ld, tol=1e-12, max_iter=int(gz["sweeps"]))
+    d1 = s.d1
+    states = [P.SplitState.fresh(gz[f"x_{n}"][:d1], gz[f"x_{n}"][d1:], n * T / N)
+              for n in gz["sample"]]
+    res = wr.solve_all(states)
+    for n, r in zip(gz["sample"], res):
+        assert r.iterations == int(gz["sweeps"]) and r.stop_reason == "max_iter"
+        assert rel_rows(r.trajectory.final.stacked(), gz[f"final_{n}"]) < REL
+        assert rel_rows(r.trajectory.U[5], gz[f"U5_{n}"]) < REL
+        np.testing.assert_allclose(r.residuals, gz[f"res_{n}"], rtol=1e-8)
+
+
+def test_config4_ensemble_iterations_and_histories():
+    """BASELINE config 4: 64 members (contrast 1e2..1e8) in one batch; every member's
+    parareal iteration count equals the reference's, four members' histories within 1e-10."""
+    P = _pkg()
+    zm = _data("cfg4_members.npz")
+    zr = _data("cfg4_runs.npz")
+    E = zm["f1"].shape[0]
+    systems = [P.CoarseSystem(*(zm[k][m] for k in ("M11", "A11", "M12", "A12", "M22", "A22")))
+               for m in range(E)]
+    loads = [P.ConstantLoads(zm["f1"][m], zm["f2"][m]) for m in range(E)]
+    d1, d2 = systems[0].d1, systems[0].d2
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(1.0, 32, 32), alpha=0.1, epsilon=1e-8, k_max=32,
+                           fine_kind="sequential", stop_rule="relative")
+    runs = P.run_parareal_ensemble(cfg, systems, loads,
+                                   [P.SplitState.fresh(np.zeros(d1), np.zeros(d2))] * E)
+    its = np.array([r.iterations for r in runs])
+    np.testing.assert_array_equal(its, zr["iterations"])
+    assert all(r.converged for r in runs)
+    for m in (0, 1, 2, 3):
+        assert rel_rows(np.array(runs[m].history), zr[f"hist_{m}"]) < REL
