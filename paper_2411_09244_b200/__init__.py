@@ -10,7 +10,8 @@ from .allatonce import (TimeMatrixB, WaveformRelaxation, WRResult,  # noqa: F401
                         build_time_matrix, wr_fine_solve)
 from .engine import PeContext  # noqa: F401
 from .msbasis import CoarseSystem  # noqa: F401
-from .parareal import (AllAtOnceFine, ParerealConfig, ParerealRun,  # noqa: F401
+from .parareal import (AllAtOnceFine, ParerealConfig, ParerealEnsemble,  # noqa: F401
+                       ParerealRun,
                        SequentialFine, build_fine_propagator, check_stop, initial_sweep,
                        max_state_diff, run_parareal, run_parareal_ensemble)
 from .stepping import (ConstantLoads, SplitPropagators, SplitState,  # noqa: F401

@@ -47,6 +47,32 @@ struct CoarseArgs {
   const int* active;   // (E) or null
 };
 
+__device__ __forceinline__ unsigned cs_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned cs_map_rank(unsigned a, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cs_st_async(unsigned addr, double v, unsigned bar) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+               ::"r"(addr), "l"(__double_as_longlong(v)), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void cs_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cs_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+
+// x_{n+1} rows travel point to point: each new row is pushed (st.async, 8 bytes) into
+// every peer's double-buffered x with complete_tx on the peer's mbarrier; a CTA waits
+// only for the d*8 bytes of the step it consumes (same protocol as recur.cu).
 __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_constant__ CoarseArgs a) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -58,7 +84,7 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
   double* X_new = a.X_new + (long long)e * (N + 1) * d;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (a.active && a.active[e] == 0) {  // converged member: iterate frozen
+  if (a.active && a.active[e] == 0) {  // converged member: iterate frozen (whole cluster)
     for (long long t = threadIdx.x; t < (long long)(N + 1) * nrows; t += COARSE_THREADS) {
       const int n = (int)(t / nrows), r = r0 + (int)(t % nrows);
       X_new[(long long)n * d + r] = X_old[(long long)n * d + r];
@@ -66,10 +92,11 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
     return;
   }
 
-  extern __shared__ double sm[];
-  double* xs = sm;                    // d
-  double* wpart = xs + d;             // COARSE_WARPS * 2
+  extern __shared__ __align__(16) double sm[];
+  double* xs2 = sm;                         // 2 x d
+  double* wpart = xs2 + 2 * d;              // COARSE_WARPS * 2
   double* phis = wpart + 2 * COARSE_WARPS;  // nrows * d (optional)
+  __shared__ __align__(8) unsigned long long mbar[2];
   const double* Phi = a.Phi + (long long)e * d * d;
   const double* gv = a.gvec + (long long)e * d;
   const double* F = a.F_hat ? a.F_hat + (long long)e * N * d : nullptr;
@@ -79,26 +106,50 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
     const double* src = Phi + (long long)r0 * d;
     for (long long t = threadIdx.x; t < (long long)nrows * d; t += COARSE_THREADS) phis[t] = src[t];
   }
-  for (int k = threadIdx.x; k < d; k += COARSE_THREADS) xs[k] = X_old[k];
+  for (int k = threadIdx.x; k < d; k += COARSE_THREADS) xs2[k] = X_old[k];
   for (int r = r0 + threadIdx.x; r < r1; r += COARSE_THREADS) X_new[r] = X_old[r];
-  __syncthreads();
+  const unsigned bytes = (unsigned)(d * 8);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cs_smem_u32(&mbar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cs_smem_u32(&mbar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster.sync();
+  if (threadIdx.x == 0) {
+    cs_expect(cs_smem_u32(&mbar[1]), bytes);            // x_1 (pushed at step 0)
+    if (N > 2) cs_expect(cs_smem_u32(&mbar[0]), bytes);  // x_2 (pushed at step 1)
+  }
+  const unsigned bar0 = cs_smem_u32(&mbar[0]);
+  const unsigned xs_base = cs_smem_u32(xs2);
 
-  for (int n = 0; n < N; ++n) {
-    double sd = 0.0, sn = 0.0;  // this warp's partial ||x_new - x_old||^2, ||x_new||^2
-    // prefetch this warp's per-row operands across lanes (lane i <-> i-th row of the warp)
-    double pf_f = 0.0, pf_g = 0.0, pf_b = 0.0, pf_o = 0.0;
-    {
-      const int rr = warp + COARSE_WARPS * lane;
-      if (rr < nrows) {
-        const long long o = (long long)n * d + r0 + rr;
-        pf_b = gv[r0 + rr];
-        pf_o = X_old[o + d];
-        if (F) {
-          pf_f = F[o];
-          pf_g = Gc[o];
-        }
+  // per-row operands of step n (lane i <-> i-th row of the warp), fetched one step
+  // ahead so their L2 latency hides under the previous step
+  double nf_f = 0.0, nf_g = 0.0, nf_b = 0.0, nf_o = 0.0;
+  auto prefetch = [&](int n) {
+    const int rr = warp + COARSE_WARPS * lane;
+    if (n < N && rr < nrows) {
+      const long long o = (long long)n * d + r0 + rr;
+      nf_b = gv[r0 + rr];
+      nf_o = X_old[o + d];
+      if (F) {
+        nf_f = F[o];
+        nf_g = Gc[o];
       }
     }
+  };
+  prefetch(0);
+  for (int n = 0; n < N; ++n) {
+    const int cur = n & 1;
+    if (n > 0) {
+      cs_wait(bar0 + 8 * cur, ((n - 1) >> 1) & 1);
+      if (threadIdx.x == 0 && n + 2 < N) cs_expect(bar0 + 8 * cur, bytes);
+    }
+    const double* xs = xs2 + (size_t)cur * d;
+    double sd = 0.0, sn = 0.0;  // this warp's partial ||x_new - x_old||^2, ||x_new||^2
+    const double pf_f = nf_f, pf_g = nf_g, pf_b = nf_b, pf_o = nf_o;
+    const bool push = (n + 1 < N);
+    const unsigned nbar = bar0 + 8 * ((n + 1) & 1);
+    const unsigned nbuf = xs_base + (unsigned)(((n + 1) & 1) * d * 8);
     int i = 0;
     for (int rr = warp; rr < nrows; rr += COARSE_WARPS, ++i) {
       const int r = r0 + rr;
@@ -119,20 +170,21 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
           fg = Gc[o];
         }
       }
+      // every lane holds the warp sum: compute the row's value redundantly
+      const double g = acc + fb;
+      const double x = F ? ff + (g - fg) : g;
       if (lane == 0) {
-        const double g = acc + fb;
-        double x;
-        if (F)
-          x = ff + (g - fg);
-        else
-          x = g;
         Gc[o] = g;
         X_new[o + d] = x;
         const double df = x - xo;
         sd += df * df;
         sn += x * x;
       }
+      if (push)  // lane q pushes row r of x_{n+1} into CTA q
+        for (int q = lane; q < a.cs; q += 32)
+          cs_st_async(cs_map_rank(nbuf + (unsigned)(r * 8), q), x, cs_map_rank(nbar, q));
     }
+    prefetch(n + 1);
     if (lane == 0) {
       wpart[2 * warp] = sd;
       wpart[2 * warp + 1] = sn;
@@ -148,23 +200,9 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
       p[0] = td;
       p[1] = tn;
     }
-    cluster.sync();  // publishes X_new[n+1] (release/acquire at cluster scope)
-    const double* xn = X_new + (long long)(n + 1) * d;
-    for (int base = 0; base < d; base += 4 * COARSE_THREADS) {  // 4 loads in flight per thread
-      double v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int k = base + u * COARSE_THREADS + threadIdx.x;
-        v[u] = k < d ? __ldcg(xn + k) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int k = base + u * COARSE_THREADS + threadIdx.x;
-        if (k < d) xs[k] = v[u];
-      }
-    }
-    __syncthreads();
+    __syncthreads();  // wpart reused next step
   }
+  cluster.sync();  // partials published; no CTA exits with pushes in flight
 
   if (rank == 0 && threadIdx.x == 0 && a.diff) {
     double md = 0.0, mn = 0.0;
@@ -183,7 +221,6 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
     a.diff[2 * e + 1] = mn;
   }
 }
-
 
 // ---------------------------------------------------------------------------------------
 // Large-d path (Phi slice does not fit in a cluster's shared memory, e.g. config 3 with
@@ -332,7 +369,7 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   a.N = N;
   a.cs = coarse_cluster_size(d);
   const int rows_max = (d + a.cs - 1) / a.cs;
-  size_t base = sizeof(double) * (d + 2 * COARSE_WARPS);
+  size_t base = sizeof(double) * (2 * d + 2 * COARSE_WARPS);
   size_t with_phi = base + sizeof(double) * (size_t)rows_max * d;
   a.phi_in_smem = with_phi <= 200 * 1024;
   // Large d (Phi not smem-resident) or many members (more member clusters than fit at

@@ -317,9 +317,10 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   }
   cp_async_wait<0>();
 
-  if (p.ksplit > 1) {  // raw partial tile -> ws[sp][z][j][i]
+  if (p.ksplit > 1) {  // raw partial tile -> ws[sp][z][j][i]; splitk_reduce_kernel finishes
     const int batch = p.nb1 * p.nb2;
-    double* W = p.ws + ((size_t)sp * batch + z) * (size_t)p.M * p.N;
+    const size_t plane = (size_t)batch * p.M * p.N;
+    double* W = p.ws + (size_t)sp * plane + (size_t)z * p.M * p.N;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       const int gi = i0 + wm * 32 + a * 8 + g;

@@ -44,6 +44,13 @@ static void require(bool ok, int code, const char* msg) {
 
 static void bind(pe_ctx* c) { PE_CUDA_CHECK(cudaSetDevice(c->device)); }
 
+// Split-K workspace: partial planes + per-tile tickets that must start (and are left) zero.
+static void ensure_zeroed(DevBuf& b, size_t bytes) {
+  if (bytes <= b.bytes) return;
+  b.ensure(bytes);
+  PE_CUDA_CHECK(cudaMemset(b.p, 0, b.bytes));
+}
+
 // Launch `fn` (one DMMA-class kernel doing `flops` algorithmic flops) with optional
 // per-launch CUDA-event timing (bench roofline pass).
 template <class F>
@@ -94,7 +101,7 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
   c->Xb.ensure(sizeof(double) * n + 8);
   c->Da.ensure(sizeof(double) * n + 8);
   c->Db.ensure(sizeof(double) * n + 8);
-  c->splitws.ensure(sizeof(double) * 8 * n + 8);
+  ensure_zeroed(c->splitws, sizeof(double) * (8 * n + 32768));
   c->stats = FineStats();
   const double* Xs = X_in;
   const double* Ds = nullptr;  // D_0 = 0 at the interval start (lags reset, stepping.py:180)
@@ -174,7 +181,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
   c->nrm.ensure(sizeof(double) * 2 * E * nc * J + 8);
   c->rhist.ensure(sizeof(double) * (size_t)E * nc * max_iter + 8);
-  c->splitws.ensure(sizeof(double) * 8 * (size_t)E * L1 + 8);
+  ensure_zeroed(c->splitws, sizeof(double) * (8 * (size_t)E * L1 + 32768));
   c->counter.ensure(sizeof(int) * 2);
   c->stats = FineStats();
   double* Uc = c->Ux_cur.d();

@@ -216,25 +216,41 @@ def run_parareal(config: ParerealConfig, propagators: SplitPropagators, fine,
                       time.perf_counter() - t0)[0]
 
 
+class ParerealEnsemble:
+    """E independent problems of equal (d1, d2) solved as one batch (BASELINE config 4).
+
+    Construction uploads the members and factorises (setup, outside any timed region);
+    `run(initials)` runs the device-resident parareal loop for all members at once.  Each
+    member stops on its own rule and its iterate is frozen afterwards, so every run equals
+    the single-member run.
+    """
+
+    def __init__(self, config: ParerealConfig, systems, loads, device: int | None = None):
+        if config.fine_kind not in ("sequential", "all-at-once"):
+            raise ValueError(f"unknown fine propagator kind {config.fine_kind!r}")
+        if config.stop_rule not in ("absolute", "relative"):
+            raise ValueError(f"unknown stop rule {config.stop_rule!r}")
+        self.config = config
+        self.d1 = systems[0].d1
+        tg = config.time_grid
+        self.ctx = PeContext(systems, loads, tg.substeps, device)
+        self.ctx.prepare_coarse(tg.dt)
+        if config.fine_kind == "sequential":
+            self.ctx.prepare_sequential(tg.dt_sub)
+        else:
+            self.ctx.prepare_allatonce(tg.dt_sub, config.alpha, config.resolved_fine_tol(),
+                                       config.fine_max_iter)
+
+    def run(self, initials):
+        cfg = self.config
+        t0 = time.perf_counter()
+        X0 = self.ctx.to_dev(np.array([s.stacked() for s in initials]))
+        res = self.ctx.parareal(cfg.fine_kind, cfg.time_grid.n_intervals, X0, cfg.k_max,
+                                cfg.epsilon, cfg.stop_rule)
+        return _runs_from(res, cfg, self.d1, cfg.fine_kind, time.perf_counter() - t0)
+
+
 def run_parareal_ensemble(config: ParerealConfig, systems, loads, initials,
                           device: int | None = None):
-    """E independent problems of equal (d1, d2) as one batch (BASELINE config 4).
-
-    Returns one ParerealRun per member; each member stops on its own rule and its
-    iterate is frozen afterwards, so every run equals the single-member run.
-    """
-    tg = config.time_grid
-    t0 = time.perf_counter()
-    ctx = PeContext(systems, loads, tg.substeps, device)
-    ctx.prepare_coarse(tg.dt)
-    if config.fine_kind == "sequential":
-        ctx.prepare_sequential(tg.dt_sub)
-    elif config.fine_kind == "all-at-once":
-        ctx.prepare_allatonce(tg.dt_sub, config.alpha, config.resolved_fine_tol(),
-                              config.fine_max_iter)
-    else:
-        raise ValueError(f"unknown fine propagator kind {config.fine_kind!r}")
-    X0 = ctx.to_dev(np.array([s.stacked() for s in initials]))
-    res = ctx.parareal(config.fine_kind, tg.n_intervals, X0, config.k_max, config.epsilon,
-                       config.stop_rule)
-    return _runs_from(res, config, systems[0].d1, config.fine_kind, time.perf_counter() - t0)
+    """One-shot ensemble solve (setup + run); see ParerealEnsemble."""
+    return ParerealEnsemble(config, systems, loads, device).run(initials)
