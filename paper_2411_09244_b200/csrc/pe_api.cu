@@ -173,8 +173,9 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   c->Wx_cur.ensure(sizeof(double) * E * (J + 2) * L2 + 8);
   c->Wx_new.ensure(sizeof(double) * E * (J + 2) * L2 + 8);
   c->R.ensure(sizeof(double) * E * J * L1 + 8);
-  c->P.ensure(sizeof(double) * E * 2 * J * L1 + 8);
-  c->Q.ensure(sizeof(double) * E * 2 * J * L1 + 8);
+  const int nk = c->wr_nk;  // half-spectrum modes
+  c->P.ensure(sizeof(double) * E * 2 * nk * L1 + 8);
+  c->Q.ensure(sizeof(double) * E * 2 * nk * L1 + 8);
   c->DU.ensure(sizeof(double) * E * J * L1 + 8);
   c->DW.ensure(sizeof(double) * E * J * L2 + 8);
   c->V.ensure(sizeof(double) * E * L1 + 8);
@@ -231,8 +232,8 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     r0.ws = c->splitws.d();
     r0.ws_doubles = c->splitws.bytes / sizeof(double);
     pre.push_back(r0);
-    GemmParams tf;  // P = S^{-1} R along time (planar re/im per mode)
-    tf.M = 2 * J;
+    GemmParams tf;  // P = S^{-1} R along time (planar re/im per mode, modes 0..nk-1)
+    tf.M = 2 * nk;
     tf.N = (int)L1;
     tf.nb1 = E;
     tf.nseg = 1;
@@ -242,12 +243,12 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     tf.C = c->P.d();
     tf.c_i = L1;
     tf.c_j = 1;
-    tf.c_b1 = 2 * J * L1;
+    tf.c_b1 = 2 * nk * L1;
     pre.push_back(tf);
     GemmParams sh;  // Q_k = (d_k M11 + A11)^{-1} P_k   (einsum, allatonce.py:118)
     sh.M = d1;
     sh.N = nc;
-    sh.nb1 = E * J;
+    sh.nb1 = E * nk;
     sh.nb2 = 2;
     sh.nseg = 2;
     sh.seg[0].A = Operand{c->Bk.d(), 2LL * d1, 1, 4LL * d1 * d1, 2LL * d1 * d1};
@@ -262,14 +263,14 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     sh.c_b1 = 2 * L1;
     sh.c_b2 = L1;
     pre.push_back(sh);
-    GemmParams tb;  // U = Re(S Q)
+    GemmParams tb;  // U = Re(S Q), conjugate pairs folded into the weights
     tb.M = J;
     tb.N = (int)L1;
     tb.nb1 = E;
     tb.nseg = 1;
-    tb.seg[0].A = Operand{c->Fw.d(), 2LL * J, 1, 0, 0};
-    tb.seg[0].B = Operand{c->Q.d(), L1, 1, 2 * J * L1, 0};
-    tb.seg[0].K = 2 * J;
+    tb.seg[0].A = Operand{c->Fw.d(), 2LL * nk, 1, 0, 0};
+    tb.seg[0].B = Operand{c->Q.d(), L1, 1, 2 * nk * L1, 0};
+    tb.seg[0].K = 2 * nk;
     tb.C = Un + 2 * L1;
     tb.c_i = L1;
     tb.c_j = 1;
@@ -347,7 +348,8 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
         c->rhist.p, cnt, host_cnt, c->splitws.p, c->Bk.p, c->RW.p, c->GW.p, c->Emat.p, c->Finv.p, c->Fw.p,
         c->M11dt.p, c->cg.p, c->f1.p, (const void*)(intptr_t)max_iter,
         (const void*)(intptr_t)(c->use_recur ? 1 : 0),
-        (const void*)(intptr_t)(alpha * 1e6), (const void*)(intptr_t)(tol * 1e18)};
+        (const void*)(intptr_t)(alpha * 1e6), (const void*)(intptr_t)(tol * 1e18),
+        (const void*)(intptr_t)nk};
     sg = &c->sweep_graphs[nc];
     if (sg->key != key) {
       for (auto& ex : sg->exec)

@@ -74,6 +74,7 @@ struct pe_ctx {
   bool wr_ready = false;
   double wr_dt = 0, wr_alpha = 0, wr_tol = 0;
   int wr_max_iter = 0;
+  int wr_nk = 0;  // solved time modes (half spectrum, floor(J/2) + 1)
   pe::DevBuf Bk, RW, M11dt, GW, cg, Emat, Finv, Fw;
 
   // work buffers

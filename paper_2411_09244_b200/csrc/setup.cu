@@ -280,11 +280,17 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
   const int d1 = c->d1, d2 = c->d2, J = c->J, E = c->E;
   cudaStream_t st = c->setup_stream;
   cublasHandle_t h = c->blas;
+  // Half spectrum: the WR right-hand side is real, Finv[J-k, s] = conj(Finv[k, s]) and
+  // d_{J-k} = conj(d_k), so Q_{J-k} = conj(Q_k).  Only modes k = 0..floor(J/2) are solved;
+  // the backward transform weights each conjugate pair by 2 (k = 0 and k = J/2 are real).
+  const int nk = J / 2 + 1;
+  c->wr_nk = nk;
   // time transforms (host, exact index reduction k*s mod J)
   {
-    std::vector<double> finv((size_t)2 * J * J), fw((size_t)J * 2 * J);
+    std::vector<double> finv((size_t)2 * nk * J), fw((size_t)J * 2 * nk);
     const double two_pi = 6.283185307179586476925286766559;
-    for (int k = 0; k < J; ++k)
+    for (int k = 0; k < nk; ++k) {
+      const double wgt = (k == 0 || 2 * k == J) ? 1.0 : 2.0;
       for (int s = 0; s < J; ++s) {
         const long long ks = ((long long)k * s) % J;
         const double ang = two_pi * (double)ks / (double)J;
@@ -293,16 +299,17 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
         // S^{-1}: p_k = (1/J) sum_s e^{-i ang} alpha^{s/J} r_s
         finv[(size_t)(2 * k) * J + s] = lam_inv * std::cos(ang) / J;
         finv[(size_t)(2 * k + 1) * J + s] = -lam_inv * std::sin(ang) / J;
-        // Re(S q)_s = sum_k alpha^{-s/J} (cos ang Re q_k - sin ang Im q_k)
-        fw[(size_t)s * 2 * J + 2 * k] = lam * std::cos(ang);
-        fw[(size_t)s * 2 * J + 2 * k + 1] = -lam * std::sin(ang);
+        // Re(S q)_s = sum_k alpha^{-s/J} (cos ang Re q_k - sin ang Im q_k), pairs folded
+        fw[(size_t)s * 2 * nk + 2 * k] = wgt * lam * std::cos(ang);
+        fw[(size_t)s * 2 * nk + 2 * k + 1] = -wgt * lam * std::sin(ang);
       }
+    }
     c->Finv.ensure(sizeof(double) * finv.size());
     c->Fw.ensure(sizeof(double) * fw.size());
     PE_CUDA_CHECK(cudaMemcpy(c->Finv.p, finv.data(), sizeof(double) * finv.size(), cudaMemcpyHostToDevice));
     PE_CUDA_CHECK(cudaMemcpy(c->Fw.p, fw.data(), sizeof(double) * fw.size(), cudaMemcpyHostToDevice));
   }
-  c->Bk.ensure(sizeof(double) * (size_t)E * J * 4 * d1 * d1 + 8);
+  c->Bk.ensure(sizeof(double) * (size_t)E * nk * 4 * d1 * d1 + 8);
   c->RW.ensure(sizeof(double) * (size_t)E * d1 * 2 * d2 + 8);
   c->M11dt.ensure(sizeof(double) * (size_t)E * d1 * d1 + 8);
   c->GW.ensure(sizeof(double) * (size_t)E * d2 * 2 * d1 + 8);
@@ -322,7 +329,7 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
     const double* A22 = c->A22.d() + (size_t)e * d2 * d2;
     const double* f2 = c->f2.d() + (size_t)e * d2;
     if (d1) {
-      for (int k = 0; k < J; ++k) {
+      for (int k = 0; k < nk; ++k) {
         // d_k = (1 - alpha^{1/J} e^{-2 pi i k/J}) / dt   (allatonce.py:58-62)
         const double ang = -6.283185307179586476925286766559 * (double)k / J;
         const double dre = (1.0 - om_r * std::cos(ang)) / dt;
@@ -331,7 +338,7 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
             d1, dre, dim, M11, A11, (cuDoubleComplex*)S.p);
         zinverse(c, d1, (cuDoubleComplex*)S.p, (cuDoubleComplex*)Sinv.p, ipiv, info, work);
         realify_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
-            d1, (const cuDoubleComplex*)Sinv.p, c->Bk.d() + ((size_t)e * J + k) * 4 * d1 * d1);
+            d1, (const cuDoubleComplex*)Sinv.p, c->Bk.d() + ((size_t)e * nk + k) * 4 * d1 * d1);
         PE_CUDA_CHECK(cudaGetLastError());
       }
       double* RW = c->RW.d() + (size_t)e * d1 * 2 * d2;
