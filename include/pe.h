@@ -135,10 +135,10 @@ int pe_parareal_run(pe_ctx* ctx, int kind, int N, const double* X0, int k_max,
                     void* stream);
 
 /* The FP64 DMMA GEMM underneath every contraction, exposed for kernel tests:
- * C(i,j) = sum_k A(i,k) B(k,j) with element strides (device pointers). */
-int pe_gemm_f64(int M, int N, int K, const double* A, long long a_i, long long a_k,
-                const double* B, long long b_k, long long b_j, double* C, long long c_i,
-                long long c_j, void* stream);
+ * C[b](i,j) = sum_k A[b](i,k) B[b](k,j), element and batch strides (device pointers). */
+int pe_gemm_f64(int M, int N, int K, int batch, const double* A, long long a_i, long long a_k,
+                long long a_b, const double* B, long long b_k, long long b_j, long long b_b,
+                double* C, long long c_i, long long c_j, long long c_b, void* stream);
 
 /* Launch counter: number of libpe kernels launched since context creation
  * (bench/driver evidence that the native path ran). */

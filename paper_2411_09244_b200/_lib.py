@@ -50,8 +50,9 @@ SIGNATURES = {
     "pe_coarse_correct": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
     "pe_parareal_run": (C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int, C.c_double, C.c_int, _P,
                                   _D, _I, _I, _P, _P, _P, _F, _F, _I, _P]),
-    "pe_gemm_f64": (C.c_int, [C.c_int, C.c_int, C.c_int, _P, C.c_longlong, C.c_longlong, _P,
-                              C.c_longlong, C.c_longlong, _P, C.c_longlong, C.c_longlong, _P]),
+    "pe_gemm_f64": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P, C.c_longlong,
+                              C.c_longlong, C.c_longlong, _P, C.c_longlong, C.c_longlong,
+                              C.c_longlong, _P, C.c_longlong, C.c_longlong, C.c_longlong, _P]),
     "pe_parareal_iterate": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P,
                                       _P]),
     "pe_set_profiling": (C.c_int, [_P, C.c_int]),

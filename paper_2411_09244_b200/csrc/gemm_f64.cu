@@ -515,21 +515,11 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
   if (lay >= 0 && (tiles64 >= 96 || tiles_n32 >= 96)) {
     // pick the tile / pipeline variant with the best wave-quantised cost (N <= 32:
     // narrow 128x32 tiles, no wasted half tile)
-    double c[4];
-    if (lay == 0) {
-      c[0] = fast_cost<64, 64, 32, 3, false>(p, 1.0);
-      c[1] = fast_cost<64, 64, 16, 3, false>(p, 0.9);
-      c[2] = fast_cost<128, 64, 16, 3, false>(p, 1.05);
-      c[3] = fast_cost<128, 32, 32, 3, false>(p, 0.95);
-    } else {
-      c[0] = fast_cost<64, 64, 32, 3, true>(p, 1.0);
-      c[1] = fast_cost<64, 64, 16, 3, true>(p, 0.9);
-      c[2] = fast_cost<128, 64, 16, 3, true>(p, 1.05);
-      c[3] = fast_cost<128, 32, 32, 3, true>(p, 0.95);
-    }
-    int best = 0;
-    for (int i = 1; i < 4; ++i)
-      if (c[i] < c[best]) best = i;
+    // measured on B200 (tools/gemm_bench.py): 64x64 / BK16 / 3 stages (3 CTAs/SM) is the
+    // best variant on every hot-path shape except N <= 32 (128x32 tiles)
+    int best = (p.N <= 32) ? 3 : 1;
+    static const int forced = getenv("PE_GEMM_VARIANT") ? atoi(getenv("PE_GEMM_VARIANT")) : -1;
+    if (forced >= 0 && forced < 4) best = forced;  // tuning experiments only
     if (lay == 0) {
       if (best == 0) launch_fast<64, 64, 32, 3, false>(p, st);
       else if (best == 1) launch_fast<64, 64, 16, 3, false>(p, st);

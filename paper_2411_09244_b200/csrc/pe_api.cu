@@ -193,6 +193,9 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   int* cnt = c->counter.i();
 
   wr_init(E, nc, d1, d2, J, alpha, X_in, Uc, Un, Wc, Wn, c->V.d(), cs, c->rhist.d(), max_iter, st);
+  // W is seeded constant in time, so DW = W_s - W_{s-1} starts at zero; afterwards the
+  // commit kernel maintains it for the intervals it commits
+  if (d1 && d2) PE_CUDA_CHECK(cudaMemsetAsync(c->DW.p, 0, sizeof(double) * E * J * L2, st));
 
   // sweep recipe (GEMM parameter blocks are loop-invariant)
   std::vector<GemmParams> pre, post;
@@ -322,7 +325,6 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   int* host_cnt = c->pinned_count;
   auto body = [&](int par, cudaStream_t s) {
     PE_CUDA_CHECK(cudaMemsetAsync(cnt + par, 0, sizeof(int), s));
-    if (d1 && d2) wr_diff_u(E, nc, d2, J, Wc, c->DW.d(), s);  // DW_s = Wx[s+1] - Wx[s]
     for (auto& p : pre) run_gemm(c, p, s);
     if (d1) wr_diff_u(E, nc, d1, J, Un, c->DU.d(), s);
     if (d2) {
@@ -333,7 +335,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
                  [&] { recur_wr(E, d2, nc, J, c->Emat.d(), Wn, s); });
     }
     wr_commit(E, nc, d1, d2, J, alpha, tol, max_iter, 0, Uc, Un, Wc, Wn, c->V.d(), cs,
-              c->rhist.d(), cnt + par, c->nrm.d(), s);
+              c->rhist.d(), cnt + par, c->nrm.d(), (d1 && d2) ? c->DW.d() : nullptr, s);
     PE_CUDA_CHECK(cudaMemcpyAsync(host_cnt + par, cnt + par, sizeof(int), cudaMemcpyDeviceToHost, s));
   };
   // CUDA graphs (one per counter parity) replace the per-sweep host launch sequence when
@@ -393,7 +395,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   };
   if (sg)  // kernels per graph replay, for the native-launch evidence counter
     c->graph_kernels = (int)(pre.size() + (d2 ? 1 + post.size() + (use_rw ? 1 : 0) : 0) +
-                             (d1 && d2 ? 1 : 0) + (d1 ? 1 : 0) + 2);
+                             (d1 ? 1 : 0) + 2);
   int sweep = 0;
   enqueue_sweep(0);
   for (sweep = 1; sweep <= max_iter; ++sweep) {
@@ -760,21 +762,23 @@ int pe_set_profiling(pe_ctx* c, int on) {
   });
 }
 
-int pe_gemm_f64(int M, int N, int K, const double* A, long long a_i, long long a_k,
-                const double* B, long long b_k, long long b_j, double* C, long long c_i,
-                long long c_j, void* stream) {
+int pe_gemm_f64(int M, int N, int K, int batch, const double* A, long long a_i, long long a_k,
+                long long a_b, const double* B, long long b_k, long long b_j, long long b_b,
+                double* C, long long c_i, long long c_j, long long c_b, void* stream) {
   return guarded([&] {
-    require(M >= 0 && N >= 0 && K >= 0 && C, PE_ERR_ARG, "bad gemm arguments");
+    require(M >= 0 && N >= 0 && K >= 0 && batch >= 1 && C, PE_ERR_ARG, "bad gemm arguments");
     GemmParams p;
     p.M = M;
     p.N = N;
+    p.nb1 = batch;
     p.nseg = K > 0 ? 1 : 0;
-    p.seg[0].A = Operand{A, a_i, a_k, 0, 0};
-    p.seg[0].B = Operand{B, b_k, b_j, 0, 0};
+    p.seg[0].A = Operand{A, a_i, a_k, a_b, 0};
+    p.seg[0].B = Operand{B, b_k, b_j, b_b, 0};
     p.seg[0].K = K;
     p.C = C;
     p.c_i = c_i;
     p.c_j = c_j;
+    p.c_b1 = c_b;
     gemm_f64(p, (cudaStream_t)stream);
   });
 }

@@ -114,6 +114,14 @@ __global__ void realify_kernel(int n, const cuDoubleComplex* inv, double* B) {
   }
 }
 
+// Re(inv) into diagonal block `which` of a (2n x 2n) row-major block matrix (real modes)
+__global__ void real_block_kernel(int n, const cuDoubleComplex* inv, double* B, int which) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long n2 = 2LL * n, o = (long long)which * n;
+  for (; t < (long long)n * n; t += (long long)gridDim.x * blockDim.x)
+    B[(t / n + o) * n2 + o + t % n] = cuCreal(inv[t]);
+}
+
 static int grid_for(long long n) { return (int)std::max<long long>(1, std::min<long long>(4096, (n + 255) / 256)); }
 
 // Ainv = A^{-1} for a row-major n x n buffer (inv(A^T) = inv(A)^T, so the
@@ -280,28 +288,46 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
   const int d1 = c->d1, d2 = c->d2, J = c->J, E = c->E;
   cudaStream_t st = c->setup_stream;
   cublasHandle_t h = c->blas;
-  // Half spectrum: the WR right-hand side is real, Finv[J-k, s] = conj(Finv[k, s]) and
-  // d_{J-k} = conj(d_k), so Q_{J-k} = conj(Q_k).  Only modes k = 0..floor(J/2) are solved;
-  // the backward transform weights each conjugate pair by 2 (k = 0 and k = J/2 are real).
-  const int nk = J / 2 + 1;
-  c->wr_nk = nk;
-  // time transforms (host, exact index reduction k*s mod J)
+  // Half spectrum in half-complex packing.  The WR right-hand side is real, so
+  // Finv[J-k, s] = conj(Finv[k, s]) and d_{J-k} = conj(d_k): Q_{J-k} = conj(Q_k).  Only modes
+  // k = 0..floor(J/2) are solved, as npm = ceil(J/2) "pseudo-modes" of two planes each:
+  // pseudo-mode 0 carries the real modes k = 0 and (J even) k = J/2, pseudo-mode m >= 1 the
+  // re/im planes of mode m.  The transforms are then exactly J (even J) rows deep, and the
+  // backward transform weights each conjugate pair by 2.
+  const int npm = (J + 1) / 2;
+  const bool even = (J % 2) == 0;
+  c->wr_nk = npm;
   {
-    std::vector<double> finv((size_t)2 * nk * J), fw((size_t)J * 2 * nk);
+    std::vector<double> finv((size_t)2 * npm * J, 0.0), fw((size_t)J * 2 * npm, 0.0);
     const double two_pi = 6.283185307179586476925286766559;
-    for (int k = 0; k < nk; ++k) {
-      const double wgt = (k == 0 || 2 * k == J) ? 1.0 : 2.0;
-      for (int s = 0; s < J; ++s) {
-        const long long ks = ((long long)k * s) % J;
-        const double ang = two_pi * (double)ks / (double)J;
-        const double lam_inv = std::pow(alpha, (double)s / J);   // Lambda^{-1}_s
-        const double lam = std::pow(alpha, -(double)s / J);      // Lambda_s
-        // S^{-1}: p_k = (1/J) sum_s e^{-i ang} alpha^{s/J} r_s
-        finv[(size_t)(2 * k) * J + s] = lam_inv * std::cos(ang) / J;
-        finv[(size_t)(2 * k + 1) * J + s] = -lam_inv * std::sin(ang) / J;
-        // Re(S q)_s = sum_k alpha^{-s/J} (cos ang Re q_k - sin ang Im q_k), pairs folded
-        fw[(size_t)s * 2 * nk + 2 * k] = wgt * lam * std::cos(ang);
-        fw[(size_t)s * 2 * nk + 2 * k + 1] = -wgt * lam * std::sin(ang);
+    auto coef = [&](int k, int s, double& fr, double& fi, double& wr, double& wi) {
+      const long long ks = ((long long)k * s) % J;
+      const double ang = two_pi * (double)ks / (double)J;
+      const double lam_inv = std::pow(alpha, (double)s / J);  // Lambda^{-1}_s
+      const double lam = std::pow(alpha, -(double)s / J);     // Lambda_s
+      // S^{-1}: p_k = (1/J) sum_s e^{-i ang} alpha^{s/J} r_s
+      fr = lam_inv * std::cos(ang) / J;
+      fi = -lam_inv * std::sin(ang) / J;
+      // Re(S q)_s = sum_k alpha^{-s/J} (cos ang Re q_k - sin ang Im q_k)
+      wr = lam * std::cos(ang);
+      wi = -lam * std::sin(ang);
+    };
+    for (int s = 0; s < J; ++s) {
+      double fr, fi, wr, wi;
+      coef(0, s, fr, fi, wr, wi);  // pseudo-mode 0, plane 0: real mode 0
+      finv[(size_t)0 * J + s] = fr;
+      fw[(size_t)s * 2 * npm + 0] = wr;
+      if (even) {  // plane 1: real mode J/2
+        coef(J / 2, s, fr, fi, wr, wi);
+        finv[(size_t)1 * J + s] = fr;
+        fw[(size_t)s * 2 * npm + 1] = wr;
+      }
+      for (int m = 1; m < npm; ++m) {
+        coef(m, s, fr, fi, wr, wi);
+        finv[(size_t)(2 * m) * J + s] = fr;
+        finv[(size_t)(2 * m + 1) * J + s] = fi;
+        fw[(size_t)s * 2 * npm + 2 * m] = 2.0 * wr;
+        fw[(size_t)s * 2 * npm + 2 * m + 1] = 2.0 * wi;
       }
     }
     c->Finv.ensure(sizeof(double) * finv.size());
@@ -309,7 +335,7 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
     PE_CUDA_CHECK(cudaMemcpy(c->Finv.p, finv.data(), sizeof(double) * finv.size(), cudaMemcpyHostToDevice));
     PE_CUDA_CHECK(cudaMemcpy(c->Fw.p, fw.data(), sizeof(double) * fw.size(), cudaMemcpyHostToDevice));
   }
-  c->Bk.ensure(sizeof(double) * (size_t)E * nk * 4 * d1 * d1 + 8);
+  c->Bk.ensure(sizeof(double) * (size_t)E * npm * 4 * d1 * d1 + 8);
   c->RW.ensure(sizeof(double) * (size_t)E * d1 * 2 * d2 + 8);
   c->M11dt.ensure(sizeof(double) * (size_t)E * d1 * d1 + 8);
   c->GW.ensure(sizeof(double) * (size_t)E * d2 * 2 * d1 + 8);
@@ -329,7 +355,9 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
     const double* A22 = c->A22.d() + (size_t)e * d2 * d2;
     const double* f2 = c->f2.d() + (size_t)e * d2;
     if (d1) {
-      for (int k = 0; k < nk; ++k) {
+      double* Bk0 = c->Bk.d() + (size_t)e * npm * 4 * d1 * d1;
+      PE_CUDA_CHECK(cudaMemsetAsync(Bk0, 0, sizeof(double) * 4 * d1 * d1, st));
+      for (int k = 0; k <= J / 2; ++k) {
         // d_k = (1 - alpha^{1/J} e^{-2 pi i k/J}) / dt   (allatonce.py:58-62)
         const double ang = -6.283185307179586476925286766559 * (double)k / J;
         const double dre = (1.0 - om_r * std::cos(ang)) / dt;
@@ -337,8 +365,12 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
         shifted_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
             d1, dre, dim, M11, A11, (cuDoubleComplex*)S.p);
         zinverse(c, d1, (cuDoubleComplex*)S.p, (cuDoubleComplex*)Sinv.p, ipiv, info, work);
-        realify_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
-            d1, (const cuDoubleComplex*)Sinv.p, c->Bk.d() + ((size_t)e * nk + k) * 4 * d1 * d1);
+        if (k == 0 || (even && 2 * k == J))  // real modes: diagonal block of pseudo-mode 0
+          real_block_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
+              d1, (const cuDoubleComplex*)Sinv.p, Bk0, k == 0 ? 0 : 1);
+        else
+          realify_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
+              d1, (const cuDoubleComplex*)Sinv.p, c->Bk.d() + ((size_t)e * npm + k) * 4 * d1 * d1);
         PE_CUDA_CHECK(cudaGetLastError());
       }
       double* RW = c->RW.d() + (size_t)e * d1 * 2 * d2;

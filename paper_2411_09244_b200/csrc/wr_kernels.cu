@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(COMMIT_THREADS)
     wr_commit_norms_kernel(int nc, int d1, int d2, int J, double* Ux_cur,
                            const double* __restrict__ Ux_new, double* Wx_cur,
                            const double* __restrict__ Wx_new, const WrColumnState* cs,
-                           double* nrm) {
+                           double* nrm, double* DW) {
   const int en = blockIdx.x;
   const int s = blockIdx.y * COMMIT_WARPS + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -133,11 +133,16 @@ __global__ void __launch_bounds__(COMMIT_THREADS)
     a += x * x;
     Ux_cur[bu + i] = un;
   }
+  // DW_{s+1} = W_s - W_{s-1} for the next sweep's build_rhs (DW_0 = 0 stays from init)
+  double* dw = (DW && s + 1 < J)
+                   ? DW + (long long)e * J * L2 + (long long)(s + 1) * L2 + (long long)n * d2
+                   : nullptr;
   for (int i = lane; i < d2; i += 32) {
     const double wn = Wx_new[bw + i];
     const double x = wn - Wx_cur[bw + i];
     b += x * x;
     Wx_cur[bw + i] = wn;
+    if (dw) dw[i] = wn - Wx_new[bw - L2 + i];
   }
   a = warp_sum(a);
   b = warp_sum(b);
@@ -215,10 +220,10 @@ __global__ void __launch_bounds__(COMMIT_THREADS)
 void wr_commit(int E, int nc, int d1, int d2, int J, double alpha, double tol, int max_iter,
                int /*sweep*/, double* Ux_cur, const double* Ux_new, double* Wx_cur,
                const double* Wx_new, double* V, WrColumnState* cs, double* resid_hist,
-               int* active_count, double* nrm, cudaStream_t st) {
+               int* active_count, double* nrm, double* DW, cudaStream_t st) {
   dim3 g1(E * nc, (J + COMMIT_WARPS - 1) / COMMIT_WARPS);
   wr_commit_norms_kernel<<<g1, COMMIT_THREADS, 0, st>>>(nc, d1, d2, J, Ux_cur, Ux_new, Wx_cur,
-                                                        Wx_new, cs, nrm);
+                                                        Wx_new, cs, nrm, DW);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
   const int cols = E * nc;

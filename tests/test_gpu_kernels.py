@@ -16,9 +16,9 @@ def _gemm(A, B, a_str, b_str, M, N, K, c_layout="col"):
     lib = _lib.require_cuda()
     Cm = torch.full((M * N + 1,), float("nan"), dtype=torch.float64, device="cuda")
     ci, cj = (1, M) if c_layout == "col" else (N, 1)
-    _lib.check(lib.pe_gemm_f64(M, N, K, C.c_void_p(A.data_ptr()), a_str[0], a_str[1],
-                               C.c_void_p(B.data_ptr()), b_str[0], b_str[1],
-                               C.c_void_p(Cm.data_ptr()), ci, cj, None))
+    _lib.check(lib.pe_gemm_f64(M, N, K, 1, C.c_void_p(A.data_ptr()), a_str[0], a_str[1], 0,
+                               C.c_void_p(B.data_ptr()), b_str[0], b_str[1], 0,
+                               C.c_void_p(Cm.data_ptr()), ci, cj, 0, None))
     torch.cuda.synchronize()
     out = Cm[: M * N].reshape(N, M).T if c_layout == "col" else Cm[: M * N].reshape(M, N)
     return out.cpu().numpy()

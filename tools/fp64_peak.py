@@ -42,9 +42,9 @@ def main():
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
         def mine():
-            _lib.check(lib.pe_gemm_f64(n, n, n, C.c_void_p(a.data_ptr()), n, 1,
-                                       C.c_void_p(bt.data_ptr()), 1, n,
-                                       C.c_void_p(c.data_ptr()), 1, n, st))
+            _lib.check(lib.pe_gemm_f64(n, n, n, 1, C.c_void_p(a.data_ptr()), n, 1, 0,
+                                       C.c_void_p(bt.data_ptr()), 1, n, 0,
+                                       C.c_void_p(c.data_ptr()), 1, n, 0, st))
 
         ms = time_it(mine, reps=5)
         out[f"libpe_dmma_{n}_tflops"] = 2 * n ** 3 / ms / 1e9
