@@ -380,6 +380,10 @@ def gpu_arm(args, wl, units_member):
     achieved = st["gemm_flops"] / (st["gemm_ms"] / 1e3) / 1e12 if st["gemm_ms"] > 0 else 0.0
     gemm_share = st["gemm_ms"] / (total_ms / args.steps)
 
+    traffic = {}
+    tpath = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(args.workload, {})
     line = None
     if rank == 0:
         # end to end through the public API: run_parareal with host initial state in and
@@ -441,7 +445,10 @@ def gpu_arm(args, wl, units_member):
                                 "coarse sweep/correction/norm"),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                         "traffic": None,
+                         "traffic": traffic.get("dram_bytes_per_launch"),
+                         "traffic_kernel": traffic.get("kernel"),
+                         "traffic_algorithmic_bytes": traffic.get("algorithmic_bytes_per_launch"),
+                         "traffic_source": traffic.get("source"),
                          "kernel": "pe::gemm_f64_kernel (FP64 DMMA m8n8k4), all launches of "
                                    "one instrumented step",
                          "gemm_launches": st["launches"], "gemm_ms": st["gemm_ms"],
