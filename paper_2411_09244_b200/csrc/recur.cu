@@ -120,8 +120,9 @@ __global__ void __launch_bounds__(RC_THREADS) recur_kernel(const __grid_constant
   double* opS = sm;                                 // rpc x SKO
   double* xs2 = opS + (size_t)a.rpc * SKO;          // 2 x KTP x RC_CGP  (x[k][c], 2 buffers)
   double* red = xs2 + (size_t)2 * KTP * RC_CGP;     // RC_WARPS x rpc x RC_CG
-  double* ybuf = red + (size_t)RC_WARPS * a.rpc * RC_CG;  // rpc x RC_CG (x part)
-  double* dbuf = ybuf + (size_t)a.rpc * RC_CG;            // rpc x RC_CG (SEQ d part)
+  // step results staged for the bulk DSMEM copies: [2 parities][rpc][RC_CGP] (x, and d)
+  double* ybuf2 = red + (size_t)RC_WARPS * a.rpc * RC_CG;
+  double* dbuf2 = ybuf2 + (size_t)2 * a.rpc * RC_CGP;
   __shared__ __align__(8) unsigned long long mbar[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(RC_THREADS) recur_kernel(const __grid_constant
     xs2[(size_t)KTP * RC_CGP + idx] = 0.0;
   }
   // one mbarrier per x buffer; bytes per phase = all M rows x 8 columns (x, and d for SEQ)
-  const unsigned bytes = (unsigned)(M * RC_CG * 8 * (a.mode == 1 ? 2 : 1));
+  const unsigned bytes = (unsigned)(M * RC_CGP * 8 * (a.mode == 1 ? 2 : 1));
   if (tid == 0) {
     mbar_init(smem_u32(&mbar[0]), 1);
     mbar_init(smem_u32(&mbar[1]), 1);
@@ -190,6 +191,10 @@ __global__ void __launch_bounds__(RC_THREADS) recur_kernel(const __grid_constant
   for (int s = 0; s < a.S; ++s) {
     const int cur = s & 1;
     const double* xs = xs2 + (size_t)cur * KTP * RC_CGP;
+    double* ybuf = ybuf2 + (size_t)cur * a.rpc * RC_CGP;
+    double* dbuf = dbuf2 + (size_t)cur * a.rpc * RC_CGP;
+    // the bulk copies issued two steps ago read this parity's staging buffer: done?
+    if (tid < a.cs) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     if (s > 0) {
       mbar_wait(bar_base + 8 * cur, ((s - 1) >> 1) & 1);
       // re-arm this buffer for the rows of step s+1 (consumed at step s+2)
@@ -248,40 +253,43 @@ __global__ void __launch_bounds__(RC_THREADS) recur_kernel(const __grid_constant
         }
         if (gc >= a.nc) v = dv = 0.0;  // padding columns stay zero
       }
-      ybuf[idx] = v;
-      dbuf[idx] = dv;
+      ybuf[r * RC_CGP + c] = v;
+      dbuf[r * RC_CGP + c] = dv;
     }
     if (!last) {
+      // push: one bulk DSMEM copy per peer (and per d block for SEQ) of this CTA's row block
+      // into the peer's next x buffer, completing on the peer's mbarrier
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
-      // push: (row, peer) pairs; 4 x 16-byte st.async per row (8 columns), + d rows for SEQ
-      const int nrow = min(a.rpc, M - r0);
-      const unsigned nbuf = xs_base + (unsigned)(((s + 1) & 1) * KTP * RC_CGP * 8);
-      const unsigned nbar = bar_base + 8 * ((s + 1) & 1);
-      const int pairs = nrow * a.cs;
-      for (int p = tid; p < pairs; p += RC_THREADS) {
-        const int r = p / a.cs, q = p - (p / a.cs) * a.cs;
-        const unsigned rbar = map_rank(nbar, q);
-        const unsigned dst = map_rank(nbuf + (unsigned)((r0 + r) * RC_CGP * 8), q);
-        const double* y = ybuf + r * RC_CG;
-#pragma unroll
-        for (int h = 0; h < 4; ++h) st_async_v2(dst + 16 * h, y[2 * h], y[2 * h + 1], rbar);
+      if (tid < a.cs) {
+        const int q = tid;
+        const int nrow = min(a.rpc, M - r0);
+        const unsigned nbuf = xs_base + (unsigned)(((s + 1) & 1) * KTP * RC_CGP * 8);
+        const unsigned rbar = map_rank(bar_base + 8 * ((s + 1) & 1), q);
+        const unsigned bytes_blk = (unsigned)(nrow * RC_CGP * 8);
+        const unsigned dst = map_rank(nbuf + (unsigned)(r0 * RC_CGP * 8), q);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(dst), "r"(smem_u32(ybuf)), "r"(bytes_blk), "r"(rbar) : "memory");
         if (a.mode == 1) {
-          const unsigned dd = map_rank(nbuf + (unsigned)((M + r0 + r) * RC_CGP * 8), q);
-          const double* dy = dbuf + r * RC_CG;
-#pragma unroll
-          for (int h = 0; h < 4; ++h) st_async_v2(dd + 16 * h, dy[2 * h], dy[2 * h + 1], rbar);
+          const unsigned dd = map_rank(nbuf + (unsigned)((M + r0) * RC_CGP * 8), q);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(dd), "r"(smem_u32(dbuf)), "r"(bytes_blk), "r"(rbar) : "memory");
         }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
     TRACE(4 + 4 * s)
     TRACE(5 + 4 * s)
   }
-  cluster.sync();  // no CTA leaves while peers' stores to it may be in flight
+  if (tid < a.cs) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  cluster.sync();  // no CTA leaves while copies to or from it may be in flight
 }
 
 static size_t recur_smem(int r, int KTP) {
   return sizeof(double) * ((size_t)r * (KTP + 4) + 2 * (size_t)KTP * RC_CGP +
-                           (size_t)RC_WARPS * r * RC_CG + 2 * (size_t)r * RC_CG);
+                           (size_t)RC_WARPS * r * RC_CG + 4 * (size_t)r * RC_CGP);
 }
 
 static int pad_k(int KT) { return (KT + 4 * RC_WARPS - 1) / (4 * RC_WARPS) * (4 * RC_WARPS); }
