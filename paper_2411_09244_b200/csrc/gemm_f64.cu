@@ -226,11 +226,12 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   // fixed per-thread chunk coordinates
   constexpr int ACPR = BK / 2;                 // 16-byte chunks per A row
   constexpr int AROWS = NT / ACPR;             // rows covered per pass
-  constexpr int APASS = BM / AROWS;
+  constexpr int APASS = (BM + AROWS - 1) / AROWS;
   const int akc = tid % ACPR, ar = tid / ACPR;
   constexpr int BCPR = BJC ? BN / 2 : BK / 2;
   constexpr int BROWS = NT / BCPR;
-  constexpr int BPASS = (BJC ? BK : BN) / BROWS;
+  constexpr int BLEN = BJC ? BK : BN;
+  constexpr int BPASS = (BLEN + BROWS - 1) / BROWS;
   const int bkc = tid % BCPR, br = tid / BCPR;
 
   auto load_tile = [&](int t, int slot) {
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
 #pragma unroll
       for (int i = 0; i < APASS; ++i) {
         const int r = ar + i * AROWS, gi = i0 + r;
+        if ((BM % AROWS) && r >= BM) break;
         const int bytes = (gi < p.M) ? 8 * kv : 0;
         const double* src = bytes ? A + (long long)gi * sg.A.s0 + kk : A;
         cp_async16(as + r * SA + 2 * akc, src, bytes);
@@ -259,6 +261,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
 #pragma unroll
       for (int i = 0; i < BPASS; ++i) {
         const int r = br + i * BROWS, gj = j0 + r;
+        if ((BLEN % BROWS) && r >= BLEN) break;
         const int bytes = (gj < p.N) ? 8 * kv : 0;
         const double* src = bytes ? B + (long long)gj * sg.B.s1 + kk : B;
         cp_async16(bs + r * SB + 2 * bkc, src, bytes);
@@ -269,6 +272,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
 #pragma unroll
       for (int i = 0; i < BPASS; ++i) {
         const int r = br + i * BROWS, gk = k0 + r;
+        if ((BLEN % BROWS) && r >= BLEN) break;
         const int bytes = (gk < K) ? 8 * jv : 0;
         const double* src = bytes ? B + (long long)gk * sg.B.s0 + jj : B;
         cp_async16(bs + r * SB + 2 * bkc, src, bytes);
@@ -515,21 +519,26 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
   if (lay >= 0 && (tiles64 >= 96 || tiles_n32 >= 96)) {
     // pick the tile / pipeline variant with the best wave-quantised cost (N <= 32:
     // narrow 128x32 tiles, no wasted half tile)
-    // measured on B200 (tools/gemm_bench.py): 64x64 / BK16 / 3 stages (3 CTAs/SM) is the
-    // best variant on every hot-path shape except N <= 32 (128x32 tiles)
-    int best = (p.N <= 32) ? 3 : 1;
+    // measured on B200 (tools/gemm_bench.py): 64x64 / BK16 / 2 stages (4 CTAs/SM: more
+    // warps to cover the DMMA and barrier latencies) is the best variant on every hot-path
+    // shape except N <= 32 (128x32 tiles)
+    int best = (p.N <= 32) ? 3 : 5;
     static const int forced = getenv("PE_GEMM_VARIANT") ? atoi(getenv("PE_GEMM_VARIANT")) : -1;
-    if (forced >= 0 && forced < 4) best = forced;  // tuning experiments only
+    if (forced >= 0 && forced < 7) best = forced;  // tuning experiments only
     if (lay == 0) {
       if (best == 0) launch_fast<64, 64, 32, 3, false>(p, st);
       else if (best == 1) launch_fast<64, 64, 16, 3, false>(p, st);
       else if (best == 2) launch_fast<128, 64, 16, 3, false>(p, st);
-      else launch_fast<128, 32, 32, 3, false>(p, st);
+      else if (best == 3) launch_fast<128, 32, 32, 3, false>(p, st);
+      else if (best == 5) launch_fast<64, 64, 16, 2, false>(p, st);
+      else launch_fast<64, 64, 32, 2, false>(p, st);
     } else {
       if (best == 0) launch_fast<64, 64, 32, 3, true>(p, st);
       else if (best == 1) launch_fast<64, 64, 16, 3, true>(p, st);
       else if (best == 2) launch_fast<128, 64, 16, 3, true>(p, st);
-      else launch_fast<128, 32, 32, 3, true>(p, st);
+      else if (best == 3) launch_fast<128, 32, 32, 3, true>(p, st);
+      else if (best == 5) launch_fast<64, 64, 16, 2, true>(p, st);
+      else launch_fast<64, 64, 32, 2, true>(p, st);
     }
   } else if (tiles64 >= 2 * 148) {
     launch_cfg<64, 64, 16, 32, 32>(p, ak, bk, st);
