@@ -266,6 +266,20 @@ __global__ void __launch_bounds__(CS_THREADS)
     const double* row = Pm + (long long)r * d;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int k = lane;
+    // 8 independent loads in flight per lane (HBM-bound stream of Phi)
+    for (; k + 224 < d; k += 256) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(row + k + 32 * u);
+      a0 = fma(v[0], xs[k], a0);
+      a1 = fma(v[1], xs[k + 32], a1);
+      a2 = fma(v[2], xs[k + 64], a2);
+      a3 = fma(v[3], xs[k + 96], a3);
+      a0 = fma(v[4], xs[k + 128], a0);
+      a1 = fma(v[5], xs[k + 160], a1);
+      a2 = fma(v[6], xs[k + 192], a2);
+      a3 = fma(v[7], xs[k + 224], a3);
+    }
     for (; k + 96 < d; k += 128) {
       a0 = fma(__ldcs(row + k), xs[k], a0);
       a1 = fma(__ldcs(row + k + 32), xs[k + 32], a1);
@@ -305,12 +319,15 @@ __global__ void __launch_bounds__(CS_THREADS)
   }
 }
 
+// One block per member; thread n sums interval n's block partials in block order (fixed),
+// then the max over intervals is taken in a fixed smem tree (NaN propagates).
 __global__ void coarse_norm_reduce_kernel(int N, int nblocks, const double* partial,
                                           double* diff, const int* active) {
   const int e = blockIdx.x;
-  if (threadIdx.x != 0 || (active && active[e] == 0)) return;
-  double md = 0.0, mn = 0.0;
-  for (int n = 0; n < N; ++n) {
+  if (active && active[e] == 0) return;
+  __shared__ double md[256], mn[256];
+  double bd = 0.0, bn = 0.0;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
     const double* p = partial + ((long long)e * N + n) * nblocks * 2;
     double td = 0.0, tn = 0.0;
     for (int b = 0; b < nblocks; ++b) {
@@ -318,11 +335,24 @@ __global__ void coarse_norm_reduce_kernel(int N, int nblocks, const double* part
       tn += p[2 * b + 1];
     }
     const double nd = sqrt(td), nn = sqrt(tn);
-    md = (nd > md || nd != nd) ? nd : md;
-    mn = (nn > mn || nn != nn) ? nn : mn;
+    bd = (nd > bd || nd != nd) ? nd : bd;
+    bn = (nn > bn || nn != nn) ? nn : bn;
   }
-  diff[2 * e] = md;
-  diff[2 * e + 1] = mn;
+  md[threadIdx.x] = bd;
+  mn[threadIdx.x] = bn;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double a = md[threadIdx.x + o], b = mn[threadIdx.x + o];
+      if (a > md[threadIdx.x] || a != a) md[threadIdx.x] = a;
+      if (b > mn[threadIdx.x] || b != b) mn[threadIdx.x] = b;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    diff[2 * e] = md[0];
+    diff[2 * e + 1] = mn[0];
+  }
 }
 
 int coarse_stream_blocks(int d) { return std::min(296, (d + CS_WARPS - 1) / CS_WARPS); }
@@ -347,7 +377,7 @@ static void coarse_correct_stream(int E, int d, int N, const double* Phi, const 
     PE_CUDA_CHECK(cudaGetLastError());
   }
   if (diff) {
-    coarse_norm_reduce_kernel<<<E, 32, 0, st>>>(N, nb, partial, diff, active);
+    coarse_norm_reduce_kernel<<<E, 256, 0, st>>>(N, nb, partial, diff, active);
     ++g_launches;
     PE_CUDA_CHECK(cudaGetLastError());
   }

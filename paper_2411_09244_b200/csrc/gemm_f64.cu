@@ -521,24 +521,26 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
     // narrow 128x32 tiles, no wasted half tile)
     // measured on B200 (tools/gemm_bench.py): 64x64 / BK16 / 2 stages (4 CTAs/SM: more
     // warps to cover the DMMA and barrier latencies) is the best variant on every hot-path
-    // shape except N <= 32 (128x32 tiles)
-    int best = (p.N <= 32) ? 3 : 5;
+    // shape except N <= 32 (64x32 / BK16 / 2 stages, 2 warps)
+    int best = (p.N <= 32) ? 7 : 5;
     static const int forced = getenv("PE_GEMM_VARIANT") ? atoi(getenv("PE_GEMM_VARIANT")) : -1;
-    if (forced >= 0 && forced < 7) best = forced;  // tuning experiments only
+    if (forced >= 0 && forced < 8) best = forced;  // tuning experiments only
     if (lay == 0) {
       if (best == 0) launch_fast<64, 64, 32, 3, false>(p, st);
       else if (best == 1) launch_fast<64, 64, 16, 3, false>(p, st);
       else if (best == 2) launch_fast<128, 64, 16, 3, false>(p, st);
       else if (best == 3) launch_fast<128, 32, 32, 3, false>(p, st);
       else if (best == 5) launch_fast<64, 64, 16, 2, false>(p, st);
-      else launch_fast<64, 64, 32, 2, false>(p, st);
+      else if (best == 6) launch_fast<64, 64, 32, 2, false>(p, st);
+      else launch_fast<64, 32, 16, 2, false>(p, st);
     } else {
       if (best == 0) launch_fast<64, 64, 32, 3, true>(p, st);
       else if (best == 1) launch_fast<64, 64, 16, 3, true>(p, st);
       else if (best == 2) launch_fast<128, 64, 16, 3, true>(p, st);
       else if (best == 3) launch_fast<128, 32, 32, 3, true>(p, st);
       else if (best == 5) launch_fast<64, 64, 16, 2, true>(p, st);
-      else launch_fast<64, 64, 32, 2, true>(p, st);
+      else if (best == 6) launch_fast<64, 64, 32, 2, true>(p, st);
+      else launch_fast<64, 32, 16, 2, true>(p, st);
     }
   } else if (tiles64 >= 2 * 148) {
     launch_cfg<64, 64, 16, 32, 32>(p, ak, bk, st);
