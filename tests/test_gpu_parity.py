@@ -530,3 +530,81 @@ def test_config4_ensemble_iterations_and_histories():
     assert all(r.converged for r in runs)
     for m in (0, 1, 2, 3):
         assert rel_rows(np.array(runs[m].history), zr[f"hist_{m}"]) < REL
+
+
+SHAPES = [  # (d1, d2, N, J)
+    (1, 1, 1, 1), (5, 3, 3, 2), (3, 5, 4, 3), (0, 4, 3, 5), (4, 0, 3, 5), (7, 9, 5, 7),
+    (16, 24, 9, 16), (33, 40, 6, 9), (48, 17, 2, 12), (64, 64, 10, 4),
+]
+
+
+@pytest.mark.parametrize("d1,d2,N,J", SHAPES)
+@pytest.mark.parametrize("kind", ["sequential", "all-at-once"])
+def test_shape_sweep_against_oracle(d1, d2, N, J, kind):
+    """Odd, degenerate and unaligned shapes (generic-stride GEMM path, odd-J pseudo-modes,
+    empty subspaces, single interval / single substep) against the CPU oracle."""
+    P = _pkg()
+    mass, stiff, f = _random_coupled(d1, d2, 100 * d1 + 10 * d2 + J)
+    blocks = dict(M11=mass[:d1, :d1], A11=stiff[:d1, :d1], M12=mass[:d1, d1:],
+                  A12=stiff[:d1, d1:], M22=mass[d1:, d1:], A22=stiff[d1:, d1:])
+    s = P.CoarseSystem(**{k: np.ascontiguousarray(v) for k, v in blocks.items()})
+    ld = P.ConstantLoads(f[:d1], f[d1:])
+    osys = po.OSystem(*(blocks[k] for k in ("M11", "A11", "M12", "A12", "M22", "A22")),
+                      f[:d1], f[d1:])
+    x0 = np.random.default_rng(J).standard_normal(d1 + d2) * 0.3
+    T = 0.05 * N
+    props = P.SplitPropagators(s, ld)
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(T, N, J), alpha=0.2, epsilon=1e-11,
+                           k_max=N + 1, fine_kind=kind, fine_tol=1e-13)
+    run = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld),
+                         P.SplitState.fresh(x0[:d1], x0[d1:]))
+    ref = po.run_parareal(osys, x0, T, N, J, kind=kind, alpha=0.2, epsilon=1e-11,
+                          k_max=N + 1, fine_tol=1e-13)
+    assert run.iterations == ref["iterations"]
+    assert rel_rows(np.array(run.history), np.array(ref["history"])) < REL
+    if kind == "all-at-once":
+        its = np.array([[i["iterations"] for i in sw] for sw in run.fine_info])
+        rits = np.array([[i["iterations"] for i in sw] for sw in ref["fine_info"]])
+        assert np.abs(its - rits).max() <= 2
+
+
+def test_allatonce_ensemble_members_equal_single_runs():
+    P = _pkg()
+    z = golden("sys_cfg0.npz")
+    s, ld = _system(z)
+    systems, loads = [], []
+    for m, scale in enumerate((1.0, 0.7, 0.4)):
+        systems.append(P.CoarseSystem(s.M11, s.A11 * scale, s.M12, s.A12 * scale, s.M22,
+                                      s.A22 * scale))
+        loads.append(P.ConstantLoads(ld.f1 * (m + 1), ld.f2 * (m + 1)))
+    inits = [P.SplitState.fresh(np.zeros(s.d1), np.zeros(s.d2))] * 3
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(1.0, 10, 10), alpha=0.1, epsilon=1e-8, k_max=10,
+                           fine_kind="all-at-once", fine_tol=1e-12, stop_rule="relative")
+    runs = P.ParerealEnsemble(cfg, systems, loads).run(inits)
+    for sysm, ldm, run in zip(systems, loads, runs):
+        props = P.SplitPropagators(sysm, ldm)
+        single = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ldm), inits[0])
+        assert run.iterations == single.iterations
+        assert rel_rows(np.array(run.history), np.array(single.history)) < 1e-13
+        a = np.array([[i["iterations"] for i in sw] for sw in run.fine_info])
+        b = np.array([[i["iterations"] for i in sw] for sw in single.fine_info])
+        np.testing.assert_array_equal(a, b)
+
+
+def test_graph_replay_equals_direct_launches_bitwise():
+    """The captured per-sweep CUDA graphs and direct launches (profiling mode) run the
+    same kernels in the same order: identical bits."""
+    P = _pkg()
+    s, ld = _system(golden("sys_cfg2.npz"))
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((1, 16, s.d1 + s.d2)) * 0.1
+    ctx = P.PeContext([s], [ld], 64)
+    ctx.prepare_allatonce(1.0 / 64 / 64, 0.1, 1e-12, 400)
+    y1, sw1, _, rh1 = ctx.fine_allatonce(ctx.to_dev(X))
+    ctx.set_profiling(True)
+    y2, sw2, _, rh2 = ctx.fine_allatonce(ctx.to_dev(X))
+    ctx.set_profiling(False)
+    assert np.array_equal(y1.cpu().numpy(), y2.cpu().numpy())
+    assert np.array_equal(sw1.cpu().numpy(), sw2.cpu().numpy())
+    assert np.array_equal(np.nan_to_num(rh1.cpu().numpy(), nan=-1.0),
+                          np.nan_to_num(rh2.cpu().numpy(), nan=-1.0))
