@@ -192,6 +192,15 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   WrColumnState* cs = (WrColumnState*)c->colstate.p;
   int* cnt = c->counter.i();
 
+  if (c->use_recur && wr_tiny_eligible(d1, d2, J, nk)) {
+    // latency regime: the whole WR solve of each interval in one CTA, one launch
+    TinyArgsPublic tp{E, d1, d2, J, nk, nc, max_iter, alpha, tol,
+                      c->RW.d(), c->M11dt.d(), c->Finv.d(), c->Bk.d(), c->Fw.d(), c->GW.d(),
+                      c->cg.d(), c->Emat.d(), c->f1.d(), c->BkT.d(), X_in, X_out, sweeps,
+                      reasons, resid_hist, Uc, Wc};
+    wr_tiny(tp, st);
+    return;
+  }
   wr_init(E, nc, d1, d2, J, alpha, X_in, Uc, Un, Wc, Wn, c->V.d(), cs, c->rhist.d(), max_iter, st);
   // W is seeded constant in time, so DW = W_s - W_{s-1} starts at zero; afterwards the
   // commit kernel maintains it for the intervals it commits

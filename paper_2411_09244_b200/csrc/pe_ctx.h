@@ -75,7 +75,7 @@ struct pe_ctx {
   double wr_dt = 0, wr_alpha = 0, wr_tol = 0;
   int wr_max_iter = 0;
   int wr_nk = 0;  // solved time modes (half spectrum, floor(J/2) + 1)
-  pe::DevBuf Bk, RW, M11dt, GW, cg, Emat, Finv, Fw;
+  pe::DevBuf Bk, BkT, RW, M11dt, GW, cg, Emat, Finv, Fw;
 
   // work buffers
   pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs;

@@ -101,6 +101,23 @@ bool recur_wr(int E, int d2, int nc, int J, const double* Emat, double* Wx, cuda
 bool recur_seq(int E, int d, int nc, int S, const double* T, const double* c, const double* Xin,
                double* Xout, double* scratch, cudaStream_t st);
 
+// ---------------------------------------------------------------- fused small-problem WR
+struct TinyArgsPublic {
+  int E, d1, d2, J, npm, nc, max_iter;
+  double alpha, tol;
+  const double *RW, *M11dt, *Finv, *Bk, *Fw, *GW, *cg, *Emat, *f1;
+  const double* BkT;
+  const double* X_in;
+  double* X_out;
+  int* sweeps;
+  int* reasons;
+  double* resid_hist;
+  double *Ux_cur, *Wx_cur;
+};
+bool wr_tiny_eligible(int d1, int d2, int J, int npm);
+void transpose_blocks(int nblocks, int n, const double* src, double* dst, cudaStream_t st);
+void wr_tiny(const TinyArgsPublic& p, cudaStream_t st);
+
 // ---------------------------------------------------------------- coarse sweep
 // Row-partitioned cluster kernel; see coarse.cu.
 void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,

@@ -122,6 +122,24 @@ __global__ void real_block_kernel(int n, const cuDoubleComplex* inv, double* B, 
     B[(t / n + o) * n2 + o + t % n] = cuCreal(inv[t]);
 }
 
+__global__ void transpose_blocks_kernel(int nblocks, int n, const double* src, double* dst) {
+  const long long per = (long long)n * n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < per * nblocks;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long b = t / per, r = t - b * per;
+    const long long i = r / n, j = r - i * n;
+    dst[b * per + j * n + i] = src[t];
+  }
+}
+
+void transpose_blocks(int nblocks, int n, const double* src, double* dst, cudaStream_t st) {
+  const long long tot = (long long)n * n * nblocks;
+  if (tot == 0) return;
+  transpose_blocks_kernel<<<(int)std::min<long long>(4096, (tot + 255) / 256), 256, 0, st>>>(
+      nblocks, n, src, dst);
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
 static int grid_for(long long n) { return (int)std::max<long long>(1, std::min<long long>(4096, (n + 255) / 256)); }
 
 // Ainv = A^{-1} for a row-major n x n buffer (inv(A^T) = inv(A)^T, so the
@@ -395,6 +413,10 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
         rm_gemm(h, true, true, d2, d1, d2, -1.0, M22inv.d(), d2, M12, d2, 0.0, GW + d1, 2 * d1);
       }
     }
+  }
+  if (wr_tiny_eligible(d1, d2, J, npm)) {  // transposed Bk for the fused small-problem path
+    c->BkT.ensure(sizeof(double) * (size_t)E * npm * 4 * d1 * d1 + 8);
+    transpose_blocks(E * npm, 2 * d1, c->Bk.d(), c->BkT.d(), st);
   }
   PE_CUDA_CHECK(cudaStreamSynchronize(st));
   c->wr_ready = true;
