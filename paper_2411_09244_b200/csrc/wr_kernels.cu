@@ -126,23 +126,56 @@ __global__ void __launch_bounds__(COMMIT_THREADS)
   const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
   const long long bu = (long long)e * (J + 2) * L1 + (long long)(s + 2) * L1 + (long long)n * d1;
   const long long bw = (long long)e * (J + 2) * L2 + (long long)(s + 2) * L2 + (long long)n * d2;
+  // Each lane keeps the lane-strided element order (i = lane + 32 c) of the summation but
+  // issues all loads of a chunk before using them (memory-level parallelism; the row is
+  // ~300 doubles, one chunk).
+  constexpr int CPL = 10;
   double a = 0.0, b = 0.0;
-  for (int i = lane; i < d1; i += 32) {
-    const double un = Ux_new[bu + i];
-    const double x = un - Ux_cur[bu + i];
-    a += x * x;
-    Ux_cur[bu + i] = un;
+  for (int base = 0; base < d1; base += 32 * CPL) {
+    double vn[CPL], vc[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int i = base + c * 32 + lane;
+      if (i < d1) {
+        vn[c] = Ux_new[bu + i];
+        vc[c] = Ux_cur[bu + i];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int i = base + c * 32 + lane;
+      if (i < d1) {
+        const double x = vn[c] - vc[c];
+        a += x * x;
+        Ux_cur[bu + i] = vn[c];
+      }
+    }
   }
   // DW_{s+1} = W_s - W_{s-1} for the next sweep's build_rhs (DW_0 = 0 stays from init)
   double* dw = (DW && s + 1 < J)
                    ? DW + (long long)e * J * L2 + (long long)(s + 1) * L2 + (long long)n * d2
                    : nullptr;
-  for (int i = lane; i < d2; i += 32) {
-    const double wn = Wx_new[bw + i];
-    const double x = wn - Wx_cur[bw + i];
-    b += x * x;
-    Wx_cur[bw + i] = wn;
-    if (dw) dw[i] = wn - Wx_new[bw - L2 + i];
+  for (int base = 0; base < d2; base += 32 * CPL) {
+    double vn[CPL], vc[CPL], vp[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int i = base + c * 32 + lane;
+      if (i < d2) {
+        vn[c] = Wx_new[bw + i];
+        vc[c] = Wx_cur[bw + i];
+        if (dw) vp[c] = Wx_new[bw - L2 + i];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int i = base + c * 32 + lane;
+      if (i < d2) {
+        const double x = vn[c] - vc[c];
+        b += x * x;
+        Wx_cur[bw + i] = vn[c];
+        if (dw) dw[i] = vn[c] - vp[c];
+      }
+    }
   }
   a = warp_sum(a);
   b = warp_sum(b);
