@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <stdexcept>
@@ -188,9 +189,13 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
 }
 
-template <int BM, int BN, int BK, int STAGES, bool BJC>
+// Warp tile = (8 FM) x (8 FN) DMMA fragments, CTA = WGM x WGN warps.  Tile shapes that are
+// not powers of two (64x72, 80x64) let the chooser fit the tile count to the 148 SMs.
+template <int WGM, int WGN, int FM, int FN, int BK, int STAGES, bool BJC>
 struct FastCfg {
-  static constexpr int NT = (BM / 32) * (BN / 32) * 32;
+  static constexpr int BM = WGM * 8 * FM;
+  static constexpr int BN = WGN * 8 * FN;
+  static constexpr int NT = WGM * WGN * 32;
   static constexpr int SA = BK + 4;
   static constexpr int SB = BJC ? (BN + 4) : (BK + 4);
   static constexpr int A_TILE = BM * SA;
@@ -198,12 +203,14 @@ struct FastCfg {
   static constexpr size_t SMEM = sizeof(double) * (size_t)STAGES * (A_TILE + B_TILE);
 };
 
-template <int BM, int BN, int BK, int STAGES, bool BJC>
-__global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
+template <int WGM, int WGN, int FM, int FN, int BK, int STAGES, bool BJC>
+__global__ void __launch_bounds__(WGM * WGN * 32)
     gemm_fast_kernel(const __grid_constant__ GemmParams p) {
-  using Cfg = FastCfg<BM, BN, BK, STAGES, BJC>;
+  using Cfg = FastCfg<WGM, WGN, FM, FN, BK, STAGES, BJC>;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN;
   constexpr int NT = Cfg::NT, SA = Cfg::SA, SB = Cfg::SB;
-  constexpr int WARPS_M = BM / 32;
+  constexpr int WARPS_M = WGM;
+  constexpr int WTM = 8 * FM, WTN = 8 * FN;
   extern __shared__ __align__(16) double smf[];
   double* As = smf;
   double* Bs = smf + STAGES * Cfg::A_TILE;
@@ -233,6 +240,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   constexpr int BLEN = BJC ? BK : BN;
   constexpr int BPASS = (BLEN + BROWS - 1) / BROWS;
   const int bkc = tid % BCPR, br = tid / BCPR;
+  const bool bload = br < BROWS;  // NT % BCPR threads left over (e.g. BN = 72) stay idle
 
   auto load_tile = [&](int t, int slot) {
     int s = 0, tt = t + tbeg;
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
 #pragma unroll
       for (int i = 0; i < APASS; ++i) {
         const int r = ar + i * AROWS, gi = i0 + r;
-        if ((BM % AROWS) && r >= BM) break;
+        if (ar >= AROWS || ((BM % AROWS) && r >= BM)) break;
         const int bytes = (gi < p.M) ? 8 * kv : 0;
         const double* src = bytes ? A + (long long)gi * sg.A.s0 + kk : A;
         cp_async16(as + r * SA + 2 * akc, src, bytes);
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
 #pragma unroll
       for (int i = 0; i < BPASS; ++i) {
         const int r = br + i * BROWS, gj = j0 + r;
-        if ((BLEN % BROWS) && r >= BLEN) break;
+        if (!bload || ((BLEN % BROWS) && r >= BLEN)) break;
         const int bytes = (gj < p.N) ? 8 * kv : 0;
         const double* src = bytes ? B + (long long)gj * sg.B.s1 + kk : B;
         cp_async16(bs + r * SB + 2 * bkc, src, bytes);
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
 #pragma unroll
       for (int i = 0; i < BPASS; ++i) {
         const int r = br + i * BROWS, gk = k0 + r;
-        if ((BLEN % BROWS) && r >= BLEN) break;
+        if (!bload || ((BLEN % BROWS) && r >= BLEN)) break;
         const int bytes = (gk < K) ? 8 * jv : 0;
         const double* src = bytes ? B + (long long)gk * sg.B.s0 + jj : B;
         cp_async16(bs + r * SB + 2 * bkc, src, bytes);
@@ -283,11 +291,11 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
-  double acc[4][4][2];
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < FM; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
@@ -300,23 +308,23 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
     if (t + STAGES - 1 < ntile) load_tile(t + STAGES - 1, (t + STAGES - 1) % STAGES);
     cp_async_commit();
     const int slot = t % STAGES;
-    const double* as = As + slot * Cfg::A_TILE + (wm * 32 + g) * SA + t4;
+    const double* as = As + slot * Cfg::A_TILE + (wm * WTM + g) * SA + t4;
     const double* bs;
     if (!BJC)
-      bs = Bs + slot * Cfg::B_TILE + (wn * 32 + g) * SB + t4;
+      bs = Bs + slot * Cfg::B_TILE + (wn * WTN + g) * SB + t4;
     else
-      bs = Bs + slot * Cfg::B_TILE + t4 * SB + wn * 32 + g;
+      bs = Bs + slot * Cfg::B_TILE + t4 * SB + wn * WTN + g;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
+      double af[FM], bf[FN];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) af[a] = as[a * 8 * SA + kk];
+      for (int a = 0; a < FM; ++a) af[a] = as[a * 8 * SA + kk];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = BJC ? bs[kk * SB + b * 8] : bs[b * 8 * SB + kk];
+      for (int b = 0; b < FN; ++b) bf[b] = BJC ? bs[kk * SB + b * 8] : bs[b * 8 * SB + kk];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < FM; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        for (int b = 0; b < FN; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
   }
   cp_async_wait<0>();
@@ -326,14 +334,14 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
     const size_t plane = (size_t)batch * p.M * p.N;
     double* W = p.ws + (size_t)sp * plane + (size_t)z * p.M * p.N;
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int gi = i0 + wm * 32 + a * 8 + g;
+    for (int a = 0; a < FM; ++a) {
+      const int gi = i0 + wm * WTM + a * 8 + g;
       if (gi >= p.M) continue;
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < FN; ++b)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int gj = j0 + wn * 32 + b * 8 + 2 * t4 + h;
+          const int gj = j0 + wn * WTN + b * 8 + 2 * t4 + h;
           if (gj < p.N) W[(size_t)gj * p.M + gi] = acc[a][b][h];
         }
     }
@@ -348,16 +356,16 @@ __global__ void __launch_bounds__((BM / 32) * (BN / 32) * 32)
   const double* bias = p.bias ? p.bias + z1 * p.bias_b1 + z2 * p.bias_b2 : nullptr;
   const bool alpha1 = (p.alpha == 1.0), beta1 = (p.beta == 1.0);
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int gi = i0 + wm * 32 + a * 8 + g;
+  for (int a = 0; a < FM; ++a) {
+    const int gi = i0 + wm * WTM + a * 8 + g;
     if (gi >= p.M) continue;
     const double bv = bias ? bias[gi] : 0.0;
     const long long ro = gi * p.c_i;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < FN; ++b) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int gj = j0 + wn * 32 + b * 8 + 2 * t4 + h;
+        const int gj = j0 + wn * WTN + b * 8 + 2 * t4 + h;
         if (gj >= p.N) continue;
         const long long off = ro + gj * p.c_j;
         double v = alpha1 ? acc[a][b][h] : __dmul_rn(p.alpha, acc[a][b][h]);
@@ -393,27 +401,27 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ GemmParams p) {
   }
 }
 
-template <int BM, int BN, int BK, int STAGES, bool BJC>
+template <int WGM, int WGN, int FM, int FN, int BK, int STAGES, bool BJC>
 static int fast_occupancy() {
   static int occ = -1;
   if (occ < 0) {
-    using Cfg = FastCfg<BM, BN, BK, STAGES, BJC>;
-    PE_CUDA_CHECK(cudaFuncSetAttribute(gemm_fast_kernel<BM, BN, BK, STAGES, BJC>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+    using Cfg = FastCfg<WGM, WGN, FM, FN, BK, STAGES, BJC>;
+    auto kern = gemm_fast_kernel<WGM, WGN, FM, FN, BK, STAGES, BJC>;
+    PE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Cfg::SMEM));
     int n = 0;
-    PE_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &n, gemm_fast_kernel<BM, BN, BK, STAGES, BJC>, Cfg::NT, Cfg::SMEM));
+    PE_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, Cfg::NT, Cfg::SMEM));
     occ = n;
   }
   return occ;
 }
 
-template <int BM, int BN, int BK, int STAGES, bool BJC>
+template <int WGM, int WGN, int FM, int FN, int BK, int STAGES, bool BJC>
 static void launch_fast(const GemmParams& p, cudaStream_t st) {
-  using Cfg = FastCfg<BM, BN, BK, STAGES, BJC>;
-  fast_occupancy<BM, BN, BK, STAGES, BJC>();
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.nb1 * p.nb2 * p.ksplit);
-  gemm_fast_kernel<BM, BN, BK, STAGES, BJC><<<grid, Cfg::NT, Cfg::SMEM, st>>>(p);
+  using Cfg = FastCfg<WGM, WGN, FM, FN, BK, STAGES, BJC>;
+  fast_occupancy<WGM, WGN, FM, FN, BK, STAGES, BJC>();
+  dim3 grid((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM, p.nb1 * p.nb2 * p.ksplit);
+  gemm_fast_kernel<WGM, WGN, FM, FN, BK, STAGES, BJC><<<grid, Cfg::NT, Cfg::SMEM, st>>>(p);
   ++g_launches;
 }
 
@@ -438,22 +446,71 @@ static int fast_layout(const GemmParams& p) {
   return bjc;
 }
 
-struct FastChoice {
-  int id;
-  double cost;
-};
+// Fast-path variants: id, warps (M, N), fragments per warp (M, N), BK, stages, auto.
+// Every variant accumulates k in the same order, so the choice never changes a result bit.
+// auto = 1: considered by the cost model; 0: reachable through PE_GEMM_VARIANT only
+// (measured slower on every hot-path shape, tools/gemm_bench.py).
+#define PE_FAST_VARIANTS(X)   \
+  X(0, 2, 2, 4, 4, 32, 3, 0)  \
+  X(1, 2, 2, 4, 4, 16, 3, 0)  \
+  X(2, 4, 2, 4, 4, 16, 3, 0)  \
+  X(3, 4, 1, 4, 4, 32, 3, 0)  \
+  X(5, 2, 2, 4, 4, 16, 2, 1)  \
+  X(6, 2, 2, 4, 4, 32, 2, 0)  \
+  X(7, 2, 1, 4, 4, 16, 2, 1)  \
+  X(8, 2, 3, 4, 3, 16, 2, 1)  \
+  X(9, 2, 2, 5, 4, 16, 2, 1)  \
+  X(10, 1, 2, 5, 4, 16, 2, 1) \
+  X(11, 2, 3, 4, 3, 16, 3, 0) \
+  X(12, 4, 1, 5, 4, 16, 2, 1) \
+  X(13, 3, 1, 5, 4, 16, 2, 0)
 
-template <int BM, int BN, int BK, int STAGES, bool BJC>
-static double fast_cost(const GemmParams& p, double tile_eff) {
-  const int occ = fast_occupancy<BM, BN, BK, STAGES, BJC>();
+static constexpr int kMaxVariant = 14;
+
+// Wave-quantised cost: CTAs are spread round-robin over the 148 SMs and the SM with the
+// most tiles finishes last; its work is max_tiles x tile area (padding included).
+// 2-warp CTAs sustain ~20 % less DMMA issue per SM (measured: 64x32 vs 64x64).
+template <int WGM, int WGN, int FM, int FN, int BK, int STAGES, bool BJC>
+static double fast_cost(const GemmParams& p) {
+  using Cfg = FastCfg<WGM, WGN, FM, FN, BK, STAGES, BJC>;
+  const int occ = fast_occupancy<WGM, WGN, FM, FN, BK, STAGES, BJC>();
   if (occ <= 0) return 1e300;
-  const double ctas = (double)((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN) * p.nb1 * p.nb2;
-  if (p.N < BN / 2) return 1e300;  // mostly padding
-  const double slots = 148.0 * occ;
-  const double rounds = std::ceil(ctas / slots);
-  // per-round time ~ one CTA's tile work at the SM's share of DMMA throughput
-  const double per_sm = std::min(ctas, slots) / 148.0;  // CTAs sharing an SM in a round
-  return rounds * (double)BM * BN * std::max(1.0, per_sm) / tile_eff;
+  const double ctas = (double)((p.M + Cfg::BM - 1) / Cfg::BM) * ((p.N + Cfg::BN - 1) / Cfg::BN) *
+                      p.nb1 * p.nb2;
+  const double per_sm = std::ceil(ctas / 148.0);
+  const double eff = (WGM * WGN <= 2) ? 0.8 : 1.0;
+  return per_sm * Cfg::BM * Cfg::BN / eff;
+}
+
+template <bool BJC>
+static void launch_variant(int id, const GemmParams& p, cudaStream_t st) {
+  switch (id) {
+#define PE_X(ID, WGM, WGN, FM, FN, BK, ST, AUTO) \
+  case ID:                                       \
+    launch_fast<WGM, WGN, FM, FN, BK, ST, BJC>(p, st); \
+    return;
+    PE_FAST_VARIANTS(PE_X)
+#undef PE_X
+    default:
+      launch_fast<2, 2, 4, 4, 16, 2, BJC>(p, st);
+  }
+}
+
+template <bool BJC>
+static int choose_variant(const GemmParams& p) {
+  int best = 5;
+  double bc = 1e300;
+#define PE_X(ID, WGM, WGN, FM, FN, BK, ST, AUTO)                     \
+  if (AUTO) {                                                        \
+    const double c = fast_cost<WGM, WGN, FM, FN, BK, ST, BJC>(p);   \
+    if (c < bc * 0.97) {                                             \
+      bc = c;                                                        \
+      best = ID;                                                     \
+    }                                                                \
+  }
+  PE_FAST_VARIANTS(PE_X)
+#undef PE_X
+  return best;
 }
 
 template <int BM, int BN, int BK, int WM, int WN>
@@ -506,9 +563,9 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
       GemmParams q = p;
       q.ksplit = ks;
       if (lay == 0)
-        launch_fast<64, 64, 32, 3, false>(q, st);
+        launch_fast<2, 2, 4, 4, 32, 3, false>(q, st);
       else
-        launch_fast<64, 64, 32, 3, true>(q, st);
+        launch_fast<2, 2, 4, 4, 32, 3, true>(q, st);
       const long long total = (long long)batch * p.M * p.N;
       splitk_reduce_kernel<<<(int)std::min<long long>(148 * 8, (total + 255) / 256), 256, 0, st>>>(q);
       ++g_launches;
@@ -517,31 +574,19 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
     }
   }
   if (lay >= 0 && (tiles64 >= 96 || tiles_n32 >= 96)) {
-    // pick the tile / pipeline variant with the best wave-quantised cost (N <= 32:
-    // narrow 128x32 tiles, no wasted half tile)
-    // measured on B200 (tools/gemm_bench.py): 64x64 / BK16 / 2 stages (4 CTAs/SM: more
-    // warps to cover the DMMA and barrier latencies) is the best variant on every hot-path
-    // shape except N <= 32 (64x32 / BK16 / 2 stages, 2 warps)
-    int best = (p.N <= 32) ? 7 : 5;
+    // pick the tile / pipeline variant with the best wave-quantised cost; the choice is a
+    // function of the shape only and never changes the arithmetic
     static const int forced = getenv("PE_GEMM_VARIANT") ? atoi(getenv("PE_GEMM_VARIANT")) : -1;
-    if (forced >= 0 && forced < 8) best = forced;  // tuning experiments only
-    if (lay == 0) {
-      if (best == 0) launch_fast<64, 64, 32, 3, false>(p, st);
-      else if (best == 1) launch_fast<64, 64, 16, 3, false>(p, st);
-      else if (best == 2) launch_fast<128, 64, 16, 3, false>(p, st);
-      else if (best == 3) launch_fast<128, 32, 32, 3, false>(p, st);
-      else if (best == 5) launch_fast<64, 64, 16, 2, false>(p, st);
-      else if (best == 6) launch_fast<64, 64, 32, 2, false>(p, st);
-      else launch_fast<64, 32, 16, 2, false>(p, st);
-    } else {
-      if (best == 0) launch_fast<64, 64, 32, 3, true>(p, st);
-      else if (best == 1) launch_fast<64, 64, 16, 3, true>(p, st);
-      else if (best == 2) launch_fast<128, 64, 16, 3, true>(p, st);
-      else if (best == 3) launch_fast<128, 32, 32, 3, true>(p, st);
-      else if (best == 5) launch_fast<64, 64, 16, 2, true>(p, st);
-      else if (best == 6) launch_fast<64, 64, 32, 2, true>(p, st);
-      else launch_fast<64, 32, 16, 2, true>(p, st);
-    }
+    int best = (lay == 0) ? choose_variant<false>(p) : choose_variant<true>(p);
+    if (forced >= 0 && forced < kMaxVariant && forced != 4) best = forced;  // tuning only
+    static const bool trace = getenv("PE_GEMM_TRACE") != nullptr;
+    if (trace)
+      fprintf(stderr, "pe_gemm M=%d N=%d K=%d batch=%lld lay=%d variant=%d\n", p.M, p.N,
+              p.seg[0].K, batch, lay, best);
+    if (lay == 0)
+      launch_variant<false>(best, p, st);
+    else
+      launch_variant<true>(best, p, st);
   } else if (tiles64 >= 2 * 148) {
     launch_cfg<64, 64, 16, 32, 32>(p, ak, bk, st);
   } else {

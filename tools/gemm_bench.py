@@ -1,5 +1,6 @@
 """Time libpe's DMMA GEMM (pe_gemm_f64, col-major C) against cuBLAS on the hot-path
-shapes.  PE_GEMM_VARIANT=0..3 forces a fast-path tile variant (tuning only)."""
+shapes.  PE_GEMM_VARIANT=<id> forces a fast-path tile variant (tuning only);
+PE_GEMM_TRACE=1 prints the variant the cost model picks."""
 import ctypes as C
 import os
 import sys
