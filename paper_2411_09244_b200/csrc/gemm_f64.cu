@@ -39,6 +39,54 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 }
 
 // AK: A is k-contiguous (s1 == 1); BKC: B is k-contiguous (s0 == 1).
+// Fused epilogue shared by both kernels: C = alpha acc + beta Cin + bias, D = C - Xp.
+// Per fragment row the Cin / Xp loads are all issued before any store: C may alias Cin (the
+// in-place recursion steps), which otherwise pins every load behind the previous store
+// (one global-latency round trip per element).  Each thread reads only the elements it
+// writes, so the hoisting is safe in place.
+template <int FM, int FN>
+__device__ __forceinline__ void gemm_epilogue(const GemmParams& p, int z1, int z2, int ibase,
+                                              int jbase, const double (&acc)[FM][FN][2]) {
+  const long long cb = z1 * p.c_b1 + z2 * p.c_b2;
+  double* C = p.C + cb;
+  const double* Cin = p.Cin ? p.Cin + cb : nullptr;
+  double* D = p.D ? p.D + cb : nullptr;
+  const double* Xp = p.Xp ? p.Xp + cb : nullptr;
+  const double* bias = p.bias ? p.bias + z1 * p.bias_b1 + z2 * p.bias_b2 : nullptr;
+  const bool alpha1 = (p.alpha == 1.0), beta1 = (p.beta == 1.0);
+#pragma unroll
+  for (int a = 0; a < FM; ++a) {
+    const int gi = ibase + a * 8;
+    if (gi >= p.M) continue;
+    const long long ro = gi * p.c_i;
+    // one prefetched operand per element: Cin when accumulating, else Xp for the D output
+    // (no call site uses both; if one did, Xp is read late)
+    const double* pf = Cin ? Cin : Xp;
+    double pre[FN][2];
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gj = jbase + b * 8 + h;
+        pre[b][h] = (pf && gj < p.N) ? pf[ro + gj * p.c_j] : 0.0;
+      }
+    const double bv = bias ? bias[gi] : 0.0;
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gj = jbase + b * 8 + h;
+        if (gj >= p.N) continue;
+        const long long off = ro + gj * p.c_j;
+        double v = alpha1 ? acc[a][b][h] : __dmul_rn(p.alpha, acc[a][b][h]);
+        if (Cin) v = __dadd_rn(v, beta1 ? pre[b][h] : __dmul_rn(p.beta, pre[b][h]));
+        if (bias) v = __dadd_rn(v, bv);
+        C[off] = v;
+        if (D) D[off] = __dsub_rn(v, Cin ? Xp[off] : pre[b][h]);
+      }
+  }
+}
+
 template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     gemm_f64_kernel(const __grid_constant__ GemmParams p) {
@@ -148,32 +196,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   }
 
   // fused epilogue
-  const long long cb = z1 * p.c_b1 + z2 * p.c_b2;
-  double* C = p.C + cb;
-  const double* Cin = p.Cin ? p.Cin + cb : nullptr;
-  double* D = p.D ? p.D + cb : nullptr;
-  const double* Xp = p.Xp ? p.Xp + cb : nullptr;
-  const double* bias = p.bias ? p.bias + z1 * p.bias_b1 + z2 * p.bias_b2 : nullptr;
-#pragma unroll
-  for (int a = 0; a < FM; ++a) {
-    const int gi = i0 + wm * WM + a * 8 + g;
-    if (gi >= p.M) continue;
-    const double bv = bias ? bias[gi] : 0.0;
-#pragma unroll
-    for (int b = 0; b < FN; ++b) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int gj = j0 + wn * WN + b * 8 + 2 * t4 + h;
-        if (gj >= p.N) continue;
-        const long long off = gi * p.c_i + gj * p.c_j;
-        double v = (p.alpha == 1.0) ? acc[a][b][h] : __dmul_rn(p.alpha, acc[a][b][h]);
-        if (Cin) v = __dadd_rn(v, (p.beta == 1.0) ? Cin[off] : __dmul_rn(p.beta, Cin[off]));
-        if (bias) v = __dadd_rn(v, bv);
-        C[off] = v;
-        if (D) D[off] = __dsub_rn(v, Xp[off]);
-      }
-    }
-  }
+  gemm_epilogue<FM, FN>(p, z1, z2, i0 + wm * WM + g, j0 + wn * WN + 2 * t4, acc);
 }
 
 
@@ -348,34 +371,7 @@ __global__ void __launch_bounds__(WGM * WGN * 32)
     return;
   }
 
-  const long long cb = z1 * p.c_b1 + z2 * p.c_b2;
-  double* C = p.C + cb;
-  const double* Cin = p.Cin ? p.Cin + cb : nullptr;
-  double* D = p.D ? p.D + cb : nullptr;
-  const double* Xp = p.Xp ? p.Xp + cb : nullptr;
-  const double* bias = p.bias ? p.bias + z1 * p.bias_b1 + z2 * p.bias_b2 : nullptr;
-  const bool alpha1 = (p.alpha == 1.0), beta1 = (p.beta == 1.0);
-#pragma unroll
-  for (int a = 0; a < FM; ++a) {
-    const int gi = i0 + wm * WTM + a * 8 + g;
-    if (gi >= p.M) continue;
-    const double bv = bias ? bias[gi] : 0.0;
-    const long long ro = gi * p.c_i;
-#pragma unroll
-    for (int b = 0; b < FN; ++b) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int gj = j0 + wn * WTN + b * 8 + 2 * t4 + h;
-        if (gj >= p.N) continue;
-        const long long off = ro + gj * p.c_j;
-        double v = alpha1 ? acc[a][b][h] : __dmul_rn(p.alpha, acc[a][b][h]);
-        if (Cin) v = __dadd_rn(v, beta1 ? Cin[off] : __dmul_rn(p.beta, Cin[off]));
-        if (bias) v = __dadd_rn(v, bv);
-        C[off] = v;
-        if (D) D[off] = __dsub_rn(v, Xp[off]);
-      }
-    }
-  }
+  gemm_epilogue<FM, FN>(p, z1, z2, i0 + wm * WTM + g, j0 + wn * WTN + 2 * t4, acc);
 }
 
 // Split-K reduction: C = alpha * sum_sp ws[sp] (splits in order) + epilogue.

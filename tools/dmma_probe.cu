@@ -42,6 +42,36 @@ __global__ void k_dfma(int iters, double* out) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// half the warps issue DMMA chains, the other half DFMA chains: do the two share a pipe?
+__global__ void k_mixed(int iters, int dfma_iters, double* out) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0;
+  if ((warp >> 2) & 1) {  // warps 4-7: DFMA on all four SMSPs; warps 0-3: DMMA
+    double c[8];
+    double a = threadIdx.x * 1e-3, b = 1.0 + blockIdx.x * 1e-6;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = i;
+    for (int it = 0; it < dfma_iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c[i] = fma(a, c[i], b);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i];
+  } else {
+    double c[8][2];
+    double a = threadIdx.x * 1e-3, b = 1.0 + blockIdx.x * 1e-6;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], a, b);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
   double* out;
   long long* cyc;
@@ -88,6 +118,18 @@ int main() {
   run_dfma(k_dfma<4>, 4, 148, 256);
   run_dfma(k_dfma<8>, 8, 296, 256);
   run_dfma(k_dfma<8>, 8, 592, 256);
+  for (int dfi : {0, 8000, 16000, 32000, 64000}) {
+    k_mixed<<<148, 256>>>(100, 100, out);
+    cudaEventRecord(a);
+    k_mixed<<<148, 256>>>(iters / 4, dfi, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    const double fd = 512.0 * 8 * (iters / 4) * 148.0 * 4, ff = 2.0 * 8 * dfi * 148.0 * 128;
+    printf("mixed dmma %.2f TF/s + dfma %.2f TF/s = %.2f TF/s (%.3f ms)\n", fd / ms / 1e9,
+           ff / ms / 1e9, (fd + ff) / ms / 1e9, ms);
+  }
   cudaError_t e = cudaGetLastError();
   printf("%s\n", cudaGetErrorString(e));
   return 0;

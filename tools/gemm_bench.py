@@ -11,8 +11,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2411_09244_b200 import _lib  # noqa: E402
 
-SHAPES = [  # (M, N, K, batch, label)
+SHAPES = [  # (M, N, K, batch, label); label ending in "jc": B stored j-contiguous (K x N)
+    (64, 19200, 64, 1, "cfg2 time transform jc"),
     (300, 4096, 600, 1, "cfg2 rhs/g"),
+    (300, 64, 300, 16, "cfg2 blocked-w H step"),
+    (300, 64, 300, 48, "cfg2 blocked-w fill"),
     (300, 64, 600, 66, "cfg2 shifted (batched)"),
     (600, 64, 1200, 1, "cfg2 seq step"),
     (600, 32, 1200, 64, "cfg4 seq step"),
@@ -25,18 +28,27 @@ SHAPES = [  # (M, N, K, batch, label)
 def main():
     lib = _lib.require_cuda()
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    only = os.environ.get("GEMM_BENCH_ONLY")
     for M, N, K, b, label in SHAPES:
+        if only and only not in label:
+            continue
         A = torch.randn(b, M, K, dtype=torch.float64, device="cuda")
-        B = torch.randn(b, N, K, dtype=torch.float64, device="cuda")  # k-contiguous columns
+        jc = label.endswith("jc")
+        if jc:
+            B = torch.randn(b, K, N, dtype=torch.float64, device="cuda")  # j-contiguous rows
+            bk, bj = N, 1
+        else:
+            B = torch.randn(b, N, K, dtype=torch.float64, device="cuda")  # k-contiguous columns
+            bk, bj = 1, K
         Cm = torch.empty(b, N, M, dtype=torch.float64, device="cuda")
 
         def mine():
             _lib.check(lib.pe_gemm_f64(M, N, K, b, C.c_void_p(A.data_ptr()), K, 1, M * K,
-                                       C.c_void_p(B.data_ptr()), 1, K, N * K,
+                                       C.c_void_p(B.data_ptr()), bk, bj, N * K,
                                        C.c_void_p(Cm.data_ptr()), 1, M, M * N, st))
 
         def cublas():
-            torch.bmm(A, B.transpose(1, 2))
+            torch.bmm(A, B if jc else B.transpose(1, 2))
 
         res = {}
         for name, fn in (("libpe", mine), ("cublas", cublas)):
