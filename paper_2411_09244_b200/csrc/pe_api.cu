@@ -114,11 +114,24 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
   } else {
     int rpc_, cs_;
     size_t sm_;
+    // algorithmic flops of J split steps: u rows contract [X; Dw], w rows [X; Dw; Du]
+    const double chain_flops = 2.0 * nc * E * J * ((double)c->d1 * (d + c->d2) + (double)c->d2 * 2 * d);
     if (J > 0 && c->use_recur && recur_plan(d, 2 * d, &rpc_, &cs_, &sm_)) {
       // all J substeps in one persistent cluster launch (T's row slices fit in smem)
       c->Xs.ensure(sizeof(double) * 4 * n + 8);
-      profiled(c, 2.0 * d * (2.0 * d) * nc * E * J, st, [&] {
+      profiled(c, chain_flops, st, [&] {
         recur_seq(E, d, nc, J, c->T.d(), c->cvec.d(), X_in, X_out, c->Xs.d(), st);
+      });
+      collect_profile(c, st);
+      return;
+    }
+    if (J > 0 && c->use_recur && seqgrid_fits(E, c->d1, c->d2, nc)) {
+      // T too large for a cluster: all SMs, T row slices resident, state through L2
+      c->Zg.ensure(sizeof(double) * 2 * (size_t)nc * 2 * d + 16);
+      c->gcnt.ensure(sizeof(unsigned) * ((size_t)nc + 8));
+      profiled(c, chain_flops, st, [&] {
+        seqgrid_seq(c->d1, c->d2, nc, J, c->T.d(), c->cvec.d(), X_in, X_out, c->Zg.d(),
+                    (unsigned*)c->gcnt.p, st);
       });
       collect_profile(c, st);
       return;

@@ -78,7 +78,7 @@ struct pe_ctx {
   pe::DevBuf Bk, BkT, RW, M11dt, GW, cg, Emat, Finv, Fw;
 
   // work buffers
-  pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs;
+  pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs, Zg, gcnt;
   pe::DevBuf Ux_cur, Ux_new, Wx_cur, Wx_new, R, P, Q, DU, DW, V, colstate, counter;
   pe::DevBuf partial, diff, Gc, active, hist_tmp, nrm, rhist, splitws;
   cudaStream_t work = nullptr;           // capture stream for the sweep graphs

@@ -97,6 +97,10 @@ void sub(long long n, const double* a, const double* b, double* out, cudaStream_
 
 // ---------------------------------------------------------------- recurrences (recur.cu)
 bool recur_plan(int M, int KT, int* rpc, int* cs, size_t* smem, int nclusters = 0);
+// sequential fine chain on all SMs when T is too large for one cluster (seqgrid.cu)
+bool seqgrid_fits(int E, int d1, int d2, int nc);
+bool seqgrid_seq(int d1, int d2, int nc, int S, const double* T, const double* c,
+                 const double* Xin, double* Xout, double* Z, unsigned* cnt, cudaStream_t st);
 bool recur_wr(int E, int d2, int nc, int J, const double* Emat, double* Wx, cudaStream_t st);
 bool recur_seq(int E, int d, int nc, int S, const double* T, const double* c, const double* Xin,
                double* Xout, double* scratch, cudaStream_t st);

@@ -65,7 +65,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[slot] = gtimer();
 
 __device__ __forceinline__ void dmma_rc(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }

@@ -608,3 +608,29 @@ def test_graph_replay_equals_direct_launches_bitwise():
     assert np.array_equal(sw1.cpu().numpy(), sw2.cpu().numpy())
     assert np.array_equal(np.nan_to_num(rh1.cpu().numpy(), nan=-1.0),
                           np.nan_to_num(rh2.cpu().numpy(), nan=-1.0))
+
+
+@pytest.mark.parametrize("d1,d2,nc,J", [(260, 301, 37, 5), (300, 300, 150, 3), (9, 560, 20, 4)])
+def test_sequential_all_sm_chain_against_oracle(d1, d2, nc, J):
+    """T too large for one cluster (d > ~500): the persistent all-SM chain (seqgrid.cu) with
+    ragged column groups and u/w row tiles that straddle the split, against the oracle's
+    split steps per interval and against the per-step GEMM path."""
+    P = _pkg()
+    mass, stiff, f = _random_coupled(d1, d2, 7 * d1 + d2 + nc)
+    blocks = dict(M11=mass[:d1, :d1], A11=stiff[:d1, :d1], M12=mass[:d1, d1:],
+                  A12=stiff[:d1, d1:], M22=mass[d1:, d1:], A22=stiff[d1:, d1:])
+    s = P.CoarseSystem(**{k: np.ascontiguousarray(v) for k, v in blocks.items()})
+    osys = po.OSystem(*(blocks[k] for k in ("M11", "A11", "M12", "A12", "M22", "A22")),
+                      f[:d1], f[d1:])
+    d, dt_int = d1 + d2, 0.02
+    X = np.random.default_rng(nc).standard_normal((1, nc, d)) * 0.3
+    ctx = P.PeContext([s], [P.ConstantLoads(f[:d1], f[d1:])], J)
+    ctx.prepare_sequential(dt_int / J)
+    Y = ctx.fine_sequential(ctx.to_dev(X)).cpu().numpy()[0]
+    ctx.set_recurrence(False)
+    Yg = ctx.fine_sequential(ctx.to_dev(X)).cpu().numpy()[0]
+    assert rel_rows(Y, Yg) < 1e-12
+    osp = po.OracleSplit(osys)
+    for n in range(0, nc, max(1, nc // 7)):
+        U, W = osp.fine_interval(X[0, n, :d1], X[0, n, d1:], dt_int, J)
+        assert rel_rows(Y[n][None], np.concatenate([U[-1], W[-1]])[None]) < REL
