@@ -16,6 +16,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "pe.h"
 #include "pe_internal.h"
@@ -45,7 +49,16 @@ struct CoarseArgs {
   double* partial;     // (E, N, cs, 2)
   double* diff;        // (E, 2)
   const int* active;   // (E) or null
+  unsigned long long* trace;  // optional per-step timestamps (CTA 0, thread 0), debug only
 };
+
+__device__ __forceinline__ unsigned long long cs_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CS_TRACE(slot) \
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[slot] = cs_timer();
 
 __device__ __forceinline__ unsigned cs_smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -70,19 +83,170 @@ __device__ __forceinline__ void cs_wait(unsigned bar, unsigned parity) {
       "@!p bra W_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
 }
 
-// x_{n+1} rows travel point to point: each new row is pushed (st.async, 8 bytes) into
-// every peer's double-buffered x with complete_tx on the peer's mbarrier; a CTA waits
-// only for the d*8 bytes of the step it consumes (same protocol as recur.cu).
-__global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_constant__ CoarseArgs a) {
+// x_{n+1} rows travel as one bulk DSMEM copy per peer: each CTA stages its new rows in a
+// double-buffered smem block and copies it into every peer's next x buffer, completing on
+// the peer's mbarrier (same protocol as recur.cu); a CTA waits only on its own mbarrier.
+// Rows are dealt in pairs so every copy is 16-byte aligned and sized (an odd d pads one
+// trailing zero).  Each warp computes all of its rows together (independent accumulators
+// sharing the x loads), and the per-warp norm partials go straight to global memory, so a
+// step has one CTA barrier (before the copies).
+__device__ __forceinline__ void cs_fence_proxy() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int RPW, bool PHIS>  // rows per warp (max); Phi slice in shared memory
+__device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int e, int r0, int nrows,
+                                             int ncopy, double* xs2, double* ybuf2,
+                                             const double* phis, unsigned bar0, unsigned xs_base,
+                                             unsigned yb_base, unsigned bytes) {
+  const int d = a.d, N = a.N;
+  const int xsd = 2 * ((d + 1) / 2) + 2;  // x buffer stride: even, so copies stay 16-byte aligned
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* X_old = a.X_old + (long long)e * (N + 1) * d;
+  double* X_new = a.X_new + (long long)e * (N + 1) * d;
+  const double* Phi = a.Phi + (long long)e * d * d;
+  const double* gv = a.gvec + (long long)e * d;
+  const double* F = a.F_hat ? a.F_hat + (long long)e * N * d : nullptr;
+  double* Gc = a.G_cache + (long long)e * N * d;
+  const double* rowp[RPW];
+  bool rv[RPW];
+  const int wrows = nrows > warp ? (nrows - warp + COARSE_WARPS - 1) / COARSE_WARPS : 0;
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) {
+    const int rr = warp + COARSE_WARPS * j;
+    rv[j] = rr < nrows;
+    rowp[j] = PHIS ? phis + (long long)(rv[j] ? rr : 0) * d
+                   : Phi + (long long)(r0 + (rv[j] ? rr : 0)) * d;
+  }
+  // lane j < RPW owns row warp + 8 j: its operands for step n are fetched one step ahead
+  const int myrr = warp + COARSE_WARPS * lane;
+  const bool mine = lane < RPW && myrr < nrows;
+  double nf_f = 0.0, nf_g = 0.0, nf_b = 0.0, nf_o = 0.0;
+  auto prefetch = [&](int n) {
+    if (n < N && mine) {
+      const long long o = (long long)n * d + r0 + myrr;
+      nf_b = gv[r0 + myrr];
+      nf_o = X_old[o + d];
+      if (F) {
+        nf_f = F[o];
+        nf_g = Gc[o];
+      }
+    }
+  };
+  prefetch(0);
+  for (int n = 0; n < N; ++n) {
+    const int cur = n & 1;
+    CS_TRACE(1 + 3 * n)
+    if (n > 0) {
+      cs_wait(bar0 + 8 * cur, ((n - 1) >> 1) & 1);
+      if (threadIdx.x == 0 && n + 2 < N) cs_expect(bar0 + 8 * cur, bytes);
+    }
+    CS_TRACE(2 + 3 * n)
+    const double* xs = xs2 + (size_t)cur * xsd;
+    double acc[RPW];
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) acc[j] = 0.0;
+    // lane-strided k (lane, lane+32, ...) in order, four k per pass with all loads issued
+    // before the FMAs; specialised on this warp's exact row count (warp-uniform) so that no
+    // load is issued for an absent row (the pass is shared-memory-bandwidth bound)
+    auto dot = [&](auto WR) {
+      constexpr int W = decltype(WR)::value;
+      for (int k0 = 0; k0 < d; k0 += 128) {
+        double xk[4], rk[W][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + 32 * u + lane;
+          xk[u] = (k < d) ? xs[k] : 0.0;
+#pragma unroll
+          for (int j = 0; j < W; ++j) rk[j][u] = (k < d) ? rowp[j][k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (k0 + 32 * u + lane < d)
+#pragma unroll
+            for (int j = 0; j < W; ++j) acc[j] = fma(rk[j][u], xk[u], acc[j]);
+      }
+    };
+    switch (wrows) {
+      case 0: break;
+      case 1: dot(std::integral_constant<int, 1>{}); break;
+      case 2: if constexpr (RPW >= 2) dot(std::integral_constant<int, 2>{}); break;
+      case 3: if constexpr (RPW >= 3) dot(std::integral_constant<int, 3>{}); break;
+      case 4: if constexpr (RPW >= 4) dot(std::integral_constant<int, 4>{}); break;
+      case 5: if constexpr (RPW >= 5) dot(std::integral_constant<int, 5>{}); break;
+      case 6: if constexpr (RPW >= 6) dot(std::integral_constant<int, 6>{}); break;
+      case 7: if constexpr (RPW >= 7) dot(std::integral_constant<int, 7>{}); break;
+      default: if constexpr (RPW >= 8) dot(std::integral_constant<int, 8>{}); break;
+    }
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[3 * N + 4 + 2 * n] = cs_timer();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[3 * N + 5 + 2 * n] = cs_timer();
+    double mya = 0.0;  // lane j keeps row j's sum
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+      if (lane == j) mya = acc[j];
+    const double pf_f = nf_f, pf_g = nf_g, pf_b = nf_b, pf_o = nf_o;
+    prefetch(n + 1);
+    double sd = 0.0, sn = 0.0;
+    double* ybuf = ybuf2 + (size_t)cur * ncopy;
+    if (mine) {
+      const long long o = (long long)n * d + r0 + myrr;
+      const double g = mya + pf_b;
+      const double x = F ? pf_f + (g - pf_g) : g;  // grouping kept exactly (parareal.py:209)
+      Gc[o] = g;
+      X_new[o + d] = x;
+      const double df = x - pf_o;
+      sd = df * df;
+      sn = x * x;
+      ybuf[myrr] = x;
+    }
+    // per-warp norm partials, summed later in (rank, warp) order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sd += __shfl_xor_sync(0xffffffffu, sd, o);
+      sn += __shfl_xor_sync(0xffffffffu, sn, o);
+    }
+    if (lane == 0) {
+      double* p = a.partial + ((((long long)e * N + n) * a.cs + rank) * COARSE_WARPS + warp) * 2;
+      p[0] = sd;
+      p[1] = sn;
+    }
+    CS_TRACE(3 + 3 * n)
+    if (n + 1 < N) {
+      // copies issued last step read the other ybuf parity; wait before it is rewritten next
+      if ((int)threadIdx.x < a.cs) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      cs_fence_proxy();
+      __syncthreads();
+      if ((int)threadIdx.x < a.cs) {
+        const int q = threadIdx.x;
+        const unsigned nbar = cs_map_rank(bar0 + 8 * ((n + 1) & 1), q);
+        const unsigned dst =
+            cs_map_rank(xs_base + (unsigned)((((n + 1) & 1) * xsd + r0) * 8), q);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(dst), "r"(yb_base + (unsigned)(cur * ncopy * 8)), "r"((unsigned)(ncopy * 8)), "r"(nbar)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+  }
+  if ((int)threadIdx.x < a.cs) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(COARSE_THREADS, 1) coarse_kernel(const __grid_constant__ CoarseArgs a) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int e = blockIdx.x / a.cs;
   const int d = a.d, N = a.N;
-  const int r0 = (int)((long long)rank * d / a.cs), r1 = (int)((long long)(rank + 1) * d / a.cs);
-  const int nrows = r1 - r0;
+  const int half = (d + 1) / 2;  // row pairs
+  const int p0 = (int)((long long)rank * half / a.cs), p1 = (int)((long long)(rank + 1) * half / a.cs);
+  const int r0 = 2 * p0, r1 = min(d, 2 * p1);
+  const int nrows = max(0, r1 - r0), ncopy = 2 * (p1 - p0);
   const double* X_old = a.X_old + (long long)e * (N + 1) * d;
   double* X_new = a.X_new + (long long)e * (N + 1) * d;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (a.active && a.active[e] == 0) {  // converged member: iterate frozen (whole cluster)
     for (long long t = threadIdx.x; t < (long long)(N + 1) * nrows; t += COARSE_THREADS) {
@@ -93,22 +257,22 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
   }
 
   extern __shared__ __align__(16) double sm[];
-  double* xs2 = sm;                         // 2 x d
-  double* wpart = xs2 + 2 * d;              // COARSE_WARPS * 2
-  double* phis = wpart + 2 * COARSE_WARPS;  // nrows * d (optional)
+  const int xsd = 2 * half + 2;                // even stride: 16-byte aligned copies
+  double* xs2 = sm;                            // 2 x xsd
+  double* ybuf2 = xs2 + 2 * xsd;               // 2 x ncopy_max
+  const int ncmax = 2 * ((half + a.cs - 1) / a.cs);
+  double* phis = ybuf2 + 2 * ncmax;            // nrows * d (optional)
   __shared__ __align__(8) unsigned long long mbar[2];
   const double* Phi = a.Phi + (long long)e * d * d;
-  const double* gv = a.gvec + (long long)e * d;
-  const double* F = a.F_hat ? a.F_hat + (long long)e * N * d : nullptr;
-  double* Gc = a.G_cache + (long long)e * N * d;
 
   if (a.phi_in_smem) {
     const double* src = Phi + (long long)r0 * d;
     for (long long t = threadIdx.x; t < (long long)nrows * d; t += COARSE_THREADS) phis[t] = src[t];
   }
-  for (int k = threadIdx.x; k < d; k += COARSE_THREADS) xs2[k] = X_old[k];
+  for (int k = threadIdx.x; k < 2 * xsd; k += COARSE_THREADS) xs2[k] = (k < d) ? X_old[k] : 0.0;
+  for (int k = threadIdx.x; k < 2 * ncmax; k += COARSE_THREADS) ybuf2[k] = 0.0;  // pad rows
   for (int r = r0 + threadIdx.x; r < r1; r += COARSE_THREADS) X_new[r] = X_old[r];
-  const unsigned bytes = (unsigned)(d * 8);
+  const unsigned bytes = (unsigned)(2 * half * 8);  // all CTAs' copies of one step
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cs_smem_u32(&mbar[0])) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cs_smem_u32(&mbar[1])) : "memory");
@@ -120,96 +284,34 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
     if (N > 2) cs_expect(cs_smem_u32(&mbar[0]), bytes);  // x_2 (pushed at step 1)
   }
   const unsigned bar0 = cs_smem_u32(&mbar[0]);
-  const unsigned xs_base = cs_smem_u32(xs2);
-
-  // per-row operands of step n (lane i <-> i-th row of the warp), fetched one step
-  // ahead so their L2 latency hides under the previous step
-  double nf_f = 0.0, nf_g = 0.0, nf_b = 0.0, nf_o = 0.0;
-  auto prefetch = [&](int n) {
-    const int rr = warp + COARSE_WARPS * lane;
-    if (n < N && rr < nrows) {
-      const long long o = (long long)n * d + r0 + rr;
-      nf_b = gv[r0 + rr];
-      nf_o = X_old[o + d];
-      if (F) {
-        nf_f = F[o];
-        nf_g = Gc[o];
-      }
-    }
+  const unsigned xs_base = cs_smem_u32(xs2), yb_base = cs_smem_u32(ybuf2);
+  const int rpw = (nrows + COARSE_WARPS - 1) / COARSE_WARPS;
+  auto run = [&](auto R, auto S) {
+    coarse_steps<decltype(R)::value, decltype(S)::value>(a, rank, e, r0, nrows, ncopy, xs2, ybuf2,
+                                                          phis, bar0, xs_base, yb_base, bytes);
   };
-  prefetch(0);
-  for (int n = 0; n < N; ++n) {
-    const int cur = n & 1;
-    if (n > 0) {
-      cs_wait(bar0 + 8 * cur, ((n - 1) >> 1) & 1);
-      if (threadIdx.x == 0 && n + 2 < N) cs_expect(bar0 + 8 * cur, bytes);
-    }
-    const double* xs = xs2 + (size_t)cur * d;
-    double sd = 0.0, sn = 0.0;  // this warp's partial ||x_new - x_old||^2, ||x_new||^2
-    const double pf_f = nf_f, pf_g = nf_g, pf_b = nf_b, pf_o = nf_o;
-    const bool push = (n + 1 < N);
-    const unsigned nbar = bar0 + 8 * ((n + 1) & 1);
-    const unsigned nbuf = xs_base + (unsigned)(((n + 1) & 1) * d * 8);
-    int i = 0;
-    for (int rr = warp; rr < nrows; rr += COARSE_WARPS, ++i) {
-      const int r = r0 + rr;
-      const double* row = a.phi_in_smem ? phis + (long long)rr * d : Phi + (long long)r * d;
-      double acc = 0.0;
-      for (int k = lane; k < d; k += 32) acc = fma(row[k], xs[k], acc);
-      acc = warp_sum_c(acc);
-      const long long o = (long long)n * d + r;
-      double fb = __shfl_sync(0xffffffffu, pf_b, i & 31);
-      double ff = __shfl_sync(0xffffffffu, pf_f, i & 31);
-      double fg = __shfl_sync(0xffffffffu, pf_g, i & 31);
-      double xo = __shfl_sync(0xffffffffu, pf_o, i & 31);
-      if (i >= 32) {  // more rows per warp than lanes: plain loads
-        fb = gv[r];
-        xo = X_old[o + d];
-        if (F) {
-          ff = F[o];
-          fg = Gc[o];
-        }
-      }
-      // every lane holds the warp sum: compute the row's value redundantly
-      const double g = acc + fb;
-      const double x = F ? ff + (g - fg) : g;
-      if (lane == 0) {
-        Gc[o] = g;
-        X_new[o + d] = x;
-        const double df = x - xo;
-        sd += df * df;
-        sn += x * x;
-      }
-      if (push)  // lane q pushes row r of x_{n+1} into CTA q
-        for (int q = lane; q < a.cs; q += 32)
-          cs_st_async(cs_map_rank(nbuf + (unsigned)(r * 8), q), x, cs_map_rank(nbar, q));
-    }
-    prefetch(n + 1);
-    if (lane == 0) {
-      wpart[2 * warp] = sd;
-      wpart[2 * warp + 1] = sn;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double td = 0.0, tn = 0.0;
-      for (int w = 0; w < COARSE_WARPS; ++w) {
-        td += wpart[2 * w];
-        tn += wpart[2 * w + 1];
-      }
-      double* p = a.partial + (((long long)e * N + n) * a.cs + rank) * 2;
-      p[0] = td;
-      p[1] = tn;
-    }
-    __syncthreads();  // wpart reused next step
-  }
-  cluster.sync();  // partials published; no CTA exits with pushes in flight
+  using T1 = std::true_type;
+  using F1 = std::false_type;
+  if (rpw <= 1)
+    a.phi_in_smem ? run(std::integral_constant<int, 1>{}, T1{}) : run(std::integral_constant<int, 1>{}, F1{});
+  else if (rpw <= 2)
+    a.phi_in_smem ? run(std::integral_constant<int, 2>{}, T1{}) : run(std::integral_constant<int, 2>{}, F1{});
+  else if (rpw <= 4)
+    a.phi_in_smem ? run(std::integral_constant<int, 4>{}, T1{}) : run(std::integral_constant<int, 4>{}, F1{});
+  else
+    a.phi_in_smem ? run(std::integral_constant<int, 8>{}, T1{}) : run(std::integral_constant<int, 8>{}, F1{});
+  cluster.sync();  // partials published; no CTA exits with copies in flight
 
-  if (rank == 0 && threadIdx.x == 0 && a.diff) {
+  if (rank == 0 && a.diff) {
+    // thread n sums interval n's (rank, warp) partials in order; max over intervals in a
+    // fixed smem tree (NaN propagates)
+    __shared__ double rd[COARSE_THREADS], rn[COARSE_THREADS];
+    const int nb = a.cs * COARSE_WARPS;
     double md = 0.0, mn = 0.0;
-    for (int n = 0; n < N; ++n) {
-      const double* p = a.partial + ((long long)e * N + n) * a.cs * 2;
+    for (int n = threadIdx.x; n < N; n += COARSE_THREADS) {
+      const double* p = a.partial + ((long long)e * N + n) * nb * 2;
       double td = 0.0, tn = 0.0;
-      for (int c = 0; c < a.cs; ++c) {
+      for (int c = 0; c < nb; ++c) {
         td += p[2 * c];
         tn += p[2 * c + 1];
       }
@@ -217,8 +319,21 @@ __global__ void __launch_bounds__(COARSE_THREADS) coarse_kernel(const __grid_con
       md = (nd > md || nd != nd) ? nd : md;
       mn = (nn > mn || nn != nn) ? nn : mn;
     }
-    a.diff[2 * e] = md;
-    a.diff[2 * e + 1] = mn;
+    rd[threadIdx.x] = md;
+    rn[threadIdx.x] = mn;
+    __syncthreads();
+    for (int o = COARSE_THREADS / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) {
+        const double x = rd[threadIdx.x + o], y = rn[threadIdx.x + o];
+        if (x > rd[threadIdx.x] || x != x) rd[threadIdx.x] = x;
+        if (y > rn[threadIdx.x] || y != y) rn[threadIdx.x] = y;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      a.diff[2 * e] = rd[0];
+      a.diff[2 * e + 1] = rn[0];
+    }
   }
 }
 
@@ -398,8 +513,9 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   a.d = d;
   a.N = N;
   a.cs = coarse_cluster_size(d);
-  const int rows_max = (d + a.cs - 1) / a.cs;
-  size_t base = sizeof(double) * (2 * d + 2 * COARSE_WARPS);
+  const int half = (d + 1) / 2;
+  const int rows_max = 2 * ((half + a.cs - 1) / a.cs);
+  size_t base = sizeof(double) * (2 * (size_t)(2 * half + 2) + 2 * (size_t)rows_max);
   size_t with_phi = base + sizeof(double) * (size_t)rows_max * d;
   a.phi_in_smem = with_phi <= 200 * 1024;
   // Large d (Phi not smem-resident) or many members (more member clusters than fit at
@@ -419,6 +535,12 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   a.partial = partial;
   a.diff = diff;
   a.active = active;
+  static const bool trace = getenv("PE_COARSE_TRACE") != nullptr;
+  a.trace = nullptr;
+  if (trace) {
+    PE_CUDA_CHECK(cudaMalloc(&a.trace, sizeof(unsigned long long) * (5 * N + 8)));
+    PE_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * (5 * N + 8), st));
+  }
   static bool attr_done = false;
   if (!attr_done) {
     PE_CUDA_CHECK(cudaFuncSetAttribute(coarse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -441,6 +563,23 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   cfg.numAttrs = 1;
   PE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, coarse_kernel, a));
   ++g_launches;
+  if (trace) {
+    std::vector<unsigned long long> h(5 * N + 8);
+    PE_CUDA_CHECK(cudaStreamSynchronize(st));
+    PE_CUDA_CHECK(cudaMemcpy(h.data(), a.trace, sizeof(unsigned long long) * h.size(),
+                             cudaMemcpyDeviceToHost));
+    double w = 0, cmp = 0, rest = 0, dot = 0, shf = 0;
+    for (int n = 0; n < N; ++n) {
+      dot += (h[3 * N + 4 + 2 * n] - h[2 + 3 * n]) * 1e-3;
+      shf += (h[3 * N + 5 + 2 * n] - h[3 * N + 4 + 2 * n]) * 1e-3;
+      w += (h[2 + 3 * n] - h[1 + 3 * n]) * 1e-3;
+      cmp += (h[3 + 3 * n] - h[2 + 3 * n]) * 1e-3;
+      if (n + 1 < N) rest += (h[1 + 3 * (n + 1)] - h[3 + 3 * n]) * 1e-3;
+    }
+    fprintf(stderr, "coarse trace (d=%d cs=%d): per step wait %.3f compute %.3f (dot %.3f shfl %.3f)"
+            " copy %.3f us\n", d, a.cs, w / N, cmp / N, dot / N, shf / N, rest / N);
+    cudaFree(a.trace);
+  }
 }
 
 }  // namespace pe
