@@ -449,8 +449,9 @@ def gpu_arm(args, wl, units_member):
                          "traffic_kernel": traffic.get("kernel"),
                          "traffic_algorithmic_bytes": traffic.get("algorithmic_bytes_per_launch"),
                          "traffic_source": traffic.get("source"),
-                         "kernel": "pe::gemm_f64_kernel (FP64 DMMA m8n8k4), all launches of "
-                                   "one instrumented step",
+                         "kernel": "every FP64 DMMA (m8n8k4) launch of one instrumented step: "
+                                   "GEMMs + recurrence / all-SM chains; algorithmic flops "
+                                   "(structural zeros and re-associated work not counted)",
                          "gemm_launches": st["launches"], "gemm_ms": st["gemm_ms"],
                          "gemm_flops": st["gemm_flops"], "gemm_share_of_step": gemm_share,
                          "peak_source": "cuBLAS DGEMM 8192^3 burst measured in this run "

@@ -554,7 +554,7 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
     int ktiles = 0;
     for (int sgi = 0; sgi < p.nseg; ++sgi) ktiles += (p.seg[sgi].K + 31) / 32;
     int ks = (int)std::min<long long>(8, 148 / std::max<long long>(1, mt));
-    ks = std::min(ks, ktiles / 4);
+    ks = std::min(ks, ktiles / 2);  // >= 2 k-tiles of 32 per split
     if (ks >= 2 && (size_t)ks * batch * p.M * p.N <= p.ws_doubles) {
       GemmParams q = p;
       q.ksplit = ks;

@@ -194,6 +194,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   c->V.ensure(sizeof(double) * E * L1 + 8);
   c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
   c->nrm.ensure(sizeof(double) * 2 * E * nc * J + 8);
+  ensure_zeroed(c->wticket, sizeof(unsigned) * (size_t)E * nc + 8);  // self-resetting tickets
   c->rhist.ensure(sizeof(double) * (size_t)E * nc * max_iter + 8);
   ensure_zeroed(c->splitws, sizeof(double) * (8 * (size_t)E * L1 + 32768));
   c->counter.ensure(sizeof(int) * 2);
@@ -338,6 +339,10 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
       rc.c_b1 = (J + 2) * L2;
       rc.Cin = rc.C;
       rc.beta = 1.0;
+      // N = nc columns only: split K when the row tiles alone leave SMs idle (cfg3: 64 row
+      // tiles x 2 column tiles); the split depends on (M, K, batch) only
+      rc.ws = c->splitws.d();
+      rc.ws_doubles = c->splitws.bytes / sizeof(double);
       post.push_back(rc);
     }
   }
@@ -357,7 +362,8 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
                  [&] { recur_wr(E, d2, nc, J, c->Emat.d(), Wn, s); });
     }
     wr_commit(E, nc, d1, d2, J, alpha, tol, max_iter, 0, Uc, Un, Wc, Wn, c->V.d(), cs,
-              c->rhist.d(), cnt + par, c->nrm.d(), (d1 && d2) ? c->DW.d() : nullptr, s);
+              c->rhist.d(), cnt + par, c->nrm.d(), (d1 && d2) ? c->DW.d() : nullptr,
+              (unsigned*)c->wticket.p, s);
     PE_CUDA_CHECK(cudaMemcpyAsync(host_cnt + par, cnt + par, sizeof(int), cudaMemcpyDeviceToHost, s));
   };
   // CUDA graphs (one per counter parity) replace the per-sweep host launch sequence when
@@ -370,7 +376,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     const std::vector<const void*> key = {
         Uc, Un, Wc, Wn, c->R.p, c->P.p, c->Q.p, c->DU.p, c->DW.p, c->V.p, cs, c->nrm.p,
         c->rhist.p, cnt, host_cnt, c->splitws.p, c->Bk.p, c->RW.p, c->GW.p, c->Emat.p, c->Finv.p, c->Fw.p,
-        c->M11dt.p, c->cg.p, c->f1.p, (const void*)(intptr_t)max_iter,
+        c->M11dt.p, c->cg.p, c->f1.p, c->wticket.p, (const void*)(intptr_t)max_iter,
         (const void*)(intptr_t)(c->use_recur ? 1 : 0),
         (const void*)(intptr_t)(alpha * 1e6), (const void*)(intptr_t)(tol * 1e18),
         (const void*)(intptr_t)nk};
@@ -396,6 +402,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
         PE_CUDA_CHECK(cudaGraphDestroy(g));
       }
       sg->key = key;
+      sg->kernels = (int)((g_launches - launches_before) / 2);  // kernel nodes per graph
       g_launches = launches_before;
     }
   }
@@ -415,9 +422,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     PE_CUDA_CHECK(cudaEventRecord(ev[sweep & 1], st));
     collect_profile(c, st);
   };
-  if (sg)  // kernels per graph replay, for the native-launch evidence counter
-    c->graph_kernels = (int)(pre.size() + (d2 ? 1 + post.size() + (use_rw ? 1 : 0) : 0) +
-                             (d1 ? 1 : 0) + 2);
+  if (sg) c->graph_kernels = sg->kernels;  // kernels per graph replay (launch evidence)
   int sweep = 0;
   enqueue_sweep(0);
   for (sweep = 1; sweep <= max_iter; ++sweep) {

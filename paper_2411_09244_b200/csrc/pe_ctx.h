@@ -44,6 +44,7 @@ struct DevBuf {
 struct SweepGraphs {
   std::vector<const void*> key;
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  int kernels = 0;  // kernel launches recorded per captured sweep
 };
 
 struct FineStats {
@@ -78,7 +79,7 @@ struct pe_ctx {
   pe::DevBuf Bk, BkT, RW, M11dt, GW, cg, Emat, Finv, Fw;
 
   // work buffers
-  pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs, Zg, gcnt;
+  pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs, Zg, gcnt, wticket;
   pe::DevBuf Ux_cur, Ux_new, Wx_cur, Wx_new, R, P, Q, DU, DW, V, colstate, counter;
   pe::DevBuf partial, diff, Gc, active, hist_tmp, nrm, rhist, splitws;
   cudaStream_t work = nullptr;           // capture stream for the sweep graphs

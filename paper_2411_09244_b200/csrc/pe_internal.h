@@ -87,7 +87,7 @@ void wr_diff_u(int E, int ncols, int d1, int J, const double* Ux_new, double* DU
 void wr_commit(int E, int ncols, int d1, int d2, int J, double alpha, double tol,
                int max_iter, int sweep, double* Ux_cur, const double* Ux_new, double* Wx_cur,
                const double* Wx_new, double* V, WrColumnState* cs, double* resid_hist,
-               int* active_count, double* nrm, double* DW, cudaStream_t st);
+               int* active_count, double* nrm, double* DW, unsigned* ticket, cudaStream_t st);
 void wr_finish(int E, int ncols, int d1, int d2, int J, const double* Ux_cur,
                const double* Wx_cur, const WrColumnState* cs, double* X_out, int* sweeps,
                int* reasons, cudaStream_t st);

@@ -111,17 +111,12 @@ __device__ __forceinline__ double warp_sum(double v) {
 constexpr int COMMIT_THREADS = 256;
 constexpr int COMMIT_WARPS = COMMIT_THREADS / 32;
 
-// Phase 1 (wide): one warp per (member, interval, substep) row: ||dU_s||, ||dW_s|| into
-// nrm[en][s][2] and, for intervals still iterating, commit new -> cur (allatonce.py:256).
-__global__ void __launch_bounds__(COMMIT_THREADS)
-    wr_commit_norms_kernel(int nc, int d1, int d2, int J, double* Ux_cur,
-                           const double* __restrict__ Ux_new, double* Wx_cur,
-                           const double* __restrict__ Wx_new, const WrColumnState* cs,
-                           double* nrm, double* DW) {
-  const int en = blockIdx.x;
-  const int s = blockIdx.y * COMMIT_WARPS + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (s >= J || !cs[en].active) return;
+// One warp per (interval, substep) row: ||dU_s||, ||dW_s|| into nrm[en][s][2], commit
+// new -> cur (allatonce.py:256) and DW for the next rhs.
+__device__ __forceinline__ void wr_commit_rows(int en, int s, int lane, int nc, int d1, int d2,
+                                               int J, double* Ux_cur, const double* __restrict__ Ux_new,
+                                               double* Wx_cur, const double* __restrict__ Wx_new,
+                                               double* nrm, double* DW) {
   const int e = en / nc, n = en - (en / nc) * nc;
   const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
   const long long bu = (long long)e * (J + 2) * L1 + (long long)(s + 2) * L1 + (long long)n * d1;
@@ -185,20 +180,17 @@ __global__ void __launch_bounds__(COMMIT_THREADS)
   }
 }
 
-// Phase 2: one warp per interval.  Residual = max_s ||dU_s|| + max_s ||dW_s||
+// Stop decision for one interval, one warp: residual = max_s ||dU_s|| + max_s ||dW_s||
 // (:250-254), u_final_prev update (:257), stop tests tol / diverged / floor (:258-271)
-// and the max_iter cap.
-__global__ void __launch_bounds__(COMMIT_THREADS)
-    wr_commit_decide_kernel(int ncols_total, int nc, int d1, int d2, int J, double alpha,
-                            double tol, int max_iter, const double* __restrict__ Ux_new,
-                            double* V, WrColumnState* cs, const double* __restrict__ nrm,
-                            double* resid_hist, int* active_count) {
-  const int en = blockIdx.x * COMMIT_WARPS + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (en >= ncols_total || !cs[en].active) return;
+// and the max_iter cap.  nrm was written by other CTAs of the same launch: read from L2.
+__device__ void wr_decide_interval(int en, int lane, int nc, int d1, int d2, int J, double alpha,
+                                   double tol, int max_iter, const double* __restrict__ Ux_new,
+                                   double* V, WrColumnState* cs, const double* nrm,
+                                   double* resid_hist, int* active_count) {
   double mu = 0.0, mw = 0.0;
   for (int s = lane; s < J; s += 32) {
-    const double a = nrm[((long long)en * J + s) * 2], b = nrm[((long long)en * J + s) * 2 + 1];
+    const double a = __ldcg(nrm + ((long long)en * J + s) * 2);
+    const double b = __ldcg(nrm + ((long long)en * J + s) * 2 + 1);
     mu = (a > mu || a != a) ? a : mu;
     mw = (b > mw || b != b) ? b : mw;
   }
@@ -250,18 +242,44 @@ __global__ void __launch_bounds__(COMMIT_THREADS)
   }
 }
 
+// One CTA per (member, interval, 8 substeps): the rows, then (last CTA) the decision.
+// Phase 1 (wide): one warp per (member, interval, substep) row: ||dU_s||, ||dW_s|| into
+// nrm[en][s][2] and, for intervals still iterating, commit new -> cur (allatonce.py:256).
+__global__ void __launch_bounds__(COMMIT_THREADS)
+    wr_commit_norms_kernel(int nc, int d1, int d2, int J, double* Ux_cur,
+                           const double* __restrict__ Ux_new, double* Wx_cur,
+                           const double* __restrict__ Wx_new, WrColumnState* cs,
+                           double* nrm, double* DW, double alpha, double tol, int max_iter,
+                           double* V, double* resid_hist, int* active_count,
+                           unsigned* ticket) {
+  const int en = blockIdx.x;
+  const int s = blockIdx.y * COMMIT_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (!cs[en].active) return;  // block-uniform
+  if (s < J) wr_commit_rows(en, s, lane, nc, d1, d2, J, Ux_cur, Ux_new, Wx_cur, Wx_new, nrm, DW);
+  // the last CTA of this interval (ticket) runs the stop decision: no second launch
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (threadIdx.x == 0) last = (atomicAdd(ticket + en, 1u) == gridDim.y - 1);
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x == 0) ticket[en] = 0u;  // self-resetting for the next sweep
+  __threadfence();
+  if ((threadIdx.x >> 5) == 0)
+    wr_decide_interval(en, lane, nc, d1, d2, J, alpha, tol, max_iter, Ux_new, V, cs, nrm,
+                       resid_hist, active_count);
+}
+
 void wr_commit(int E, int nc, int d1, int d2, int J, double alpha, double tol, int max_iter,
                int /*sweep*/, double* Ux_cur, const double* Ux_new, double* Wx_cur,
                const double* Wx_new, double* V, WrColumnState* cs, double* resid_hist,
-               int* active_count, double* nrm, double* DW, cudaStream_t st) {
+               int* active_count, double* nrm, double* DW, unsigned* ticket, cudaStream_t st) {
   dim3 g1(E * nc, (J + COMMIT_WARPS - 1) / COMMIT_WARPS);
   wr_commit_norms_kernel<<<g1, COMMIT_THREADS, 0, st>>>(nc, d1, d2, J, Ux_cur, Ux_new, Wx_cur,
-                                                        Wx_new, cs, nrm, DW);
-  ++g_launches;
-  PE_CUDA_CHECK(cudaGetLastError());
-  const int cols = E * nc;
-  wr_commit_decide_kernel<<<(cols + COMMIT_WARPS - 1) / COMMIT_WARPS, COMMIT_THREADS, 0, st>>>(
-      cols, nc, d1, d2, J, alpha, tol, max_iter, Ux_new, V, cs, nrm, resid_hist, active_count);
+                                                        Wx_new, cs, nrm, DW, alpha, tol,
+                                                        max_iter, V, resid_hist, active_count,
+                                                        ticket);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
 }
