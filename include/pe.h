@@ -152,6 +152,14 @@ int pe_set_profiling(pe_ctx* ctx, int on);
 /* Select the persistent cluster-resident recurrence kernels for the sequential-in-time
  * chains (default on) or one DMMA GEMM launch per step (reference-like structure). */
 int pe_set_recurrence(pe_ctx* ctx, int on);
+/* Select the modal form of the all-at-once w recursion (default on).  When M22 is SPD
+ * and A22 symmetric, pe_prepare_allatonce diagonalises E = I - dt M22^-1 A22 =
+ * V diag(lam) V^-1 (M22-orthonormal pencil eigenvectors, accepted only if it reproduces E
+ * to 1e-9); each sweep then runs the J-step w chain of WaveformRelaxation._w_sweep
+ * (allatonce.py:220-230) as an elementwise scan in z = V^-1 w plus one W = V Z GEMM.
+ * pe_wr_is_modal returns 1 when the prepared solver uses it, 0 otherwise. */
+int pe_set_modal(pe_ctx* ctx, int on);
+int pe_wr_is_modal(pe_ctx* ctx);
 int pe_last_fine_stats(pe_ctx* ctx, double* gemm_ms, double* gemm_flops, int* launches);
 
 #ifdef __cplusplus

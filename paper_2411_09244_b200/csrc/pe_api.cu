@@ -305,17 +305,21 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
   }
   int rpc_, cs_;
   size_t sm_;
-  const bool use_rw = c->use_recur && d2 > 0 && recur_plan(d2, d2, &rpc_, &cs_, &sm_);
+  // modal w recursion (setup_modal): h = V^-1 g by the g GEMM, z scan, W = V Z
+  const bool modal = c->wr_modal && c->use_modal && d2 > 0;
+  const bool use_rw = !modal && c->use_recur && d2 > 0 && recur_plan(d2, d2, &rpc_, &cs_, &sm_);
   GemmParams gw;  // g_s = [Gu|Gd][U_s; U_{s-1}-U_{s-2}] + dt M22^-T f2   (_w_sweep :222-224)
+  GemmParams wb;  // modal back-transform W_s = V Z_s, all s in one launch
   if (d2) {
     gw.M = d2;
     gw.N = J * nc;
     gw.nb1 = E;
     gw.nseg = d1 ? 2 : 0;
-    gw.seg[0].A = Operand{c->GW.d(), 2LL * d1, 1, 2LL * d1 * d2, 0};
+    const double* G = modal ? c->GZ.d() : c->GW.d();
+    gw.seg[0].A = Operand{G, 2LL * d1, 1, 2LL * d1 * d2, 0};
     gw.seg[0].B = Operand{Un + 2 * L1, 1, d1, (J + 2) * L1, 0};
     gw.seg[0].K = d1;
-    gw.seg[1].A = Operand{c->GW.d() + d1, 2LL * d1, 1, 2LL * d1 * d2, 0};
+    gw.seg[1].A = Operand{G + d1, 2LL * d1, 1, 2LL * d1 * d2, 0};
     gw.seg[1].B = Operand{c->DU.d(), 1, d1, J * L1, 0};
     gw.seg[1].K = d1;
     gw.C = Wn + 2 * L2;
@@ -324,7 +328,40 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     gw.c_b1 = (J + 2) * L2;
     gw.bias = c->cg.d();
     gw.bias_b1 = d2;
-    for (int s = 0; s < J && !use_rw; ++s) {  // w_{s+1} = E w_s + g_s   (:226-229)
+    if (modal) {
+      c->Z0.ensure(sizeof(double) * E * L2 + 8);
+      c->Hz.ensure(sizeof(double) * E * J * L2 + 8);
+      gw.C = c->Hz.d();
+      gw.c_b1 = J * L2;
+      gw.bias = c->cgz.d();
+      GemmParams z0;  // Z0 = V^-1 w0, once per solve (w0 is fixed across sweeps)
+      z0.M = d2;
+      z0.N = nc;
+      z0.nb1 = E;
+      z0.nseg = 1;
+      z0.seg[0].A = Operand{c->Vinv.d(), d2, 1, (long long)d2 * d2, 0};
+      z0.seg[0].B = Operand{Wn + L2, 1, d2, (J + 2) * L2, 0};
+      z0.seg[0].K = d2;
+      z0.C = c->Z0.d();
+      z0.c_i = 1;
+      z0.c_j = d2;
+      z0.c_b1 = L2;
+      z0.ws = c->splitws.d();
+      z0.ws_doubles = c->splitws.bytes / sizeof(double);
+      gemm_f64(z0, st);
+      wb.M = d2;
+      wb.N = J * nc;
+      wb.nb1 = E;
+      wb.nseg = 1;
+      wb.seg[0].A = Operand{c->Vm.d(), d2, 1, (long long)d2 * d2, 0};
+      wb.seg[0].B = Operand{c->Hz.d(), 1, d2, J * L2, 0};
+      wb.seg[0].K = d2;
+      wb.C = Wn + 2 * L2;
+      wb.c_i = 1;
+      wb.c_j = d2;
+      wb.c_b1 = (J + 2) * L2;
+    }
+    for (int s = 0; s < J && !use_rw && !modal; ++s) {  // w_{s+1} = E w_s + g_s   (:226-229)
       GemmParams rc;
       rc.M = d2;
       rc.N = nc;
@@ -356,6 +393,10 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
     if (d1) wr_diff_u(E, nc, d1, J, Un, c->DU.d(), s);
     if (d2) {
       run_gemm(c, gw, s);
+      if (modal) {
+        wr_modal_scan(E, nc, d2, J, c->lam.d(), c->Z0.d(), c->Hz.d(), s);
+        run_gemm(c, wb, s);
+      }
       for (auto& p : post) run_gemm(c, p, s);
       if (use_rw)  // all J steps of the w recursion in one cluster-resident launch
         profiled(c, 2.0 * d2 * d2 * nc * E * J, s,
@@ -379,7 +420,8 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
         c->M11dt.p, c->cg.p, c->f1.p, c->wticket.p, (const void*)(intptr_t)max_iter,
         (const void*)(intptr_t)(c->use_recur ? 1 : 0),
         (const void*)(intptr_t)(alpha * 1e6), (const void*)(intptr_t)(tol * 1e18),
-        (const void*)(intptr_t)nk};
+        (const void*)(intptr_t)nk, (const void*)(intptr_t)(modal ? 1 : 0), c->Vm.p, c->lam.p,
+        c->GZ.p, c->cgz.p, c->Z0.p, c->Hz.p};
     sg = &c->sweep_graphs[nc];
     if (sg->key != key) {
       for (auto& ex : sg->exec)
@@ -779,6 +821,18 @@ int pe_set_recurrence(pe_ctx* c, int on) {
     require(c != nullptr, PE_ERR_ARG, "ctx is NULL");
     c->use_recur = on != 0;
   });
+}
+
+int pe_set_modal(pe_ctx* c, int on) {
+  return guarded([&] {
+    require(c != nullptr, PE_ERR_ARG, "ctx is NULL");
+    c->use_modal = on != 0;
+  });
+}
+
+int pe_wr_is_modal(pe_ctx* c) {
+  if (!c) return PE_ERR_ARG;
+  return (c->wr_ready && c->wr_modal && c->use_modal) ? 1 : 0;
 }
 
 int pe_set_profiling(pe_ctx* c, int on) {

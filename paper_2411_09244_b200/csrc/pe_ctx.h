@@ -77,6 +77,10 @@ struct pe_ctx {
   int wr_max_iter = 0;
   int wr_nk = 0;  // solved time modes (half spectrum, floor(J/2) + 1)
   pe::DevBuf Bk, BkT, RW, M11dt, GW, cg, Emat, Finv, Fw;
+  // modal w recursion (setup_modal): E = Vm diag(lam) Vinv; GZ = Vinv GW, cgz = Vinv cg
+  bool wr_modal = false;   // decided by setup (every member passed the reconstruction check)
+  bool use_modal = true;   // user switch (pe_set_modal)
+  pe::DevBuf Vm, Vinv, lam, GZ, cgz, Z0, Hz;
 
   // work buffers
   pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs, Zg, gcnt, wticket;

@@ -92,6 +92,8 @@ void wr_finish(int E, int ncols, int d1, int d2, int J, const double* Ux_cur,
                const double* Wx_cur, const WrColumnState* cs, double* X_out, int* sweeps,
                int* reasons, cudaStream_t st);
 
+void wr_modal_scan(int E, int nc, int d2, int J, const double* lam, const double* Z0, double* Z,
+                   cudaStream_t st);
 void wr_gather(int E, int nc, int dd, int J, const double* X, double* out, cudaStream_t st);
 void sub(long long n, const double* a, const double* b, double* out, cudaStream_t st);
 

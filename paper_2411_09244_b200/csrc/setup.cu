@@ -302,6 +302,70 @@ void setup_coarse(pe_ctx* c, double dt) {
   c->coarse_dt = dt;
 }
 
+// Modal form of the w recursion w_{s+1} = E w_s + g_s (allatonce.py:226-229).
+// E = I - dt M22^-1 A22 is similar to a symmetric matrix when A22 is symmetric and M22 is
+// SPD: with the M22-orthonormal eigenvectors V of the pencil A22 v = mu M22 v
+// (V^T M22 V = I), E = V diag(lam) V^-1 with lam = 1 - dt mu and V^-1 = V^T M22.  In
+// z = V^-1 w the J-step chain decouples into d2 scalar recurrences z_{s+1} = lam z_s + h_s,
+// h_s = V^-1 g_s, so the sequential-in-time part of a sweep becomes an elementwise scan and
+// W = V Z one parallel GEMM.  The decomposition is accepted only when V diag(lam) V^-1
+// reproduces the E the reference forms (`e_mat`, :207) to 1e-9 relative in max norm; a
+// non-symmetric A22 or indefinite M22 fails that check and keeps the direct recursion.
+static bool setup_modal(pe_ctx* c, int e, double dt, const double* M22, const double* A22,
+                        const double* Em, const double* GW, const double* cg) {
+  const int d1 = c->d1, n = c->d2;
+  cudaStream_t st = c->setup_stream;
+  cublasHandle_t h = c->blas;
+  DevBuf A, B, W, info, work, Vl, Er;
+  A.ensure(sizeof(double) * (size_t)n * n);
+  B.ensure(sizeof(double) * (size_t)n * n);
+  W.ensure(sizeof(double) * n);
+  info.ensure(sizeof(int));
+  PE_CUDA_CHECK(cudaMemcpyAsync(A.p, A22, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, st));
+  PE_CUDA_CHECK(cudaMemcpyAsync(B.p, M22, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, st));
+  int lwork = 0;
+  SOLVER_CHECK(cusolverDnDsygvd_bufferSize(c->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                           CUBLAS_FILL_MODE_LOWER, n, A.d(), n, B.d(), n, W.d(), &lwork));
+  work.ensure(sizeof(double) * std::max(lwork, 1));
+  SOLVER_CHECK(cusolverDnDsygvd(c->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                CUBLAS_FILL_MODE_LOWER, n, A.d(), n, B.d(), n, W.d(), work.d(),
+                                lwork, info.i()));
+  int h_info = 0;
+  PE_CUDA_CHECK(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (h_info != 0) return false;  // M22 not positive definite (or no convergence)
+  // A now holds the eigenvectors column-major, i.e. V^T when read row-major
+  double* V = c->Vm.d() + (size_t)e * n * n;
+  double* Vi = c->Vinv.d() + (size_t)e * n * n;
+  double* lam = c->lam.d() + (size_t)e * n;
+  rm_geam(h, true, false, n, n, 1.0, A.d(), n, 0.0, A.d(), n, V, n);
+  rm_gemm(h, false, false, n, n, n, 1.0, A.d(), n, M22, n, 0.0, Vi, n);  // V^T M22
+  std::vector<double> hl(n);
+  PE_CUDA_CHECK(cudaMemcpyAsync(hl.data(), W.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  for (auto& x : hl) x = 1.0 - dt * x;
+  PE_CUDA_CHECK(cudaMemcpyAsync(lam, hl.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  // reconstruction check against the reference-form E
+  Vl.ensure(sizeof(double) * (size_t)n * n);
+  Er.ensure(sizeof(double) * (size_t)n * n);
+  // row-major V scaled by columns == column-major V^T scaled by rows
+  BLAS_CHECK(cublasDdgmm(h, CUBLAS_SIDE_LEFT, n, n, V, n, lam, 1, Vl.d(), n));
+  rm_gemm(h, false, false, n, n, n, 1.0, Vl.d(), n, Vi, n, 0.0, Er.d(), n);
+  rm_geam(h, false, false, n, n, 1.0, Er.d(), n, -1.0, Em, n, Er.d(), n);
+  int idiff = 0, iref = 0;
+  BLAS_CHECK(cublasIdamax(h, n * n, Er.d(), 1, &idiff));
+  BLAS_CHECK(cublasIdamax(h, n * n, Em, 1, &iref));
+  double vdiff = 0, vref = 0;
+  PE_CUDA_CHECK(cudaMemcpyAsync(&vdiff, Er.d() + idiff - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+  PE_CUDA_CHECK(cudaMemcpyAsync(&vref, Em + iref - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (!(std::fabs(vdiff) <= 1e-9 * std::fabs(vref))) return false;
+  if (d1) rm_gemm(h, false, false, n, 2 * d1, n, 1.0, Vi, n, GW, 2 * d1, 0.0,
+                  c->GZ.d() + (size_t)e * n * 2 * d1, 2 * d1);
+  rm_gemm(h, false, false, n, 1, n, 1.0, Vi, n, cg, 1, 0.0, c->cgz.d() + (size_t)e * n, 1);
+  return true;
+}
+
 void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_iter) {
   const int d1 = c->d1, d2 = c->d2, J = c->J, E = c->E;
   cudaStream_t st = c->setup_stream;
@@ -417,6 +481,21 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
   if (wr_tiny_eligible(d1, d2, J, npm)) {  // transposed Bk for the fused small-problem path
     c->BkT.ensure(sizeof(double) * (size_t)E * npm * 4 * d1 * d1 + 8);
     transpose_blocks(E * npm, 2 * d1, c->Bk.d(), c->BkT.d(), st);
+  }
+  c->wr_modal = false;
+  if (d2 > 0 && !wr_tiny_eligible(d1, d2, J, npm)) {
+    c->Vm.ensure(sizeof(double) * (size_t)E * d2 * d2 + 8);
+    c->Vinv.ensure(sizeof(double) * (size_t)E * d2 * d2 + 8);
+    c->lam.ensure(sizeof(double) * (size_t)E * d2 + 8);
+    c->GZ.ensure(sizeof(double) * (size_t)E * d2 * 2 * d1 + 8);
+    c->cgz.ensure(sizeof(double) * (size_t)E * d2 + 8);
+    PE_CUDA_CHECK(cudaStreamSynchronize(st));
+    bool ok = true;
+    for (int e = 0; e < E && ok; ++e)
+      ok = setup_modal(c, e, dt, c->M22.d() + (size_t)e * d2 * d2, c->A22.d() + (size_t)e * d2 * d2,
+                       c->Emat.d() + (size_t)e * d2 * d2, c->GW.d() + (size_t)e * d2 * 2 * d1,
+                       c->cg.d() + (size_t)e * d2);
+    c->wr_modal = ok;
   }
   PE_CUDA_CHECK(cudaStreamSynchronize(st));
   c->wr_ready = true;

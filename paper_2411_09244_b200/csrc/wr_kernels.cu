@@ -101,6 +101,51 @@ void wr_diff_u(int E, int nc, int d1, int J, const double* Ux_new, double* DU,
   PE_CUDA_CHECK(cudaGetLastError());
 }
 
+// Modal w recursion (setup_modal): z_{s+1} = lam z_s + h_s for every (member, mode i,
+// interval n), in place over Z = H (J blocks of a d2 x nc column-major matrix), z_{-1} = Z0.
+// One thread per (e, i, n); consecutive threads walk consecutive modes, so every block
+// access is coalesced.  The loads of 8 steps are issued before their dependent FMAs.
+constexpr int SCAN_DEPTH = 8;
+__global__ void wr_modal_scan_kernel(long long L2, int d2, int J, int E,
+                                     const double* __restrict__ lam,
+                                     const double* __restrict__ Z0, double* __restrict__ Z) {
+  const long long total = L2 * E;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(t / L2);
+    const long long r = t - e * L2;
+    const double l = lam[(long long)e * d2 + (int)(r % d2)];
+    double z = Z0[t];
+    double* p = Z + (long long)e * J * L2 + r;
+    int s = 0;
+    for (; s + SCAN_DEPTH <= J; s += SCAN_DEPTH) {
+      double h[SCAN_DEPTH];
+#pragma unroll
+      for (int q = 0; q < SCAN_DEPTH; ++q) h[q] = p[(long long)(s + q) * L2];
+#pragma unroll
+      for (int q = 0; q < SCAN_DEPTH; ++q) {
+        z = fma(l, z, h[q]);
+        p[(long long)(s + q) * L2] = z;
+      }
+    }
+    for (; s < J; ++s) {
+      z = fma(l, z, p[(long long)s * L2]);
+      p[(long long)s * L2] = z;
+    }
+  }
+}
+
+void wr_modal_scan(int E, int nc, int d2, int J, const double* lam, const double* Z0, double* Z,
+                   cudaStream_t st) {
+  const long long L2 = (long long)d2 * nc;
+  const long long total = L2 * E;
+  if (total == 0 || J == 0) return;
+  int blocks = (int)std::min<long long>((total + 127) / 128, 148 * 16);
+  wr_modal_scan_kernel<<<blocks, 128, 0, st>>>(L2, d2, J, E, lam, Z0, Z);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
 // Deterministic warp sum: lane-strided partial sums then a fixed xor tree.
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

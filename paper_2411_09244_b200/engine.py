@@ -171,6 +171,15 @@ class PeContext:
     def set_recurrence(self, on: bool):
         check(self.lib.pe_set_recurrence(self.ptr, 1 if on else 0))
 
+    def set_modal(self, on: bool):
+        """Modal (diagonalised) w recursion for the all-at-once solver (pe_set_modal)."""
+        check(self.lib.pe_set_modal(self.ptr, 1 if on else 0))
+
+    def is_modal(self) -> bool:
+        rc = self.lib.pe_wr_is_modal(self.ptr)
+        check(min(rc, 0))
+        return rc == 1
+
     def set_profiling(self, on: bool):
         check(self.lib.pe_set_profiling(self.ptr, 1 if on else 0))
 

@@ -370,6 +370,7 @@ def test_recurrence_kernels_match_per_step_gemms(sysname, kind, N, J):
     for on in (True, False):
         ctx = P.PeContext([s], [ld], J)
         ctx.set_recurrence(on)
+        ctx.set_modal(False)  # the direct w recursion (the modal path has no per-step form)
         dt = 1.0 / 64 / J
         if kind == "sequential":
             ctx.prepare_sequential(dt)
@@ -634,3 +635,54 @@ def test_sequential_all_sm_chain_against_oracle(d1, d2, nc, J):
     for n in range(0, nc, max(1, nc // 7)):
         U, W = osp.fine_interval(X[0, n, :d1], X[0, n, d1:], dt_int, J)
         assert rel_rows(Y[n][None], np.concatenate([U[-1], W[-1]])[None]) < REL
+
+
+@pytest.mark.parametrize("symmetric", [True, False])
+def test_modal_w_recursion_against_oracle(symmetric):
+    """All-at-once solver above the fused small-system size (d2 = 130): with a symmetric A22
+    the modal recursion (E = V diag(lam) V^-1, scan + W = V Z GEMM) is selected; with a
+    non-symmetric A22 the reconstruction check rejects it and the direct recursion runs.
+    Both match the CPU oracle's WR solve per interval."""
+    P = _pkg()
+    d1, d2, nc, J = 100, 130, 12, 24
+    mass, stiff, f = _random_coupled(d1, d2, 77 + symmetric)
+    if not symmetric:
+        rng = np.random.default_rng(3)
+        stiff = stiff.copy()
+        stiff[d1:, d1:] += 0.05 * np.triu(rng.standard_normal((d2, d2)), 1)
+    blocks = dict(M11=mass[:d1, :d1], A11=stiff[:d1, :d1], M12=mass[:d1, d1:],
+                  A12=stiff[:d1, d1:], M22=mass[d1:, d1:], A22=stiff[d1:, d1:])
+    s = P.CoarseSystem(**{k: np.ascontiguousarray(v) for k, v in blocks.items()})
+    osys = po.OSystem(*(blocks[k] for k in ("M11", "A11", "M12", "A12", "M22", "A22")),
+                      f[:d1], f[d1:])
+    dt_int = 0.05
+    X = np.random.default_rng(nc).standard_normal((1, nc, d1 + d2)) * 0.3
+    ctx = P.PeContext([s], [P.ConstantLoads(f[:d1], f[d1:])], J)
+    ctx.prepare_allatonce(dt_int / J, 0.2, 1e-13, 400)
+    assert ctx.is_modal() == symmetric
+    Y, sw, _, _ = ctx.fine_allatonce(ctx.to_dev(X), record=False)
+    Y, sw = Y.cpu().numpy()[0], sw.cpu().numpy().ravel()
+    owr = po.OracleWR(osys, J, dt_int, 0.2, tol=1e-13, max_iter=400)
+    for n in range(0, nc, 3):
+        r = owr.solve(X[0, n, :d1], X[0, n, d1:])
+        ref = np.concatenate([r["U"][-1], r["W"][-1]])
+        assert rel_rows(Y[n][None], ref[None]) < REL
+        assert abs(int(sw[n]) - r["iterations"]) <= 2
+
+
+def test_modal_equals_direct_recursion_cfg2():
+    """cfg2 operators: the modal w recursion and the cluster-resident direct recursion
+    converge to the same waveform fixed point (same final states to 1e-11)."""
+    P = _pkg()
+    s, ld = _system(golden("sys_cfg2.npz"))
+    X = np.random.default_rng(11).standard_normal((1, 16, s.d1 + s.d2)) * 0.1
+    outs = []
+    for modal in (True, False):
+        ctx = P.PeContext([s], [ld], 64)
+        ctx.set_modal(modal)
+        ctx.prepare_allatonce(1.0 / 64 / 64, 0.1, 1e-12, 400)
+        assert ctx.is_modal() == modal
+        Y, sw, _, _ = ctx.fine_allatonce(ctx.to_dev(X), record=False)
+        outs.append((Y.cpu().numpy()[0], sw.cpu().numpy().ravel()))
+    assert rel_rows(outs[0][0], outs[1][0]) < 1e-11
+    assert np.abs(outs[0][1].astype(int) - outs[1][1].astype(int)).max() <= 0.1 * outs[1][1].max()
