@@ -157,7 +157,11 @@ int pe_set_recurrence(pe_ctx* ctx, int on);
  * V diag(lam) V^-1 (M22-orthonormal pencil eigenvectors, accepted only if it reproduces E
  * to 1e-9); each sweep then runs the J-step w chain of WaveformRelaxation._w_sweep
  * (allatonce.py:220-230) as an elementwise scan in z = V^-1 w plus one W = V Z GEMM.
- * pe_wr_is_modal returns 1 when the prepared solver uses it, 0 otherwise. */
+ * When A11 is symmetric and M11 SPD as well, the whole sweep runs in the generalized
+ * eigenbases of both pencils (wr_modal.cu): the shifted solves of ImplicitAllAtOnce
+ * (allatonce.py:100-133) become one scalar time recurrence per mode.
+ * pe_wr_is_modal returns 2 for the full modal sweep, 1 for the modal w recursion only and
+ * 0 for the direct path.  Changing the switch invalidates pe_prepare_allatonce. */
 int pe_set_modal(pe_ctx* ctx, int on);
 int pe_wr_is_modal(pe_ctx* ctx);
 int pe_last_fine_stats(pe_ctx* ctx, double* gemm_ms, double* gemm_flops, int* launches);

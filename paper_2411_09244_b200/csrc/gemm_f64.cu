@@ -47,6 +47,26 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 template <int FM, int FN>
 __device__ __forceinline__ void gemm_epilogue(const GemmParams& p, int z1, int z2, int ibase,
                                               int jbase, const double (&acc)[FM][FN][2]) {
+  if (p.nrm) {  // per-8-row-block column sums of squares; every lane takes part in the shuffles
+    const int g = (threadIdx.x & 31) >> 2;
+    const long long zc = (long long)(z1 * p.nb2 + z2) * p.N;
+#pragma unroll
+    for (int a = 0; a < FM; ++a) {
+      const int r0 = ibase - g + a * 8;  // first row of this fragment's 8-row block
+#pragma unroll
+      for (int b = 0; b < FN; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double v = acc[a][b][h] * acc[a][b][h];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          const int gj = jbase + b * 8 + h;
+          if (g == 0 && r0 < p.M && gj < p.N) p.nrm[(long long)(r0 >> 3) * p.nrm_ld + zc + gj] = v;
+        }
+    }
+    return;
+  }
   const long long cb = z1 * p.c_b1 + z2 * p.c_b2;
   double* C = p.C + cb;
   const double* Cin = p.Cin ? p.Cin + cb : nullptr;
@@ -549,7 +569,7 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
   const int lay = no_fast ? -1 : fast_layout(p);
   // skinny launch (few row tiles x batch): split K over extra CTAs, decided from
   // (M, K, batch) only so that any column count gives the same arithmetic
-  if (lay >= 0 && p.ws) {
+  if (lay >= 0 && p.ws && !p.nrm) {
     const long long mt = (long long)((p.M + 63) / 64) * batch;
     int ktiles = 0;
     for (int sgi = 0; sgi < p.nseg; ++sgi) ktiles += (p.seg[sgi].K + 31) / 32;

@@ -175,8 +175,256 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
 }
 
 // ------------------------------------------------------------------ all-at-once fine
+// Replays one captured sweep graph per buffer parity (or launches `body` directly), with
+// the pipelined host loop: sweep i+1 is enqueued before the host reads sweep i's
+// active-interval count, so the device never waits on the host; the extra sweep after the
+// last interval stopped is fully masked.  `key` lists every pointer / value baked into the
+// nodes, so any reallocation or re-setup forces a recapture.
+template <class Body>
+static void run_sweeps(pe_ctx* c, int nc, int max_iter, const std::vector<const void*>& key,
+                       Body&& body, cudaStream_t st) {
+  int* host_cnt = c->pinned_count;
+  static const bool no_graphs = getenv("PE_NO_GRAPHS") != nullptr;
+  const bool graphs = c->use_graphs && !c->profiling && !no_graphs &&
+                      getenv("PE_RECUR_TRACE") == nullptr;
+  SweepGraphs* sg = nullptr;
+  if (graphs) {
+    sg = &c->sweep_graphs[nc];
+    if (sg->key != key) {
+      for (auto& ex : sg->exec)
+        if (ex) {
+          cudaGraphExecDestroy(ex);
+          ex = nullptr;
+        }
+      const long long launches_before = g_launches;  // capture launches nothing
+      for (int par = 0; par < 2; ++par) {
+        cudaGraph_t g;
+        PE_CUDA_CHECK(cudaStreamBeginCapture(c->work, cudaStreamCaptureModeThreadLocal));
+        try {
+          body(par, c->work);
+        } catch (...) {
+          cudaStreamEndCapture(c->work, &g);
+          throw;
+        }
+        PE_CUDA_CHECK(cudaStreamEndCapture(c->work, &g));
+        PE_CUDA_CHECK(cudaGraphInstantiate(&sg->exec[par], g, 0));
+        PE_CUDA_CHECK(cudaGraphDestroy(g));
+      }
+      sg->key = key;
+      sg->kernels = (int)((g_launches - launches_before) / 2);  // kernel nodes per graph
+      g_launches = launches_before;
+    }
+  }
+  cudaEvent_t ev[2];
+  PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  auto enqueue_sweep = [&](int sweep) {
+    if (sg) {
+      PE_CUDA_CHECK(cudaGraphLaunch(sg->exec[sweep & 1], st));
+      g_launches += c->graph_kernels;
+    } else {
+      body(sweep & 1, st);
+    }
+    PE_CUDA_CHECK(cudaEventRecord(ev[sweep & 1], st));
+    collect_profile(c, st);
+  };
+  if (sg) c->graph_kernels = sg->kernels;  // kernels per graph replay (launch evidence)
+  enqueue_sweep(0);
+  for (int sweep = 1; sweep <= max_iter; ++sweep) {
+    if (sweep < max_iter) enqueue_sweep(sweep);
+    PE_CUDA_CHECK(cudaEventSynchronize(ev[(sweep - 1) & 1]));
+    if (host_cnt[(sweep - 1) & 1] == 0) break;
+  }
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+}
+
+// The modal sweep (wr_modal.cu; setup_modal_full): per sweep the rhs GEMM, the u scan, the
+// g GEMM, the w scan, the residual-norm GEMM(s) and the stop decision.
+static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, int nc,
+                                 int* sweeps, int* reasons, double* resid_hist, cudaStream_t st) {
+  const int d1 = c->d1, d2 = c->d2, d = c->d, E = c->E, J = c->J;
+  const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
+  const double alpha = c->wr_alpha, tol = c->wr_tol, dt = c->wr_dt;
+  const int max_iter = c->wr_max_iter;
+  const long long vstride = (long long)d1 * d1 + (long long)d2 * d2;
+  const long long NJ = (long long)J * nc;
+  const int g1 = (d1 + 7) / 8, g2 = (d2 + 7) / 8;
+  for (int b = 0; b < 2; ++b) {
+    c->Yb[b].ensure(sizeof(double) * E * (J + 2) * L1 + 8);
+    c->Zb[b].ensure(sizeof(double) * E * (J + 2) * L2 + 8);
+  }
+  c->R.ensure(sizeof(double) * E * J * L1 + 8);
+  c->Hz.ensure(sizeof(double) * E * J * L2 + 8);
+  c->DYm.ensure(sizeof(double) * E * J * L1 + 8);
+  c->DW.ensure(sizeof(double) * E * J * L2 + 8);  // DZ
+  c->EYZ.ensure(sizeof(double) * E * J * (L1 + L2) + 8);
+  c->Y0m.ensure(sizeof(double) * E * L1 + 8);
+  c->Z0.ensure(sizeof(double) * E * L2 + 8);
+  c->nrmp.ensure(sizeof(double) * (size_t)(g1 + g2) * E * NJ + 8);
+  c->Ux_cur.ensure(sizeof(double) * E * (J + 2) * L1 + 8);
+  c->Ux_new.ensure(sizeof(double) * E * (J + 2) * L1 + 8);
+  c->Wx_cur.ensure(sizeof(double) * E * (J + 2) * L2 + 8);
+  c->Wx_new.ensure(sizeof(double) * E * (J + 2) * L2 + 8);
+  c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
+  c->rhist.ensure(sizeof(double) * (size_t)E * nc * max_iter + 8);
+  c->counter.ensure(sizeof(int) * 2);
+  c->stats = FineStats();
+  WrColumnState* cs = (WrColumnState*)c->colstate.p;
+  int* cnt = c->counter.i();
+  double* EY = c->EYZ.d();
+  double* EZ = EY + E * J * L1;
+  double* DZ = c->DW.d();
+
+  // seeds: y0 = V1^-1 u0, z0 = V2^-1 w0 (X_in: (E, nc, d))
+  wr_state_init((long long)E * nc, cs, c->rhist.d(), max_iter, st);
+  auto basis_gemm = [&](int M, const double* A, const double* B, long long b_j, long long b_b,
+                        double* C, long long c_b, int ncols) {
+    GemmParams p;
+    p.M = M;
+    p.N = ncols;
+    p.nb1 = E;
+    p.nseg = 1;
+    p.seg[0].A = Operand{A, M, 1, vstride, 0};
+    p.seg[0].B = Operand{B, 1, b_j, b_b, 0};
+    p.seg[0].K = M;
+    p.C = C;
+    p.c_i = 1;
+    p.c_j = M;
+    p.c_b1 = c_b;
+    gemm_f64(p, st);
+  };
+  basis_gemm(d1, c->Vicat.d(), X_in, d, (long long)nc * d, c->Y0m.d(), L1, nc);
+  basis_gemm(d2, c->Vicat.d() + (long long)d1 * d1, X_in + d1, d, (long long)nc * d, c->Z0.d(), L2, nc);
+  modal_seed(E, nc, d1, d2, J, c->Y0m.d(), c->Z0.d(), c->Yb[0].d(), c->Yb[1].d(), c->Zb[0].d(),
+             c->Zb[1].d(), DZ, st);
+
+  // loop-invariant GEMM parameter blocks (buffer parity fills in the B / C pointers)
+  auto rhs_params = [&](const double* Zcur) {
+    GemmParams r;  // r~ = [A~ | M~][Z_s; DZ_s] + V1^T f1   (build_rhs, allatonce.py:136-158)
+    r.M = d1;
+    r.N = (int)NJ;
+    r.nb1 = E;
+    r.nseg = 2;
+    r.seg[0].A = Operand{c->RT.d(), 2LL * d2, 1, 2LL * d1 * d2, 0};
+    r.seg[0].B = Operand{Zcur + L2, 1, d2, (J + 2) * L2, 0};
+    r.seg[0].K = d2;
+    r.seg[1].A = Operand{c->RT.d() + d2, 2LL * d2, 1, 2LL * d1 * d2, 0};
+    r.seg[1].B = Operand{DZ, 1, d2, J * L2, 0};
+    r.seg[1].K = d2;
+    r.C = c->R.d();
+    r.c_i = 1;
+    r.c_j = d1;
+    r.c_b1 = J * L1;
+    r.bias = c->f1t.d();
+    r.bias_b1 = d1;
+    return r;
+  };
+  auto g_params = [&](const double* Ynew) {
+    GemmParams g;  // h = [G~u | G~d][Y_s; DY_s] + dt V2^T f2   (_w_sweep, allatonce.py:220-224)
+    g.M = d2;
+    g.N = (int)NJ;
+    g.nb1 = E;
+    g.nseg = 2;
+    g.seg[0].A = Operand{c->GT.d(), 2LL * d1, 1, 2LL * d1 * d2, 0};
+    g.seg[0].B = Operand{Ynew + 2 * L1, 1, d1, (J + 2) * L1, 0};
+    g.seg[0].K = d1;
+    g.seg[1].A = Operand{c->GT.d() + d1, 2LL * d1, 1, 2LL * d1 * d2, 0};
+    g.seg[1].B = Operand{c->DYm.d(), 1, d1, J * L1, 0};
+    g.seg[1].K = d1;
+    g.C = c->Hz.d();
+    g.c_i = 1;
+    g.c_j = d2;
+    g.c_b1 = J * L2;
+    g.bias = c->cgt.d();
+    g.bias_b1 = d2;
+    return g;
+  };
+  // residual norms: ||V1 EY_s||, ||V2 EZ_s|| per (s, interval) as 8-row block partials
+  std::vector<GemmParams> norms;
+  long long nu_g, nu_m, nw_g, nw_m;
+  const double *nu, *nw;
+  if (d1 == d2) {  // one launch, the two sides as the inner batch level
+    GemmParams q;
+    q.M = d1;
+    q.N = (int)NJ;
+    q.nb1 = E;
+    q.nb2 = 2;
+    q.nseg = 1;
+    q.seg[0].A = Operand{c->Vcat.d(), d1, 1, vstride, (long long)d1 * d1};
+    q.seg[0].B = Operand{EY, 1, d1, J * L1, E * J * L1};
+    q.seg[0].K = d1;
+    q.nrm = c->nrmp.d();
+    q.nrm_ld = 2LL * E * NJ;
+    norms.push_back(q);
+    nu = c->nrmp.d();
+    nw = c->nrmp.d() + NJ;
+    nu_g = nw_g = 2LL * E * NJ;
+    nu_m = nw_m = 2 * NJ;
+  } else {
+    for (int side = 0; side < 2; ++side) {
+      const int M = side ? d2 : d1;
+      GemmParams q;
+      q.M = M;
+      q.N = (int)NJ;
+      q.nb1 = E;
+      q.nseg = 1;
+      q.seg[0].A = Operand{c->Vcat.d() + (side ? (long long)d1 * d1 : 0), M, 1, vstride, 0};
+      q.seg[0].B = Operand{side ? EZ : EY, 1, M, J * (side ? L2 : L1), 0};
+      q.seg[0].K = M;
+      q.nrm = c->nrmp.d() + (side ? (long long)g1 * E * NJ : 0);
+      q.nrm_ld = E * NJ;
+      norms.push_back(q);
+    }
+    nu = c->nrmp.d();
+    nw = c->nrmp.d() + (long long)g1 * E * NJ;
+    nu_g = nw_g = E * NJ;
+    nu_m = nw_m = NJ;
+  }
+
+  auto body = [&](int par, cudaStream_t s) {
+    const int cur = par, nxt = par ^ 1;
+    PE_CUDA_CHECK(cudaMemsetAsync(cnt + par, 0, sizeof(int), s));
+    run_gemm(c, rhs_params(c->Zb[cur].d()), s);
+    modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), c->R.d(), c->Yb[cur].d(),
+                c->Yb[nxt].d(), c->DYm.d(), EY, cs, s);
+    run_gemm(c, g_params(c->Yb[nxt].d()), s);
+    modal_wscan(E, nc, d2, J, c->lam.d(), c->Hz.d(), c->Zb[cur].d(), c->Zb[nxt].d(), DZ, EZ, cs, s);
+    for (auto& q : norms) run_gemm(c, q, s);
+    modal_decide(E, nc, d1, d2, J, nu, nu_g, nu_m, nw, nw_g, nw_m, cs, tol, max_iter,
+                 c->rhist.d(), cnt + par, nxt, s);
+    PE_CUDA_CHECK(cudaMemcpyAsync(c->pinned_count + par, cnt + par, sizeof(int),
+                                  cudaMemcpyDeviceToHost, s));
+  };
+  const std::vector<const void*> key = {
+      (const void*)(intptr_t)2, c->Yb[0].p, c->Yb[1].p, c->Zb[0].p, c->Zb[1].p, c->R.p, c->Hz.p,
+      c->DYm.p, c->DW.p, c->EYZ.p, c->nrmp.p, cs, c->rhist.p, cnt, c->pinned_count, c->RT.p,
+      c->GT.p, c->f1t.p, c->cgt.p, c->acoef.p, c->cden.p, c->lam.p, c->Vcat.p,
+      (const void*)(intptr_t)max_iter, (const void*)(intptr_t)(alpha * 1e6),
+      (const void*)(intptr_t)(tol * 1e18), (const void*)(intptr_t)(dt * 1e18)};
+  run_sweeps(c, nc, max_iter, key, body, st);
+
+  // final waveforms in the original bases: U = V1 Y, W = V2 Z from each interval's buffer
+  modal_gather(E, nc, d1, J, c->Yb[0].d(), c->Yb[1].d(), cs, c->Ux_new.d(), st);
+  modal_gather(E, nc, d2, J, c->Zb[0].d(), c->Zb[1].d(), cs, c->Wx_new.d(), st);
+  basis_gemm(d1, c->Vcat.d(), c->Ux_new.d(), d1, (J + 2) * L1, c->Ux_cur.d(), (J + 2) * L1,
+             (int)((J + 2) * nc));
+  basis_gemm(d2, c->Vcat.d() + (long long)d1 * d1, c->Wx_new.d(), d2, (J + 2) * L2, c->Wx_cur.d(),
+             (J + 2) * L2, (int)((J + 2) * nc));
+  wr_finish(E, nc, d1, d2, J, c->Ux_cur.d(), c->Wx_cur.d(), cs, X_out, sweeps, reasons, st);
+  if (resid_hist)
+    PE_CUDA_CHECK(cudaMemcpyAsync(resid_hist, c->rhist.p, sizeof(double) * (size_t)E * nc * max_iter,
+                                  cudaMemcpyDeviceToDevice, st));
+  (void)d;
+}
+
 static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc, int* sweeps,
                            int* reasons, double* resid_hist, cudaStream_t st) {
+  if (c->wr_modal_full) {
+    fine_allatonce_modal(c, X_in, X_out, nc, sweeps, reasons, resid_hist, st);
+    return;
+  }
   const int d1 = c->d1, d2 = c->d2, E = c->E, J = c->J;
   const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
   const double alpha = c->wr_alpha, tol = c->wr_tol;
@@ -407,14 +655,8 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
               (unsigned*)c->wticket.p, s);
     PE_CUDA_CHECK(cudaMemcpyAsync(host_cnt + par, cnt + par, sizeof(int), cudaMemcpyDeviceToHost, s));
   };
-  // CUDA graphs (one per counter parity) replace the per-sweep host launch sequence when
-  // not profiling; the graphs are captured on the context's stream and replayed on `st`.
-  static const bool no_graphs = getenv("PE_NO_GRAPHS") != nullptr;
-  const bool graphs = c->use_graphs && !c->profiling && !no_graphs &&
-                      getenv("PE_RECUR_TRACE") == nullptr;
-  SweepGraphs* sg = nullptr;
-  if (graphs) {
-    const std::vector<const void*> key = {
+  const std::vector<const void*> key = {
+        (const void*)(intptr_t)1,
         Uc, Un, Wc, Wn, c->R.p, c->P.p, c->Q.p, c->DU.p, c->DW.p, c->V.p, cs, c->nrm.p,
         c->rhist.p, cnt, host_cnt, c->splitws.p, c->Bk.p, c->RW.p, c->GW.p, c->Emat.p, c->Finv.p, c->Fw.p,
         c->M11dt.p, c->cg.p, c->f1.p, c->wticket.p, (const void*)(intptr_t)max_iter,
@@ -422,59 +664,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
         (const void*)(intptr_t)(alpha * 1e6), (const void*)(intptr_t)(tol * 1e18),
         (const void*)(intptr_t)nk, (const void*)(intptr_t)(modal ? 1 : 0), c->Vm.p, c->lam.p,
         c->GZ.p, c->cgz.p, c->Z0.p, c->Hz.p};
-    sg = &c->sweep_graphs[nc];
-    if (sg->key != key) {
-      for (auto& ex : sg->exec)
-        if (ex) {
-          cudaGraphExecDestroy(ex);
-          ex = nullptr;
-        }
-      const long long launches_before = g_launches;  // capture launches nothing
-      for (int par = 0; par < 2; ++par) {
-        cudaGraph_t g;
-        PE_CUDA_CHECK(cudaStreamBeginCapture(c->work, cudaStreamCaptureModeThreadLocal));
-        try {
-          body(par, c->work);
-        } catch (...) {
-          cudaStreamEndCapture(c->work, &g);
-          throw;
-        }
-        PE_CUDA_CHECK(cudaStreamEndCapture(c->work, &g));
-        PE_CUDA_CHECK(cudaGraphInstantiate(&sg->exec[par], g, 0));
-        PE_CUDA_CHECK(cudaGraphDestroy(g));
-      }
-      sg->key = key;
-      sg->kernels = (int)((g_launches - launches_before) / 2);  // kernel nodes per graph
-      g_launches = launches_before;
-    }
-  }
-  // Pipelined sweep loop: sweep i+1 is enqueued before the host reads sweep i's
-  // active-interval count, so the device never waits on the host; the extra sweep
-  // after the last interval stopped is fully masked (commit skips inactive columns).
-  cudaEvent_t ev[2];
-  PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-  PE_CUDA_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-  auto enqueue_sweep = [&](int sweep) {
-    if (sg) {
-      PE_CUDA_CHECK(cudaGraphLaunch(sg->exec[sweep & 1], st));
-      g_launches += c->graph_kernels;
-    } else {
-      body(sweep & 1, st);
-    }
-    PE_CUDA_CHECK(cudaEventRecord(ev[sweep & 1], st));
-    collect_profile(c, st);
-  };
-  if (sg) c->graph_kernels = sg->kernels;  // kernels per graph replay (launch evidence)
-  int sweep = 0;
-  enqueue_sweep(0);
-  for (sweep = 1; sweep <= max_iter; ++sweep) {
-    if (sweep < max_iter) enqueue_sweep(sweep);
-    PE_CUDA_CHECK(cudaEventSynchronize(ev[(sweep - 1) & 1]));
-    if (host_cnt[(sweep - 1) & 1] == 0) break;
-  }
-  PE_CUDA_CHECK(cudaStreamSynchronize(st));
-  cudaEventDestroy(ev[0]);
-  cudaEventDestroy(ev[1]);
+  run_sweeps(c, nc, max_iter, key, body, st);
   wr_finish(E, nc, d1, d2, J, Uc, Wc, cs, X_out, sweeps, reasons, st);
   if (resid_hist)
     PE_CUDA_CHECK(cudaMemcpyAsync(resid_hist, c->rhist.p, sizeof(double) * (size_t)E * nc * max_iter,
@@ -826,13 +1016,15 @@ int pe_set_recurrence(pe_ctx* c, int on) {
 int pe_set_modal(pe_ctx* c, int on) {
   return guarded([&] {
     require(c != nullptr, PE_ERR_ARG, "ctx is NULL");
+    if (c->use_modal != (on != 0)) c->wr_ready = false;  // operators depend on the choice
     c->use_modal = on != 0;
   });
 }
 
 int pe_wr_is_modal(pe_ctx* c) {
   if (!c) return PE_ERR_ARG;
-  return (c->wr_ready && c->wr_modal && c->use_modal) ? 1 : 0;
+  if (!c->wr_ready) return 0;
+  return c->wr_modal_full ? 2 : (c->wr_modal ? 1 : 0);
 }
 
 int pe_set_profiling(pe_ctx* c, int on) {

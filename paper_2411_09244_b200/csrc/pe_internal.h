@@ -54,6 +54,11 @@ struct GemmParams {
   const double* Cin = nullptr;  // same strides as C
   const double* bias = nullptr;
   long long bias_b1 = 0, bias_b2 = 0;
+  // norm epilogue (no C output): for every 8-row block g of C and column j of batch z,
+  // nrm[g * nrm_ld + z * N + j] = sum of the block's squared entries, summed in a fixed
+  // xor-shuffle order that does not depend on the tile shape (batch invariance)
+  double* nrm = nullptr;
+  long long nrm_ld = 0;
   double* D = nullptr;          // optional D = C - Xp, same strides as C
   const double* Xp = nullptr;
   // split-K for skinny launches: partial tiles go to `ws`, a reduction kernel sums the
@@ -77,6 +82,8 @@ struct WrColumnState {
   int reason;
   double prev;
   double r0;
+  int fpar;  // modal path: ping-pong buffer holding this interval's latest waveforms
+  int pad;
 };
 
 void wr_init(int E, int ncols, int d1, int d2, int J, double alpha, const double* X_in,
@@ -95,6 +102,24 @@ void wr_finish(int E, int ncols, int d1, int d2, int J, const double* Ux_cur,
 void wr_modal_scan(int E, int nc, int d2, int J, const double* lam, const double* Z0, double* Z,
                    cudaStream_t st);
 void wr_gather(int E, int nc, int dd, int J, const double* X, double* out, cudaStream_t st);
+
+// ---------------------------------------------------------------- modal WR (wr_modal.cu)
+void wr_state_init(long long ncs, WrColumnState* cs, double* resid_hist, int max_iter,
+                   cudaStream_t st);
+void modal_seed(int E, int nc, int d1, int d2, int J, const double* Y0, const double* Z0,
+                double* Yb0, double* Yb1, double* Zb0, double* Zb1, double* DZ, cudaStream_t st);
+void modal_uscan(int E, int nc, int d1, int J, double dt, double alpha, const double* acoef,
+                 const double* cden, const double* R, const double* Yc, double* Yn, double* DY,
+                 double* EY, const WrColumnState* cs, cudaStream_t st);
+void modal_wscan(int E, int nc, int d2, int J, const double* lam, const double* H,
+                 const double* Zc, double* Zn, double* DZ, double* EZ, const WrColumnState* cs,
+                 cudaStream_t st);
+void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long long nu_g,
+                  long long nu_m, const double* nw, long long nw_g, long long nw_m,
+                  WrColumnState* cs, double tol, int max_iter, double* resid_hist,
+                  int* active_count, int par_new, cudaStream_t st);
+void modal_gather(int E, int nc, int dd, int J, const double* B0, const double* B1,
+                  const WrColumnState* cs, double* out, cudaStream_t st);
 void sub(long long n, const double* a, const double* b, double* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- recurrences (recur.cu)

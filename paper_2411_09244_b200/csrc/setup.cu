@@ -366,10 +366,140 @@ static bool setup_modal(pe_ctx* c, int e, double dt, const double* M22, const do
   return true;
 }
 
-void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_iter) {
-  const int d1 = c->d1, d2 = c->d2, J = c->J, E = c->E;
+__global__ void sub_diag_kernel(int n, double* P, int ld, const double* d, double scale) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    P[(long long)t * ld + t] -= d ? d[t] : scale;
+}
+
+static double max_abs(pe_ctx* c, long long n, const double* x) {
+  if (n == 0) return 0.0;
+  int idx = 0;
+  BLAS_CHECK(cublasIdamax(c->blas, (int)n, x, 1, &idx));
+  double v = 0;
+  PE_CUDA_CHECK(cudaMemcpyAsync(&v, x + idx - 1, sizeof(double), cudaMemcpyDeviceToHost, c->setup_stream));
+  PE_CUDA_CHECK(cudaStreamSynchronize(c->setup_stream));
+  return std::fabs(v);
+}
+
+// Generalized symmetric-definite eigenproblem A v = mu M v (cuSOLVER sygvd): V (row-major,
+// eigenvectors as columns), Vi = V^T M = V^-1 and mu (host).  Accepted only if
+// V^T A V = diag(mu) and V^T M V = I hold to 1e-9 (relative to max |mu| for the former):
+// a non-symmetric A or an indefinite M fails here.
+static bool pencil_eig(pe_ctx* c, int n, const double* A, const double* M, double* V, double* Vi,
+                       std::vector<double>& mu) {
   cudaStream_t st = c->setup_stream;
   cublasHandle_t h = c->blas;
+  const size_t nn = (size_t)n * n;
+  DevBuf a, b, w, info, work, t1, t2;
+  a.ensure(sizeof(double) * nn);
+  b.ensure(sizeof(double) * nn);
+  w.ensure(sizeof(double) * n);
+  info.ensure(sizeof(int));
+  PE_CUDA_CHECK(cudaMemcpyAsync(a.p, A, sizeof(double) * nn, cudaMemcpyDeviceToDevice, st));
+  PE_CUDA_CHECK(cudaMemcpyAsync(b.p, M, sizeof(double) * nn, cudaMemcpyDeviceToDevice, st));
+  int lwork = 0;
+  SOLVER_CHECK(cusolverDnDsygvd_bufferSize(c->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                           CUBLAS_FILL_MODE_LOWER, n, a.d(), n, b.d(), n, w.d(), &lwork));
+  work.ensure(sizeof(double) * std::max(lwork, 1));
+  SOLVER_CHECK(cusolverDnDsygvd(c->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                CUBLAS_FILL_MODE_LOWER, n, a.d(), n, b.d(), n, w.d(), work.d(),
+                                lwork, info.i()));
+  int h_info = 0;
+  PE_CUDA_CHECK(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (h_info != 0) return false;
+  mu.assign(n, 0.0);
+  PE_CUDA_CHECK(cudaMemcpyAsync(mu.data(), w.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  // a holds the eigenvectors column-major, i.e. V^T read row-major
+  rm_geam(h, true, false, n, n, 1.0, a.d(), n, 0.0, a.d(), n, V, n);
+  rm_gemm(h, false, false, n, n, n, 1.0, a.d(), n, M, n, 0.0, Vi, n);
+  t1.ensure(sizeof(double) * nn);
+  t2.ensure(sizeof(double) * nn);
+  rm_gemm(h, false, false, n, n, n, 1.0, A, n, V, n, 0.0, t1.d(), n);          // A V
+  rm_gemm(h, false, false, n, n, n, 1.0, a.d(), n, t1.d(), n, 0.0, t2.d(), n);  // V^T A V
+  sub_diag_kernel<<<grid_for(n), 256, 0, st>>>(n, t2.d(), n, w.d(), 0.0);
+  rm_gemm(h, false, false, n, n, n, 1.0, Vi, n, V, n, 0.0, t1.d(), n);          // V^T M V
+  sub_diag_kernel<<<grid_for(n), 256, 0, st>>>(n, t1.d(), n, nullptr, 1.0);
+  PE_CUDA_CHECK(cudaGetLastError());
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  double mmax = 0.0;
+  for (double x : mu) mmax = std::max(mmax, std::fabs(x));
+  const double ep = max_abs(c, (long long)nn, t2.d()), eq = max_abs(c, (long long)nn, t1.d());
+  return ep <= 1e-9 * std::max(mmax, 1e-300) && eq <= 1e-9;
+}
+
+// Operators of the modal WR sweep (wr_modal.cu) for every member; false (and the general
+// path is used) unless both pencils pass pencil_eig and every modal time recurrence is
+// well posed (1 + mu1 dt > 0, |1 - alpha a^J| >= 1e-6).
+static bool setup_modal_full(pe_ctx* c, double dt, double alpha) {
+  const int d1 = c->d1, d2 = c->d2, J = c->J, E = c->E;
+  if (d1 == 0 || d2 == 0) return false;
+  cublasHandle_t h = c->blas;
+  cudaStream_t st = c->setup_stream;
+  const size_t vstride = (size_t)d1 * d1 + (size_t)d2 * d2;
+  c->Vcat.ensure(sizeof(double) * E * vstride + 8);
+  c->Vicat.ensure(sizeof(double) * E * vstride + 8);
+  c->RT.ensure(sizeof(double) * (size_t)E * d1 * 2 * d2 + 8);
+  c->GT.ensure(sizeof(double) * (size_t)E * d2 * 2 * d1 + 8);
+  c->f1t.ensure(sizeof(double) * (size_t)E * d1 + 8);
+  c->cgt.ensure(sizeof(double) * (size_t)E * d2 + 8);
+  c->acoef.ensure(sizeof(double) * (size_t)E * d1 + 8);
+  c->cden.ensure(sizeof(double) * (size_t)E * d1 + 8);
+  c->lam.ensure(sizeof(double) * (size_t)E * d2 + 8);
+  DevBuf t12, t21;
+  t12.ensure(sizeof(double) * (size_t)d1 * d2);
+  t21.ensure(sizeof(double) * (size_t)d2 * d1);
+  std::vector<double> mu1, mu2, ha(d1), hc(d1), hl(d2);
+  for (int e = 0; e < E; ++e) {
+    const double* M11 = c->M11.d() + (size_t)e * d1 * d1;
+    const double* A11 = c->A11.d() + (size_t)e * d1 * d1;
+    const double* M12 = c->M12.d() + (size_t)e * d1 * d2;
+    const double* A12 = c->A12.d() + (size_t)e * d1 * d2;
+    const double* M22 = c->M22.d() + (size_t)e * d2 * d2;
+    const double* A22 = c->A22.d() + (size_t)e * d2 * d2;
+    double* V1 = c->Vcat.d() + e * vstride;
+    double* V2 = V1 + (size_t)d1 * d1;
+    double* V1i = c->Vicat.d() + e * vstride;
+    double* V2i = V1i + (size_t)d1 * d1;
+    if (!pencil_eig(c, d1, A11, M11, V1, V1i, mu1)) return false;
+    if (!pencil_eig(c, d2, A22, M22, V2, V2i, mu2)) return false;
+    for (int i = 0; i < d1; ++i) {
+      const double q = 1.0 + mu1[i] * dt;
+      if (!(q > 0.0)) return false;
+      ha[i] = 1.0 / q;
+      const double den = 1.0 - alpha * std::pow(ha[i], (double)J);
+      if (!(std::fabs(den) >= 1e-6)) return false;
+      hc[i] = 1.0 / den;
+    }
+    for (int i = 0; i < d2; ++i) hl[i] = 1.0 - dt * mu2[i];
+    PE_CUDA_CHECK(cudaMemcpyAsync(c->acoef.d() + (size_t)e * d1, ha.data(), 8 * d1, cudaMemcpyHostToDevice, st));
+    PE_CUDA_CHECK(cudaMemcpyAsync(c->cden.d() + (size_t)e * d1, hc.data(), 8 * d1, cudaMemcpyHostToDevice, st));
+    PE_CUDA_CHECK(cudaMemcpyAsync(c->lam.d() + (size_t)e * d2, hl.data(), 8 * d2, cudaMemcpyHostToDevice, st));
+    // V1^T X = (V1^-1 M11^-1) X is not formed: V1^T is read as the transpose of V1
+    double* RT = c->RT.d() + (size_t)e * d1 * 2 * d2;
+    rm_gemm(h, false, false, d1, d2, d2, 1.0, A12, d2, V2, d2, 0.0, t12.d(), d2);       // A12 V2
+    rm_gemm(h, true, false, d1, d2, d1, -1.0, V1, d1, t12.d(), d2, 0.0, RT, 2 * d2);    // -V1^T A12 V2
+    rm_gemm(h, false, false, d1, d2, d2, 1.0, M12, d2, V2, d2, 0.0, t12.d(), d2);       // M12 V2
+    rm_gemm(h, true, false, d1, d2, d1, -1.0 / dt, V1, d1, t12.d(), d2, 0.0, RT + d2, 2 * d2);
+    rm_gemm(h, true, false, d1, 1, d1, 1.0, V1, d1, c->f1.d() + (size_t)e * d1, 1, 0.0,
+            c->f1t.d() + (size_t)e * d1, 1);
+    double* GT = c->GT.d() + (size_t)e * d2 * 2 * d1;
+    rm_gemm(h, true, false, d2, d1, d1, 1.0, A12, d2, V1, d1, 0.0, t21.d(), d1);        // A12^T V1
+    rm_gemm(h, true, false, d2, d1, d2, -dt, V2, d2, t21.d(), d1, 0.0, GT, 2 * d1);     // -dt V2^T A12^T V1
+    rm_gemm(h, true, false, d2, d1, d1, 1.0, M12, d2, V1, d1, 0.0, t21.d(), d1);        // M12^T V1
+    rm_gemm(h, true, false, d2, d1, d2, -1.0, V2, d2, t21.d(), d1, 0.0, GT + d1, 2 * d1);
+    rm_gemm(h, true, false, d2, 1, d2, dt, V2, d2, c->f2.d() + (size_t)e * d2, 1, 0.0,
+            c->cgt.d() + (size_t)e * d2, 1);
+    PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  return true;
+}
+
+static void setup_allatonce_general(pe_ctx* c, double dt, double alpha, int npm, bool even);
+
+void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_iter) {
+  const int d1 = c->d1, d2 = c->d2, J = c->J;
+  cudaStream_t st = c->setup_stream;
   // Half spectrum in half-complex packing.  The WR right-hand side is real, so
   // Finv[J-k, s] = conj(Finv[k, s]) and d_{J-k} = conj(d_k): Q_{J-k} = conj(Q_k).  Only modes
   // k = 0..floor(J/2) are solved, as npm = ceil(J/2) "pseudo-modes" of two planes each:
@@ -417,6 +547,24 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
     PE_CUDA_CHECK(cudaMemcpy(c->Finv.p, finv.data(), sizeof(double) * finv.size(), cudaMemcpyHostToDevice));
     PE_CUDA_CHECK(cudaMemcpy(c->Fw.p, fw.data(), sizeof(double) * fw.size(), cudaMemcpyHostToDevice));
   }
+  // modal sweep when both pencils diagonalise (wr_modal.cu); otherwise the general path
+  c->wr_modal = false;
+  c->wr_modal_full = c->use_modal && !wr_tiny_eligible(d1, d2, J, npm) && setup_modal_full(c, dt, alpha);
+  if (!c->wr_modal_full) setup_allatonce_general(c, dt, alpha, npm, even);
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  c->wr_ready = true;
+  c->wr_dt = dt;
+  c->wr_alpha = alpha;
+  c->wr_tol = tol;
+  c->wr_max_iter = max_iter;
+}
+
+// The general all-at-once operators: shifted inverses, rhs / g operators, E (direct or
+// modal w recursion).
+static void setup_allatonce_general(pe_ctx* c, double dt, double alpha, int npm, bool even) {
+  const int d1 = c->d1, d2 = c->d2, J = c->J, E = c->E;
+  cudaStream_t st = c->setup_stream;
+  cublasHandle_t h = c->blas;
   c->Bk.ensure(sizeof(double) * (size_t)E * npm * 4 * d1 * d1 + 8);
   c->RW.ensure(sizeof(double) * (size_t)E * d1 * 2 * d2 + 8);
   c->M11dt.ensure(sizeof(double) * (size_t)E * d1 * d1 + 8);
@@ -482,8 +630,7 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
     c->BkT.ensure(sizeof(double) * (size_t)E * npm * 4 * d1 * d1 + 8);
     transpose_blocks(E * npm, 2 * d1, c->Bk.d(), c->BkT.d(), st);
   }
-  c->wr_modal = false;
-  if (d2 > 0 && !wr_tiny_eligible(d1, d2, J, npm)) {
+  if (c->use_modal && d2 > 0 && !wr_tiny_eligible(d1, d2, J, npm)) {
     c->Vm.ensure(sizeof(double) * (size_t)E * d2 * d2 + 8);
     c->Vinv.ensure(sizeof(double) * (size_t)E * d2 * d2 + 8);
     c->lam.ensure(sizeof(double) * (size_t)E * d2 + 8);
@@ -497,12 +644,6 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
                        c->cg.d() + (size_t)e * d2);
     c->wr_modal = ok;
   }
-  PE_CUDA_CHECK(cudaStreamSynchronize(st));
-  c->wr_ready = true;
-  c->wr_dt = dt;
-  c->wr_alpha = alpha;
-  c->wr_tol = tol;
-  c->wr_max_iter = max_iter;
 }
 
 }  // namespace pe

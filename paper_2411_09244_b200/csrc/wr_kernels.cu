@@ -10,6 +10,7 @@
 
 #include "pe.h"
 #include "pe_internal.h"
+#include "wr_stop.cuh"
 
 namespace pe {
 
@@ -54,6 +55,8 @@ __global__ void wr_init_kernel(int E, int nc, int d1, int d2, int J, double alph
     s.reason = PE_STOP_MAX_ITER;
     s.prev = INFINITY;
     s.r0 = 0.0;
+    s.fpar = 0;
+    s.pad = 0;
     cs[t] = s;
   }
   if (resid_hist) {
@@ -258,32 +261,10 @@ __device__ void wr_decide_interval(int en, int lane, int nc, int d1, int d2, int
     if (d1 > 0) resid += mu;
     if (d2 > 0) resid += mw;
     WrColumnState c = cs[en];
-    const int it = c.iterations;
-    if (resid_hist) resid_hist[(long long)en * max_iter + it] = resid;
-    if (it == 0) c.r0 = resid;
-    c.iterations = it + 1;
-    bool stop = false;
-    if (resid <= tol) {
-      c.reason = PE_STOP_TOL;
-      stop = true;
-    } else if (!isfinite(resid) || resid > 1e8 * fmax(1.0, c.r0)) {
-      c.reason = PE_STOP_DIVERGED;
-      stop = true;
-    } else {
-      c.stall = (resid >= c.prev) ? c.stall + 1 : 0;
-      if (c.stall >= 2 && resid <= 1e3 * tol) {
-        c.reason = PE_STOP_FLOOR;
-        stop = true;
-      }
-      c.prev = resid;
-    }
-    if (!stop && c.iterations >= max_iter) {
-      c.reason = PE_STOP_MAX_ITER;
-      stop = true;
-    }
-    c.active = stop ? 0 : 1;
+    const bool go = wr_stop_update(c, resid, tol, max_iter,
+                                   resid_hist ? resid_hist + (long long)en * max_iter : nullptr);
     cs[en] = c;
-    if (!stop) atomicAdd(active_count, 1);
+    if (go) atomicAdd(active_count, 1);
   }
 }
 

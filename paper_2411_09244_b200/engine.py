@@ -175,10 +175,14 @@ class PeContext:
         """Modal (diagonalised) w recursion for the all-at-once solver (pe_set_modal)."""
         check(self.lib.pe_set_modal(self.ptr, 1 if on else 0))
 
-    def is_modal(self) -> bool:
+    def modal_level(self) -> int:
+        """2: full modal WR sweep, 1: modal w recursion only, 0: direct (pe_wr_is_modal)."""
         rc = self.lib.pe_wr_is_modal(self.ptr)
         check(min(rc, 0))
-        return rc == 1
+        return int(rc)
+
+    def is_modal(self) -> bool:
+        return self.modal_level() > 0
 
     def set_profiling(self, on: bool):
         check(self.lib.pe_set_profiling(self.ptr, 1 if on else 0))

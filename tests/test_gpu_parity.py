@@ -637,18 +637,21 @@ def test_sequential_all_sm_chain_against_oracle(d1, d2, nc, J):
         assert rel_rows(Y[n][None], np.concatenate([U[-1], W[-1]])[None]) < REL
 
 
-@pytest.mark.parametrize("symmetric", [True, False])
-def test_modal_w_recursion_against_oracle(symmetric):
-    """All-at-once solver above the fused small-system size (d2 = 130): with a symmetric A22
-    the modal recursion (E = V diag(lam) V^-1, scan + W = V Z GEMM) is selected; with a
-    non-symmetric A22 the reconstruction check rejects it and the direct recursion runs.
-    Both match the CPU oracle's WR solve per interval."""
+@pytest.mark.parametrize("case,level", [("symmetric", 2), ("a11_nonsym", 1), ("a22_nonsym", 0)])
+def test_modal_paths_against_oracle(case, level):
+    """All-at-once solver above the fused small-system size (d1 = 100, d2 = 130, so the two
+    residual-norm products are separate launches).  Both pencils symmetric-definite: the
+    full modal sweep (level 2).  Non-symmetric A11: the shifted-inverse path with the modal
+    w recursion (level 1).  Non-symmetric A22: both reconstruction checks fail and the
+    direct recursion runs (level 0).  Every path matches the CPU oracle's WR solve."""
     P = _pkg()
     d1, d2, nc, J = 100, 130, 12, 24
-    mass, stiff, f = _random_coupled(d1, d2, 77 + symmetric)
-    if not symmetric:
-        rng = np.random.default_rng(3)
-        stiff = stiff.copy()
+    mass, stiff, f = _random_coupled(d1, d2, 77)
+    rng = np.random.default_rng(3)
+    stiff = stiff.copy()
+    if case == "a11_nonsym":
+        stiff[:d1, :d1] += 0.05 * np.triu(rng.standard_normal((d1, d1)), 1)
+    if case == "a22_nonsym":
         stiff[d1:, d1:] += 0.05 * np.triu(rng.standard_normal((d2, d2)), 1)
     blocks = dict(M11=mass[:d1, :d1], A11=stiff[:d1, :d1], M12=mass[:d1, d1:],
                   A12=stiff[:d1, d1:], M22=mass[d1:, d1:], A22=stiff[d1:, d1:])
@@ -659,14 +662,17 @@ def test_modal_w_recursion_against_oracle(symmetric):
     X = np.random.default_rng(nc).standard_normal((1, nc, d1 + d2)) * 0.3
     ctx = P.PeContext([s], [P.ConstantLoads(f[:d1], f[d1:])], J)
     ctx.prepare_allatonce(dt_int / J, 0.2, 1e-13, 400)
-    assert ctx.is_modal() == symmetric
-    Y, sw, _, _ = ctx.fine_allatonce(ctx.to_dev(X), record=False)
+    assert ctx.modal_level() == level
+    Y, sw, rs, _ = ctx.fine_allatonce(ctx.to_dev(X), record=False)
     Y, sw = Y.cpu().numpy()[0], sw.cpu().numpy().ravel()
+    U, W = ctx.wr_waveforms(nc)
+    U, W = U.cpu().numpy()[0], W.cpu().numpy()[0]
     owr = po.OracleWR(osys, J, dt_int, 0.2, tol=1e-13, max_iter=400)
     for n in range(0, nc, 3):
         r = owr.solve(X[0, n, :d1], X[0, n, d1:])
         ref = np.concatenate([r["U"][-1], r["W"][-1]])
         assert rel_rows(Y[n][None], ref[None]) < REL
+        assert rel_rows(U[n], r["U"]) < REL and rel_rows(W[n], r["W"]) < REL
         assert abs(int(sw[n]) - r["iterations"]) <= 2
 
 
@@ -686,3 +692,21 @@ def test_modal_equals_direct_recursion_cfg2():
         outs.append((Y.cpu().numpy()[0], sw.cpu().numpy().ravel()))
     assert rel_rows(outs[0][0], outs[1][0]) < 1e-11
     assert np.abs(outs[0][1].astype(int) - outs[1][1].astype(int)).max() <= 0.1 * outs[1][1].max()
+
+
+def test_modal_sweep_batch_invariant_and_deterministic():
+    """Full modal sweep at cfg2: reruns are bitwise identical and an interval solved alone
+    equals the same interval inside the batch, bitwise (fixed-order norm partials)."""
+    P = _pkg()
+    s, ld = _system(golden("sys_cfg2.npz"))
+    X = np.random.default_rng(5).standard_normal((1, 12, s.d1 + s.d2)) * 0.1
+    ctx = P.PeContext([s], [ld], 64)
+    ctx.prepare_allatonce(1.0 / 64 / 64, 0.1, 1e-12, 400)
+    assert ctx.modal_level() == 2
+    a, sa, _, ra = ctx.fine_allatonce(ctx.to_dev(X))
+    b, sb, _, rb = ctx.fine_allatonce(ctx.to_dev(X))
+    assert np.array_equal(a.cpu().numpy(), b.cpu().numpy())
+    assert np.array_equal(sa.cpu().numpy(), sb.cpu().numpy())
+    one, s1, _, r1 = ctx.fine_allatonce(ctx.to_dev(X[:, 7:8]))
+    assert np.array_equal(one.cpu().numpy()[0, 0], a.cpu().numpy()[0, 7])
+    assert int(s1.cpu().numpy().ravel()[0]) == int(sa.cpu().numpy().ravel()[7])
