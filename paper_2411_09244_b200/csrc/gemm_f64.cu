@@ -184,10 +184,11 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 #pragma unroll
     for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  if (ntile > 0) {
-    load_tile(0, 0);
+  const int t0 = p.tri_upper ? min(ntile, i0 / BK) : 0;  // zero k-tiles of a triangular A
+  if (ntile > t0) {
+    load_tile(t0, t0 & 1);
     cp_async_commit();
-    for (int t = 0; t < ntile; ++t) {
+    for (int t = t0; t < ntile; ++t) {
       const int buf = t & 1;
       if (t + 1 < ntile) {
         load_tile(t + 1, buf ^ 1);
@@ -270,8 +271,9 @@ __global__ void __launch_bounds__(WGM * WGN * 32)
   if (p.nseg > 2) kt2 = (p.seg[2].K + BK - 1) / BK;
   const int ktot = kt0 + kt1 + kt2;
   const int kper = (ktot + p.ksplit - 1) / p.ksplit;
-  const int tbeg = min(ktot, sp * kper);
-  const int ntile = min(ktot, tbeg + kper) - tbeg;  // this split's k-tiles
+  const int tskip = p.tri_upper ? min(ktot, i0 / BK) : 0;  // zero k-tiles of a triangular A
+  const int tbeg = max(tskip, min(ktot, sp * kper));
+  const int ntile = max(0, min(ktot, sp * kper + kper) - tbeg);  // this split's k-tiles
 
   // fixed per-thread chunk coordinates
   constexpr int ACPR = BK / 2;                 // 16-byte chunks per A row
@@ -479,9 +481,15 @@ static int fast_layout(const GemmParams& p) {
   X(10, 1, 2, 5, 4, 16, 2, 1) \
   X(11, 2, 3, 4, 3, 16, 3, 0) \
   X(12, 4, 1, 5, 4, 16, 2, 1) \
-  X(13, 3, 1, 5, 4, 16, 2, 0)
+  X(13, 3, 1, 5, 4, 16, 2, 0) \
+  X(14, 2, 3, 4, 3, 32, 2, 0) \
+  X(15, 2, 3, 4, 3, 32, 3, 0) \
+  X(16, 4, 3, 4, 3, 16, 3, 0) \
+  X(17, 2, 3, 5, 3, 16, 2, 0) \
+  X(18, 2, 3, 5, 3, 32, 2, 0) \
+  X(19, 2, 2, 5, 4, 32, 2, 0)
 
-static constexpr int kMaxVariant = 14;
+static constexpr int kMaxVariant = 20;
 
 // Wave-quantised cost: CTAs are spread round-robin over the 148 SMs and the SM with the
 // most tiles finishes last; its work is max_tiles x tile area (padding included).
@@ -547,7 +555,12 @@ static void launch_cfg(const GemmParams& p, bool ak, bool bk, cudaStream_t st) {
 double gemm_flops(const GemmParams& p) {
   double k = 0;
   for (int s = 0; s < p.nseg; ++s) k += p.seg[s].K;
-  return 2.0 * p.M * (double)p.N * k * p.nb1 * p.nb2;
+  double mk = p.M * k;
+  if (p.tri_upper && p.nseg == 1) {  // nonzeros of an upper-triangular M x K operator
+    const double m = std::min<double>(p.M, k);
+    mk = m * k - m * (m - 1) / 2;
+  }
+  return 2.0 * mk * (double)p.N * p.nb1 * p.nb2;
 }
 
 void gemm_f64(const GemmParams& p, cudaStream_t st) {

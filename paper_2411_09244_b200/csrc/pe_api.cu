@@ -270,6 +270,9 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
   c->rhist.ensure(sizeof(double) * (size_t)E * nc * max_iter + 8);
   c->counter.ensure(sizeof(int) * 2);
+  ensure_zeroed(c->wticket, sizeof(unsigned) * (size_t)E * nc + 8);  // self-resetting ticket
+  c->colmax.ensure(sizeof(unsigned long long) * 2 * (size_t)E * nc + 8);
+  PE_CUDA_CHECK(cudaMemsetAsync(c->colmax.p, 0, c->colmax.bytes, st));
   c->stats = FineStats();
   WrColumnState* cs = (WrColumnState*)c->colstate.p;
   int* cnt = c->counter.i();
@@ -341,7 +344,8 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     g.bias_b1 = d2;
     return g;
   };
-  // residual norms: ||V1 EY_s||, ||V2 EZ_s|| per (s, interval) as 8-row block partials
+  // residual norms ||V1 EY_s|| = ||U1 EY_s|| (U1 upper-triangular, setup.cu norm_factor),
+  // likewise W, per (s, interval) as 8-row block partials
   std::vector<GemmParams> norms;
   long long nu_g, nu_m, nw_g, nw_m;
   const double *nu, *nw;
@@ -352,9 +356,10 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     q.nb1 = E;
     q.nb2 = 2;
     q.nseg = 1;
-    q.seg[0].A = Operand{c->Vcat.d(), d1, 1, vstride, (long long)d1 * d1};
+    q.seg[0].A = Operand{c->Ucat.d(), d1, 1, vstride, (long long)d1 * d1};
     q.seg[0].B = Operand{EY, 1, d1, J * L1, E * J * L1};
     q.seg[0].K = d1;
+    q.tri_upper = 1;
     q.nrm = c->nrmp.d();
     q.nrm_ld = 2LL * E * NJ;
     norms.push_back(q);
@@ -370,9 +375,10 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
       q.N = (int)NJ;
       q.nb1 = E;
       q.nseg = 1;
-      q.seg[0].A = Operand{c->Vcat.d() + (side ? (long long)d1 * d1 : 0), M, 1, vstride, 0};
+      q.seg[0].A = Operand{c->Ucat.d() + (side ? (long long)d1 * d1 : 0), M, 1, vstride, 0};
       q.seg[0].B = Operand{side ? EZ : EY, 1, M, J * (side ? L2 : L1), 0};
       q.seg[0].K = M;
+      q.tri_upper = 1;
       q.nrm = c->nrmp.d() + (side ? (long long)g1 * E * NJ : 0);
       q.nrm_ld = E * NJ;
       norms.push_back(q);
@@ -392,7 +398,8 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     run_gemm(c, g_params(c->Yb[nxt].d()), s);
     modal_wscan(E, nc, d2, J, c->lam.d(), c->Hz.d(), c->Zb[cur].d(), c->Zb[nxt].d(), DZ, EZ, cs, s);
     for (auto& q : norms) run_gemm(c, q, s);
-    modal_decide(E, nc, d1, d2, J, nu, nu_g, nu_m, nw, nw_g, nw_m, cs, tol, max_iter,
+    modal_decide(E, nc, d1, d2, J, nu, nu_g, nu_m, nw, nw_g, nw_m,
+                 (unsigned long long*)c->colmax.p, (unsigned*)c->wticket.p, cs, tol, max_iter,
                  c->rhist.d(), cnt + par, nxt, s);
     PE_CUDA_CHECK(cudaMemcpyAsync(c->pinned_count + par, cnt + par, sizeof(int),
                                   cudaMemcpyDeviceToHost, s));
@@ -400,7 +407,8 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   const std::vector<const void*> key = {
       (const void*)(intptr_t)2, c->Yb[0].p, c->Yb[1].p, c->Zb[0].p, c->Zb[1].p, c->R.p, c->Hz.p,
       c->DYm.p, c->DW.p, c->EYZ.p, c->nrmp.p, cs, c->rhist.p, cnt, c->pinned_count, c->RT.p,
-      c->GT.p, c->f1t.p, c->cgt.p, c->acoef.p, c->cden.p, c->lam.p, c->Vcat.p,
+      c->GT.p, c->f1t.p, c->cgt.p, c->acoef.p, c->cden.p, c->lam.p, c->Vcat.p, c->Ucat.p, c->colmax.p,
+      c->wticket.p,
       (const void*)(intptr_t)max_iter, (const void*)(intptr_t)(alpha * 1e6),
       (const void*)(intptr_t)(tol * 1e18), (const void*)(intptr_t)(dt * 1e18)};
   run_sweeps(c, nc, max_iter, key, body, st);

@@ -83,8 +83,8 @@ struct pe_ctx {
   pe::DevBuf Vm, Vinv, lam, GZ, cgz, Z0, Hz;
   // full modal sweep (setup_modal_full, wr_modal.cu): both pencils diagonalised
   bool wr_modal_full = false;
-  pe::DevBuf Vcat, Vicat, RT, GT, f1t, cgt, acoef, cden;
-  pe::DevBuf Yb[2], Zb[2], DYm, EYZ, Y0m, nrmp;
+  pe::DevBuf Vcat, Vicat, Ucat, RT, GT, f1t, cgt, acoef, cden;
+  pe::DevBuf Yb[2], Zb[2], DYm, EYZ, Y0m, nrmp, colmax;
 
   // work buffers
   pe::DevBuf Xin, Xout, Xa, Xb, Da, Db, Xs, Zg, gcnt, wticket;

@@ -59,6 +59,9 @@ struct GemmParams {
   // xor-shuffle order that does not depend on the tile shape (batch invariance)
   double* nrm = nullptr;
   long long nrm_ld = 0;
+  // A (single segment) is upper triangular: k-tiles entirely left of a row tile's first
+  // row hold exact zeros and are skipped (their DMMA steps would add +0)
+  int tri_upper = 0;
   double* D = nullptr;          // optional D = C - Xp, same strides as C
   const double* Xp = nullptr;
   // split-K for skinny launches: partial tiles go to `ws`, a reduction kernel sums the
@@ -116,8 +119,9 @@ void modal_wscan(int E, int nc, int d2, int J, const double* lam, const double* 
                  cudaStream_t st);
 void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long long nu_g,
                   long long nu_m, const double* nw, long long nw_g, long long nw_m,
-                  WrColumnState* cs, double tol, int max_iter, double* resid_hist,
-                  int* active_count, int par_new, cudaStream_t st);
+                  unsigned long long* colmax, unsigned* ticket, WrColumnState* cs, double tol,
+                  int max_iter, double* resid_hist, int* active_count, int par_new,
+                  cudaStream_t st);
 void modal_gather(int E, int nc, int dd, int J, const double* B0, const double* B1,
                   const WrColumnState* cs, double* out, cudaStream_t st);
 void sub(long long n, const double* a, const double* b, double* out, cudaStream_t st);

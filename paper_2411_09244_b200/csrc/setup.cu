@@ -428,6 +428,33 @@ static bool pencil_eig(pe_ctx* c, int n, const double* A, const double* M, doubl
   return ep <= 1e-9 * std::max(mmax, 1e-300) && eq <= 1e-9;
 }
 
+__global__ void zero_strict_lower_kernel(int n, double* U) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)n * n;
+       t += (long long)gridDim.x * blockDim.x)
+    if (t / n > t % n) U[t] = 0.0;
+}
+
+// Upper-triangular norm factor: U = L^T with L L^T = V^T V (Cholesky), so ||U e|| = ||V e||
+// at half the flops of V e (the residual-norm GEMM skips U's zero k-tiles).
+static bool norm_factor(pe_ctx* c, int n, const double* V, double* U) {
+  cudaStream_t st = c->setup_stream;
+  rm_gemm(c->blas, true, false, n, n, n, 1.0, V, n, V, n, 0.0, U, n);  // V^T V (symmetric)
+  DevBuf work, info;
+  info.ensure(sizeof(int));
+  int lwork = 0;
+  SOLVER_CHECK(cusolverDnDpotrf_bufferSize(c->solver, CUBLAS_FILL_MODE_LOWER, n, U, n, &lwork));
+  work.ensure(sizeof(double) * std::max(lwork, 1));
+  SOLVER_CHECK(cusolverDnDpotrf(c->solver, CUBLAS_FILL_MODE_LOWER, n, U, n, work.d(), lwork, info.i()));
+  int h_info = 0;
+  PE_CUDA_CHECK(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (h_info != 0) return false;
+  // column-major lower L read row-major is L^T in the upper triangle; clear the rest
+  zero_strict_lower_kernel<<<grid_for((long long)n * n), 256, 0, st>>>(n, U);
+  PE_CUDA_CHECK(cudaGetLastError());
+  return true;
+}
+
 // Operators of the modal WR sweep (wr_modal.cu) for every member; false (and the general
 // path is used) unless both pencils pass pencil_eig and every modal time recurrence is
 // well posed (1 + mu1 dt > 0, |1 - alpha a^J| >= 1e-6).
@@ -439,6 +466,7 @@ static bool setup_modal_full(pe_ctx* c, double dt, double alpha) {
   const size_t vstride = (size_t)d1 * d1 + (size_t)d2 * d2;
   c->Vcat.ensure(sizeof(double) * E * vstride + 8);
   c->Vicat.ensure(sizeof(double) * E * vstride + 8);
+  c->Ucat.ensure(sizeof(double) * E * vstride + 8);
   c->RT.ensure(sizeof(double) * (size_t)E * d1 * 2 * d2 + 8);
   c->GT.ensure(sizeof(double) * (size_t)E * d2 * 2 * d1 + 8);
   c->f1t.ensure(sizeof(double) * (size_t)E * d1 + 8);
@@ -463,6 +491,8 @@ static bool setup_modal_full(pe_ctx* c, double dt, double alpha) {
     double* V2i = V1i + (size_t)d1 * d1;
     if (!pencil_eig(c, d1, A11, M11, V1, V1i, mu1)) return false;
     if (!pencil_eig(c, d2, A22, M22, V2, V2i, mu2)) return false;
+    double* U1 = c->Ucat.d() + e * vstride;
+    if (!norm_factor(c, d1, V1, U1) || !norm_factor(c, d2, V2, U1 + (size_t)d1 * d1)) return false;
     for (int i = 0; i < d1; ++i) {
       const double q = 1.0 + mu1[i] * dt;
       if (!(q > 0.0)) return false;

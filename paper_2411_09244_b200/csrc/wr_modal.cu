@@ -79,7 +79,37 @@ void modal_seed(int E, int nc, int d1, int d2, int J, const double* Y0, const do
   PE_CUDA_CHECK(cudaGetLastError());
 }
 
-constexpr int MSCAN_DEPTH = 16;  // loads of this many time steps are issued before their use
+// Software-pipelined time walk for the scans: the loads of chunk c+1 (MSCAN_DEPTH steps of
+// one or two J-block arrays) are in flight while chunk c is consumed, so a thread keeps
+// ~2 x MSCAN_DEPTH loads outstanding for the whole walk (one chain per thread is all the
+// parallelism there is: E x d x nc chains).
+constexpr int MSCAN_DEPTH = 8;
+template <bool TWO, class Step>
+__device__ __forceinline__ void scan_walk(int s_begin, int J, long long stride,
+                                          const double* __restrict__ a, long long a_off,
+                                          const double* __restrict__ b, long long b_off, Step&& step) {
+  double va[MSCAN_DEPTH], wa[MSCAN_DEPTH], vb[MSCAN_DEPTH], wb[MSCAN_DEPTH];
+  auto load = [&](double (&v)[MSCAN_DEPTH], double (&w)[MSCAN_DEPTH], int s0) {
+#pragma unroll
+    for (int q = 0; q < MSCAN_DEPTH; ++q)
+      if (s0 + q < J) {
+        v[q] = a[(long long)(s0 + q + a_off) * stride];
+        if (TWO) w[q] = b[(long long)(s0 + q + b_off) * stride];
+      }
+  };
+  auto run = [&](const double (&v)[MSCAN_DEPTH], const double (&w)[MSCAN_DEPTH], int s0) {
+#pragma unroll
+    for (int q = 0; q < MSCAN_DEPTH; ++q)
+      if (s0 + q < J) step(s0 + q, v[q], TWO ? w[q] : 0.0);
+  };
+  load(va, wa, s_begin);
+  for (int s0 = s_begin; s0 < J; s0 += 2 * MSCAN_DEPTH) {
+    load(vb, wb, s0 + MSCAN_DEPTH);
+    run(va, wa, s0);
+    load(va, wa, s0 + 2 * MSCAN_DEPTH);
+    run(vb, wb, s0 + MSCAN_DEPTH);
+  }
+}
 
 // u solve in modal coordinates: one thread per (member, mode i, interval n).
 // In:  R (J blocks, r~ without the row-0 term), Yc (current buffer).
@@ -108,40 +138,19 @@ __global__ void modal_uscan_kernel(int nc, int d1, int J, int E, double dt, doub
     const double y0 = yc[0], yJ = yc[(long long)(J + 1) * L1];
     // pass 1: c = sum_{s=1}^{J-1} a^{J-s} dt r_s
     double c = 0.0;
-    for (int s0 = 1; s0 < J; s0 += MSCAN_DEPTH) {
-      double v[MSCAN_DEPTH];
-#pragma unroll
-      for (int q = 0; q < MSCAN_DEPTH; ++q)
-        if (s0 + q < J) v[q] = rp[(long long)(s0 + q) * L1];
-#pragma unroll
-      for (int q = 0; q < MSCAN_DEPTH; ++q)
-        if (s0 + q < J) c = a * fma(dt, v[q], c);
-    }
+    scan_walk<false>(1, J, L1, rp, 0, rp, 0, [&](int, double v, double) { c = a * fma(dt, v, c); });
     const double r0 = rp[0] + (y0 - alpha * yJ) / dt;
     double y = a * fma(alpha, c, dt * r0) * cd;
     // pass 2: y_s = a (y_{s-1} + dt r_s)
     double p1 = y0, p2 = y0;  // Y_{s-1}, Y_{s-2}
-    for (int s0 = 0; s0 < J; s0 += MSCAN_DEPTH) {
-      double v[MSCAN_DEPTH], w[MSCAN_DEPTH];
-#pragma unroll
-      for (int q = 0; q < MSCAN_DEPTH; ++q)
-        if (s0 + q < J) {
-          v[q] = rp[(long long)(s0 + q) * L1];
-          w[q] = yc[(long long)(s0 + q + 2) * L1];
-        }
-#pragma unroll
-      for (int q = 0; q < MSCAN_DEPTH; ++q) {
-        const int s = s0 + q;
-        if (s < J) {
-          if (s > 0) y = a * fma(dt, v[q], y);
-          yn[(long long)(s + 2) * L1] = y;
-          ey[(long long)s * L1] = y - w[q];
-          dy[(long long)s * L1] = p1 - p2;
-          p2 = p1;
-          p1 = y;
-        }
-      }
-    }
+    scan_walk<true>(0, J, L1, rp, 0, yc, 2, [&](int s, double v, double w) {
+      if (s > 0) y = a * fma(dt, v, y);
+      yn[(long long)(s + 2) * L1] = y;
+      ey[(long long)s * L1] = y - w;
+      dy[(long long)s * L1] = p1 - p2;
+      p2 = p1;
+      p1 = y;
+    });
   }
 }
 
@@ -150,7 +159,7 @@ void modal_uscan(int E, int nc, int d1, int J, double dt, double alpha, const do
                  double* EY, const WrColumnState* cs, cudaStream_t st) {
   const long long total = (long long)E * d1 * nc;
   if (total == 0 || J == 0) return;
-  modal_uscan_kernel<<<grid_1d(total, 128), 128, 0, st>>>(nc, d1, J, E, dt, alpha, acoef, cden, R,
+  modal_uscan_kernel<<<grid_1d(total, 64), 64, 0, st>>>(nc, d1, J, E, dt, alpha, acoef, cden, R,
                                                           Yc, Yn, DY, EY, cs);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
@@ -179,27 +188,14 @@ __global__ void modal_wscan_kernel(int nc, int d2, int J, int E, const double* _
     double* ez = EZ + (long long)e * J * L2 + r;
     double z = zc[L2];
     double p1 = z, p2 = z;
-    for (int s0 = 0; s0 < J; s0 += MSCAN_DEPTH) {
-      double v[MSCAN_DEPTH], w[MSCAN_DEPTH];
-#pragma unroll
-      for (int q = 0; q < MSCAN_DEPTH; ++q)
-        if (s0 + q < J) {
-          v[q] = hp[(long long)(s0 + q) * L2];
-          w[q] = zc[(long long)(s0 + q + 2) * L2];
-        }
-#pragma unroll
-      for (int q = 0; q < MSCAN_DEPTH; ++q) {
-        const int s = s0 + q;
-        if (s < J) {
-          z = fma(l, z, v[q]);
-          zn[(long long)(s + 2) * L2] = z;
-          ez[(long long)s * L2] = z - w[q];
-          dz[(long long)s * L2] = p1 - p2;
-          p2 = p1;
-          p1 = z;
-        }
-      }
-    }
+    scan_walk<true>(0, J, L2, hp, 0, zc, 2, [&](int s, double v, double w) {
+      z = fma(l, z, v);
+      zn[(long long)(s + 2) * L2] = z;
+      ez[(long long)s * L2] = z - w;
+      dz[(long long)s * L2] = p1 - p2;
+      p2 = p1;
+      p1 = z;
+    });
   }
 }
 
@@ -208,67 +204,66 @@ void modal_wscan(int E, int nc, int d2, int J, const double* lam, const double* 
                  cudaStream_t st) {
   const long long total = (long long)E * d2 * nc;
   if (total == 0 || J == 0) return;
-  modal_wscan_kernel<<<grid_1d(total, 128), 128, 0, st>>>(nc, d2, J, E, lam, H, Zc, Zn, DZ, EZ, cs);
+  modal_wscan_kernel<<<grid_1d(total, 64), 64, 0, st>>>(nc, d2, J, E, lam, H, Zc, Zn, DZ, EZ, cs);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
 }
 
-// Stop decision, one CTA per (member, interval): ||dU_s|| = sqrt(sum of the 8-row block
-// partials of the norm GEMM, blocks in ascending order), residual = max_s ||dU_s|| +
-// max_s ||dW_s|| (allatonce.py:250-254), then the reference stop tests.
+// Stop decision.  Phase 1, one thread per (side, member, column (s, n)):
+// ||dU_s|| = sqrt(sum of the norm GEMM's 8-row block partials, blocks in ascending order),
+// max over s by an atomic max on the IEEE bits (exact and order-free for the non-negative
+// norms; NaN / inf propagate as the largest bit patterns).  Phase 2, the last CTA (ticket):
+// residual = max_s ||dU_s|| + max_s ||dW_s|| (allatonce.py:250-254) and the reference stop
+// tests per interval; it also re-zeroes the maxima and the ticket for the next sweep.
 constexpr int DECIDE_THREADS = 256;
 __global__ void __launch_bounds__(DECIDE_THREADS)
-    modal_decide_kernel(int nc, int d1, int d2, int J, const double* __restrict__ nu, long long nu_g,
-                        long long nu_m, const double* __restrict__ nw, long long nw_g,
-                        long long nw_m, WrColumnState* cs, double tol, int max_iter,
+    modal_decide_kernel(int E, int nc, int d1, int d2, int J, const double* __restrict__ nu,
+                        long long nu_g, long long nu_m, const double* __restrict__ nw,
+                        long long nw_g, long long nw_m, unsigned long long* colmax,
+                        unsigned* ticket, WrColumnState* cs, double tol, int max_iter,
                         double* resid_hist, int* active_count, int par_new) {
-  const int en = blockIdx.x;
-  if (!cs[en].active) return;  // block-uniform
-  const int e = en / nc, n = en - (en / nc) * nc;
+  const long long NJ = (long long)J * nc, per = (long long)E * NJ;
   const int gu = (d1 + 7) / 8, gw = (d2 + 7) / 8;
-  double mu = 0.0, mw = 0.0;
-  for (int q = threadIdx.x; q < 2 * J; q += DECIDE_THREADS) {
-    const bool w = q >= J;
-    const int s = w ? q - J : q;
-    const int G = w ? gw : gu;
-    if (G == 0) continue;
-    const double* p = w ? nw + e * nw_m + (long long)s * nc + n : nu + e * nu_m + (long long)s * nc + n;
-    const long long gs = w ? nw_g : nu_g;
-    double acc = 0.0;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t < 2 * per) {
+    const int side = (int)(t / per);
+    const long long rem = t - side * per;
+    const int e = (int)(rem / NJ);
+    const long long j = rem - e * NJ;
+    const int n = (int)(j % nc);
+    const int G = side ? gw : gu;
+    if (G > 0 && cs[(long long)e * nc + n].active) {
+      const double* p = side ? nw + e * nw_m + j : nu + e * nu_m + j;
+      const long long gs = side ? nw_g : nu_g;
+      double acc = 0.0;
 #pragma unroll 8
-    for (int g = 0; g < G; ++g) acc += p[g * gs];
-    const double v = sqrt(acc);
-    if (w)
-      mw = (v > mw || v != v) ? v : mw;
-    else
-      mu = (v > mu || v != v) ? v : mu;
-  }
-  // exact (order-free) max reduction
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double a = __shfl_xor_sync(0xffffffffu, mu, o), b = __shfl_xor_sync(0xffffffffu, mw, o);
-    mu = (a > mu || a != a) ? a : mu;
-    mw = (b > mw || b != b) ? b : mw;
-  }
-  __shared__ double su[DECIDE_THREADS / 32], sw[DECIDE_THREADS / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    su[warp] = mu;
-    sw[warp] = mw;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < DECIDE_THREADS / 32; ++k) {
-      mu = (su[k] > mu || su[k] != su[k]) ? su[k] : mu;
-      mw = (sw[k] > mw || sw[k] != sw[k]) ? sw[k] : mw;
+      for (int g = 0; g < G; ++g) acc += p[g * gs];
+      atomicMax(colmax + (long long)side * E * nc + (long long)e * nc + n,
+                (unsigned long long)__double_as_longlong(sqrt(acc)));
     }
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *ticket = 0u;
+  const long long ncs = (long long)E * nc;
+  for (long long en = threadIdx.x; en < ncs; en += blockDim.x) {
+    WrColumnState c = cs[en];
+    if (!c.active) continue;
+    const double mu = __longlong_as_double((long long)__ldcg(colmax + en));
+    const double mw = __longlong_as_double((long long)__ldcg(colmax + ncs + en));
+    colmax[en] = 0ull;
+    colmax[ncs + en] = 0ull;
     double resid = 0.0;
     if (d1 > 0) resid += mu;
     if (d2 > 0) resid += mw;
-    WrColumnState c = cs[en];
     c.fpar = par_new;  // this sweep wrote the interval's latest waveforms
     const bool go = wr_stop_update(c, resid, tol, max_iter,
-                                   resid_hist ? resid_hist + (long long)en * max_iter : nullptr);
+                                   resid_hist ? resid_hist + en * max_iter : nullptr);
     cs[en] = c;
     if (go) atomicAdd(active_count, 1);
   }
@@ -276,11 +271,15 @@ __global__ void __launch_bounds__(DECIDE_THREADS)
 
 void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long long nu_g,
                   long long nu_m, const double* nw, long long nw_g, long long nw_m,
-                  WrColumnState* cs, double tol, int max_iter, double* resid_hist,
-                  int* active_count, int par_new, cudaStream_t st) {
-  modal_decide_kernel<<<E * nc, DECIDE_THREADS, 0, st>>>(nc, d1, d2, J, nu, nu_g, nu_m, nw, nw_g,
-                                                         nw_m, cs, tol, max_iter, resid_hist,
-                                                         active_count, par_new);
+                  unsigned long long* colmax, unsigned* ticket, WrColumnState* cs, double tol,
+                  int max_iter, double* resid_hist, int* active_count, int par_new,
+                  cudaStream_t st) {
+  const long long total = 2LL * E * J * nc;
+  const int blocks = (int)std::max<long long>(1, (total + DECIDE_THREADS - 1) / DECIDE_THREADS);
+  modal_decide_kernel<<<blocks, DECIDE_THREADS, 0, st>>>(E, nc, d1, d2, J, nu, nu_g, nu_m, nw,
+                                                         nw_g, nw_m, colmax, ticket, cs, tol,
+                                                         max_iter, resid_hist, active_count,
+                                                         par_new);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
 }

@@ -14,6 +14,7 @@ from paper_2411_09244_b200 import _lib  # noqa: E402
 SHAPES = [  # (M, N, K, batch, label); label ending in "jc": B stored j-contiguous (K x N)
     (64, 19200, 64, 1, "cfg2 time transform jc"),
     (300, 4096, 600, 1, "cfg2 rhs/g"),
+    (300, 4096, 300, 2, "cfg2 modal norms"),
     (300, 64, 300, 16, "cfg2 blocked-w H step"),
     (300, 64, 300, 48, "cfg2 blocked-w fill"),
     (300, 64, 600, 66, "cfg2 shifted (batched)"),
