@@ -14,8 +14,14 @@
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <string>
 #include <stdexcept>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "mbar.cuh"
 #include "pe.h"
 #include "pe_internal.h"
 
@@ -36,6 +42,36 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+// Canonical k order of every libpe GEMM kernel: within each 16-deep k block, DMMA step q
+// (q = 0..3) contracts k = q, q+4, q+8, q+12, lane t4 holding k = 4 t4 + q.  A lane's four
+// fragments of one row are then one contiguous 32-byte run: two LDS.128 per fragment row
+// per k block instead of four LDS.64, conflict-free for a row stride of 18 doubles (and for
+// the 128-byte-swizzled TMA tiles).  Every kernel and variant uses this order, so results
+// never depend on the tile choice (batch invariance).
+template <int FM, int FN>
+__device__ __forceinline__ void dmma_block16(const double* as, int sa, const double* bs, int sb,
+                                             double (&acc)[FM][FN][2]) {
+  double af[FM][4], bf[FN][4];
+#pragma unroll
+  for (int x = 0; x < FM; ++x) {
+    const double2 u = *reinterpret_cast<const double2*>(as + x * 8 * sa);
+    const double2 v = *reinterpret_cast<const double2*>(as + x * 8 * sa + 2);
+    af[x][0] = u.x; af[x][1] = u.y; af[x][2] = v.x; af[x][3] = v.y;
+  }
+#pragma unroll
+  for (int y = 0; y < FN; ++y) {
+    const double2 u = *reinterpret_cast<const double2*>(bs + y * 8 * sb);
+    const double2 v = *reinterpret_cast<const double2*>(bs + y * 8 * sb + 2);
+    bf[y][0] = u.x; bf[y][1] = u.y; bf[y][2] = v.x; bf[y][3] = v.y;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int x = 0; x < FM; ++x)
+#pragma unroll
+      for (int y = 0; y < FN; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x][q], bf[y][q]);
 }
 
 // AK: A is k-contiguous (s1 == 1); BKC: B is k-contiguous (s0 == 1).
@@ -110,10 +146,12 @@ __device__ __forceinline__ void gemm_epilogue(const GemmParams& p, int z1, int z
 template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKC>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     gemm_f64_kernel(const __grid_constant__ GemmParams p) {
+  pdl_enter();
   constexpr int WARPS_M = BM / WM;
   constexpr int NT = WARPS_M * (BN / WN) * 32;
   constexpr int FM = WM / 8, FN = WN / 8;
-  constexpr int SK = BK + 4;  // row stride in doubles: 16-lane half-warps hit distinct banks
+  static_assert(BK % 16 == 0, "k blocks of 16 (canonical k order)");
+  constexpr int SK = BK + 2;  // row stride in doubles: conflict-free LDS.128 fragment runs
   __shared__ __align__(16) double As[2][BM * SK];
   __shared__ __align__(16) double Bs[2][BN * SK];
 
@@ -198,20 +236,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
         cp_async_wait<0>();
       }
       __syncthreads();
-      const double* as = &As[buf][(wm * WM + g) * SK + t4];
-      const double* bs = &Bs[buf][(wn * WN + g) * SK + t4];
+      const double* as = &As[buf][(wm * WM + g) * SK + 4 * t4];
+      const double* bs = &Bs[buf][(wn * WN + g) * SK + 4 * t4];
 #pragma unroll
-      for (int kk = 0; kk < BK; kk += 4) {
-        double af[FM], bf[FN];
-#pragma unroll
-        for (int a = 0; a < FM; ++a) af[a] = as[a * 8 * SK + kk];
-#pragma unroll
-        for (int b = 0; b < FN; ++b) bf[b] = bs[b * 8 * SK + kk];
-#pragma unroll
-        for (int a = 0; a < FM; ++a)
-#pragma unroll
-          for (int b = 0; b < FN; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-      }
+      for (int kb = 0; kb < BK; kb += 16) dmma_block16<FM, FN>(as + kb, SK, bs + kb, SK, acc);
       __syncthreads();
     }
   }
@@ -240,8 +268,8 @@ struct FastCfg {
   static constexpr int BM = WGM * 8 * FM;
   static constexpr int BN = WGN * 8 * FN;
   static constexpr int NT = WGM * WGN * 32;
-  static constexpr int SA = BK + 4;
-  static constexpr int SB = BJC ? (BN + 4) : (BK + 4);
+  static constexpr int SA = BK + 2;
+  static constexpr int SB = BJC ? (BN + 2) : (BK + 2);
   static constexpr int A_TILE = BM * SA;
   static constexpr int B_TILE = BJC ? BK * SB : BN * SB;
   static constexpr size_t SMEM = sizeof(double) * (size_t)STAGES * (A_TILE + B_TILE);
@@ -250,6 +278,7 @@ struct FastCfg {
 template <int WGM, int WGN, int FM, int FN, int BK, int STAGES, bool BJC>
 __global__ void __launch_bounds__(WGM * WGN * 32)
     gemm_fast_kernel(const __grid_constant__ GemmParams p) {
+  pdl_enter();
   using Cfg = FastCfg<WGM, WGN, FM, FN, BK, STAGES, BJC>;
   constexpr int BM = Cfg::BM, BN = Cfg::BN;
   constexpr int NT = Cfg::NT, SA = Cfg::SA, SB = Cfg::SB;
@@ -353,23 +382,33 @@ __global__ void __launch_bounds__(WGM * WGN * 32)
     if (t + STAGES - 1 < ntile) load_tile(t + STAGES - 1, (t + STAGES - 1) % STAGES);
     cp_async_commit();
     const int slot = t % STAGES;
-    const double* as = As + slot * Cfg::A_TILE + (wm * WTM + g) * SA + t4;
-    const double* bs;
-    if (!BJC)
-      bs = Bs + slot * Cfg::B_TILE + (wn * WTN + g) * SB + t4;
-    else
-      bs = Bs + slot * Cfg::B_TILE + t4 * SB + wn * WTN + g;
+    const double* as = As + slot * Cfg::A_TILE + (wm * WTM + g) * SA + 4 * t4;
+    if (!BJC) {
+      const double* bs = Bs + slot * Cfg::B_TILE + (wn * WTN + g) * SB + 4 * t4;
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[FM], bf[FN];
+      for (int kb = 0; kb < BK; kb += 16) dmma_block16<FM, FN>(as + kb, SA, bs + kb, SB, acc);
+    } else {  // B stored [k][j]: the lane's k run is strided; same canonical k order
+      const double* bs = Bs + slot * Cfg::B_TILE + (4 * t4) * SB + wn * WTN + g;
 #pragma unroll
-      for (int a = 0; a < FM; ++a) af[a] = as[a * 8 * SA + kk];
+      for (int kb = 0; kb < BK; kb += 16) {
+        double af[FM][4], bf[FN][4];
 #pragma unroll
-      for (int b = 0; b < FN; ++b) bf[b] = BJC ? bs[kk * SB + b * 8] : bs[b * 8 * SB + kk];
+        for (int x = 0; x < FM; ++x) {
+          const double2 u = *reinterpret_cast<const double2*>(as + kb + x * 8 * SA);
+          const double2 v = *reinterpret_cast<const double2*>(as + kb + x * 8 * SA + 2);
+          af[x][0] = u.x; af[x][1] = u.y; af[x][2] = v.x; af[x][3] = v.y;
+        }
 #pragma unroll
-      for (int a = 0; a < FM; ++a)
+        for (int y = 0; y < FN; ++y)
 #pragma unroll
-        for (int b = 0; b < FN; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+          for (int q = 0; q < 4; ++q) bf[y][q] = bs[(kb + q) * SB + y * 8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int x = 0; x < FM; ++x)
+#pragma unroll
+            for (int y = 0; y < FN; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x][q], bf[y][q]);
+      }
     }
   }
   cp_async_wait<0>();
@@ -398,6 +437,7 @@ __global__ void __launch_bounds__(WGM * WGN * 32)
 
 // Split-K reduction: C = alpha * sum_sp ws[sp] (splits in order) + epilogue.
 __global__ void splitk_reduce_kernel(const __grid_constant__ GemmParams p) {
+  pdl_enter();
   const int batch = p.nb1 * p.nb2;
   const long long per = (long long)p.M * p.N;
   const long long total = per * batch;
@@ -439,7 +479,7 @@ static void launch_fast(const GemmParams& p, cudaStream_t st) {
   using Cfg = FastCfg<WGM, WGN, FM, FN, BK, STAGES, BJC>;
   fast_occupancy<WGM, WGN, FM, FN, BK, STAGES, BJC>();
   dim3 grid((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM, p.nb1 * p.nb2 * p.ksplit);
-  gemm_fast_kernel<WGM, WGN, FM, FN, BK, STAGES, BJC><<<grid, Cfg::NT, Cfg::SMEM, st>>>(p);
+  launch_k(gemm_fast_kernel<WGM, WGN, FM, FN, BK, STAGES, BJC>, grid, dim3(Cfg::NT), Cfg::SMEM, st, p);
   ++g_launches;
 }
 
@@ -542,13 +582,13 @@ static void launch_cfg(const GemmParams& p, bool ak, bool bk, cudaStream_t st) {
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.nb1 * p.nb2);
   dim3 block((BM / WM) * (BN / WN) * 32);
   if (ak && bk)
-    gemm_f64_kernel<BM, BN, BK, WM, WN, true, true><<<grid, block, 0, st>>>(p);
+    launch_k(gemm_f64_kernel<BM, BN, BK, WM, WN, true, true>, grid, block, 0, st, p);
   else if (ak && !bk)
-    gemm_f64_kernel<BM, BN, BK, WM, WN, true, false><<<grid, block, 0, st>>>(p);
+    launch_k(gemm_f64_kernel<BM, BN, BK, WM, WN, true, false>, grid, block, 0, st, p);
   else if (!ak && bk)
-    gemm_f64_kernel<BM, BN, BK, WM, WN, false, true><<<grid, block, 0, st>>>(p);
+    launch_k(gemm_f64_kernel<BM, BN, BK, WM, WN, false, true>, grid, block, 0, st, p);
   else
-    gemm_f64_kernel<BM, BN, BK, WM, WN, false, false><<<grid, block, 0, st>>>(p);
+    launch_k(gemm_f64_kernel<BM, BN, BK, WM, WN, false, false>, grid, block, 0, st, p);
   ++g_launches;
 }
 
@@ -561,6 +601,250 @@ double gemm_flops(const GemmParams& p) {
     mk = m * k - m * (m - 1) / 2;
   }
   return 2.0 * mk * (double)p.N * p.nb1 * p.nb2;
+}
+
+// ----------------------------------------------------------------------------------------
+// TMA path (both operands k-contiguous): one producer warp streams the A and B k-tiles of
+// every segment with cp.async.bulk.tensor into a STAGES-deep ring of 128-byte-swizzled
+// shared tiles, signalling a "full" mbarrier per stage by transaction bytes; the DMMA
+// warps wait on it, consume the 16-deep k-tile and release the stage through an "empty"
+// mbarrier.  No CTA barrier and no per-thread address arithmetic in the main loop.  Tiles
+// are zero-filled out of bounds, the k order is the cp.async kernels' (segment by segment,
+// k ascending in DMMA steps of 4), so every path gives the same bits.
+struct alignas(64) TmaArgs {
+  CUtensorMap ta[3];
+  CUtensorMap tb[3];
+  GemmParams p;
+  int za[3][2], zb[3][2];  // per segment: use (z1, z2) as TMA batch coordinates (0: shared)
+};
+
+template <int WGM, int WGN, int FM, int FN, int STAGES>
+struct TmaCfg {
+  static constexpr int BM = WGM * 8 * FM, BN = WGN * 8 * FN, BK = 16;
+  static constexpr int NCW = WGM * WGN;         // DMMA (consumer) warps
+  static constexpr int NT = (NCW + 1) * 32;     // + one producer warp
+  static constexpr int A_BYTES = BM * 128, B_BYTES = BN * 128;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024 + 2 * STAGES * 8;
+};
+
+// byte offset of element (r, k) (k < 16) in a 128B-swizzled [rows][16 doubles] tile
+__device__ __forceinline__ unsigned swz(int r, int k) {
+  return (unsigned)(r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3));
+}
+
+template <int WGM, int WGN, int FM, int FN, int STAGES>
+__global__ void __launch_bounds__((WGM * WGN + 1) * 32)
+    gemm_tma_kernel(const __grid_constant__ TmaArgs a) {
+  using Cfg = TmaCfg<WGM, WGN, FM, FN, STAGES>;
+  constexpr int NCW = Cfg::NCW;
+  constexpr int WTM = 8 * FM, WTN = 8 * FN;
+  extern __shared__ unsigned char smraw[];
+  const unsigned sbase = (smem_u32(smraw) + 1023u) & ~1023u;
+  const unsigned char* sgen = smraw + (sbase - smem_u32(smraw));
+  const unsigned bar_full = sbase + STAGES * Cfg::STAGE;
+  const unsigned bar_empty = bar_full + STAGES * 8;
+  const GemmParams& p = a.p;
+  const int z = blockIdx.z;
+  const int z1 = z / p.nb2, z2 = z - (z / p.nb2) * p.nb2;
+  const int i0 = blockIdx.y * Cfg::BM, j0 = blockIdx.x * Cfg::BN;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  int kt[3] = {0, 0, 0};
+  for (int s = 0; s < p.nseg; ++s) kt[s] = (p.seg[s].K + 15) / 16;
+  const int ktot = kt[0] + kt[1] + kt[2];
+  const int tskip = p.tri_upper ? min(ktot, i0 / 16) : 0;
+  const int ntile = ktot - tskip;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_enter();
+
+  if (warp == NCW) {  // producer
+    if (lane == 0) {
+      for (int t = 0; t < ntile; ++t) {
+        const int st = t % STAGES;
+        if (t >= STAGES) mbar_wait_cta(bar_empty + 8 * st, ((t / STAGES) - 1) & 1);
+        int g = t + tskip, s = 0;
+        if (g >= kt[0]) { g -= kt[0]; s = 1; if (g >= kt[1]) { g -= kt[1]; s = 2; } }
+        const unsigned full = bar_full + 8 * st;
+        mbar_expect_tx(full, Cfg::STAGE);
+        const unsigned dA = sbase + st * Cfg::STAGE;
+        tma_load_4d(dA, &a.ta[s], g * 16, i0, a.za[s][1] ? z2 : 0, a.za[s][0] ? z1 : 0, full);
+        tma_load_4d(dA + Cfg::A_BYTES, &a.tb[s], g * 16, j0, a.zb[s][1] ? z2 : 0,
+                    a.zb[s][0] ? z1 : 0, full);
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = warp % WGM, wn = warp / WGM;
+  // swizzled offsets of the lane's k run (row g, k = 4 t4 .. 4 t4 + 3): two 16-byte chunks
+  const unsigned ko0 = swz(g, 4 * t4), ko1 = swz(g, 4 * t4 + 2);
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int x = 0; x < FM; ++x)
+#pragma unroll
+    for (int y = 0; y < FN; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+
+  for (int t = 0; t < ntile; ++t) {
+    const int st = t % STAGES;
+    mbar_wait_cta(bar_full + 8 * st, (t / STAGES) & 1);
+    const unsigned char* sa = sgen + st * Cfg::STAGE + (wm * WTM) * 128;
+    const unsigned char* sb = sgen + st * Cfg::STAGE + Cfg::A_BYTES + (wn * WTN) * 128;
+    double af[FM][4], bf[FN][4];
+#pragma unroll
+    for (int x = 0; x < FM; ++x) {
+      const double2 u = *reinterpret_cast<const double2*>(sa + x * 8 * 128 + ko0);
+      const double2 v = *reinterpret_cast<const double2*>(sa + x * 8 * 128 + ko1);
+      af[x][0] = u.x; af[x][1] = u.y; af[x][2] = v.x; af[x][3] = v.y;
+    }
+#pragma unroll
+    for (int y = 0; y < FN; ++y) {
+      const double2 u = *reinterpret_cast<const double2*>(sb + y * 8 * 128 + ko0);
+      const double2 v = *reinterpret_cast<const double2*>(sb + y * 8 * 128 + ko1);
+      bf[y][0] = u.x; bf[y][1] = u.y; bf[y][2] = v.x; bf[y][3] = v.y;
+    }
+    // the fragments are in registers: hand the stage back before the DMMAs
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_empty + 8 * st);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int x = 0; x < FM; ++x)
+#pragma unroll
+        for (int y = 0; y < FN; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x][q], bf[y][q]);
+  }
+  gemm_epilogue<FM, FN>(p, z1, z2, i0 + wm * WTM + g, j0 + wn * WTN + 2 * t4, acc);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    PE_CUDA_CHECK(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000,
+                                                   cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess)
+      throw Error{PE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable"};
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// 4-D map {k, row, z2, z1} of a k-contiguous FP64 operand; a zero batch stride collapses
+// that level (extent 1, coordinate 0).  Box = 16 k x box_rows rows, 128-byte swizzle.
+static void encode_operand(CUtensorMap* m, int use[2], const double* base, int K, int rows,
+                           long long row_stride, long long b1, int n1, long long b2, int n2,
+                           int box_rows) {
+  const cuuint64_t span = (cuuint64_t)row_stride * rows * 8;
+  cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)(b2 ? n2 : 1),
+                        (cuuint64_t)(b1 ? n1 : 1)};
+  cuuint64_t strides[3] = {(cuuint64_t)row_stride * 8, (cuuint64_t)(b2 ? b2 * 8 : ((span + 15) & ~15ull)),
+                           (cuuint64_t)(b1 ? b1 * 8 : ((span + 15) & ~15ull))};
+  cuuint32_t box[4] = {16, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  use[0] = b1 != 0;
+  use[1] = b2 != 0;
+  const CUresult r = tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                                          const_cast<double*>(base), dims, strides, box, es,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error{PE_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
+}
+
+// TMA eligibility: every segment k-contiguous in both operands, 16-byte aligned bases,
+// even (16-byte) row and batch strides, no split-K.
+static bool tma_ok(const GemmParams& p) {
+  static const bool off = getenv("PE_GEMM_NO_TMA") != nullptr;
+  if (off || p.nseg == 0) return false;
+  for (int s = 0; s < p.nseg; ++s) {
+    const Operand& A = p.seg[s].A;
+    const Operand& B = p.seg[s].B;
+    if (A.s1 != 1 || B.s0 != 1) return false;
+    if ((A.s0 & 1) || (B.s1 & 1) || (A.b1 & 1) || (A.b2 & 1) || (B.b1 & 1) || (B.b2 & 1)) return false;
+    if (A.s0 <= 0 || B.s1 <= 0 || A.b1 < 0 || A.b2 < 0 || B.b1 < 0 || B.b2 < 0) return false;
+    if (!aligned16(A.p) || !aligned16(B.p) || p.seg[s].K <= 0) return false;
+  }
+  return true;
+}
+
+template <int WGM, int WGN, int FM, int FN, int STAGES>
+static void launch_tma(const GemmParams& p, cudaStream_t st) {
+  using Cfg = TmaCfg<WGM, WGN, FM, FN, STAGES>;
+  static bool attr = false;
+  auto kern = gemm_tma_kernel<WGM, WGN, FM, FN, STAGES>;
+  if (!attr) {
+    PE_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+    attr = true;
+  }
+  TmaArgs a;
+  memset(static_cast<void*>(&a), 0, sizeof(a));
+  a.p = p;
+  a.p.ksplit = 1;
+  for (int s = 0; s < p.nseg; ++s) {
+    const GemmSeg& g = p.seg[s];
+    encode_operand(&a.ta[s], a.za[s], g.A.p, g.K, p.M, g.A.s0, g.A.b1, p.nb1, g.A.b2, p.nb2, Cfg::BM);
+    encode_operand(&a.tb[s], a.zb[s], g.B.p, g.K, p.N, g.B.s1, g.B.b1, p.nb1, g.B.b2, p.nb2, Cfg::BN);
+  }
+  dim3 grid((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM, p.nb1 * p.nb2);
+  launch_k(kern, grid, dim3(Cfg::NT), Cfg::SMEM, st, a);
+  ++g_launches;
+}
+
+// TMA variants: id, consumer warps (M, N), fragments per warp (M, N), stages.
+#define PE_TMA_VARIANTS(X) \
+  X(0, 2, 3, 4, 3, 4)      \
+  X(1, 2, 2, 4, 4, 4)      \
+  X(2, 4, 2, 4, 4, 3)      \
+  X(3, 2, 2, 5, 4, 4)      \
+  X(4, 1, 2, 4, 4, 4)      \
+  X(5, 2, 4, 4, 4, 3)
+
+template <int WGM, int WGN, int FM, int FN, int STAGES>
+static double tma_cost(const GemmParams& p) {
+  using Cfg = TmaCfg<WGM, WGN, FM, FN, STAGES>;
+  const double ctas = (double)((p.M + Cfg::BM - 1) / Cfg::BM) * ((p.N + Cfg::BN - 1) / Cfg::BN) *
+                      p.nb1 * p.nb2;
+  const double per_sm = std::ceil(ctas / 148.0);
+  const double eff = (Cfg::NCW <= 2) ? 0.8 : 1.0;
+  return per_sm * Cfg::BM * Cfg::BN / eff;
+}
+
+static void launch_tma_best(const GemmParams& p, cudaStream_t st) {
+  static const int forced = getenv("PE_TMA_VARIANT") ? atoi(getenv("PE_TMA_VARIANT")) : -1;
+  int best = 0;
+  double bc = 1e300;
+#define PE_X(ID, WGM, WGN, FM, FN, ST)                         \
+  {                                                            \
+    const double c = tma_cost<WGM, WGN, FM, FN, ST>(p);        \
+    if (c < bc * 0.97) {                                       \
+      bc = c;                                                  \
+      best = ID;                                               \
+    }                                                          \
+  }
+  PE_TMA_VARIANTS(PE_X)
+#undef PE_X
+  if (forced >= 0) best = forced;
+  switch (best) {
+#define PE_X(ID, WGM, WGN, FM, FN, ST) \
+  case ID:                             \
+    launch_tma<WGM, WGN, FM, FN, ST>(p, st); \
+    return;
+    PE_TMA_VARIANTS(PE_X)
+#undef PE_X
+    default:
+      launch_tma<2, 3, 4, 3, 4>(p, st);
+  }
 }
 
 void gemm_f64(const GemmParams& p, cudaStream_t st) {
@@ -596,13 +880,20 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
       else
         launch_fast<2, 2, 4, 4, 32, 3, true>(q, st);
       const long long total = (long long)batch * p.M * p.N;
-      splitk_reduce_kernel<<<(int)std::min<long long>(148 * 8, (total + 255) / 256), 256, 0, st>>>(q);
+      launch_k(splitk_reduce_kernel, dim3((unsigned)std::min<long long>(148 * 8, (total + 255) / 256)),
+               dim3(256), 0, st, q);
       ++g_launches;
       PE_CUDA_CHECK(cudaGetLastError());
       return;
     }
   }
-  if (lay >= 0 && (tiles64 >= 96 || tiles_n32 >= 96)) {
+  // TMA pipeline: measured faster than the cp.async kernels only for many skinny batched
+  // products (the shifted solves: N <= 128 per batch, long K); slower on the wide rhs / g /
+  // norm / ensemble-step shapes (tools/gemm_bench.py, profiles/r01/README.md)
+  const bool tma_shape = batch >= 16 && p.N <= 128 && p.seg[0].K >= 512;
+  if (lay == 0 && (tiles64 >= 96 || tiles_n32 >= 96) && tma_shape && tma_ok(p)) {
+    launch_tma_best(p, st);
+  } else if (lay >= 0 && (tiles64 >= 96 || tiles_n32 >= 96)) {
     // pick the tile / pipeline variant with the best wave-quantised cost; the choice is a
     // function of the shape only and never changes the arithmetic
     static const int forced = getenv("PE_GEMM_VARIANT") ? atoi(getenv("PE_GEMM_VARIANT")) : -1;

@@ -14,6 +14,7 @@
 namespace pe {
 
 long long g_launches = 0;
+bool g_pdl = getenv("PE_NO_PDL") == nullptr;
 static thread_local std::string t_err;
 void set_error(const std::string& m) { t_err = m; }
 
@@ -391,7 +392,6 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
 
   auto body = [&](int par, cudaStream_t s) {
     const int cur = par, nxt = par ^ 1;
-    PE_CUDA_CHECK(cudaMemsetAsync(cnt + par, 0, sizeof(int), s));
     run_gemm(c, rhs_params(c->Zb[cur].d()), s);
     modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), c->R.d(), c->Yb[cur].d(),
                 c->Yb[nxt].d(), c->DYm.d(), EY, cs, s);

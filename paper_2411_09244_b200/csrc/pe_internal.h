@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 
 namespace pe {
 
@@ -21,6 +22,34 @@ struct Error {
     if (_e != cudaSuccess)                                                                \
       throw ::pe::Error{PE_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
   } while (0)
+
+// ---------------------------------------------------------------- launches
+// Programmatic dependent launch (PDL): the sweep kernels are launched with programmatic
+// stream serialization, so a kernel's CTAs are scheduled while its predecessor drains.
+// Every such kernel first triggers its own dependents (all of its CTAs are resident by
+// then) and then waits for its predecessor grid to complete and flush before touching any
+// global memory; because every kernel of the chain waits, completion stays transitive.
+extern bool g_pdl;
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+              Args&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = g_pdl ? at : nullptr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  PE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // ---------------------------------------------------------------- FP64 DMMA GEMM
 //

@@ -121,6 +121,7 @@ __global__ void modal_uscan_kernel(int nc, int d1, int J, int E, double dt, doub
                                    const double* __restrict__ Yc, double* __restrict__ Yn,
                                    double* __restrict__ DY, double* __restrict__ EY,
                                    const WrColumnState* __restrict__ cs) {
+  pdl_enter();
   const long long L1 = (long long)d1 * nc;
   const long long total = (long long)E * L1;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -159,8 +160,8 @@ void modal_uscan(int E, int nc, int d1, int J, double dt, double alpha, const do
                  double* EY, const WrColumnState* cs, cudaStream_t st) {
   const long long total = (long long)E * d1 * nc;
   if (total == 0 || J == 0) return;
-  modal_uscan_kernel<<<grid_1d(total, 64), 64, 0, st>>>(nc, d1, J, E, dt, alpha, acoef, cden, R,
-                                                          Yc, Yn, DY, EY, cs);
+  launch_k(modal_uscan_kernel, dim3(grid_1d(total, 64)), dim3(64), 0, st, nc, d1, J, E, dt, alpha,
+           acoef, cden, R, Yc, Yn, DY, EY, cs);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
 }
@@ -172,6 +173,7 @@ __global__ void modal_wscan_kernel(int nc, int d2, int J, int E, const double* _
                                    const double* __restrict__ H, const double* __restrict__ Zc,
                                    double* __restrict__ Zn, double* __restrict__ DZ,
                                    double* __restrict__ EZ, const WrColumnState* __restrict__ cs) {
+  pdl_enter();
   const long long L2 = (long long)d2 * nc;
   const long long total = (long long)E * L2;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -204,7 +206,8 @@ void modal_wscan(int E, int nc, int d2, int J, const double* lam, const double* 
                  cudaStream_t st) {
   const long long total = (long long)E * d2 * nc;
   if (total == 0 || J == 0) return;
-  modal_wscan_kernel<<<grid_1d(total, 64), 64, 0, st>>>(nc, d2, J, E, lam, H, Zc, Zn, DZ, EZ, cs);
+  launch_k(modal_wscan_kernel, dim3(grid_1d(total, 64)), dim3(64), 0, st, nc, d2, J, E, lam, H, Zc,
+           Zn, DZ, EZ, cs);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
 }
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(DECIDE_THREADS)
                         long long nw_g, long long nw_m, unsigned long long* colmax,
                         unsigned* ticket, WrColumnState* cs, double tol, int max_iter,
                         double* resid_hist, int* active_count, int par_new) {
+  pdl_enter();
   const long long NJ = (long long)J * nc, per = (long long)E * NJ;
   const int gu = (d1 + 7) / 8, gw = (d2 + 7) / 8;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -251,9 +255,12 @@ __global__ void __launch_bounds__(DECIDE_THREADS)
   __threadfence();
   if (threadIdx.x == 0) *ticket = 0u;
   const long long ncs = (long long)E * nc;
-  for (long long en = threadIdx.x; en < ncs; en += blockDim.x) {
+  int still = 0;  // intervals that keep iterating (written, not accumulated: no memset)
+  for (long long base = 0; base < ncs; base += blockDim.x) {
+    const long long en = base + threadIdx.x;
+    bool go = false;
+    if (en < ncs && cs[en].active) {
     WrColumnState c = cs[en];
-    if (!c.active) continue;
     const double mu = __longlong_as_double((long long)__ldcg(colmax + en));
     const double mw = __longlong_as_double((long long)__ldcg(colmax + ncs + en));
     colmax[en] = 0ull;
@@ -262,11 +269,12 @@ __global__ void __launch_bounds__(DECIDE_THREADS)
     if (d1 > 0) resid += mu;
     if (d2 > 0) resid += mw;
     c.fpar = par_new;  // this sweep wrote the interval's latest waveforms
-    const bool go = wr_stop_update(c, resid, tol, max_iter,
-                                   resid_hist ? resid_hist + en * max_iter : nullptr);
+    go = wr_stop_update(c, resid, tol, max_iter, resid_hist ? resid_hist + en * max_iter : nullptr);
     cs[en] = c;
-    if (go) atomicAdd(active_count, 1);
+    }
+    still += __syncthreads_count(go);
   }
+  if (threadIdx.x == 0) *active_count = still;
 }
 
 void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long long nu_g,
@@ -276,10 +284,9 @@ void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long l
                   cudaStream_t st) {
   const long long total = 2LL * E * J * nc;
   const int blocks = (int)std::max<long long>(1, (total + DECIDE_THREADS - 1) / DECIDE_THREADS);
-  modal_decide_kernel<<<blocks, DECIDE_THREADS, 0, st>>>(E, nc, d1, d2, J, nu, nu_g, nu_m, nw,
-                                                         nw_g, nw_m, colmax, ticket, cs, tol,
-                                                         max_iter, resid_hist, active_count,
-                                                         par_new);
+  launch_k(modal_decide_kernel, dim3(blocks), dim3(DECIDE_THREADS), 0, st, E, nc, d1, d2, J, nu,
+           nu_g, nu_m, nw, nw_g, nw_m, colmax, ticket, cs, tol, max_iter, resid_hist, active_count,
+           par_new);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
 }
