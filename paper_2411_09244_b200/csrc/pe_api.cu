@@ -1,6 +1,7 @@
 // C ABI of libpe (include/pe.h): context, uploads, fine propagators, fused coarse
 // correction and the device-resident parareal loop.
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -138,38 +139,57 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
       return;
     }
   }
-  for (int s = 0; s < J; ++s) {
-    const bool last = (s == J - 1);
-    double* Xn = last ? X_out : bufX[s & 1];
-    double* Dn = last ? nullptr : bufD[s & 1];
-    GemmParams p;
-    p.M = d;
-    p.N = nc;
-    p.nb1 = E;
-    p.nseg = Ds ? 2 : 1;
-    p.seg[0].A = Operand{c->T.d(), 2LL * d, 1, 2LL * d * d, 0};
-    p.seg[0].B = Operand{Xs, 1, d, (long long)nc * d, 0};
-    p.seg[0].K = d;
-    if (Ds) {
-      p.seg[1].A = Operand{c->T.d() + d, 2LL * d, 1, 2LL * d * d, 0};
-      p.seg[1].B = Operand{Ds, 1, d, (long long)nc * d, 0};
-      p.seg[1].K = d;
+  // Ensembles whose operators exceed L2 (cfg4: 64 x 5.8 MB) run member chunks through all
+  // J steps, so a chunk's T stays L2-resident across its steps instead of streaming every
+  // member's T from HBM once per step.  Members are independent: same arithmetic.
+  static const int chunk_env = getenv("PE_SEQ_CHUNK") ? atoi(getenv("PE_SEQ_CHUNK")) : 0;
+  // measured at cfg4 (E = 64, d = 600, tools/chunk_sweep.sh): 2 chunks of 32 members
+  // 8.6 ms, 1 chunk 9.8 ms, 4 chunks 15.5 ms (the per-step launches underfill the SMs)
+  const double t_total = 16.0 * d * d * E;
+  const int nchunks = (int)std::ceil(t_total / 190e6);
+  int EC = chunk_env > 0 ? chunk_env : (E + nchunks - 1) / nchunks;
+  if (EC >= E || J < 2) EC = E;
+  const long long xs = (long long)nc * d;
+  const double* X0 = Xs;
+  const double* D0 = Ds;
+  for (int e0 = 0; e0 < E; e0 += EC) {
+    const int ec = std::min(EC, E - e0);
+    const long long xo = e0 * xs;
+    Xs = X0 + xo;
+    Ds = D0 ? D0 + xo : nullptr;
+    for (int s = 0; s < J; ++s) {
+      const bool last = (s == J - 1);
+      double* Xn = (last ? X_out : bufX[s & 1]) + xo;
+      double* Dn = last ? nullptr : bufD[s & 1] + xo;
+      GemmParams p;
+      p.M = d;
+      p.N = nc;
+      p.nb1 = ec;
+      p.nseg = Ds ? 2 : 1;
+      p.seg[0].A = Operand{c->T.d() + e0 * 2LL * d * d, 2LL * d, 1, 2LL * d * d, 0};
+      p.seg[0].B = Operand{Xs, 1, d, xs, 0};
+      p.seg[0].K = d;
+      if (Ds) {
+        p.seg[1].A = Operand{c->T.d() + e0 * 2LL * d * d + d, 2LL * d, 1, 2LL * d * d, 0};
+        p.seg[1].B = Operand{Ds, 1, d, xs, 0};
+        p.seg[1].K = d;
+      }
+      p.C = Xn;
+      p.c_i = 1;
+      p.c_j = d;
+      p.c_b1 = xs;
+      p.ws = c->splitws.d();
+      p.ws_doubles = c->splitws.bytes / sizeof(double);
+      p.bias = c->cvec.d() + (long long)e0 * d;
+      p.bias_b1 = d;
+      if (Dn) {
+        p.D = Dn;
+        p.Xp = Xs;
+      }
+      run_gemm(c, p, st);
+      Xs = Xn;
+      Ds = Dn;
     }
-    p.C = Xn;
-    p.c_i = 1;
-    p.c_j = d;
-    p.c_b1 = (long long)nc * d;
-    p.ws = c->splitws.d();
-    p.ws_doubles = c->splitws.bytes / sizeof(double);
-    p.bias = c->cvec.d();
-    p.bias_b1 = d;
-    if (Dn) {
-      p.D = Dn;
-      p.Xp = Xs;
-    }
-    run_gemm(c, p, st);
-    Xs = Xn;
-    Ds = Dn;
   }
   if (J == 0) PE_CUDA_CHECK(cudaMemcpyAsync(X_out, X_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   collect_profile(c, st);

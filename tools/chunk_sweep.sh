@@ -1,0 +1,3 @@
+for c in 64 32 16 8 4; do
+  PE_SEQ_CHUNK=$c timeout 300 python bench.py --workload cfg4-seq --steps 5 --warmup 3 --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('chunk $c', d['ms_per_step'], d['value'])"
+done
