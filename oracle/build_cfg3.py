@@ -7,7 +7,8 @@ aux-eigenproblem cache (boundary blocks of a range are solved twice, which is ha
 `aux_eigen_cem` is deterministic).  Columns are stacked in ascending block order exactly
 as `make_golden.build_system` does, then `project_coarse` and the F2 rescaling.
 
-Output: data/sys_cfg3.npz (~0.8 GB, git-ignored; travels to the GPU box with gpurun).
+Output: data/sys_cfg3.npz (zlib-compressed: the blocks are 13 % nonzero, 110 MB instead of
+0.8 GB; git-ignored; travels to the GPU box with gpurun, whose snapshot limit is 512 MiB).
 """
 
 from __future__ import annotations
@@ -109,7 +110,7 @@ def main():
                 dt_over_bound=R_STABILITY, d1=d1, d2=d2, n_rects=n_rects,
                 build_seconds=build_s, workers=workers)
     os.makedirs("data", exist_ok=True)
-    np.savez("data/sys_cfg3.npz", M11=system.M11, A11=scale * system.A11, M12=system.M12,
+    np.savez_compressed("data/sys_cfg3.npz", M11=system.M11, A11=scale * system.A11, M12=system.M12,
              A12=scale * system.A12, M22=system.M22, A22=scale * system.A22, f1=f1, f2=f2,
              meta=json.dumps(meta))
     print(json.dumps(meta))
