@@ -366,44 +366,58 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     return g;
   };
   // residual norms ||V1 EY_s|| = ||U1 EY_s|| (U1 upper-triangular, setup.cu norm_factor),
-  // likewise W, per (s, interval) as 8-row block partials.  The U product depends only on
-  // the u scan, so it runs on a forked branch concurrently with the h GEMM and the w scan.
-  GemmParams normq[2];
-  for (int side = 0; side < 2; ++side) {
-    const int M = side ? d2 : d1;
-    GemmParams& q = normq[side];
-    q.M = M;
+  // likewise W, per (s, interval) as 8-row block partials
+  std::vector<GemmParams> norms;
+  long long nu_g, nu_m, nw_g, nw_m;
+  const double *nu, *nw;
+  if (d1 == d2) {  // one launch, the two sides as the inner batch level
+    GemmParams q;
+    q.M = d1;
     q.N = (int)NJ;
     q.nb1 = E;
+    q.nb2 = 2;
     q.nseg = 1;
-    q.seg[0].A = Operand{c->Ucat.d() + (side ? (long long)d1 * d1 : 0), M, 1, vstride, 0};
-    q.seg[0].B = Operand{side ? EZ : EY, 1, M, J * (side ? L2 : L1), 0};
-    q.seg[0].K = M;
+    q.seg[0].A = Operand{c->Ucat.d(), d1, 1, vstride, (long long)d1 * d1};
+    q.seg[0].B = Operand{EY, 1, d1, J * L1, E * J * L1};
+    q.seg[0].K = d1;
     q.tri_upper = 1;
-    q.nrm = c->nrmp.d() + (side ? (long long)g1 * E * NJ : 0);
-    q.nrm_ld = E * NJ;
+    q.nrm = c->nrmp.d();
+    q.nrm_ld = 2LL * E * NJ;
+    norms.push_back(q);
+    nu = c->nrmp.d();
+    nw = c->nrmp.d() + NJ;
+    nu_g = nw_g = 2LL * E * NJ;
+    nu_m = nw_m = 2 * NJ;
+  } else {
+    for (int side = 0; side < 2; ++side) {
+      const int M = side ? d2 : d1;
+      GemmParams q;
+      q.M = M;
+      q.N = (int)NJ;
+      q.nb1 = E;
+      q.nseg = 1;
+      q.seg[0].A = Operand{c->Ucat.d() + (side ? (long long)d1 * d1 : 0), M, 1, vstride, 0};
+      q.seg[0].B = Operand{side ? EZ : EY, 1, M, J * (side ? L2 : L1), 0};
+      q.seg[0].K = M;
+      q.tri_upper = 1;
+      q.nrm = c->nrmp.d() + (side ? (long long)g1 * E * NJ : 0);
+      q.nrm_ld = E * NJ;
+      norms.push_back(q);
+    }
+    nu = c->nrmp.d();
+    nw = c->nrmp.d() + (long long)g1 * E * NJ;
+    nu_g = nw_g = E * NJ;
+    nu_m = nw_m = NJ;
   }
-  const double* nu = c->nrmp.d();
-  const double* nw = c->nrmp.d() + (long long)g1 * E * NJ;
-  const long long nu_g = E * NJ, nw_g = E * NJ, nu_m = NJ, nw_m = NJ;
 
   auto body = [&](int par, cudaStream_t s) {
     const int cur = par, nxt = par ^ 1;
     run_gemm(c, rhs_params(c->Zb[cur].d()), s);
     modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), c->R.d(), c->Yb[cur].d(),
                 c->Yb[nxt].d(), c->DYm.d(), EY, cs, s);
-    const bool fork = !c->profiling;  // profiling times launches on one stream
-    if (fork) {
-      PE_CUDA_CHECK(cudaEventRecord(c->ev_fork, s));
-      PE_CUDA_CHECK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-      run_gemm(c, normq[0], c->side);
-      PE_CUDA_CHECK(cudaEventRecord(c->ev_join, c->side));
-    }
     run_gemm(c, g_params(c->Yb[nxt].d()), s);
     modal_wscan(E, nc, d2, J, c->lam.d(), c->Hz.d(), c->Zb[cur].d(), c->Zb[nxt].d(), DZ, EZ, cs, s);
-    if (!fork) run_gemm(c, normq[0], s);
-    run_gemm(c, normq[1], s);
-    if (fork) PE_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    for (auto& q : norms) run_gemm(c, q, s);
     modal_decide(E, nc, d1, d2, J, nu, nu_g, nu_m, nw, nw_g, nw_m,
                  (unsigned long long*)c->colmax.p, (unsigned*)c->wticket.p, cs, tol, max_iter,
                  c->rhist.d(), cnt + par, nxt, s);
@@ -732,9 +746,6 @@ int pe_create(pe_ctx** out, int E, int d1, int d2, int max_cols, int J, int devi
       bind(c);
       PE_CUDA_CHECK(cudaStreamCreateWithFlags(&c->setup_stream, cudaStreamNonBlocking));
       PE_CUDA_CHECK(cudaStreamCreateWithFlags(&c->work, cudaStreamNonBlocking));
-      PE_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-      PE_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-      PE_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
       if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw Error{PE_ERR_CUDA, "cublasCreate failed"};
       if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) throw Error{PE_ERR_CUDA, "cusolverDnCreate failed"};
       cublasSetStream(c->blas, c->setup_stream);
@@ -770,9 +781,6 @@ int pe_destroy(pe_ctx* c) {
     for (auto ex : kv.second.exec)
       if (ex) cudaGraphExecDestroy(ex);
   if (c->work) cudaStreamDestroy(c->work);
-  if (c->side) cudaStreamDestroy(c->side);
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->pinned_count) cudaFreeHost(c->pinned_count);
   if (c->pinned_diff) cudaFreeHost(c->pinned_diff);
   for (auto e : c->prof_events) cudaEventDestroy(e);

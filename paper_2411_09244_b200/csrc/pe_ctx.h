@@ -91,8 +91,6 @@ struct pe_ctx {
   pe::DevBuf Ux_cur, Ux_new, Wx_cur, Wx_new, R, P, Q, DU, DW, V, colstate, counter;
   pe::DevBuf partial, diff, Gc, active, hist_tmp, nrm, rhist, splitws;
   cudaStream_t work = nullptr;           // capture stream for the sweep graphs
-  cudaStream_t side = nullptr;           // forked branch of a sweep (concurrent norm GEMM)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool use_graphs = true;
   int graph_kernels = 0;   // kernels per captured sweep (launch accounting)
   std::map<int, pe::SweepGraphs> sweep_graphs;  // keyed by interval count
