@@ -454,6 +454,8 @@ def gpu_arm(args, wl, units_member):
                                    "(structural zeros and re-associated work not counted)",
                          "gemm_launches": st["launches"], "gemm_ms": st["gemm_ms"],
                          "gemm_flops": st["gemm_flops"], "gemm_share_of_step": gemm_share,
+                         "other_kernels_ms": st.get("other_ms", 0.0),
+                         "other_share_of_step": st.get("other_ms", 0.0) / (total_ms / args.steps),
                          "peak_source": "cuBLAS DGEMM 8192^3 burst measured in this run "
                                         "(MEASURED_PEAKS.json has no FP64 entry)"},
             "cpu_baseline": cpu,

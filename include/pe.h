@@ -165,6 +165,9 @@ int pe_set_recurrence(pe_ctx* ctx, int on);
 int pe_set_modal(pe_ctx* ctx, int on);
 int pe_wr_is_modal(pe_ctx* ctx);
 int pe_last_fine_stats(pe_ctx* ctx, double* gemm_ms, double* gemm_flops, int* launches);
+/* Profiling mode: summed event time (ms) of the last fine sweep's non-DMMA kernels (the
+ * modal scans and the stop decision), for the in-situ share breakdown in bench.py. */
+int pe_last_fine_other_ms(pe_ctx* ctx, double* other_ms);
 
 #ifdef __cplusplus
 }

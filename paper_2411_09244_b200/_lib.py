@@ -58,6 +58,7 @@ SIGNATURES = {
     "pe_set_profiling": (C.c_int, [_P, C.c_int]),
     "pe_set_recurrence": (C.c_int, [_P, C.c_int]),
     "pe_set_modal": (C.c_int, [_P, C.c_int]),
+    "pe_last_fine_other_ms": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "pe_wr_is_modal": (C.c_int, [_P]),
     "pe_launch_count": (C.c_longlong, [_P]),
     "pe_last_fine_stats": (C.c_int, [_P, _D, _D, _I]),

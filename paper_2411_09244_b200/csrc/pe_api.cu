@@ -56,7 +56,7 @@ static void ensure_zeroed(DevBuf& b, size_t bytes) {
 // Launch `fn` (one DMMA-class kernel doing `flops` algorithmic flops) with optional
 // per-launch CUDA-event timing (bench roofline pass).
 template <class F>
-static void profiled(pe_ctx* c, double flops, cudaStream_t st, F&& fn) {
+static void timed(pe_ctx* c, bool dmma, cudaStream_t st, F&& fn) {
   if (c->profiling) {
     if ((int)c->prof_events.size() < 2 * (c->prof_used + 1)) {
       for (int i = 0; i < 64; ++i) {
@@ -65,6 +65,8 @@ static void profiled(pe_ctx* c, double flops, cudaStream_t st, F&& fn) {
         c->prof_events.push_back(e);
       }
     }
+    if ((int)c->prof_dmma.size() < c->prof_used + 1) c->prof_dmma.resize(c->prof_used + 64);
+    c->prof_dmma[c->prof_used] = dmma ? 1 : 0;
     PE_CUDA_CHECK(cudaEventRecord(c->prof_events[2 * c->prof_used], st));
     fn();
     PE_CUDA_CHECK(cudaEventRecord(c->prof_events[2 * c->prof_used + 1], st));
@@ -72,8 +74,17 @@ static void profiled(pe_ctx* c, double flops, cudaStream_t st, F&& fn) {
   } else {
     fn();
   }
+}
+template <class F>
+static void profiled(pe_ctx* c, double flops, cudaStream_t st, F&& fn) {
+  timed(c, true, st, fn);
   c->stats.gemm_flops += flops;
   c->stats.launches += 1;
+}
+// a non-DMMA kernel of the fine sweep (scans, decide): timed separately in profiling mode
+template <class F>
+static void profiled_other(pe_ctx* c, cudaStream_t st, F&& fn) {
+  timed(c, false, st, fn);
 }
 
 static void run_gemm(pe_ctx* c, const GemmParams& p, cudaStream_t st) {
@@ -86,7 +97,7 @@ static void collect_profile(pe_ctx* c, cudaStream_t st) {
   for (int i = 0; i < c->prof_used; ++i) {
     float ms = 0;
     PE_CUDA_CHECK(cudaEventElapsedTime(&ms, c->prof_events[2 * i], c->prof_events[2 * i + 1]));
-    c->stats.gemm_ms += ms;
+    (c->prof_dmma[i] ? c->stats.gemm_ms : c->stats.other_ms) += ms;
   }
   c->prof_used = 0;
 }
@@ -413,14 +424,21 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   auto body = [&](int par, cudaStream_t s) {
     const int cur = par, nxt = par ^ 1;
     run_gemm(c, rhs_params(c->Zb[cur].d()), s);
-    modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), c->R.d(), c->Yb[cur].d(),
-                c->Yb[nxt].d(), c->DYm.d(), EY, cs, s);
+    profiled_other(c, s, [&] {
+      modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), c->R.d(), c->Yb[cur].d(),
+                  c->Yb[nxt].d(), c->DYm.d(), EY, cs, s);
+    });
     run_gemm(c, g_params(c->Yb[nxt].d()), s);
-    modal_wscan(E, nc, d2, J, c->lam.d(), c->Hz.d(), c->Zb[cur].d(), c->Zb[nxt].d(), DZ, EZ, cs, s);
+    profiled_other(c, s, [&] {
+      modal_wscan(E, nc, d2, J, c->lam.d(), c->Hz.d(), c->Zb[cur].d(), c->Zb[nxt].d(), DZ, EZ,
+                  cs, s);
+    });
     for (auto& q : norms) run_gemm(c, q, s);
-    modal_decide(E, nc, d1, d2, J, nu, nu_g, nu_m, nw, nw_g, nw_m,
-                 (unsigned long long*)c->colmax.p, (unsigned*)c->wticket.p, cs, tol, max_iter,
-                 c->rhist.d(), cnt + par, nxt, s);
+    profiled_other(c, s, [&] {
+      modal_decide(E, nc, d1, d2, J, nu, nu_g, nu_m, nw, nw_g, nw_m,
+                   (unsigned long long*)c->colmax.p, (unsigned*)c->wticket.p, cs, tol, max_iter,
+                   c->rhist.d(), cnt + par, nxt, s);
+    });
     PE_CUDA_CHECK(cudaMemcpyAsync(c->pinned_count + par, cnt + par, sizeof(int),
                                   cudaMemcpyDeviceToHost, s));
   };
@@ -1085,6 +1103,13 @@ int pe_gemm_f64(int M, int N, int K, int batch, const double* A, long long a_i, 
 }
 
 long long pe_launch_count(pe_ctx* c) { return c ? g_launches - c->launches_at_create : g_launches; }
+
+int pe_last_fine_other_ms(pe_ctx* c, double* other_ms) {
+  return guarded([&] {
+    require(c != nullptr && other_ms != nullptr, PE_ERR_ARG, "bad arguments");
+    *other_ms = c->stats.other_ms;
+  });
+}
 
 int pe_last_fine_stats(pe_ctx* c, double* gemm_ms, double* gemm_flops_out, int* launches) {
   return guarded([&] {

@@ -50,6 +50,7 @@ struct SweepGraphs {
 struct FineStats {
   double gemm_flops = 0;   // algorithmic flops issued by the GEMM kernels of the last fine call
   double gemm_ms = 0;      // summed CUDA-event time of those launches (profiling mode only)
+  double other_ms = 0;     // summed time of the sweep's non-DMMA kernels (scans, decide)
   int launches = 0;
 };
 
@@ -103,6 +104,7 @@ struct pe_ctx {
   bool profiling = false;
   bool use_recur = true;  // persistent cluster recurrences (else one GEMM per step)
   std::vector<cudaEvent_t> prof_events;
+  std::vector<char> prof_dmma;  // per timed launch: DMMA-class (1) or other (0)
   int prof_used = 0;
   pe::FineStats stats;
 };

@@ -228,24 +228,35 @@ __global__ void __launch_bounds__(DECIDE_THREADS)
   pdl_enter();
   const long long NJ = (long long)J * nc, per = (long long)E * NJ;
   const int gu = (d1 + 7) / 8, gw = (d2 + 7) / 8;
+  // four lanes per column: lane q sums the blocks g = q, q+4, ... in ascending order,
+  // then ((s0 + s1) + (s2 + s3)) by shuffles (fixed order: deterministic)
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t < 2 * per) {
-    const int side = (int)(t / per);
-    const long long rem = t - side * per;
-    const int e = (int)(rem / NJ);
+  const long long col = t >> 2;
+  const int q = (int)(t & 3);
+  double acc = 0.0;
+  bool live = false;
+  int side = 0, e = 0, n = 0;
+  if (col < 2 * per) {
+    side = (int)(col / per);
+    const long long rem = col - side * per;
+    e = (int)(rem / NJ);
     const long long j = rem - e * NJ;
-    const int n = (int)(j % nc);
+    n = (int)(j % nc);
     const int G = side ? gw : gu;
-    if (G > 0 && cs[(long long)e * nc + n].active) {
+    live = G > 0 && cs[(long long)e * nc + n].active;
+    if (live) {
       const double* p = side ? nw + e * nw_m + j : nu + e * nu_m + j;
       const long long gs = side ? nw_g : nu_g;
-      double acc = 0.0;
-#pragma unroll 8
-      for (int g = 0; g < G; ++g) acc += p[g * gs];
-      atomicMax(colmax + (long long)side * E * nc + (long long)e * nc + n,
-                (unsigned long long)__double_as_longlong(sqrt(acc)));
+#pragma unroll 4
+      for (int g = q; g < G; g += 4) acc += p[g * gs];
     }
   }
+  const double a1 = __shfl_down_sync(0xffffffffu, acc, 1);
+  acc += a1;  // lanes q = 0, 2 now hold s0 + s1, s2 + s3
+  const double a2 = __shfl_down_sync(0xffffffffu, acc, 2);
+  if (live && q == 0)
+    atomicMax(colmax + (long long)side * E * nc + (long long)e * nc + n,
+              (unsigned long long)__double_as_longlong(sqrt(acc + a2)));
   __threadfence();
   __syncthreads();
   __shared__ int last;
@@ -282,7 +293,7 @@ void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long l
                   unsigned long long* colmax, unsigned* ticket, WrColumnState* cs, double tol,
                   int max_iter, double* resid_hist, int* active_count, int par_new,
                   cudaStream_t st) {
-  const long long total = 2LL * E * J * nc;
+  const long long total = 8LL * E * J * nc;  // four lanes per (side, member, column)
   const int blocks = (int)std::max<long long>(1, (total + DECIDE_THREADS - 1) / DECIDE_THREADS);
   launch_k(modal_decide_kernel, dim3(blocks), dim3(DECIDE_THREADS), 0, st, E, nc, d1, d2, J, nu,
            nu_g, nu_m, nw, nw_g, nw_m, colmax, ticket, cs, tol, max_iter, resid_hist, active_count,

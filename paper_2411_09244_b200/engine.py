@@ -193,7 +193,10 @@ class PeContext:
     def fine_stats(self):
         ms, fl, n = C.c_double(), C.c_double(), C.c_int()
         check(self.lib.pe_last_fine_stats(self.ptr, C.byref(ms), C.byref(fl), C.byref(n)))
-        return dict(gemm_ms=ms.value, gemm_flops=fl.value, launches=n.value)
+        other = C.c_double()
+        check(self.lib.pe_last_fine_other_ms(self.ptr, C.byref(other)))
+        return dict(gemm_ms=ms.value, gemm_flops=fl.value, launches=n.value,
+                    other_ms=other.value)
 
 
 def stop_reason_name(code: int) -> str:
