@@ -336,8 +336,35 @@ def gpu_arm(args, wl, units_member):
     sweeps_buf = (torch.zeros(E, N, dtype=torch.int32, device="cuda")
                   if kind == "all-at-once" else None)
 
-    def step(x_old, x_new):
-        ctx.iterate(kind, N, x_old, x_new, Gc, diff, wr_sweeps=sweeps_buf)
+    shard = args.shard == "intervals"
+    if shard:
+        # one problem, intervals sharded across ranks (strong scaling): fine on the local
+        # slice, one all-gather of the F endpoints, replicated coarse correction
+        # (paper_2411_09244_b200/sharded.py)
+        from paper_2411_09244_b200.dist import shard_members
+
+        ranges = [shard_members(N, r, world) for r in range(world)]
+        mine = ranges[rank]
+        m_loc = max(len(r) for r in ranges)
+        F_loc = torch.zeros(E, m_loc, d, dtype=torch.float64, device="cuda")
+        parts = [torch.empty_like(F_loc) for _ in range(world)]
+
+        def step(x_old, x_new):
+            if len(mine):
+                Xs = x_old[:, mine.start:mine.stop].contiguous()
+                if kind == "sequential":
+                    F_loc[:, : len(mine)] = ctx.fine_sequential(Xs)
+                else:
+                    F_loc[:, : len(mine)] = ctx.fine_allatonce(Xs, record=False)[0]
+            if dist:
+                dist.all_gather(parts, F_loc)
+                F = torch.cat([p[:, : len(r)] for p, r in zip(parts, ranges)], dim=1)
+            else:
+                F = F_loc[:, :N]
+            ctx.coarse_correct(N, x_old, F.contiguous(), Gc, x_new, diff)
+    else:
+        def step(x_old, x_new):
+            ctx.iterate(kind, N, x_old, x_new, Gc, diff, wr_sweeps=sweeps_buf)
 
     for _ in range(args.warmup):
         step(A, B)
@@ -367,7 +394,7 @@ def gpu_arm(args, wl, units_member):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
-    value = world * units * args.steps / (total_ms / 1e3)
+    value = (1 if shard else world) * units * args.steps / (total_ms / 1e3)
 
     # roofline pass: one extra instrumented step, every GEMM launch bracketed by events
     ctx.set_profiling(True)
@@ -393,7 +420,20 @@ def gpu_arm(args, wl, units_member):
                                fine_max_iter=MAX_ITER)
         warm = P.ParerealConfig(time_grid=cfg.time_grid, alpha=cfg.alpha, epsilon=0.0, k_max=1,
                                 fine_kind=kind, fine_tol=FINE_TOL, fine_max_iter=MAX_ITER)
-        if E == 1:
+        if shard:
+            from paper_2411_09244_b200.sharded import LibpeShardOps, run_parareal_sharded
+
+            ops = LibpeShardOps(ctx, kind)
+            run_parareal_sharded(N, np.zeros(d), ops, 1, 0.0)  # warm
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = run_parareal_sharded(N, np.zeros(d), ops, args.steps, 0.0)
+            torch.cuda.synchronize()
+            e2e_s = time.perf_counter() - t0
+            K = res["iterations"]
+            path = (f"paper_2411_09244_b200.run_parareal_sharded ({world} ranks, intervals "
+                    "sharded, host arrays in/out)")
+        elif E == 1:
             props = P.SplitPropagators(system, loads)
             fine = P.build_fine_propagator(cfg, props, loads)
             init = P.SplitState.fresh(np.zeros(system.d1), np.zeros(system.d2))
@@ -431,13 +471,17 @@ def gpu_arm(args, wl, units_member):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded kappa field per BASELINE config; reduced operators built "
                     "by the reference's offline CEM code, " + (wl.get("sys") or wl["members"]) +
                     ")",
             "config": dict(workload=args.workload, d1=system.d1, d2=system.d2, N=N, J=J,
                            E_per_gpu=E, kind=kind, alpha=wl["alpha"], fine_tol=FINE_TOL,
+                           parallelism=(f"intervals sharded over {world} ranks, one NCCL "
+                                        "all-gather of the F endpoints per iteration" if shard
+                                        else f"{world} independent replicas (no collective)"),
                            kappa_scale=meta["kappa_scale"],
                            contrast=meta.get("contrast_range", meta.get("contrast")),
                            l2="L2 flushed (320 MB write) before every timed step",
@@ -480,6 +524,9 @@ def main():
     ap.add_argument("--workload", default="cfg2-aao", choices=sorted(WORKLOADS))
     ap.add_argument("--members", type=int, default=1, help="ensemble members per GPU")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "intervals"],
+                    help="N > 1: independent replicas (weak scaling, default) or one problem "
+                         "with its intervals sharded across the ranks (strong scaling)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if "members" in wl:

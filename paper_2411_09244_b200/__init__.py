@@ -14,6 +14,7 @@ from .parareal import (AllAtOnceFine, ParerealConfig, ParerealEnsemble,  # noqa:
                        ParerealRun,
                        SequentialFine, build_fine_propagator, check_stop, initial_sweep,
                        max_state_diff, run_parareal, run_parareal_ensemble)
+from .sharded import LibpeShardOps, run_parareal_sharded  # noqa: F401
 from .stepping import (ConstantLoads, SplitPropagators, SplitState,  # noqa: F401
                        SplitTrajectory, TimeGrid, split_energy)
 

@@ -4,8 +4,8 @@ The hot path shards with no data-path exchange along the ensemble dimension: eve
 member is an independent parareal problem (BASELINE config 4), so ranks own disjoint
 member ranges and only the timing is reduced (max over ranks).  One process per GPU,
 `torch.distributed` for the plumbing (NCCL on the GPU box, gloo in the CPU tests).
-Interval sharding (one all-gather of the F endpoints per iteration) is the §8f
-"next" row and is not implemented here.
+Interval sharding of one problem (one all-gather of the F endpoints per iteration) is
+in `sharded.py`.
 """
 
 from __future__ import annotations

@@ -710,3 +710,24 @@ def test_modal_sweep_batch_invariant_and_deterministic():
     one, s1, _, r1 = ctx.fine_allatonce(ctx.to_dev(X[:, 7:8]))
     assert np.array_equal(one.cpu().numpy()[0, 0], a.cpu().numpy()[0, 7])
     assert int(s1.cpu().numpy().ravel()[0]) == int(sa.cpu().numpy().ravel()[7])
+
+
+@pytest.mark.parametrize("kind", ["sequential", "all-at-once"])
+def test_interval_sharded_driver_equals_device_loop(kind):
+    """The interval-sharded driver (fine on a slice, all-gather, replicated correction; one
+    rank here) reproduces the device-resident parareal loop bitwise on cfg0."""
+    P = _pkg()
+    from paper_2411_09244_b200.sharded import LibpeShardOps, run_parareal_sharded
+
+    z = golden("sys_cfg0.npz")
+    s, ld = _system(z)
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(1.0, 10, 10), alpha=0.1, epsilon=1e-8,
+                           k_max=10, fine_kind=kind, fine_tol=1e-12, stop_rule="relative")
+    props = P.SplitPropagators(s, ld)
+    fine = P.build_fine_propagator(cfg, props, ld)
+    x0 = np.zeros(s.d1 + s.d2)
+    run = P.run_parareal(cfg, props, fine, P.SplitState.fresh(x0[: s.d1], x0[s.d1:]))
+    sh = run_parareal_sharded(10, x0, LibpeShardOps(fine.ctx, kind), k_max=10, epsilon=1e-8,
+                              rule="relative")
+    assert sh["iterations"] == run.iterations
+    assert np.array_equal(sh["history"], np.array(run.history))
