@@ -319,12 +319,20 @@ def gpu_arm(args, wl, units_member):
     N, J, T, kind = wl["N"], wl["J"], wl["T"], wl["kind"]
     d = system.d1 + system.d2
     units = units_member * E
+    # upload + setup factorisations, timed separately (outside the step)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
     ctx = P.PeContext(systems, loads_l, J, local)
+    torch.cuda.synchronize()
+    t_upload = time.perf_counter() - t_setup
     ctx.prepare_coarse(T / N)
     if kind == "sequential":
         ctx.prepare_sequential(T / N / J)
     else:
         ctx.prepare_allatonce(T / N / J, wl["alpha"], FINE_TOL, MAX_ITER)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    modal = ctx.modal_level() if kind == "all-at-once" else None
 
     A = torch.zeros(E, N + 1, d, dtype=torch.float64, device="cuda")
     B = torch.zeros_like(A)
@@ -503,6 +511,10 @@ def gpu_arm(args, wl, units_member):
                          "peak_source": "cuBLAS DGEMM 8192^3 burst measured in this run "
                                         "(MEASURED_PEAKS.json has no FP64 entry)"},
             "cpu_baseline": cpu,
+            "setup": {"upload_s": t_upload, "factorisations_s": t_setup - t_upload,
+                      "what": ("pe_create + pe_set_system uploads; G, sequential operator T or the "
+                               "all-at-once pencil eigendecompositions (modal level "
+                               f"{modal}) on the GPU; excluded from the step")},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.result,
