@@ -20,6 +20,7 @@ SHAPES = [  # (M, N, K, batch, label); label ending in "jc": B stored j-contiguo
     (300, 64, 600, 66, "cfg2 shifted (batched)"),
     (600, 64, 1200, 1, "cfg2 seq step"),
     (600, 32, 1200, 64, "cfg4 seq step"),
+    (600, 32, 1200, 32, "cfg4 seq step chunk"),
     (4096, 12800, 8192, 1, "cfg3 rhs/g"),
     (4096, 128, 8192, 50, "cfg3 shifted (batched)"),
     (8192, 8192, 8192, 1, "square"),
