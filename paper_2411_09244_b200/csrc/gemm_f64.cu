@@ -808,7 +808,10 @@ static void launch_tma(const GemmParams& p, cudaStream_t st) {
   X(2, 4, 2, 4, 4, 3)      \
   X(3, 2, 2, 5, 4, 4)      \
   X(4, 1, 2, 4, 4, 4)      \
-  X(5, 2, 4, 4, 4, 3)
+  X(5, 2, 4, 4, 4, 3)      \
+  X(6, 4, 1, 4, 4, 4)      \
+  X(7, 3, 1, 5, 4, 4)      \
+  X(8, 2, 1, 5, 4, 4)
 
 template <int WGM, int WGN, int FM, int FN, int STAGES>
 static double tma_cost(const GemmParams& p) {
@@ -816,7 +819,9 @@ static double tma_cost(const GemmParams& p) {
   const double ctas = (double)((p.M + Cfg::BM - 1) / Cfg::BM) * ((p.N + Cfg::BN - 1) / Cfg::BN) *
                       p.nb1 * p.nb2;
   const double per_sm = std::ceil(ctas / 148.0);
-  const double eff = (Cfg::NCW <= 2) ? 0.8 : 1.0;
+  // fewer DMMA warps per CTA sustain less issue (measured at cfg4, 600 x 32 x 1200 x 32:
+  // 128x32 / 4 warps 7.26 ms per iteration, 120x32 / 3 warps 8.57, 80x32 / 2 warps 8.82)
+  const double eff = (Cfg::NCW <= 2) ? 0.6 : (Cfg::NCW == 3 ? 0.8 : 1.0);
   return per_sm * Cfg::BM * Cfg::BN / eff;
 }
 
