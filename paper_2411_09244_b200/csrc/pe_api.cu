@@ -154,11 +154,10 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
   // J steps, so a chunk's T stays L2-resident across its steps instead of streaming every
   // member's T from HBM once per step.  Members are independent: same arithmetic.
   static const int chunk_env = getenv("PE_SEQ_CHUNK") ? atoi(getenv("PE_SEQ_CHUNK")) : 0;
-  // measured at cfg4 (E = 64, d = 600, tools/chunk_sweep.sh): 2 chunks of 32 members
-  // 8.6 ms, 1 chunk 9.8 ms, 4 chunks 15.5 ms (the per-step launches underfill the SMs)
-  const double t_total = 16.0 * d * d * E;
-  const int nchunks = (int)std::ceil(t_total / 190e6);
-  int EC = chunk_env > 0 ? chunk_env : (E + nchunks - 1) / nchunks;
+  // measured at cfg4 (E = 64, d = 600, tools/chunk_sweep.sh, TMA 128x32 tiles): one chunk
+  // of 64 members 7.06 ms, 2 x 32 7.25 ms, 3 x 22 10.0 ms, 4 x 16 12.7 ms (smaller chunks
+  // underfill the SMs); larger ensembles run in chunks of 64
+  int EC = chunk_env > 0 ? chunk_env : 64;
   if (EC >= E || J < 2) EC = E;
   const long long xs = (long long)nc * d;
   const double* X0 = Xs;
