@@ -286,11 +286,13 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     c->Yb[b].ensure(sizeof(double) * E * (J + 2) * L1 + 8);
     c->Zb[b].ensure(sizeof(double) * E * (J + 2) * L2 + 8);
   }
-  c->R.ensure(sizeof(double) * E * J * L1 + 8);
-  c->Hz.ensure(sizeof(double) * E * J * L2 + 8);
-  c->DYm.ensure(sizeof(double) * E * J * L1 + 8);
+  // working set per sweep ~8 arrays of E J d nc doubles (80 MB at cfg2, against a 126 MB
+  // L2): h reuses r~'s buffer (r~ is dead once the u scan has read it) and dY shares e_Z's
+  // (dY is dead once the h GEMM has read it; the w scan writes e_Z afterwards)
+  const long long Lm = std::max(L1, L2);
+  c->R.ensure(sizeof(double) * E * J * Lm + 8);
   c->DW.ensure(sizeof(double) * E * J * L2 + 8);  // DZ
-  c->EYZ.ensure(sizeof(double) * E * J * (L1 + L2) + 8);
+  c->EYZ.ensure(sizeof(double) * E * J * (L1 + Lm) + 8);
   c->Y0m.ensure(sizeof(double) * E * L1 + 8);
   c->Z0.ensure(sizeof(double) * E * L2 + 8);
   c->nrmp.ensure(sizeof(double) * (size_t)(g1 + g2) * E * NJ + 8);
@@ -309,6 +311,8 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   int* cnt = c->counter.i();
   double* EY = c->EYZ.d();
   double* EZ = EY + E * J * L1;
+  double* Rb = c->R.d();  // r~, then h
+  double* DYb = EZ;       // dY, then e_Z
   double* DZ = c->DW.d();
 
   // seeds: y0 = V1^-1 u0, z0 = V2^-1 w0 (X_in: (E, nc, d))
@@ -347,7 +351,7 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     r.seg[1].A = Operand{c->RT.d() + d2, 2LL * d2, 1, 2LL * d1 * d2, 0};
     r.seg[1].B = Operand{DZ, 1, d2, J * L2, 0};
     r.seg[1].K = d2;
-    r.C = c->R.d();
+    r.C = Rb;
     r.c_i = 1;
     r.c_j = d1;
     r.c_b1 = J * L1;
@@ -365,9 +369,9 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     g.seg[0].B = Operand{Ynew + 2 * L1, 1, d1, (J + 2) * L1, 0};
     g.seg[0].K = d1;
     g.seg[1].A = Operand{c->GT.d() + d1, 2LL * d1, 1, 2LL * d1 * d2, 0};
-    g.seg[1].B = Operand{c->DYm.d(), 1, d1, J * L1, 0};
+    g.seg[1].B = Operand{DYb, 1, d1, J * L1, 0};
     g.seg[1].K = d1;
-    g.C = c->Hz.d();
+    g.C = Rb;
     g.c_i = 1;
     g.c_j = d2;
     g.c_b1 = J * L2;
@@ -424,12 +428,12 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     const int cur = par, nxt = par ^ 1;
     run_gemm(c, rhs_params(c->Zb[cur].d()), s);
     profiled_other(c, s, [&] {
-      modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), c->R.d(), c->Yb[cur].d(),
-                  c->Yb[nxt].d(), c->DYm.d(), EY, cs, s);
+      modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), Rb, c->Yb[cur].d(),
+                  c->Yb[nxt].d(), DYb, EY, cs, s);
     });
     run_gemm(c, g_params(c->Yb[nxt].d()), s);
     profiled_other(c, s, [&] {
-      modal_wscan(E, nc, d2, J, c->lam.d(), c->Hz.d(), c->Zb[cur].d(), c->Zb[nxt].d(), DZ, EZ,
+      modal_wscan(E, nc, d2, J, c->lam.d(), Rb, c->Zb[cur].d(), c->Zb[nxt].d(), DZ, EZ,
                   cs, s);
     });
     for (auto& q : norms) run_gemm(c, q, s);
