@@ -282,10 +282,13 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   const long long vstride = (long long)d1 * d1 + (long long)d2 * d2;
   const long long NJ = (long long)J * nc;
   const int g1 = (d1 + 7) / 8, g2 = (d2 + 7) / 8;
-  for (int b = 0; b < 2; ++b) {
-    c->Yb[b].ensure(sizeof(double) * E * (J + 2) * L1 + 8);
-    c->Zb[b].ensure(sizeof(double) * E * (J + 2) * L2 + 8);
-  }
+  // one waveform buffer per block, updated in place by the scans (each thread reads an
+  // element before it overwrites it; stopped intervals are skipped, so they keep the
+  // waveforms of their last sweep without any commit copy)
+  c->Yb[0].ensure(sizeof(double) * E * (J + 2) * L1 + 8);
+  c->Zb[0].ensure(sizeof(double) * E * (J + 2) * L2 + 8);
+  double* Yw = c->Yb[0].d();
+  double* Zw = c->Zb[0].d();
   // working set per sweep ~8 arrays of E J d nc doubles (80 MB at cfg2, against a 126 MB
   // L2): h reuses r~'s buffer (r~ is dead once the u scan has read it) and dY shares e_Z's
   // (dY is dead once the h GEMM has read it; the w scan writes e_Z afterwards)
@@ -335,8 +338,7 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   };
   basis_gemm(d1, c->Vicat.d(), X_in, d, (long long)nc * d, c->Y0m.d(), L1, nc);
   basis_gemm(d2, c->Vicat.d() + (long long)d1 * d1, X_in + d1, d, (long long)nc * d, c->Z0.d(), L2, nc);
-  modal_seed(E, nc, d1, d2, J, c->Y0m.d(), c->Z0.d(), c->Yb[0].d(), c->Yb[1].d(), c->Zb[0].d(),
-             c->Zb[1].d(), DZ, st);
+  modal_seed(E, nc, d1, d2, J, c->Y0m.d(), c->Z0.d(), Yw, nullptr, Zw, nullptr, DZ, st);
 
   // loop-invariant GEMM parameter blocks (buffer parity fills in the B / C pointers)
   auto rhs_params = [&](const double* Zcur) {
@@ -425,29 +427,27 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   }
 
   auto body = [&](int par, cudaStream_t s) {
-    const int cur = par, nxt = par ^ 1;
-    run_gemm(c, rhs_params(c->Zb[cur].d()), s);
+    run_gemm(c, rhs_params(Zw), s);
     profiled_other(c, s, [&] {
-      modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), Rb, c->Yb[cur].d(),
-                  c->Yb[nxt].d(), DYb, EY, cs, s);
+      modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), Rb, Yw, Yw, DYb, EY, cs,
+                  s);
     });
-    run_gemm(c, g_params(c->Yb[nxt].d()), s);
+    run_gemm(c, g_params(Yw), s);
     profiled_other(c, s, [&] {
-      modal_wscan(E, nc, d2, J, c->lam.d(), Rb, c->Zb[cur].d(), c->Zb[nxt].d(), DZ, EZ,
+      modal_wscan(E, nc, d2, J, c->lam.d(), Rb, Zw, Zw, DZ, EZ,
                   cs, s);
     });
     for (auto& q : norms) run_gemm(c, q, s);
     profiled_other(c, s, [&] {
       modal_decide(E, nc, d1, d2, J, nu, nu_g, nu_m, nw, nw_g, nw_m,
                    (unsigned long long*)c->colmax.p, (unsigned*)c->wticket.p, cs, tol, max_iter,
-                   c->rhist.d(), cnt + par, nxt, s);
+                   c->rhist.d(), cnt + par, 0, s);
     });
     PE_CUDA_CHECK(cudaMemcpyAsync(c->pinned_count + par, cnt + par, sizeof(int),
                                   cudaMemcpyDeviceToHost, s));
   };
   const std::vector<const void*> key = {
-      (const void*)(intptr_t)2, c->Yb[0].p, c->Yb[1].p, c->Zb[0].p, c->Zb[1].p, c->R.p, c->Hz.p,
-      c->DYm.p, c->DW.p, c->EYZ.p, c->nrmp.p, cs, c->rhist.p, cnt, c->pinned_count, c->RT.p,
+      (const void*)(intptr_t)4, c->Yb[0].p, c->Zb[0].p, c->R.p, c->DW.p, c->EYZ.p, c->nrmp.p, cs, c->rhist.p, cnt, c->pinned_count, c->RT.p,
       c->GT.p, c->f1t.p, c->cgt.p, c->acoef.p, c->cden.p, c->lam.p, c->Vcat.p, c->Ucat.p, c->colmax.p,
       c->wticket.p,
       (const void*)(intptr_t)max_iter, (const void*)(intptr_t)(alpha * 1e6),
@@ -455,11 +455,9 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   run_sweeps(c, nc, max_iter, key, body, st);
 
   // final waveforms in the original bases: U = V1 Y, W = V2 Z from each interval's buffer
-  modal_gather(E, nc, d1, J, c->Yb[0].d(), c->Yb[1].d(), cs, c->Ux_new.d(), st);
-  modal_gather(E, nc, d2, J, c->Zb[0].d(), c->Zb[1].d(), cs, c->Wx_new.d(), st);
-  basis_gemm(d1, c->Vcat.d(), c->Ux_new.d(), d1, (J + 2) * L1, c->Ux_cur.d(), (J + 2) * L1,
+  basis_gemm(d1, c->Vcat.d(), Yw, d1, (J + 2) * L1, c->Ux_cur.d(), (J + 2) * L1,
              (int)((J + 2) * nc));
-  basis_gemm(d2, c->Vcat.d() + (long long)d1 * d1, c->Wx_new.d(), d2, (J + 2) * L2, c->Wx_cur.d(),
+  basis_gemm(d2, c->Vcat.d() + (long long)d1 * d1, Zw, d2, (J + 2) * L2, c->Wx_cur.d(),
              (J + 2) * L2, (int)((J + 2) * nc));
   wr_finish(E, nc, d1, d2, J, c->Ux_cur.d(), c->Wx_cur.d(), cs, X_out, sweeps, reasons, st);
   if (resid_hist)

@@ -114,7 +114,7 @@ struct WrColumnState {
   int reason;
   double prev;
   double r0;
-  int fpar;  // modal path: ping-pong buffer holding this interval's latest waveforms
+  int fpar;  // reserved (buffer index of the interval's latest waveforms; 0 in place)
   int pad;
 };
 
@@ -151,8 +151,7 @@ void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long l
                   unsigned long long* colmax, unsigned* ticket, WrColumnState* cs, double tol,
                   int max_iter, double* resid_hist, int* active_count, int par_new,
                   cudaStream_t st);
-void modal_gather(int E, int nc, int dd, int J, const double* B0, const double* B1,
-                  const WrColumnState* cs, double* out, cudaStream_t st);
+
 void sub(long long n, const double* a, const double* b, double* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- recurrences (recur.cu)

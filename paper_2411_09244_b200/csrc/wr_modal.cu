@@ -15,9 +15,9 @@
 //         lam = 1 - dt mu2                                                      (_w_sweep)
 //   norms ||U_new,s - U_s|| = ||V1 (Y_new,s - Y_s)||, likewise W             (:250-254)
 // The two contractions (rhs, h) and the norm products are DMMA GEMMs (gemm_f64.cu); the
-// time recurrences are the elementwise scans below.  Every per-sweep buffer is
-// ping-ponged by sweep parity and the scans skip stopped intervals, so a stopped
-// interval's waveforms stay where its last sweep wrote them (WrColumnState::fpar).
+// time recurrences are the elementwise scans below.  libpe runs the scans in place (Yc == Yn,
+// Zc == Zn: every thread reads an element before it overwrites it) and they skip stopped
+// intervals, so a stopped interval keeps the waveforms of its last sweep with no commit copy.
 //
 // Layout per member: Y = [y0, y0, Y_0 .. Y_{J-1}] as J+2 blocks of a (d1 x nc)
 // column-major matrix (L1 = d1 nc); Z likewise with d2.  DY, DZ, EY, EZ, R, H: J blocks.
@@ -51,8 +51,10 @@ __global__ void modal_seed_kernel(int E, int nc, int d1, int d2, int J,
       double* a = Yb0 + (long long)e * (J + 2) * L1 + r;
       double* b = Yb1 + (long long)e * (J + 2) * L1 + r;
       for (int k = 0; k < J + 2; ++k) a[k * L1] = y;
-      b[0] = y;
-      b[L1] = y;
+      if (Yb1) {
+        b[0] = y;
+        b[L1] = y;
+      }
     } else {
       const long long q = t - tu;
       const int e = (int)(q / L2);
@@ -61,8 +63,10 @@ __global__ void modal_seed_kernel(int E, int nc, int d1, int d2, int J,
       double* a = Zb0 + (long long)e * (J + 2) * L2 + r;
       double* b = Zb1 + (long long)e * (J + 2) * L2 + r;
       for (int k = 0; k < J + 2; ++k) a[k * L2] = z;
-      b[0] = z;
-      b[L2] = z;
+      if (Zb1) {
+        b[0] = z;
+        b[L2] = z;
+      }
       double* dz = DZ + (long long)e * J * L2 + r;
       for (int k = 0; k < J; ++k) dz[k * L2] = 0.0;
     }
@@ -118,7 +122,7 @@ __device__ __forceinline__ void scan_walk(int s_begin, int J, long long stride,
 __global__ void modal_uscan_kernel(int nc, int d1, int J, int E, double dt, double alpha,
                                    const double* __restrict__ acoef,
                                    const double* __restrict__ cden, const double* __restrict__ R,
-                                   const double* __restrict__ Yc, double* __restrict__ Yn,
+                                   const double* Yc, double* Yn,  // may alias (in place)
                                    double* __restrict__ DY, double* __restrict__ EY,
                                    const WrColumnState* __restrict__ cs) {
   pdl_enter();
@@ -170,8 +174,8 @@ void modal_uscan(int E, int nc, int d1, int J, double dt, double alpha, const do
 // Out: Zn blocks 2..J+1, DZ (the next sweep's build_rhs difference: DZ_s = Z_{s-1} - Z_{s-2},
 //      Z_{-1} = Z_{-2} = z0), EZ = Z_new - Z_cur.
 __global__ void modal_wscan_kernel(int nc, int d2, int J, int E, const double* __restrict__ lam,
-                                   const double* __restrict__ H, const double* __restrict__ Zc,
-                                   double* __restrict__ Zn, double* __restrict__ DZ,
+                                   const double* __restrict__ H, const double* Zc,
+                                   double* Zn, double* __restrict__ DZ,  // Zc, Zn may alias
                                    double* __restrict__ EZ, const WrColumnState* __restrict__ cs) {
   pdl_enter();
   const long long L2 = (long long)d2 * nc;
@@ -298,33 +302,6 @@ void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long l
   launch_k(modal_decide_kernel, dim3(blocks), dim3(DECIDE_THREADS), 0, st, E, nc, d1, d2, J, nu,
            nu_g, nu_m, nw, nw_g, nw_m, colmax, ticket, cs, tol, max_iter, resid_hist, active_count,
            par_new);
-  ++g_launches;
-  PE_CUDA_CHECK(cudaGetLastError());
-}
-
-// Final modal waveforms: every (member, interval) from the ping-pong buffer its last sweep
-// wrote (all J+2 blocks) into one contiguous buffer for the V Y back-transform.
-__global__ void modal_gather_kernel(int E, int nc, int dd, int J, const double* __restrict__ B0,
-                                    const double* __restrict__ B1, const WrColumnState* __restrict__ cs,
-                                    double* __restrict__ out) {
-  const long long L = (long long)dd * nc;
-  const long long per = (long long)(J + 2) * L;
-  const long long total = per * E;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int e = (int)(t / per);
-    const long long r = t - e * per;
-    const long long b = r / L;
-    const int n = (int)((r - b * L) / dd);
-    out[t] = (cs[(long long)e * nc + n].fpar ? B1 : B0)[t];
-  }
-}
-
-void modal_gather(int E, int nc, int dd, int J, const double* B0, const double* B1,
-                  const WrColumnState* cs, double* out, cudaStream_t st) {
-  const long long total = (long long)E * (J + 2) * dd * nc;
-  if (total == 0) return;
-  modal_gather_kernel<<<grid_1d(total, 256), 256, 0, st>>>(E, nc, dd, J, B0, B1, cs, out);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
 }
