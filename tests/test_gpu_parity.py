@@ -733,3 +733,37 @@ def test_interval_sharded_driver_equals_device_loop(kind):
                               rule="relative")
     assert sh["iterations"] == run.iterations
     assert np.array_equal(sh["history"], np.array(run.history))
+
+
+def test_modal_ensemble_members_equal_single_runs():
+    """Full modal sweep with E = 3 members (d1 = 100, d2 = 130: separate U / W norm
+    launches, member-strided scans and decisions): every member's fine solve equals its
+    single-member solve bitwise, and matches the CPU oracle."""
+    P = _pkg()
+    d1, d2, nc, J = 100, 130, 6, 16
+    systems, loads, osys = [], [], []
+    for m in range(3):
+        mass, stiff, f = _random_coupled(d1, d2, 300 + m)
+        blocks = dict(M11=mass[:d1, :d1], A11=stiff[:d1, :d1], M12=mass[:d1, d1:],
+                      A12=stiff[:d1, d1:], M22=mass[d1:, d1:], A22=stiff[d1:, d1:])
+        systems.append(P.CoarseSystem(**{k: np.ascontiguousarray(v) for k, v in blocks.items()}))
+        loads.append(P.ConstantLoads(f[:d1], f[d1:]))
+        osys.append(po.OSystem(*(blocks[k] for k in ("M11", "A11", "M12", "A12", "M22", "A22")),
+                               f[:d1], f[d1:]))
+    X = np.random.default_rng(4).standard_normal((3, nc, d1 + d2)) * 0.3
+    dt_int = 0.05
+    ens = P.PeContext(systems, loads, J)
+    ens.prepare_allatonce(dt_int / J, 0.2, 1e-13, 400)
+    assert ens.modal_level() == 2
+    Y, sw, _, _ = ens.fine_allatonce(ens.to_dev(X), record=False)
+    Y, sw = Y.cpu().numpy(), sw.cpu().numpy()
+    for m in range(3):
+        one = P.PeContext([systems[m]], [loads[m]], J)
+        one.prepare_allatonce(dt_int / J, 0.2, 1e-13, 400)
+        Y1, sw1, _, _ = one.fine_allatonce(one.to_dev(X[m:m + 1]), record=False)
+        assert np.array_equal(Y1.cpu().numpy()[0], Y[m])
+        assert np.array_equal(sw1.cpu().numpy()[0], sw[m])
+        owr = po.OracleWR(osys[m], J, dt_int, 0.2, tol=1e-13, max_iter=400)
+        r = owr.solve(X[m, 2, :d1], X[m, 2, d1:])
+        ref = np.concatenate([r["U"][-1], r["W"][-1]])
+        assert rel_rows(Y[m, 2][None], ref[None]) < REL
