@@ -897,7 +897,9 @@ static void launch_tma(const GemmParams& p, cudaStream_t st) {
   X(5, 2, 4, 4, 4, 3)      \
   X(6, 4, 1, 4, 4, 4)      \
   X(7, 3, 1, 5, 4, 4)      \
-  X(8, 2, 1, 5, 4, 4)
+  X(8, 2, 1, 5, 4, 4)      \
+  X(9, 5, 1, 4, 4, 4)      \
+  X(10, 5, 1, 4, 4, 3)
 
 template <int WGM, int WGN, int FM, int FN, int STAGES>
 static double tma_cost(const GemmParams& p) {
