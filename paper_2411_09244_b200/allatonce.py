@@ -112,7 +112,7 @@ class WaveformRelaxation:
         for n, s in enumerate(states):
             it = int(sw[n])
             reason = stop_reason_name(rs[n])
-            res = [float(v) for v in rh[n, :it]]
+            res = rh[n, :it].tolist()
             conv = reason in ("tol", "floor")
             if not conv:
                 log.warning("waveform relaxation %s after %d iterations (residual %.3e)",

@@ -157,7 +157,7 @@ def _wr_info(res: dict, k: int, e: int, n: int) -> dict:
     it = int(res["wr_sweeps"][k, e, n])
     reason = stop_reason_name(res["wr_reasons"][k, e, n])
     rh = res.get("wr_resid")
-    resid = [float(v) for v in rh[k, e, n, :it]] if rh is not None else []
+    resid = rh[k, e, n, :it].tolist() if rh is not None else []  # C-level float conversion
     return {"converged": reason in ("tol", "floor"), "iterations": it, "residuals": resid,
             "stop_reason": reason}
 
