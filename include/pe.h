@@ -169,6 +169,30 @@ int pe_last_fine_stats(pe_ctx* ctx, double* gemm_ms, double* gemm_flops, int* la
  * modal scans and the stop decision), for the in-situ share breakdown in bench.py. */
 int pe_last_fine_other_ms(pe_ctx* ctx, double* other_ms);
 
+/* ---- Fine-scale accuracy path (host buffers in and out) ---------- */
+
+/* Backward Euler on the fine interior nodes, (M/dt + A) u_{s+1} = M u_s / dt + b with
+ * dt = t_end / n_steps (fem.py:292-318 reference_solve).  M, A: host CSR (int32 indptr /
+ * indices, FP64 values) of the n x n interior mass and stiffness (FineOperators.M/.A,
+ * fem.py:253-270); b: the interior load (FineOperators.load); u0: n values or NULL (zeros).
+ * states_h: (n_steps+1, n) when keep_trajectory, else (2, n) = [u0, u_final].
+ * step_ms (may be NULL): CUDA-event time of the time-step loop.  M/dt + A must be SPD
+ * (PE_ERR_SOLVER otherwise; the reference's splu raises on a singular matrix). */
+int pe_fine_reference_solve(int n, const int* M_ptr, const int* M_idx, const double* M_val,
+                            const int* A_ptr, const int* A_idx, const double* A_val,
+                            const double* b, const double* u0, double t_end, int n_steps,
+                            int keep_trajectory, double* states_h, float* step_ms,
+                            void* stream);
+
+/* M-norms of ref - [Psi1 Psi2] x_k for K coarse states x_k (K, d) and of ref itself:
+ * norms_h[k] = ||ref - reconstruct(x_k)||_M (k < K), norms_h[K] = ||ref||_M
+ * (experiment.py:320-325 relative_error, :348-354 error series; msbasis.py:448-450
+ * reconstruct; fem.py:272-274 norm).  P: host CSR (n x d) of hstack([Psi1, Psi2]). */
+int pe_relative_error_series(int n, int d, const int* P_ptr, const int* P_idx,
+                             const double* P_val, const int* M_ptr, const int* M_idx,
+                             const double* M_val, const double* ref, int K, const double* X,
+                             double* norms_h, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

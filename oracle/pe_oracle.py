@@ -363,3 +363,50 @@ def run_parareal(s: OSystem, x0, t_end, n_intervals, substeps, *, kind="sequenti
     return dict(history=history, max_diffs=max_diffs, iterations=iterations,
                 converged=converged, fine_info=fine_info, fine_seconds=fsec,
                 coarse_seconds=csec)
+
+
+# ------------------------------------------------------------------ fine-scale accuracy
+# restated from fem.py:292-318, fem.py:272-274 and experiment.py:320-325.
+
+
+def fine_reference_solve(M, A, b, t_end, n_steps, u0=None, keep_trajectory=True):
+    """Backward Euler (M/dt + A) u_{n+1} = M u_n / dt + b with a sparse LU, as
+    fem.py:292-318 (`splu` of the CSC matrix, one `lu.solve` per step)."""
+    from scipy.sparse.linalg import splu
+
+    n = M.shape[0]
+    dt = t_end / n_steps
+    u = np.zeros(n) if u0 is None else np.asarray(u0, dtype=float).copy()
+    lu = splu((M / dt + A).tocsc())
+    states = [u.copy()]
+    for _ in range(n_steps):
+        u = lu.solve(M @ u / dt + b)
+        if keep_trajectory:
+            states.append(u.copy())
+    if not keep_trajectory:
+        states.append(u.copy())
+    return np.array(states)
+
+
+def m_norm(M, v):
+    """sqrt(v^T M v), fem.py:272-274."""
+    return float(np.sqrt(v @ (M @ v)))
+
+
+def relative_error(M, fine_final, coarse_final):
+    """experiment.py:320-325."""
+    denom = m_norm(M, fine_final)
+    if denom == 0.0:
+        return float(np.inf) if m_norm(M, coarse_final) > 0 else 0.0
+    return m_norm(M, fine_final - coarse_final) / denom
+
+
+def error_series(M, psi1, psi2, ref_final, history):
+    """experiment.py:348-354: one relative error per iterate, endpoint reconstructed
+    through Psi1 u + Psi2 w (msbasis.py:448-450)."""
+    d1 = psi1.shape[1]
+    out = []
+    for rows in history:
+        x = np.asarray(rows)[-1]
+        out.append(relative_error(M, ref_final, psi1 @ x[:d1] + psi2 @ x[d1:]))
+    return out

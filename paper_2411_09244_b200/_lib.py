@@ -62,6 +62,10 @@ SIGNATURES = {
     "pe_wr_is_modal": (C.c_int, [_P]),
     "pe_launch_count": (C.c_longlong, [_P]),
     "pe_last_fine_stats": (C.c_int, [_P, _D, _D, _I]),
+    "pe_fine_reference_solve": (C.c_int, [C.c_int, _I, _I, _D, _I, _I, _D, _D, _D, C.c_double,
+                                          C.c_int, C.c_int, _D, _F, _P]),
+    "pe_relative_error_series": (C.c_int, [C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _D,
+                                           C.c_int, _D, _D, _P]),
 }
 
 _lib = None

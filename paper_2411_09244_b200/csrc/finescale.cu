@@ -1,0 +1,381 @@
+// Fine-scale accuracy path: the fine backward-Euler reference solve
+// (fem.py:292-318 reference_solve) and the Eq (31) relative-error series of the parareal
+// iterates (experiment.py:320-325 relative_error, :348-354 the per-iteration series;
+// msbasis.py:448-450 reconstruct; fem.py:272-274 norm).
+//
+// Reference solve.  The fine operator K = M/dt + A is constant, so the setup factorises it
+// once (cuSOLVER 64-bit potrf + potrs against I: explicit SPD inverse) and folds the mass term in:
+//     u_{s+1} = R u_s + c,   R = K^-1 M / dt (dense, row-major),  c = K^-1 b.
+// Every time step is then ONE HBM-streaming GEMV over R (n^2 * 8 bytes), instead of the
+// reference's two sparse triangular sweeps (splu.solve), which run one row at a time.
+// The step chain is sequential in time; each step is a grid-wide dependency, so it is one
+// launch per step on the caller's stream.
+//
+// Error series.  Fine reconstructions Y_k = [Psi1 Psi2] x_k for all K iterates at once
+// (CSR SpMM, one warp per fine row), D_k = ref - Y_k, then ||D_k||_M = sqrt(D_k^T M D_k)
+// with a deterministic two-level reduction (fixed-order block partials, then a fixed-order
+// sum per column).  Row K of D is ref itself, which gives the denominator ||ref||_M.
+
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "pe.h"
+#include "pe_internal.h"
+
+namespace pe {
+
+extern long long g_launches;
+
+namespace {
+
+#define FS_SOLVER_CHECK(x)                                                              \
+  do {                                                                                  \
+    cusolverStatus_t _s = (x);                                                          \
+    if (_s != CUSOLVER_STATUS_SUCCESS)                                                  \
+      throw Error{PE_ERR_SOLVER, std::string(#x) + " failed: " + std::to_string(_s)};   \
+  } while (0)
+
+template <class T>
+struct Dev {
+  T* p = nullptr;
+  explicit Dev(size_t n) {
+    if (n) {
+      cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+      if (e != cudaSuccess)
+        throw Error{PE_ERR_NOMEM, std::string("cudaMalloc(") + std::to_string(n * sizeof(T)) +
+                                      " B): " + cudaGetErrorString(e)};
+    }
+  }
+  ~Dev() { cudaFree(p); }
+  Dev(const Dev&) = delete;
+  Dev& operator=(const Dev&) = delete;
+};
+
+struct Csr {
+  int n = 0, nnz = 0;
+  Dev<int> ptr, idx;
+  Dev<double> val;
+  Csr(int rows, const int* hptr, const int* hidx, const double* hval)
+      : n(rows), nnz(hptr[rows]), ptr(rows + 1), idx(hptr[rows]), val(hptr[rows]) {
+    PE_CUDA_CHECK(cudaMemcpy(ptr.p, hptr, (n + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    if (nnz) {
+      PE_CUDA_CHECK(cudaMemcpy(idx.p, hidx, nnz * sizeof(int), cudaMemcpyHostToDevice));
+      PE_CUDA_CHECK(cudaMemcpy(val.p, hval, nnz * sizeof(double), cudaMemcpyHostToDevice));
+    }
+  }
+};
+
+// K(i, j) = M(i, j) / dt + A(i, j), dense column-major with leading dimension ld (K is
+// symmetric, so the storage order only matters for the padding).  One thread per row.
+__global__ void k_scatter_K(int n, long long ld, const int* mp, const int* mi, const double* mv,
+                            const int* ap, const int* ai, const double* av, double inv_dt,
+                            double* K) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int t = mp[i]; t < mp[i + 1]; ++t) K[(long long)mi[t] * ld + i] += mv[t] * inv_dt;
+  for (int t = ap[i]; t < ap[i + 1]; ++t) K[(long long)ai[t] * ld + i] += av[t];
+}
+
+// B = I (column-major, leading dimension ld): the right-hand sides of K X = I.
+__global__ void k_identity(int n, long long ld, double* B) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long j = t / n, i = t % n;
+  if (j >= n) return;
+  B[j * ld + i] = (i == j) ? 1.0 : 0.0;
+}
+
+// R(i, :) = Kinv(i, :) M / dt  (row-major R, ld).  Kinv symmetric: Kinv(i, l) is read
+// from column i of the column-major buffer, i.e. contiguous in l.  M symmetric: column j
+// of M equals row j.  One warp per (i, 32-column chunk) keeps Kinv(i, :) in L1/L2.
+__global__ void k_form_R(int n, long long ld, const double* __restrict__ Kinv,
+                         const int* __restrict__ mp, const int* __restrict__ mi,
+                         const double* __restrict__ mv, double inv_dt, double* __restrict__ R) {
+  int i = blockIdx.y;
+  const double* ki = Kinv + (long long)i * ld;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int t = mp[j]; t < mp[j + 1]; ++t) s = fma(ki[mi[t]], mv[t], s);
+    R[(long long)i * ld + j] = s * inv_dt;
+  }
+}
+
+// y = A x (+ c), A row-major n x n with leading dimension ld (multiple of 2), one warp
+// per row, 16-byte loads, four in flight per lane, fixed-order shuffle reduction.
+__global__ void __launch_bounds__(256) k_gemv_rows(int n, long long ld,
+                                                   const double* __restrict__ A,
+                                                   const double* __restrict__ x,
+                                                   const double* __restrict__ c,
+                                                   double* __restrict__ y) {
+  int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double2* a2 = reinterpret_cast<const double2*>(A + (long long)row * ld);
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  int n2 = n >> 1;
+  double s0 = 0.0, s1 = 0.0;
+  int t = lane;
+  for (; t + 96 < n2; t += 128) {
+    double2 a0 = __ldcs(a2 + t), a1 = __ldcs(a2 + t + 32), a2v = __ldcs(a2 + t + 64),
+            a3 = __ldcs(a2 + t + 96);
+    double2 b0 = __ldg(x2 + t), b1 = __ldg(x2 + t + 32), b2 = __ldg(x2 + t + 64),
+            b3 = __ldg(x2 + t + 96);
+    s0 = fma(a0.x, b0.x, s0); s1 = fma(a0.y, b0.y, s1);
+    s0 = fma(a1.x, b1.x, s0); s1 = fma(a1.y, b1.y, s1);
+    s0 = fma(a2v.x, b2.x, s0); s1 = fma(a2v.y, b2.y, s1);
+    s0 = fma(a3.x, b3.x, s0); s1 = fma(a3.y, b3.y, s1);
+  }
+  for (; t < n2; t += 32) {
+    double2 a0 = __ldcs(a2 + t), b0 = __ldg(x2 + t);
+    s0 = fma(a0.x, b0.x, s0); s1 = fma(a0.y, b0.y, s1);
+  }
+  if ((n & 1) && lane == 0) s0 = fma(A[(long long)row * ld + n - 1], x[n - 1], s0);
+  double s = s0 + s1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[row] = c ? s + c[row] : s;
+}
+
+// D(k, i) = ref(i) - sum_j P(i, j) X(k, j) for k < K, D(K, i) = ref(i).  P: CSR n x d.
+// One warp per fine row i; lanes split the row's nonzeros, fixed-order shuffle sum.
+__global__ void k_reconstruct_diff(int n, int d, int K, const int* __restrict__ pp,
+                                   const int* __restrict__ pi, const double* __restrict__ pv,
+                                   const double* __restrict__ X, const double* __restrict__ ref,
+                                   double* __restrict__ D) {
+  int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  int b = pp[i], e = pp[i + 1];
+  for (int k = 0; k < K; ++k) {
+    const double* xk = X + (long long)k * d;
+    double s = 0.0;
+    for (int t = b + lane; t < e; t += 32) s = fma(pv[t], xk[pi[t]], s);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) D[(long long)k * n + i] = ref[i] - s;
+  }
+  if (lane == 0) D[(long long)K * n + i] = ref[i];
+}
+
+// partial[k * nblk + blk] = sum over this block's rows i of D(k,i) * (M D(k,:))(i).
+__global__ void __launch_bounds__(256) k_mnorm_partial(int n, const int* __restrict__ mp,
+                                                       const int* __restrict__ mi,
+                                                       const double* __restrict__ mv,
+                                                       const double* __restrict__ D,
+                                                       double* __restrict__ partial) {
+  __shared__ double red[256];
+  int k = blockIdx.y;
+  const double* dk = D + (long long)k * n;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int t = mp[i]; t < mp[i + 1]; ++t) s = fma(mv[t], dk[mi[t]], s);
+    acc = fma(dk[i], s, acc);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[(long long)k * gridDim.x + blockIdx.x] = red[0];
+}
+
+__global__ void k_mnorm_final(int nblk, int K1, const double* __restrict__ partial,
+                              double* __restrict__ norms) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K1) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += partial[(long long)k * nblk + b];
+  norms[k] = sqrt(s);
+}
+
+long long padded_ld(int n) { return ((long long)n + 3) & ~3LL; }
+
+}  // namespace
+
+static int fs_guard(const char* what, void (*fn)(void*), void* arg) {
+  try {
+    fn(arg);
+    return PE_OK;
+  } catch (const Error& e) {
+    set_error(std::string(what) + ": " + e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(std::string(what) + ": " + e.what());
+    return PE_ERR_CUDA;
+  }
+}
+
+struct RefSolveArgs {
+  int n;
+  const int *mp, *mi, *ap, *ai;
+  const double *mv, *av, *b, *u0;
+  double t_end;
+  int n_steps;
+  double* states_h;
+  int keep;
+  cudaStream_t st;
+  float* step_ms;
+};
+
+static void ref_solve_impl(void* vp) {
+  RefSolveArgs& a = *static_cast<RefSolveArgs*>(vp);
+  const int n = a.n;
+  if (n > 65535) throw Error{PE_ERR_ARG, "fine problems above 65535 interior nodes are not supported"};
+  const double dt = a.t_end / a.n_steps;
+  const double inv_dt = 1.0 / dt;
+  const long long ld = padded_ld(n);
+  Csr M(n, a.mp, a.mi, a.mv), A(n, a.ap, a.ai, a.av);
+  Dev<double> K((size_t)ld * n), R((size_t)ld * n), bc(2 * (size_t)n);
+  Dev<int> info(1);
+  PE_CUDA_CHECK(cudaMemsetAsync(K.p, 0, sizeof(double) * ld * n, a.st));
+  PE_CUDA_CHECK(cudaMemcpyAsync(bc.p, a.b, n * sizeof(double), cudaMemcpyHostToDevice, a.st));
+  k_scatter_K<<<(n + 255) / 256, 256, 0, a.st>>>(n, ld, M.ptr.p, M.idx.p, M.val.p, A.ptr.p,
+                                                 A.idx.p, A.val.p, inv_dt, K.p);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+
+  cusolverDnHandle_t h = nullptr;
+  cusolverDnParams_t prm = nullptr;
+  FS_SOLVER_CHECK(cusolverDnCreate(&h));
+  struct HGuard {
+    cusolverDnHandle_t h;
+    cusolverDnParams_t* p;
+    ~HGuard() {
+      if (*p) cusolverDnDestroyParams(*p);
+      cusolverDnDestroy(h);
+    }
+  } hg{h, &prm};
+  FS_SOLVER_CHECK(cusolverDnCreateParams(&prm));
+  FS_SOLVER_CHECK(cusolverDnSetStream(h, a.st));
+  // 64-bit API: n * ld exceeds 2^31 at the larger fine grids
+  size_t wd = 0, wh = 0;
+  FS_SOLVER_CHECK(cusolverDnXpotrf_bufferSize(h, prm, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, K.p,
+                                              ld, CUDA_R_64F, &wd, &wh));
+  {
+    Dev<char> work(wd + 16);
+    std::vector<char> hwork(wh + 16);
+    FS_SOLVER_CHECK(cusolverDnXpotrf(h, prm, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, K.p, ld,
+                                     CUDA_R_64F, work.p, wd, hwork.data(), wh, info.p));
+    int hinfo = 0;
+    PE_CUDA_CHECK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, a.st));
+    PE_CUDA_CHECK(cudaStreamSynchronize(a.st));
+    if (hinfo != 0)
+      throw Error{PE_ERR_SOLVER, "M/dt + A is not positive definite (potrf info " +
+                                     std::to_string(hinfo) + ")"};
+  }
+  // Kinv = K^-1 I (two triangular solves against the identity; symmetric, full storage)
+  long long tot = (long long)n * n;
+  k_identity<<<(unsigned)((tot + 255) / 256), 256, 0, a.st>>>(n, ld, R.p);
+  ++g_launches;
+  FS_SOLVER_CHECK(cusolverDnXpotrs(h, prm, CUBLAS_FILL_MODE_LOWER, n, n, CUDA_R_64F, K.p, ld,
+                                   CUDA_R_64F, R.p, ld, info.p));
+  // c = Kinv b; then R = Kinv M / dt, written over the factor's buffer
+  k_gemv_rows<<<(n + 7) / 8, 256, 0, a.st>>>(n, ld, R.p, bc.p, nullptr, bc.p + n);
+  ++g_launches;
+  dim3 gR((n + 255) / 256 < 8 ? (n + 255) / 256 : 8, n);
+  k_form_R<<<gR, 256, 0, a.st>>>(n, ld, R.p, M.ptr.p, M.idx.p, M.val.p, inv_dt, K.p);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+  PE_CUDA_CHECK(cudaStreamSynchronize(a.st));
+  double* Rm = K.p;
+
+  const size_t nb = (size_t)n * sizeof(double);
+  size_t traj_rows = a.keep ? (size_t)a.n_steps + 1 : 3;  // else [u0, ping, pong]
+  Dev<double> U(traj_rows * ld);  // rows at 32-byte aligned stride ld (16-byte GEMV loads)
+  if (a.u0)
+    PE_CUDA_CHECK(cudaMemcpyAsync(U.p, a.u0, nb, cudaMemcpyHostToDevice, a.st));
+  else
+    PE_CUDA_CHECK(cudaMemsetAsync(U.p, 0, nb, a.st));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (a.step_ms) {
+    PE_CUDA_CHECK(cudaEventCreate(&e0));
+    PE_CUDA_CHECK(cudaEventCreate(&e1));
+    PE_CUDA_CHECK(cudaEventRecord(e0, a.st));
+  }
+  for (int s = 0; s < a.n_steps; ++s) {
+    const double* src = U.p + (size_t)(a.keep || s == 0 ? s : 1 + ((s - 1) & 1)) * ld;
+    double* dst = U.p + (size_t)(a.keep ? s + 1 : 1 + (s & 1)) * ld;
+    k_gemv_rows<<<(n + 7) / 8, 256, 0, a.st>>>(n, ld, Rm, src, bc.p + n, dst);
+    ++g_launches;
+  }
+  PE_CUDA_CHECK(cudaGetLastError());
+  if (a.step_ms) {
+    PE_CUDA_CHECK(cudaEventRecord(e1, a.st));
+    PE_CUDA_CHECK(cudaEventSynchronize(e1));
+    PE_CUDA_CHECK(cudaEventElapsedTime(a.step_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (a.keep) {
+    PE_CUDA_CHECK(cudaMemcpy2DAsync(a.states_h, nb, U.p, ld * sizeof(double), nb, traj_rows,
+                                    cudaMemcpyDeviceToHost, a.st));
+  } else {
+    PE_CUDA_CHECK(cudaMemcpyAsync(a.states_h, U.p, nb, cudaMemcpyDeviceToHost, a.st));
+    PE_CUDA_CHECK(cudaMemcpyAsync(a.states_h + n, U.p + (size_t)(1 + ((a.n_steps - 1) & 1)) * ld, nb,
+                                  cudaMemcpyDeviceToHost, a.st));
+  }
+  PE_CUDA_CHECK(cudaStreamSynchronize(a.st));
+}
+
+struct ErrArgs {
+  int n, d, K;
+  const int *pp, *pi, *mp, *mi;
+  const double *pv, *mv, *ref, *X;
+  double* norms_h;
+  cudaStream_t st;
+};
+
+static void err_impl(void* vp) {
+  ErrArgs& a = *static_cast<ErrArgs*>(vp);
+  const int n = a.n, K1 = a.K + 1;
+  Csr P(n, a.pp, a.pi, a.pv), M(n, a.mp, a.mi, a.mv);
+  Dev<double> X((size_t)a.K * a.d + 1), ref(n), D((size_t)K1 * n), norms(K1);
+  const int nblk = std::min(148, (n + 255) / 256);
+  Dev<double> part((size_t)K1 * nblk);
+  if (a.K)
+    PE_CUDA_CHECK(cudaMemcpyAsync(X.p, a.X, sizeof(double) * a.K * a.d, cudaMemcpyHostToDevice, a.st));
+  PE_CUDA_CHECK(cudaMemcpyAsync(ref.p, a.ref, sizeof(double) * n, cudaMemcpyHostToDevice, a.st));
+  k_reconstruct_diff<<<(n + 7) / 8, 256, 0, a.st>>>(n, a.d, a.K, P.ptr.p, P.idx.p, P.val.p, X.p,
+                                                    ref.p, D.p);
+  k_mnorm_partial<<<dim3(nblk, K1), 256, 0, a.st>>>(n, M.ptr.p, M.idx.p, M.val.p, D.p, part.p);
+  k_mnorm_final<<<(K1 + 127) / 128, 128, 0, a.st>>>(nblk, K1, part.p, norms.p);
+  g_launches += 3;
+  PE_CUDA_CHECK(cudaGetLastError());
+  PE_CUDA_CHECK(cudaMemcpyAsync(a.norms_h, norms.p, sizeof(double) * K1, cudaMemcpyDeviceToHost, a.st));
+  PE_CUDA_CHECK(cudaStreamSynchronize(a.st));
+}
+
+}  // namespace pe
+
+extern "C" int pe_fine_reference_solve(int n, const int* M_ptr, const int* M_idx,
+                                       const double* M_val, const int* A_ptr, const int* A_idx,
+                                       const double* A_val, const double* b, const double* u0,
+                                       double t_end, int n_steps, int keep_trajectory,
+                                       double* states_h, float* step_ms, void* stream) {
+  if (n <= 0 || n_steps <= 0 || !(t_end > 0.0) || !M_ptr || !A_ptr || !b || !states_h) {
+    pe::set_error("pe_fine_reference_solve: need n > 0, n_steps > 0, t_end > 0 and buffers");
+    return PE_ERR_ARG;
+  }
+  pe::RefSolveArgs a{n,     M_ptr,   M_idx, A_ptr, A_idx, M_val,          A_val,
+                     b,     u0,      t_end, n_steps, states_h, keep_trajectory,
+                     (cudaStream_t)stream, step_ms};
+  return pe::fs_guard("pe_fine_reference_solve", pe::ref_solve_impl, &a);
+}
+
+extern "C" int pe_relative_error_series(int n, int d, const int* P_ptr, const int* P_idx,
+                                        const double* P_val, const int* M_ptr,
+                                        const int* M_idx, const double* M_val,
+                                        const double* ref, int K, const double* X,
+                                        double* norms_h, void* stream) {
+  if (n <= 0 || d < 0 || K < 0 || !P_ptr || !M_ptr || !ref || !norms_h || (K > 0 && !X)) {
+    pe::set_error("pe_relative_error_series: need n > 0, K >= 0 and buffers");
+    return PE_ERR_ARG;
+  }
+  pe::ErrArgs a{n, d, K, P_ptr, P_idx, M_ptr, M_idx, P_val, M_val, ref, X, norms_h,
+                (cudaStream_t)stream};
+  return pe::fs_guard("pe_relative_error_series", pe::err_impl, &a);
+}

@@ -1,0 +1,85 @@
+"""Artifact writers for GPU parareal runs (output compatibility).
+
+Byte-compatible with the reference's experiment outputs so downstream scripts read a
+GPU run unchanged: `write_csv` / `save_matrix_txt` follow util.py:26-50, and
+`write_run_artifacts` writes the per-N files of `_emit_all` (experiment.py:398-450):
+runs.csv rows, conv_N*.csv, timings_N*.csv, wr_residuals_N*.csv and, optionally, the
+solution / reference node grids.  The accuracy numbers come from `fem.error_series`
+(GPU); nothing here computes on the CPU beyond formatting.
+"""
+
+from __future__ import annotations
+
+import csv
+from pathlib import Path
+
+import numpy as np
+
+
+def _fmt(value):
+    # util.py:46-50: floats at full round-trip precision, everything else via str()
+    if isinstance(value, (float, np.floating)):
+        return format(float(value), ".17g")
+    return value
+
+
+def write_csv(path, header, rows) -> None:
+    """Rows of mixed scalars as CSV (util.py:36-43)."""
+    with Path(path).open("w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(header)
+        for row in rows:
+            w.writerow([_fmt(v) for v in row])
+
+
+def save_matrix_txt(path, array) -> None:
+    """A matrix as plain text, one row per line, full precision (util.py:26-29)."""
+    np.savetxt(path, np.atleast_2d(np.asarray(array)), fmt="%.17g")
+
+
+def runs_rows(results, gamma):
+    """runs.csv rows (experiment.py:410-417) from (n, run, relative_error) triples."""
+    return [(n, run.iterations, int(run.converged), err, gamma, run.total_seconds)
+            for n, run, err in results]
+
+
+RUNS_HEADER = ["n", "iterations", "converged", "relative_error", "gamma", "wall_seconds"]
+
+
+def write_run_artifacts(out_dir, n, run, error_series=(), *, solution_grid=None,
+                        reference_grid=None) -> list[Path]:
+    """The per-N files of the reference's `_emit_all` (experiment.py:418-450).
+
+    `run` is a ParerealRun (ours or the reference's); `error_series[k]` is the relative
+    error of iterate k (index 0 = the initial coarse sweep), NaN where absent.
+    Returns the written paths.
+    """
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    written = []
+
+    def path(name):
+        p = out / name
+        written.append(p)
+        return p
+
+    rows = []
+    for k, diff in enumerate(run.max_diffs, start=1):
+        err_k = error_series[k] if k < len(error_series) else float("nan")
+        rows.append((k, diff, err_k))
+    write_csv(path(f"conv_N{n}.csv"), ["iteration", "max_diff", "relative_error"], rows)
+    write_csv(path(f"timings_N{n}.csv"), ["iteration", "fine_seconds", "coarse_seconds"],
+              [(k + 1, run.fine_seconds[k], run.coarse_seconds[k])
+               for k in range(len(run.fine_seconds))])
+    wr_rows = []
+    for k, sweep in enumerate(run.fine_info, start=1):
+        for interval, info in enumerate(sweep):
+            for j, res in enumerate(info.get("residuals", []), start=1):
+                wr_rows.append((k, interval, j, res))
+    write_csv(path(f"wr_residuals_N{n}.csv"), ["sweep", "interval", "iteration", "residual"],
+              wr_rows)
+    if solution_grid is not None:
+        save_matrix_txt(path(f"solution_N{n}.txt"), solution_grid)
+    if reference_grid is not None:
+        save_matrix_txt(path(f"reference_N{n}.txt"), reference_grid)
+    return written

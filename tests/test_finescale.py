@@ -1,0 +1,164 @@
+"""Fine-scale accuracy path: the GPU backward-Euler reference solve
+and Eq (31) error series against the reference's golden vectors (tests/golden/
+fine_cfg0.npz, written by oracle/make_fine_golden.py from the unmodified reference), and
+the artifact writers byte-for-byte against the reference's own CSV output.
+
+Tolerances.  The GPU reference solve applies an explicit inverse (R = K^-1 M / dt,
+c = K^-1 b) where the reference back-substitutes a sparse LU each step: rounding differs
+at cond(K) * eps per step, so trajectory rows are compared at 1e-10 relative L2.  The
+error series differs from the reference only in summation order: 1e-12 relative.
+"""
+
+import json
+import types
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import pe_oracle as po
+from tests.conftest import golden
+
+REL_TRAJ = 1e-10
+REL_SERIES = 1e-12
+
+
+def _csr(z, p):
+    return sp.csr_matrix((z[f"{p}_val"], z[f"{p}_idx"], z[f"{p}_ptr"]), shape=tuple(z[f"{p}_shape"]))
+
+
+def _fixture():
+    z = golden("fine_cfg0.npz")
+    ops = types.SimpleNamespace(M=_csr(z, "M"), A=_csr(z, "A"))
+    space = types.SimpleNamespace(Psi1=_csr(z, "P1"), Psi2=_csr(z, "P2"))
+    return z, ops, space
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ------------------------------------------------------------------ CPU: oracle pins
+
+
+def test_oracle_reference_solve_pinned():
+    z, ops, _ = _fixture()
+    traj = po.fine_reference_solve(ops.M, ops.A, z["b"], 1.0, 100)
+    assert np.array_equal(traj[::10], z["traj"])
+    short = po.fine_reference_solve(ops.M, ops.A, z["b"], 0.05, 7, u0=z["u0"],
+                                    keep_trajectory=False)
+    assert np.array_equal(short, z["short"])
+
+
+def test_oracle_error_series_pinned():
+    z, ops, space = _fixture()
+    hist = golden("run_cfg0_seq.npz")["history"]
+    s = po.error_series(ops.M, space.Psi1.tocsc(), space.Psi2.tocsc(), z["traj"][-1], hist)
+    np.testing.assert_allclose(s, z["series"], rtol=1e-14)
+    assert po.relative_error(ops.M, np.zeros(ops.M.shape[0]), np.zeros(ops.M.shape[0])) == 0.0
+    assert po.relative_error(ops.M, np.zeros(ops.M.shape[0]), np.ones(ops.M.shape[0])) == np.inf
+
+
+def test_writers_match_reference_bytes(tmp_path):
+    """conv / timings / wr_residuals CSVs are byte-identical to the reference's writers
+    (util.py:36-50 via experiment.py:418-441) for the same run record."""
+    from paper_2411_09244_b200.experiment import write_run_artifacts
+
+    z, _, _ = _fixture()
+    fine_info = [[{"residuals": r} for r in sw] for sw in json.loads(str(z["w_residuals"]))]
+    run = types.SimpleNamespace(max_diffs=list(z["w_max_diffs"]),
+                                fine_seconds=list(z["w_fine_seconds"]),
+                                coarse_seconds=list(z["w_coarse_seconds"]), fine_info=fine_info)
+    files = write_run_artifacts(tmp_path, 10, run, list(z["series"]),
+                                solution_grid=np.arange(6.0).reshape(2, 3) / 7)
+    assert [f.name for f in files] == ["conv_N10.csv", "timings_N10.csv", "wr_residuals_N10.csv",
+                                       "solution_N10.txt"]
+    assert (tmp_path / "conv_N10.csv").read_text() == str(z["csv_conv"])
+    assert (tmp_path / "timings_N10.csv").read_text() == str(z["csv_timings"])
+    assert (tmp_path / "wr_residuals_N10.csv").read_text() == str(z["csv_wr"])
+    back = np.loadtxt(tmp_path / "solution_N10.txt")
+    assert np.array_equal(back, np.arange(6.0).reshape(2, 3) / 7)
+
+
+def test_node_values_on_grid():
+    from paper_2411_09244_b200.fem import node_values_on_grid
+
+    z, _, _ = _fixture()
+    nx = int(z["nx"])
+    grid = types.SimpleNamespace(n_nodes=(nx + 1) ** 2, interior=z["interior"], nx=nx, ny=nx)
+    full = node_values_on_grid(grid, np.arange(int(z["n_interior"]), dtype=float) + 1)
+    assert full.shape == (nx + 1, nx + 1)
+    assert full[0].sum() == 0 and full[:, 0].sum() == 0 and full[-1].sum() == 0
+    assert full[1, 1] == 1.0
+
+
+# ------------------------------------------------------------------ GPU parity
+
+
+@pytest.mark.gpu
+def test_gpu_reference_solve_matches_reference():
+    from paper_2411_09244_b200 import fem
+
+    z, ops, _ = _fixture()
+    tm = {}
+    times, traj = fem.reference_solve(ops, z["b"], 1.0, 100, timing=tm)
+    assert traj.shape == (101, ops.M.shape[0]) and times[-1] == 1.0
+    for r, g in zip(traj[::10], z["traj"]):
+        assert _rel(r, g) < REL_TRAJ or np.linalg.norm(g) == 0
+    assert tm["step_ms"] > 0
+    times, short = fem.reference_solve(ops, z["b"], 0.05, 7, u0=z["u0"], keep_trajectory=False)
+    assert short.shape == (2, ops.M.shape[0]) and list(times) == [0.0, 0.05]
+    assert np.array_equal(short[0], z["u0"])
+    assert _rel(short[1], z["short"][1]) < REL_TRAJ
+
+
+@pytest.mark.gpu
+def test_gpu_reference_solve_odd_sizes_vs_oracle(rng):
+    """Odd n (unaligned rows), n < 32 and n_steps = 1 against the oracle's splu."""
+    from paper_2411_09244_b200 import fem
+
+    for n, steps in ((1, 3), (7, 1), (33, 5), (257, 9)):
+        T = sp.random(n, n, density=0.3, random_state=int(rng.integers(1 << 30))).toarray()
+        Mm = sp.csr_matrix(np.eye(n) * 2 + 0.1 * (T + T.T) / max(1, n) ** 0.5)
+        Am = sp.csr_matrix(np.eye(n) + np.diag(np.full(n - 1, -0.3), 1) + np.diag(np.full(n - 1, -0.3), -1))
+        b = rng.standard_normal(n)
+        u0 = rng.standard_normal(n)
+        ops = types.SimpleNamespace(M=Mm, A=Am)
+        ref = po.fine_reference_solve(Mm, Am, b, 0.3, steps, u0=u0)
+        _, got = fem.reference_solve(ops, b, 0.3, steps, u0=u0)
+        for r, g in zip(got, ref):
+            assert _rel(r, g) < 1e-12, (n, steps)
+
+
+@pytest.mark.gpu
+def test_gpu_error_series_matches_reference():
+    from paper_2411_09244_b200 import fem
+
+    z, ops, space = _fixture()
+    hist = golden("run_cfg0_seq.npz")["history"]
+    got = fem.error_series(ops, space, z["traj"][-1], hist[:, -1, :])
+    np.testing.assert_allclose(got, z["series"], rtol=REL_SERIES)
+    # one endpoint through relative_error on fine vectors
+    x = hist[-1, -1]
+    d1 = space.Psi1.shape[1]
+    y = space.Psi1 @ x[:d1] + space.Psi2 @ x[d1:]
+    assert abs(fem.relative_error(ops, z["traj"][-1], y) - z["series"][-1]) < REL_SERIES * z["series"][-1]
+
+
+@pytest.mark.gpu
+def test_gpu_error_edge_cases():
+    from paper_2411_09244_b200 import fem
+    from paper_2411_09244_b200._lib import PeError
+
+    z, ops, space = _fixture()
+    n = ops.M.shape[0]
+    assert fem.relative_error(ops, np.zeros(n), np.zeros(n)) == 0.0
+    assert fem.relative_error(ops, np.zeros(n), np.ones(n)) == np.inf
+    assert fem.error_series(ops, space, z["traj"][-1], np.zeros((0, 64))) == []
+    with pytest.raises(ValueError):
+        fem.reference_solve(ops, z["b"], 1.0, 0)
+    with pytest.raises(ValueError):
+        fem.reference_solve(ops, z["b"][:-1], 1.0, 5)
+    bad = types.SimpleNamespace(M=sp.csr_matrix(np.eye(3)), A=sp.csr_matrix(-5 * np.eye(3)))
+    with pytest.raises(PeError):
+        fem.reference_solve(bad, np.ones(3), 1.0, 1)
