@@ -19,6 +19,7 @@
 #include <cusolverDn.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -192,6 +193,102 @@ __global__ void k_mnorm_final(int nblk, int K1, const double* __restrict__ parti
   norms[k] = sqrt(s);
 }
 
+// ---- packed symmetric path (n >= kSymMin): K^-1 is symmetric, so each step streams only
+// its lower-triangle tiles (half the bytes of R).  Tile (I, J), J <= I, of B x B doubles is
+// stored row-major at tile index I (I + 1) / 2 + J (zero padded past n).  One CTA per tile
+// produces the tile's row sums T v_J (rowpart) and, off the diagonal, its column sums
+// T^T v_I (colpart, the mirrored upper tile); k_sym_reduce adds them per row in a fixed
+// order.  Per step: v = M u / dt + b (k_rhs), the tile pass, the reduction.
+constexpr int kB = 128;
+constexpr int kSymMin = 4096;
+
+__device__ __forceinline__ int tri_row(int t) {
+  int I = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((long long)(I + 1) * (I + 2) / 2 <= t) ++I;
+  while ((long long)I * (I + 1) / 2 > t) --I;
+  return I;
+}
+
+__global__ void k_pack_tiles(int n, long long ld, const double* __restrict__ Kinv,
+                             double* __restrict__ T) {
+  int t = blockIdx.x;
+  int I = tri_row(t), J = t - I * (I + 1) / 2;
+  double* dst = T + (size_t)t * kB * kB;
+  for (int idx = threadIdx.x; idx < kB * kB; idx += blockDim.x) {
+    int r = idx / kB, c = idx % kB;
+    long long gi = (long long)I * kB + r, gj = (long long)J * kB + c;
+    dst[idx] = (gi < n && gj < n) ? Kinv[gi * ld + gj] : 0.0;
+  }
+}
+
+// v(i) = (M u)(i) / dt + b(i), i < n (rows past n stay zero)
+__global__ void k_rhs(int n, const int* __restrict__ mp, const int* __restrict__ mi,
+                      const double* __restrict__ mv, double inv_dt, const double* __restrict__ u,
+                      const double* __restrict__ b, double* __restrict__ v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int t = mp[i]; t < mp[i + 1]; ++t) s = fma(mv[t], u[mi[t]], s);
+  v[i] = fma(s, inv_dt, b[i]);
+}
+
+__global__ void __launch_bounds__(256) k_sym_tiles(const double* __restrict__ T,
+                                                   const double* __restrict__ v,
+                                                   double* __restrict__ rowpart,
+                                                   double* __restrict__ colpart) {
+  __shared__ double rowred[2][kB];
+  __shared__ double colred[4][kB];
+  const int t = blockIdx.x;
+  const int I = tri_row(t), J = t - I * (I + 1) / 2;
+  const int cp = threadIdx.x & 63, rg = threadIdx.x >> 6, lane = threadIdx.x & 31;
+  const double2* tile = reinterpret_cast<const double2*>(T + (size_t)t * kB * kB);
+  const double2 vJ = reinterpret_cast<const double2*>(v + (size_t)J * kB)[cp];
+  const double* vI = v + (size_t)I * kB + rg * 32;
+  double rp[32];
+  double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    double2 a = __ldcs(tile + (rg * 32 + r) * (kB / 2) + cp);
+    double vi = __ldg(vI + r);
+    c0 = fma(a.x, vi, c0);
+    c1 = fma(a.y, vi, c1);
+    rp[r] = fma(a.x, vJ.x, a.y * vJ.y);
+  }
+  // transpose-reduce the 32 row partials across the warp: lane L ends with row L's sum
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = lane & s;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      double send = up ? rp[i] : rp[i + s];
+      double keep = up ? rp[i + s] : rp[i];
+      rp[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  rowred[(threadIdx.x >> 5) & 1][rg * 32 + lane] = rp[0];
+  colred[rg][2 * cp] = c0;
+  colred[rg][2 * cp + 1] = c1;
+  __syncthreads();
+  if (threadIdx.x < kB) {
+    rowpart[(size_t)t * kB + threadIdx.x] = rowred[0][threadIdx.x] + rowred[1][threadIdx.x];
+  } else if (I != J) {
+    int c = threadIdx.x - kB;
+    colpart[(size_t)t * kB + c] = ((colred[0][c] + colred[1][c]) + colred[2][c]) + colred[3][c];
+  }
+}
+
+__global__ void k_sym_reduce(int n, int nb, const double* __restrict__ rowpart,
+                             const double* __restrict__ colpart, double* __restrict__ y) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int K = i / kB, r = i % kB;
+  double s = 0.0;
+  size_t base = (size_t)K * (K + 1) / 2;
+  for (int J = 0; J <= K; ++J) s += rowpart[(base + J) * kB + r];
+  for (int I = K + 1; I < nb; ++I) s += colpart[((size_t)I * (I + 1) / 2 + K) * kB + r];
+  y[i] = s;
+}
+
 long long padded_ld(int n) { return ((long long)n + 3) & ~3LL; }
 
 }  // namespace
@@ -276,12 +373,23 @@ static void ref_solve_impl(void* vp) {
   // c = Kinv b; then R = Kinv M / dt, written over the factor's buffer
   k_gemv_rows<<<(n + 7) / 8, 256, 0, a.st>>>(n, ld, R.p, bc.p, nullptr, bc.p + n);
   ++g_launches;
-  dim3 gR((n + 255) / 256 < 8 ? (n + 255) / 256 : 8, n);
-  k_form_R<<<gR, 256, 0, a.st>>>(n, ld, R.p, M.ptr.p, M.idx.p, M.val.p, inv_dt, K.p);
-  ++g_launches;
+  const bool sym = n >= kSymMin && !getenv("PE_FINE_NO_SYM");
+  const int nbk = (n + kB - 1) / kB;
+  const size_t ntiles = sym ? (size_t)nbk * (nbk + 1) / 2 : 0;
+  Dev<double> T(ntiles * kB * kB), rowpart(ntiles * kB), colpart(ntiles * kB),
+      vpad(sym ? (size_t)nbk * kB : 0);
+  double* Rm = K.p;
+  if (sym) {
+    k_pack_tiles<<<(unsigned)ntiles, 256, 0, a.st>>>(n, ld, R.p, T.p);
+    ++g_launches;
+    PE_CUDA_CHECK(cudaMemsetAsync(vpad.p, 0, sizeof(double) * nbk * kB, a.st));
+  } else {
+    dim3 gR((n + 255) / 256 < 8 ? (n + 255) / 256 : 8, n);
+    k_form_R<<<gR, 256, 0, a.st>>>(n, ld, R.p, M.ptr.p, M.idx.p, M.val.p, inv_dt, K.p);
+    ++g_launches;
+  }
   PE_CUDA_CHECK(cudaGetLastError());
   PE_CUDA_CHECK(cudaStreamSynchronize(a.st));
-  double* Rm = K.p;
 
   const size_t nb = (size_t)n * sizeof(double);
   size_t traj_rows = a.keep ? (size_t)a.n_steps + 1 : 3;  // else [u0, ping, pong]
@@ -299,8 +407,16 @@ static void ref_solve_impl(void* vp) {
   for (int s = 0; s < a.n_steps; ++s) {
     const double* src = U.p + (size_t)(a.keep || s == 0 ? s : 1 + ((s - 1) & 1)) * ld;
     double* dst = U.p + (size_t)(a.keep ? s + 1 : 1 + (s & 1)) * ld;
-    k_gemv_rows<<<(n + 7) / 8, 256, 0, a.st>>>(n, ld, Rm, src, bc.p + n, dst);
-    ++g_launches;
+    if (sym) {
+      k_rhs<<<(n + 255) / 256, 256, 0, a.st>>>(n, M.ptr.p, M.idx.p, M.val.p, inv_dt, src, bc.p,
+                                               vpad.p);
+      k_sym_tiles<<<(unsigned)ntiles, 256, 0, a.st>>>(T.p, vpad.p, rowpart.p, colpart.p);
+      k_sym_reduce<<<(n + 255) / 256, 256, 0, a.st>>>(n, nbk, rowpart.p, colpart.p, dst);
+      g_launches += 3;
+    } else {
+      k_gemv_rows<<<(n + 7) / 8, 256, 0, a.st>>>(n, ld, Rm, src, bc.p + n, dst);
+      ++g_launches;
+    }
   }
   PE_CUDA_CHECK(cudaGetLastError());
   if (a.step_ms) {

@@ -22,6 +22,9 @@ import numpy as np
 from ._lib import check, require_cuda
 
 
+SYM_MIN = 4096  # finescale.cu kSymMin: packed symmetric K^-1 tiles from this size on
+
+
 def _csr(mat, n_rows=None):
     """(indptr int32, indices int32, data float64) of a scipy sparse / dense matrix."""
     import scipy.sparse as sp
@@ -88,7 +91,10 @@ def reference_solve(ops, source, t_end: float, n_steps: int, u0=None,
         _dp(states), C.byref(ms), _stream_ptr(stream)))
     if timing is not None:
         timing["step_ms"] = float(ms.value)
-        timing["bytes_per_step"] = 8.0 * n * (n + 2)
+        # algorithmic HBM bytes per step: R once + u, c, u' (n < 4096); from n = 4096 on the
+        # lower triangle of the symmetric K^-1 once + M, u, b, v, u' (finescale.cu)
+        timing["bytes_per_step"] = (8.0 * n * (n + 2) if n < SYM_MIN
+                                    else 8.0 * (n * (n + 1) / 2 + 4 * n) + 12.0 * ops.M.nnz)
     times = np.linspace(0.0, t_end, n_steps + 1) if keep_trajectory else np.array([0.0, t_end])
     return times, states
 

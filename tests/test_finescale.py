@@ -130,6 +130,40 @@ def test_gpu_reference_solve_odd_sizes_vs_oracle(rng):
             assert _rel(r, g) < 1e-12, (n, steps)
 
 
+def _fem_like(m, seed):
+    """Mass / stiffness with the fine operators' structure on an m x m interior grid."""
+    rng = np.random.default_rng(seed)
+    one = np.ones(m)
+    T1 = sp.diags([one[:-1], 4 * one, one[:-1]], [-1, 0, 1])
+    M = (sp.kron(T1, T1) / (36.0 * (m + 1) ** 2)).tocsr()
+    G1 = sp.diags([np.ones(m), -np.ones(m)], [0, -1], shape=(m + 1, m))
+    I = sp.identity(m)
+    Gx, Gy = sp.kron(I, G1).tocsr(), sp.kron(G1, I).tocsr()
+    kx = np.where(rng.random(Gx.shape[0]) < 0.1, 1e4, 1.0)
+    ky = np.where(rng.random(Gy.shape[0]) < 0.1, 1e4, 1.0)
+    A = (Gx.T @ sp.diags(kx) @ Gx + Gy.T @ sp.diags(ky) @ Gy).tocsr() * 1e-3
+    return M, A, rng.standard_normal(m * m)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [64, 67, 90])
+def test_gpu_reference_solve_packed_symmetric_path(m, monkeypatch):
+    """n = m^2 >= 4096 takes the packed lower-triangle path (partial last tile for m = 67,
+    90): equal to the oracle's splu and to the dense-R path within 1e-12."""
+    from paper_2411_09244_b200 import fem
+
+    M, A, u0 = _fem_like(m, m)
+    b = np.full(m * m, 1.0 / (m + 1) ** 2)
+    ops = types.SimpleNamespace(M=M, A=A)
+    ref = po.fine_reference_solve(M, A, b, 0.02, 6, u0=u0)
+    _, got = fem.reference_solve(ops, b, 0.02, 6, u0=u0)
+    for r, g in zip(got, ref):
+        assert _rel(r, g) < 1e-12
+    monkeypatch.setenv("PE_FINE_NO_SYM", "1")
+    _, dense = fem.reference_solve(ops, b, 0.02, 6, u0=u0)
+    assert _rel(dense[-1], got[-1]) < 1e-12
+
+
 @pytest.mark.gpu
 def test_gpu_error_series_matches_reference():
     from paper_2411_09244_b200 import fem
