@@ -277,16 +277,33 @@ __global__ void __launch_bounds__(256) k_sym_tiles(const double* __restrict__ T,
   }
 }
 
-__global__ void k_sym_reduce(int n, int nb, const double* __restrict__ rowpart,
-                             const double* __restrict__ colpart, double* __restrict__ y) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int K = i / kB, r = i % kB;
+// y(i) for the 64 rows of half a band K: 16 slices per row each sum a fixed strided subset
+// of the band's nb partial vectors (rowparts J <= K, then colparts I > K), coalesced over
+// rows; the slices are combined in a fixed order through shared memory.
+constexpr int kRedRows = 64, kRedSlices = 16;
+__global__ void __launch_bounds__(kRedRows * kRedSlices) k_sym_reduce(
+    int n, int nb, const double* __restrict__ rowpart, const double* __restrict__ colpart,
+    double* __restrict__ y) {
+  __shared__ double red[kRedSlices][kRedRows];
+  const int K = blockIdx.x >> 1;
+  const int r = (blockIdx.x & 1) * kRedRows + (threadIdx.x % kRedRows);
+  const int sl = threadIdx.x / kRedRows;
+  const size_t base = (size_t)K * (K + 1) / 2;
   double s = 0.0;
-  size_t base = (size_t)K * (K + 1) / 2;
-  for (int J = 0; J <= K; ++J) s += rowpart[(base + J) * kB + r];
-  for (int I = K + 1; I < nb; ++I) s += colpart[((size_t)I * (I + 1) / 2 + K) * kB + r];
-  y[i] = s;
+  for (int j = sl; j < nb; j += kRedSlices) {
+    const double* src = j <= K ? rowpart + (base + j) * kB
+                               : colpart + ((size_t)j * (j + 1) / 2 + K) * kB;
+    s += src[r];
+  }
+  red[sl][threadIdx.x % kRedRows] = s;
+  __syncthreads();
+  if (sl == 0) {
+    double t = red[0][threadIdx.x];
+#pragma unroll
+    for (int q = 1; q < kRedSlices; ++q) t += red[q][threadIdx.x];
+    int i = K * kB + r;
+    if (i < n) y[i] = t;
+  }
 }
 
 long long padded_ld(int n) { return ((long long)n + 3) & ~3LL; }
@@ -411,7 +428,7 @@ static void ref_solve_impl(void* vp) {
       k_rhs<<<(n + 255) / 256, 256, 0, a.st>>>(n, M.ptr.p, M.idx.p, M.val.p, inv_dt, src, bc.p,
                                                vpad.p);
       k_sym_tiles<<<(unsigned)ntiles, 256, 0, a.st>>>(T.p, vpad.p, rowpart.p, colpart.p);
-      k_sym_reduce<<<(n + 255) / 256, 256, 0, a.st>>>(n, nbk, rowpart.p, colpart.p, dst);
+      k_sym_reduce<<<2 * nbk, kRedRows * kRedSlices, 0, a.st>>>(n, nbk, rowpart.p, colpart.p, dst);
       g_launches += 3;
     } else {
       k_gemv_rows<<<(n + 7) / 8, 256, 0, a.st>>>(n, ld, Rm, src, bc.p + n, dst);
