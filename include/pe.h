@@ -193,6 +193,18 @@ int pe_relative_error_series(int n, int d, const int* P_ptr, const int* P_idx,
                              const double* M_val, const double* ref, int K, const double* X,
                              double* norms_h, void* stream);
 
+/* Galerkin projection (projection part of the offline build):
+ * msbasis.py:545-567 project_coarse and :570-572 project_load.  P: host CSR (n x d) of
+ * hstack([Psi1, Psi2]), d = d1 + d2; M, A: host CSR (n x n).  Mc_h, Ac_h: host (d, d)
+ * row-major = P^T X P with the (1,1) and (2,2) blocks symmetrised ((B + B^T) / 2) and the
+ * off-diagonal blocks as computed (B12 = Psi1^T X Psi2).  b (n) / f_h (d) optional: P^T b.
+ * asym_h (2) optional: the removed asymmetry max |B - B^T| for M and A. */
+int pe_project_coarse(int n, int d1, int d2, const int* P_ptr, const int* P_idx,
+                      const double* P_val, const int* M_ptr, const int* M_idx,
+                      const double* M_val, const int* A_ptr, const int* A_idx,
+                      const double* A_val, const double* b, double* Mc_h, double* Ac_h,
+                      double* f_h, double* asym_h, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

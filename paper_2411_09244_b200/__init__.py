@@ -9,7 +9,7 @@ from ._lib import LIB_PATH, NativeUnavailable, PeError  # noqa: F401
 from .allatonce import (TimeMatrixB, WaveformRelaxation, WRResult,  # noqa: F401
                         build_time_matrix, wr_fine_solve)
 from .engine import PeContext  # noqa: F401
-from .msbasis import CoarseSystem  # noqa: F401
+from .msbasis import CoarseSystem, project_coarse, project_load  # noqa: F401
 from .parareal import (AllAtOnceFine, ParerealConfig, ParerealEnsemble,  # noqa: F401
                        ParerealRun,
                        SequentialFine, build_fine_propagator, check_stop, initial_sweep,

@@ -66,6 +66,8 @@ SIGNATURES = {
                                           C.c_int, C.c_int, _D, _F, _P]),
     "pe_relative_error_series": (C.c_int, [C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _D,
                                            C.c_int, _D, _D, _P]),
+    "pe_project_coarse": (C.c_int, [C.c_int, C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _I, _I,
+                                    _D, _D, _D, _D, _D, _D, _P]),
 }
 
 _lib = None

@@ -196,3 +196,28 @@ def test_gpu_error_edge_cases():
     bad = types.SimpleNamespace(M=sp.csr_matrix(np.eye(3)), A=sp.csr_matrix(-5 * np.eye(3)))
     with pytest.raises(PeError):
         fem.reference_solve(bad, np.ones(3), 1.0, 1)
+
+
+@pytest.mark.gpu
+def test_gpu_project_coarse_matches_reference_blocks():
+    """Galerkin projection (msbasis.py:545-572) against the reference's cfg0 CoarseSystem
+    (sys_cfg0.npz: M blocks as projected; A blocks projected then scaled by kappa_scale,
+    here the fine A is scaled first) and its loads: 1e-12 relative to the block's max."""
+    import paper_2411_09244_b200 as P
+
+    z, ops, space = _fixture()
+    ref = golden("sys_cfg0.npz")
+    cs = P.project_coarse(space.Psi1, space.Psi2, ops)
+    for k in ("M11", "A11", "M12", "A12", "M22", "A22"):
+        g, r = getattr(cs, k), ref[k]
+        assert g.shape == r.shape
+        assert np.abs(g - r).max() <= 1e-12 * np.abs(r).max(), k
+    assert np.array_equal(cs.M11, cs.M11.T) and np.array_equal(cs.A22, cs.A22.T)
+    f1, f2 = P.project_load(space, z["b"], ops)
+    np.testing.assert_allclose(f1, ref["f1"], rtol=1e-12, atol=1e-14 * np.abs(ref["f1"]).max())
+    np.testing.assert_allclose(f2, ref["f2"], rtol=1e-12, atol=1e-14 * np.abs(ref["f2"]).max())
+    # degenerate split (d2 = 0) and a bad basis
+    cs0 = P.project_coarse(sp.hstack([space.Psi1, space.Psi2]).tocsr(), sp.csr_matrix((ops.M.shape[0], 0)), ops)
+    assert cs0.M22.shape == (0, 0) and cs0.M11.shape == (64, 64)
+    with pytest.raises(ValueError):
+        P.project_coarse(space.Psi1[:-1], space.Psi2[:-1], ops)

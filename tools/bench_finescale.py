@@ -48,7 +48,13 @@ def main():
     ap.add_argument("--nx", type=int, nargs="+", default=[100, 256])
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--project", type=str, default="", help="nx:d:density[:gpuonly][,...] projection runs")
     args = ap.parse_args()
+    for spec in filter(None, args.project.split(",")):
+        nx, d, dens, *flag = spec.split(":")
+        bench_project(int(nx), int(d), float(dens), cpu=not flag)
+    if args.project:
+        return
     from paper_2411_09244_b200 import fem
     from oracle import pe_oracle as po
 
@@ -82,6 +88,38 @@ def main():
                               bytes_per_step=tm["bytes_per_step"], wall_s_incl_setup=wall,
                               cpu_splu_step_ms=cpu_ms, speedup_per_step=cpu_ms / step_ms,
                               rel_vs_splu=rel, final_norm=float(np.linalg.norm(st[1])))))
+
+
+
+def bench_project(nx, d, density, seed=0, cpu=True):
+    """GPU project_coarse vs the reference's sparse products (msbasis.py:552-562) on a
+    random basis of the given density (cfg3: d = 8192, ~13 % nonzero)."""
+    import paper_2411_09244_b200 as P
+
+    M, A, b = operators(nx)
+    n = M.shape[0]
+    psi = sp.random(n, d, density=density, random_state=seed, format="csc")
+    p1, p2 = psi[:, : d // 2], psi[:, d // 2:]
+    ops = types.SimpleNamespace(M=M, A=A)
+    P.project_coarse(p1[:, :8], p2[:, :8], ops)  # warm-up
+    t0 = time.perf_counter()
+    cs = P.project_coarse(p1, p2, ops)
+    gpu = time.perf_counter() - t0
+    if not cpu:
+        print(json.dumps(dict(kind="project_coarse", nx=nx, n=n, d=d, density=density,
+                              gpu_s_both_operators_incl_upload=gpu)))
+        return
+    t1 = time.perf_counter()
+    xp1, xp2 = M @ p1, M @ p2
+    b11 = (p1.T @ xp1).toarray()
+    b12 = (p1.T @ xp2).toarray()
+    b22 = (p2.T @ xp2).toarray()
+    cpu_m = time.perf_counter() - t1
+    err = max(np.abs(cs.M11 - (b11 + b11.T) / 2).max(), np.abs(cs.M12 - b12).max(),
+              np.abs(cs.M22 - (b22 + b22.T) / 2).max()) / np.abs(b11).max()
+    print(json.dumps(dict(kind="project_coarse", nx=nx, n=n, d=d, density=density,
+                          gpu_s_both_operators_incl_upload=gpu,
+                          cpu_s_mass_only_reference_sparse=cpu_m, rel_err_vs_sparse=float(err))))
 
 
 if __name__ == "__main__":
