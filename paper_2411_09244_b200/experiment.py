@@ -11,6 +11,7 @@ solution / reference node grids.  The accuracy numbers come from `fem.error_seri
 from __future__ import annotations
 
 import csv
+from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -83,3 +84,62 @@ def write_run_artifacts(out_dir, n, run, error_series=(), *, solution_grid=None,
     if reference_grid is not None:
         save_matrix_txt(path(f"reference_N{n}.txt"), reference_grid)
     return written
+
+
+# ------------------------------------------------------------------ run_single on the GPU
+
+
+@dataclass
+class RunResult:
+    """experiment.py:309-317."""
+
+    n: int
+    run: object
+    relative_error: float
+    error_series: list
+    reference_final: np.ndarray | None
+    stability_bound: float
+    dt_sub: float
+
+
+def run_single(pipe, n: int, *, stop_rule: str = "absolute") -> RunResult:
+    """One parareal run plus its Eq (31) accuracy series, all on the GPU
+    (experiment.py:328-360).
+
+    `pipe` is the reference's `Pipeline` (or any object with `config`, `space` (system,
+    Psi1, Psi2), `loads`, `ops`, `grid`): the offline build stays in the reference.  The
+    initial state is the projection of the zero fine field (`project_initial` of zeros is
+    exactly zero).  Only the time-grid fields of `pipe.config` are read, plus
+    `compute_reference` and `to_source()`.
+    """
+    import logging
+
+    from .fem import error_series, reference_solve
+    from .parareal import ParerealConfig, build_fine_propagator, run_parareal
+    from .stepping import ConstantLoads, SplitPropagators, SplitState, TimeGrid
+
+    cfg = pipe.config
+    tg = cfg.time_grid(n)
+    tg = TimeGrid(tg.t_end, tg.n_intervals, tg.substeps)
+    loads = ConstantLoads(*pipe.loads.at(0.0)) if hasattr(pipe.loads, "at") else pipe.loads
+    props = SplitPropagators(pipe.space.system, loads)
+    bound = props.stability_max_step()
+    if tg.dt_sub > bound:
+        logging.getLogger(__name__).warning(
+            "N=%d substep %.3e exceeds stability bound %.3e", n, tg.dt_sub, bound)
+    pconfig = ParerealConfig(time_grid=tg, alpha=cfg.alpha, epsilon=cfg.epsilon,
+                             k_max=cfg.k_max, fine_kind=cfg.fine_kind, workers=cfg.workers,
+                             stop_rule=stop_rule)
+    fine = build_fine_propagator(pconfig, props, loads)
+    s = pipe.space.system
+    initial = SplitState.fresh(np.zeros(s.M11.shape[0]), np.zeros(s.M22.shape[0]))
+    run = run_parareal(pconfig, props, fine, initial)
+    ref_final, err, series = None, float("nan"), []
+    if getattr(cfg, "compute_reference", False):
+        _, states = reference_solve(pipe.ops, cfg.to_source(), cfg.t_end,
+                                    tg.n_intervals * tg.substeps, keep_trajectory=False)
+        ref_final = states[-1]
+        series = error_series(pipe.ops, pipe.space, ref_final,
+                              [np.asarray(h)[-1] for h in run.history])
+        err = series[-1]
+    return RunResult(n, run, err, series, ref_final, bound, tg.dt_sub)

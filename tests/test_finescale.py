@@ -221,3 +221,30 @@ def test_gpu_project_coarse_matches_reference_blocks():
     assert cs0.M22.shape == (0, 0) and cs0.M11.shape == (64, 64)
     with pytest.raises(ValueError):
         P.project_coarse(space.Psi1[:-1], space.Psi2[:-1], ops)
+
+
+@pytest.mark.gpu
+def test_gpu_run_single_accuracy_matches_reference(tmp_path):
+    """experiment.run_single (experiment.py:328-360) on config 0: parareal iterations and
+    history as the reference run, error series as the reference's within 1e-10, and the
+    writers on its record."""
+    import paper_2411_09244_b200 as P
+    from paper_2411_09244_b200.experiment import run_single, write_run_artifacts
+
+    z, ops, space = _fixture()
+    sysz = golden("sys_cfg0.npz")
+    gold = golden("run_cfg0_seq.npz")
+    space.system = P.CoarseSystem(*[sysz[k] for k in ("M11", "A11", "M12", "A12", "M22", "A22")])
+    cfg = types.SimpleNamespace(time_grid=lambda n: P.TimeGrid(1.0, n, n), alpha=0.1,
+                                epsilon=1e-8, k_max=10, fine_kind="sequential", workers=1,
+                                compute_reference=True, to_source=lambda: z["b"], t_end=1.0)
+    pipe = types.SimpleNamespace(config=cfg, space=space, ops=ops,
+                                 loads=P.ConstantLoads(sysz["f1"], sysz["f2"]))
+    res = run_single(pipe, 10, stop_rule="relative")
+    assert res.run.iterations == int(gold["iterations"])
+    h = np.array(res.run.history)
+    assert max(_rel(a, b) for a, b in zip(h.reshape(len(h), -1), gold["history"].reshape(len(h), -1))) < 1e-10
+    np.testing.assert_allclose(res.error_series, z["series"], rtol=1e-10)
+    assert res.relative_error == res.error_series[-1] and res.dt_sub == 0.01
+    files = write_run_artifacts(tmp_path, 10, res.run, res.error_series)
+    assert len(files) == 3 and (tmp_path / "conv_N10.csv").read_text().startswith("iteration,")
