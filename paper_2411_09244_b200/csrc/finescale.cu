@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "pe.h"
+#include "mbar.cuh"
 #include "pe_internal.h"
 
 namespace pe {
@@ -277,6 +278,96 @@ __global__ void __launch_bounds__(256) k_sym_tiles(const double* __restrict__ T,
   }
 }
 
+
+// Persistent TMA-bulk variant of k_sym_tiles: one CTA per SM walks tiles t = blockIdx.x,
+// + gridDim.x, ...; each tile is two 64 KB half-tiles (64 rows), streamed global -> shared
+// by cp.async.bulk into a 3-stage ring (mbarrier complete_tx), so the next half-tiles are
+// in flight while the CTA reduces the current one.  Same sums as k_sym_tiles, fixed order.
+constexpr int kHalfRows = 64;
+constexpr int kStages = 3;
+constexpr unsigned kHalfBytes = kHalfRows * kB * sizeof(double);
+
+__global__ void __launch_bounds__(256, 1) k_sym_tiles_tma(const double* __restrict__ T,
+                                                          const double* __restrict__ v,
+                                                          int ntiles,
+                                                          double* __restrict__ rowpart,
+                                                          double* __restrict__ colpart) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);  // kStages x (64 x 64) double2
+  __shared__ __align__(8) unsigned long long full[kStages];
+  __shared__ double rowred[2][2][kHalfRows];
+  __shared__ double colred[4][kB];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int cp = tid & 63, rg = tid >> 6;  // column pair, 16-row group
+  const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int units = 2 * my_tiles;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(smem_u32(&full[s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int u) {
+    int t = blockIdx.x + (u >> 1) * gridDim.x;
+    const double* src = T + (size_t)t * kB * kB + (size_t)(u & 1) * kHalfRows * kB;
+    unsigned bar = smem_u32(&full[u % kStages]);
+    mbar_expect_tx(bar, kHalfBytes);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(buf + (size_t)(u % kStages) * kHalfRows * (kB / 2))), "l"(src),
+        "r"(kHalfBytes), "r"(bar)
+        : "memory");
+  };
+  if (tid == 0)
+    for (int u = 0; u < kStages && u < units; ++u) issue(u);
+  double c0 = 0.0, c1 = 0.0;
+  for (int u = 0; u < units; ++u) {
+    const int t = blockIdx.x + (u >> 1) * gridDim.x, h = u & 1;
+    const int I = tri_row(t), J = t - I * (I + 1) / 2;
+    mbar_wait_cta(smem_u32(&full[u % kStages]), (u / kStages) & 1);
+    const double2* tile = buf + (size_t)(u % kStages) * kHalfRows * (kB / 2);
+    const double2 vJ = reinterpret_cast<const double2*>(v + (size_t)J * kB)[cp];
+    const double* vI = v + (size_t)I * kB + h * kHalfRows + rg * 16;
+    if (h == 0) c0 = c1 = 0.0;
+    double rp[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double2 a = tile[(rg * 16 + r) * (kB / 2) + cp];
+      double vi = __ldg(vI + r);
+      c0 = fma(a.x, vi, c0);
+      c1 = fma(a.y, vi, c1);
+      rp[r] = fma(a.x, vJ.x, a.y * vJ.y);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) rp[i] += __shfl_xor_sync(0xffffffffu, rp[i], 16);
+#pragma unroll
+    for (int s2 = 8; s2 >= 1; s2 >>= 1) {
+      const bool up = lane & s2;
+#pragma unroll
+      for (int i = 0; i < s2; ++i) {
+        double send = up ? rp[i] : rp[i + s2];
+        double keep = up ? rp[i + s2] : rp[i];
+        rp[i] = keep + __shfl_xor_sync(0xffffffffu, send, s2);
+      }
+    }
+    if (lane < 16) rowred[u & 1][w & 1][rg * 16 + lane] = rp[0];
+    if (h == 1) {
+      colred[rg][2 * cp] = c0;
+      colred[rg][2 * cp + 1] = c1;
+    }
+    __syncthreads();  // stage u % kStages fully read; rowred / colred complete
+    if (tid == 0 && u + kStages < units) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(u + kStages);
+    }
+    if (tid < kHalfRows) {
+      rowpart[(size_t)t * kB + h * kHalfRows + tid] = rowred[u & 1][0][tid] + rowred[u & 1][1][tid];
+    } else if (h == 1 && tid >= kB && I != J) {
+      int c = tid - kB;
+      colpart[(size_t)t * kB + c] = ((colred[0][c] + colred[1][c]) + colred[2][c]) + colred[3][c];
+    }
+  }
+}
+
 // y(i) for the 64 rows of half a band K: 16 slices per row each sum a fixed strided subset
 // of the band's nb partial vectors (rowparts J <= K, then colparts I > K), coalesced over
 // rows; the slices are combined in a fixed order through shared memory.
@@ -396,6 +487,16 @@ static void ref_solve_impl(void* vp) {
   Dev<double> T(ntiles * kB * kB), rowpart(ntiles * kB), colpart(ntiles * kB),
       vpad(sym ? (size_t)nbk * kB : 0);
   double* Rm = K.p;
+  const bool tma = sym && !getenv("PE_FINE_NO_TMA");
+  int tma_grid = 0;
+  if (tma) {
+    int dev = 0, nsm = 0;
+    PE_CUDA_CHECK(cudaGetDevice(&dev));
+    PE_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    tma_grid = (int)std::min<size_t>((size_t)nsm, ntiles);
+    PE_CUDA_CHECK(cudaFuncSetAttribute(k_sym_tiles_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(kStages * kHalfBytes)));
+  }
   if (sym) {
     k_pack_tiles<<<(unsigned)ntiles, 256, 0, a.st>>>(n, ld, R.p, T.p);
     ++g_launches;
@@ -427,7 +528,11 @@ static void ref_solve_impl(void* vp) {
     if (sym) {
       k_rhs<<<(n + 255) / 256, 256, 0, a.st>>>(n, M.ptr.p, M.idx.p, M.val.p, inv_dt, src, bc.p,
                                                vpad.p);
-      k_sym_tiles<<<(unsigned)ntiles, 256, 0, a.st>>>(T.p, vpad.p, rowpart.p, colpart.p);
+      if (tma)
+        k_sym_tiles_tma<<<tma_grid, 256, kStages * kHalfBytes, a.st>>>(T.p, vpad.p, (int)ntiles,
+                                                                     rowpart.p, colpart.p);
+      else
+        k_sym_tiles<<<(unsigned)ntiles, 256, 0, a.st>>>(T.p, vpad.p, rowpart.p, colpart.p);
       k_sym_reduce<<<2 * nbk, kRedRows * kRedSlices, 0, a.st>>>(n, nbk, rowpart.p, colpart.p, dst);
       g_launches += 3;
     } else {
