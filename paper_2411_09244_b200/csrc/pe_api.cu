@@ -285,17 +285,22 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   // one waveform buffer per block, updated in place by the scans (each thread reads an
   // element before it overwrites it; stopped intervals are skipped, so they keep the
   // waveforms of their last sweep without any commit copy)
-  c->Yb[0].ensure(sizeof(double) * E * (J + 2) * L1 + 8);
-  c->Zb[0].ensure(sizeof(double) * E * (J + 2) * L2 + 8);
-  double* Yw = c->Yb[0].d();
-  double* Zw = c->Zb[0].d();
-  // working set per sweep ~8 arrays of E J d nc doubles (80 MB at cfg2, against a 126 MB
-  // L2): h reuses r~'s buffer (r~ is dead once the u scan has read it) and dY shares e_Z's
-  // (dY is dead once the h GEMM has read it; the w scan writes e_Z afterwards)
+  // working set per sweep: h reuses r~'s buffer (r~ is dead once the u scan has read it)
+  // and dY shares e_Z's (dY is dead once the h GEMM has read it; the w scan writes e_Z
+  // afterwards).  The six sweep arrays are one arena (~60 MB at cfg2).
   const long long Lm = std::max(L1, L2);
-  c->R.ensure(sizeof(double) * E * J * Lm + 8);
-  c->DW.ensure(sizeof(double) * E * J * L2 + 8);  // DZ
-  c->EYZ.ensure(sizeof(double) * E * J * (L1 + Lm) + 8);
+  auto al = [](long long n) { return (n + 31) & ~31LL; };  // 256-byte aligned sub-arrays
+  const long long nEY = al(E * J * L1), nEZ = al(E * J * Lm), nR = al(E * J * Lm),
+                  nDZ = al(E * J * L2), nY = al(E * (J + 2) * L1), nZ = al(E * (J + 2) * L2);
+  const size_t arena_bytes = sizeof(double) * (size_t)(nEY + nEZ + nR + nDZ + nY + nZ) + 256;
+  c->EYZ.ensure(arena_bytes);
+  double* EY = c->EYZ.d();
+  double* EZ = EY + nEY;
+  double* Rb = EZ + nEZ;  // r~, then h
+  double* DZ = Rb + nR;
+  double* Yw = DZ + nDZ;
+  double* Zw = Yw + nY;
+  double* DYb = EZ;  // dY, then e_Z
   c->Y0m.ensure(sizeof(double) * E * L1 + 8);
   c->Z0.ensure(sizeof(double) * E * L2 + 8);
   c->nrmp.ensure(sizeof(double) * (size_t)(g1 + g2) * E * NJ + 8);
@@ -312,11 +317,6 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   c->stats = FineStats();
   WrColumnState* cs = (WrColumnState*)c->colstate.p;
   int* cnt = c->counter.i();
-  double* EY = c->EYZ.d();
-  double* EZ = EY + E * J * L1;
-  double* Rb = c->R.d();  // r~, then h
-  double* DYb = EZ;       // dY, then e_Z
-  double* DZ = c->DW.d();
 
   // seeds: y0 = V1^-1 u0, z0 = V2^-1 w0 (X_in: (E, nc, d))
   wr_state_init((long long)E * nc, cs, c->rhist.d(), max_iter, st);
