@@ -159,6 +159,8 @@ def test_gpu_reference_solve_packed_symmetric_path(m, monkeypatch):
     _, got = fem.reference_solve(ops, b, 0.02, 6, u0=u0)
     for r, g in zip(got, ref):
         assert _rel(r, g) < 1e-12
+    _, ends = fem.reference_solve(ops, b, 0.02, 6, u0=u0, keep_trajectory=False)
+    assert np.array_equal(ends[0], u0) and np.array_equal(ends[1], got[-1])  # same kernels
     monkeypatch.setenv("PE_FINE_NO_TMA", "1")  # per-tile CTAs instead of the TMA ring
     _, plain = fem.reference_solve(ops, b, 0.02, 6, u0=u0)
     assert _rel(plain[-1], got[-1]) < 1e-13
