@@ -52,6 +52,10 @@ struct Dev {
     }
   }
   ~Dev() { cudaFree(p); }
+  void reset() {
+    cudaFree(p);  // synchronises the device first
+    p = nullptr;
+  }
   Dev(const Dev&) = delete;
   Dev& operator=(const Dev&) = delete;
 };
@@ -482,6 +486,10 @@ static void ref_solve_impl(void* vp) {
   k_gemv_rows<<<(n + 7) / 8, 256, 0, a.st>>>(n, ld, R.p, bc.p, nullptr, bc.p + n);
   ++g_launches;
   const bool sym = n >= kSymMin && !getenv("PE_FINE_NO_SYM");
+  if (sym) {  // the factor is dead once K^-1 and c exist
+    PE_CUDA_CHECK(cudaStreamSynchronize(a.st));
+    K.reset();
+  }
   const int nbk = (n + kB - 1) / kB;
   const size_t ntiles = sym ? (size_t)nbk * (nbk + 1) / 2 : 0;
   Dev<double> T(ntiles * kB * kB), rowpart(ntiles * kB), colpart(ntiles * kB),
@@ -501,6 +509,8 @@ static void ref_solve_impl(void* vp) {
     k_pack_tiles<<<(unsigned)ntiles, 256, 0, a.st>>>(n, ld, R.p, T.p);
     ++g_launches;
     PE_CUDA_CHECK(cudaMemsetAsync(vpad.p, 0, sizeof(double) * nbk * kB, a.st));
+    PE_CUDA_CHECK(cudaStreamSynchronize(a.st));
+    R.reset();  // the steps read only the packed tiles (n^2 / 2)
   } else {
     dim3 gR((n + 255) / 256 < 8 ? (n + 255) / 256 : 8, n);
     k_form_R<<<gR, 256, 0, a.st>>>(n, ld, R.p, M.ptr.p, M.idx.p, M.val.p, inv_dt, K.p);
