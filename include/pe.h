@@ -205,6 +205,12 @@ int pe_project_coarse(int n, int d1, int d2, const int* P_ptr, const int* P_idx,
                       const double* A_val, const double* b, double* Mc_h, double* Ac_h,
                       double* f_h, double* asym_h, void* stream);
 
+/* Load-only projection f = P^T b (msbasis.py:570-572 project_load), without the operator
+ * products.  P: host CSC (n x d) of hstack([Psi1, Psi2]) (column pointers d + 1, row
+ * indices, values); b (n) host; f_h (d) host.  One warp per column, fixed order. */
+int pe_project_load(int n, int d, const int* P_colptr, const int* P_rowidx, const double* P_val,
+                    const double* b, double* f_h, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

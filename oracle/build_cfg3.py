@@ -7,8 +7,10 @@ aux-eigenproblem cache (boundary blocks of a range are solved twice, which is ha
 `aux_eigen_cem` is deterministic).  Columns are stacked in ascending block order exactly
 as `make_golden.build_system` does, then `project_coarse` and the F2 rescaling.
 
-Output: data/sys_cfg3.npz (zlib-compressed: the blocks are 13 % nonzero, 110 MB instead of
-0.8 GB; git-ignored; travels to the GPU box with gpurun, whose snapshot limit is 512 MiB).
+Output: data/cfg3/ (committed): one packed file per block (paper_2411_09244_b200.sysdata:
+nonzero mask + byte-shuffled zlib values, upper triangle of the symmetric blocks; the
+blocks are 13 % nonzero, 63 MB in total instead of 0.8 GB dense) plus loads.npz with the
+loads and the build meta.  Decoding is bitwise exact.
 """
 
 from __future__ import annotations
@@ -109,10 +111,11 @@ def main():
     meta = dict(name=CFG, contrast=contrast, kappa_scale=scale, bound_before=bound,
                 dt_over_bound=R_STABILITY, d1=d1, d2=d2, n_rects=n_rects,
                 build_seconds=build_s, workers=workers)
-    os.makedirs("data", exist_ok=True)
-    np.savez_compressed("data/sys_cfg3.npz", M11=system.M11, A11=scale * system.A11, M12=system.M12,
-             A12=scale * system.A12, M22=system.M22, A22=scale * system.A22, f1=f1, f2=f2,
-             meta=json.dumps(meta))
+    from paper_2411_09244_b200.sysdata import save_system
+
+    blocks = dict(M11=system.M11, A11=scale * system.A11, M12=system.M12,
+                  A12=scale * system.A12, M22=system.M22, A22=scale * system.A22)
+    save_system(os.path.join("data", "cfg3"), blocks, f1, f2, meta, split=True)
     print(json.dumps(meta))
 
 

@@ -6,8 +6,9 @@ Member m uses default_rng(m) for the contrast 10^U(2,8), 8 channel rows and 10 %
 per-member diffusion rescaling c_m; N = J = 32, T = 1; sequential fine
 solver; relative 1e-8 stop (F5).
 
-Output: data/cfg4_members.npz (stacked operators + per-member meta) and
-data/cfg4_runs.npz (reference iteration counts of all members, full histories of four).
+Output (committed): data/cfg4/mNN.npz, one packed system per member
+(paper_2411_09244_b200.sysdata, bitwise-exact decoding) with its meta, and
+data/cfg4/runs.npz (reference iteration counts of all members, full histories of four).
 """
 
 import json
@@ -47,18 +48,19 @@ def main():
             print(f"member {out[0]} iterations {out[5]} contrast {out[4]['contrast']:.3g} "
                   f"({time.time() - t0:.0f} s)", flush=True)
     res.sort(key=lambda x: x[0])
-    os.makedirs(os.path.join(ROOT, "data"), exist_ok=True)
-    stacked = {k: np.stack([r[1][k] for r in res]) for k in res[0][1]}
-    np.savez_compressed(os.path.join(ROOT, "data", "cfg4_members.npz"),
-                        f1=np.stack([r[2] for r in res]), f2=np.stack([r[3] for r in res]),
-                        meta=json.dumps([r[4] for r in res]), **stacked)
+    from paper_2411_09244_b200.sysdata import save_system
+
+    out = os.path.join(ROOT, "data", "cfg4")
+    os.makedirs(out, exist_ok=True)
+    for r in res:
+        save_system(os.path.join(out, f"m{r[0]:02d}.npz"), r[1], r[2], r[3], r[4])
     runs = {"iterations": np.array([r[5] for r in res]),
             "contrast": np.array([r[4]["contrast"] for r in res]),
             "kappa_scale": np.array([r[4]["kappa_scale"] for r in res]),
             "ref_seconds": np.array([r[7] for r in res])}
     for m in HIST_MEMBERS:
         runs[f"hist_{m}"] = res[m][6]
-    np.savez_compressed(os.path.join(ROOT, "data", "cfg4_runs.npz"), **runs)
+    np.savez_compressed(os.path.join(out, "runs.npz"), **runs)
     print("iterations per member:", runs["iterations"].tolist())
 
 

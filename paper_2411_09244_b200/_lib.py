@@ -68,6 +68,7 @@ SIGNATURES = {
                                            C.c_int, _D, _D, _P]),
     "pe_project_coarse": (C.c_int, [C.c_int, C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _I, _I,
                                     _D, _D, _D, _D, _D, _D, _P]),
+    "pe_project_load": (C.c_int, [C.c_int, C.c_int, _I, _I, _D, _D, _D, _P]),
 }
 
 _lib = None

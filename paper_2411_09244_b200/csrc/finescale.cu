@@ -482,6 +482,14 @@ static void ref_solve_impl(void* vp) {
   ++g_launches;
   FS_SOLVER_CHECK(cusolverDnXpotrs(h, prm, CUBLAS_FILL_MODE_LOWER, n, n, CUDA_R_64F, K.p, ld,
                                    CUDA_R_64F, R.p, ld, info.p));
+  {
+    int hinfo = 0;
+    PE_CUDA_CHECK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, a.st));
+    PE_CUDA_CHECK(cudaStreamSynchronize(a.st));
+    if (hinfo != 0)
+      throw Error{PE_ERR_SOLVER, "potrs against the identity failed (info " +
+                                     std::to_string(hinfo) + ")"};
+  }
   // c = Kinv b; then R = Kinv M / dt, written over the factor's buffer
   k_gemv_rows<<<(n + 7) / 8, 256, 0, a.st>>>(n, ld, R.p, bc.p, nullptr, bc.p + n);
   ++g_launches;
@@ -526,7 +534,15 @@ static void ref_solve_impl(void* vp) {
     PE_CUDA_CHECK(cudaMemcpyAsync(U.p, a.u0, nb, cudaMemcpyHostToDevice, a.st));
   else
     PE_CUDA_CHECK(cudaMemsetAsync(U.p, 0, nb, a.st));
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  struct EventPair {  // destroyed on every exit path, including a thrown CUDA error
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ~EventPair() {
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+    }
+  } ev;
+  cudaEvent_t& e0 = ev.e0;
+  cudaEvent_t& e1 = ev.e1;
   if (a.step_ms) {
     PE_CUDA_CHECK(cudaEventCreate(&e0));
     PE_CUDA_CHECK(cudaEventCreate(&e1));
@@ -555,8 +571,6 @@ static void ref_solve_impl(void* vp) {
     PE_CUDA_CHECK(cudaEventRecord(e1, a.st));
     PE_CUDA_CHECK(cudaEventSynchronize(e1));
     PE_CUDA_CHECK(cudaEventElapsedTime(a.step_ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
   }
   if (a.keep) {
     PE_CUDA_CHECK(cudaMemcpy2DAsync(a.states_h, nb, U.p, ld * sizeof(double), nb, traj_rows,

@@ -46,6 +46,14 @@ static void require(bool ok, int code, const char* msg) {
 
 static void bind(pe_ctx* c) { PE_CUDA_CHECK(cudaSetDevice(c->device)); }
 
+// Graph-cache key entry for a double baked into captured kernel arguments: the exact IEEE
+// bit pattern, so any change of alpha / tol / dt (however small) forces a recapture.
+static const void* dkey(double v) {
+  uint64_t u;
+  std::memcpy(&u, &v, sizeof u);
+  return (const void*)(uintptr_t)u;
+}
+
 // Split-K workspace: partial planes + per-tile tickets that must start (and are left) zero.
 static void ensure_zeroed(DevBuf& b, size_t bytes) {
   if (bytes <= b.bytes) return;
@@ -450,8 +458,7 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
       (const void*)(intptr_t)4, c->Yb[0].p, c->Zb[0].p, c->R.p, c->DW.p, c->EYZ.p, c->nrmp.p, cs, c->rhist.p, cnt, c->pinned_count, c->RT.p,
       c->GT.p, c->f1t.p, c->cgt.p, c->acoef.p, c->cden.p, c->lam.p, c->Vcat.p, c->Ucat.p, c->colmax.p,
       c->wticket.p,
-      (const void*)(intptr_t)max_iter, (const void*)(intptr_t)(alpha * 1e6),
-      (const void*)(intptr_t)(tol * 1e18), (const void*)(intptr_t)(dt * 1e18)};
+      (const void*)(intptr_t)max_iter, dkey(alpha), dkey(tol), dkey(dt)};
   run_sweeps(c, nc, max_iter, key, body, st);
 
   // final waveforms in the original bases: U = V1 Y, W = V2 Z from each interval's buffer
@@ -708,7 +715,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
         c->rhist.p, cnt, host_cnt, c->splitws.p, c->Bk.p, c->RW.p, c->GW.p, c->Emat.p, c->Finv.p, c->Fw.p,
         c->M11dt.p, c->cg.p, c->f1.p, c->wticket.p, (const void*)(intptr_t)max_iter,
         (const void*)(intptr_t)(c->use_recur ? 1 : 0),
-        (const void*)(intptr_t)(alpha * 1e6), (const void*)(intptr_t)(tol * 1e18),
+        dkey(alpha), dkey(tol), dkey(c->wr_dt),
         (const void*)(intptr_t)nk, (const void*)(intptr_t)(modal ? 1 : 0), c->Vm.p, c->lam.p,
         c->GZ.p, c->cgz.p, c->Z0.p, c->Hz.p};
   run_sweeps(c, nc, max_iter, key, body, st);

@@ -104,7 +104,37 @@ __global__ void k_basis_dot(int n, long long ldp, int d, const double* __restric
   if (lane == 0) f[j] = s;
 }
 
+// f(j) = sum_t val[t] b[row[t]] over column j of a CSC matrix: one warp per column,
+// lane-strided partial sums combined in a fixed xor-shuffle order (deterministic).
+__global__ void k_csc_dot(int d, const int* __restrict__ cp, const int* __restrict__ ci,
+                          const double* __restrict__ cv, const double* __restrict__ b,
+                          double* __restrict__ f) {
+  int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= d) return;
+  double s = 0.0;
+  for (int t = cp[j] + lane; t < cp[j + 1]; t += 32) s = fma(cv[t], b[ci[t]], s);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) f[j] = s;
+}
+
 }  // namespace
+
+static void project_load_impl(int n, int d, const int* cp_h, const int* ci_h, const double* cv_h,
+                              const double* b_h, double* f_h, cudaStream_t st) {
+  const int nnz = cp_h[d];
+  DevP<int> cp(d + 1), ci(nnz);
+  DevP<double> cv(nnz), b(n), f(d);
+  up(cp.p, cp_h, d + 1, st);
+  up(ci.p, ci_h, nnz, st);
+  up(cv.p, cv_h, nnz, st);
+  up(b.p, b_h, n, st);
+  k_csc_dot<<<(d + 7) / 8, 256, 0, st>>>(d, cp.p, ci.p, cv.p, b.p, f.p);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+  PE_CUDA_CHECK(cudaMemcpyAsync(f_h, f.p, sizeof(double) * d, cudaMemcpyDeviceToHost, st));
+  PE_CUDA_CHECK(cudaStreamSynchronize(st));
+}
 
 struct ProjArgs {
   int n, d1, d2, nx;
@@ -208,6 +238,34 @@ extern "C" int pe_project_coarse(int n, int d1, int d2, const int* P_ptr, const 
     return e.code;
   } catch (const std::exception& e) {
     pe::set_error(std::string("pe_project_coarse: ") + e.what());
+    return PE_ERR_CUDA;
+  }
+}
+
+extern "C" int pe_project_load(int n, int d, const int* P_colptr, const int* P_rowidx,
+                               const double* P_val, const double* b, double* f_h, void* stream) {
+  if (n <= 0 || d <= 0 || !P_colptr || !b || !f_h || (P_colptr[d] > 0 && (!P_rowidx || !P_val))) {
+    pe::set_error("pe_project_load: need n > 0, d > 0 and buffers");
+    return PE_ERR_ARG;
+  }
+  for (int j = 0; j < d; ++j)
+    if (P_colptr[j + 1] < P_colptr[j]) {
+      pe::set_error("pe_project_load: column pointers must be non-decreasing");
+      return PE_ERR_ARG;
+    }
+  for (int t = 0; t < P_colptr[d]; ++t)
+    if (P_rowidx[t] < 0 || P_rowidx[t] >= n) {
+      pe::set_error("pe_project_load: row index out of range");
+      return PE_ERR_ARG;
+    }
+  try {
+    pe::project_load_impl(n, d, P_colptr, P_rowidx, P_val, b, f_h, (cudaStream_t)stream);
+    return PE_OK;
+  } catch (const pe::Error& e) {
+    pe::set_error("pe_project_load: " + e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    pe::set_error(std::string("pe_project_load: ") + e.what());
     return PE_ERR_CUDA;
   }
 }

@@ -121,7 +121,17 @@ def run_single(pipe, n: int, *, stop_rule: str = "absolute") -> RunResult:
     cfg = pipe.config
     tg = cfg.time_grid(n)
     tg = TimeGrid(tg.t_end, tg.n_intervals, tg.substeps)
-    loads = ConstantLoads(*pipe.loads.at(0.0)) if hasattr(pipe.loads, "at") else pipe.loads
+    loads = pipe.loads
+    if not getattr(loads, "constant", False):
+        # the reference's Pipeline loads are ConstantLoads; anything time-dependent goes
+        # through the same check as SplitPropagators / WaveformRelaxation
+        raise NotImplementedError("run_single: libpe supports time-constant loads "
+                                  "(ConstantLoads); got %r" % type(loads).__name__)
+    loads = ConstantLoads(*loads.at(0.0))
+    if getattr(cfg, "compute_reference", False):
+        from .fem import check_reference_size
+
+        check_reference_size(pipe.ops.M.shape[0])
     props = SplitPropagators(pipe.space.system, loads)
     bound = props.stability_max_step()
     if tg.dt_sub > bound:

@@ -64,6 +64,18 @@ def _load_vector(ops, source, n):
     return b
 
 
+MAX_REFERENCE_NODES = 65535  # dense K^-1 formulation limit (finescale.cu)
+
+
+def check_reference_size(n: int) -> None:
+    """The GPU fine reference solve keeps a dense (packed) K^-1: above 65535 interior nodes
+    it would not fit.  Raised before any work, so `run_single` fails before its parareal run
+    rather than after it."""
+    if n > MAX_REFERENCE_NODES:
+        raise ValueError(f"fine reference solve supports at most {MAX_REFERENCE_NODES} interior "
+                         f"nodes (dense K^-1 formulation); this grid has {n}")
+
+
 def reference_solve(ops, source, t_end: float, n_steps: int, u0=None,
                     keep_trajectory: bool = True, *, stream=None, timing: dict | None = None):
     """Backward Euler on the full fine space: (M/dt + A) u_{n+1} = M u_n/dt + b.
@@ -72,8 +84,9 @@ def reference_solve(ops, source, t_end: float, n_steps: int, u0=None,
     step when `keep_trajectory`, otherwise the initial and final vectors and
     times = [0, t_end].  `timing`, if given, receives the device time of the step loop.
     """
-    lib = require_cuda()
     n = ops.M.shape[0]
+    check_reference_size(n)
+    lib = require_cuda()
     if n_steps <= 0 or not t_end > 0:
         raise ValueError("need n_steps > 0 and t_end > 0")
     mp, mi, mv = _csr(ops.M, n)

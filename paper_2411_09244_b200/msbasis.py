@@ -83,7 +83,27 @@ def project_coarse(psi1, psi2, ops, *, stream=None) -> CoarseSystem:
     return CoarseSystem(M11=m11, A11=a11, M12=m12, A12=a12, M22=m22, A22=a22)
 
 
-def project_load(space, b_fine, ops, *, stream=None):
-    """Coarse load pair (Psi1^T b, Psi2^T b) (msbasis.py:570-572)."""
-    _, _, f, _, d1 = _proj(space.Psi1, space.Psi2, ops, b=b_fine, stream=stream)
+def project_load(space, b_fine, ops=None, *, stream=None):
+    """Coarse load pair (Psi1^T b, Psi2^T b) (msbasis.py:570-572), same signature as the
+    reference (`ops` is accepted for backward compatibility and ignored).  One warp per
+    basis column over the CSC of [Psi1 Psi2] (`pe_project_load`); no operator products."""
+    import scipy.sparse as sp
+
+    from ._lib import check, require_cuda
+    from .fem import _dp, _ip, _stream_ptr
+
+    lib = require_cuda()
+    psi = sp.hstack([sp.csc_matrix(space.Psi1), sp.csc_matrix(space.Psi2)]).tocsc()
+    psi.sort_indices()
+    n, d = psi.shape
+    d1 = space.Psi1.shape[1]
+    b = np.ascontiguousarray(np.asarray(b_fine, dtype=float))
+    if b.shape != (n,):
+        raise ValueError(f"load has shape {b.shape}, expected ({n},)")
+    cp = np.ascontiguousarray(psi.indptr, dtype=np.int32)
+    ci = np.ascontiguousarray(psi.indices, dtype=np.int32)
+    cv = np.ascontiguousarray(psi.data, dtype=np.float64)
+    f = np.empty(d)
+    check(lib.pe_project_load(n, d, _ip(cp), _ip(ci), _dp(cv), _dp(b), _dp(f),
+                              _stream_ptr(stream)))
     return f[:d1].copy(), f[d1:].copy()

@@ -218,7 +218,9 @@ def test_gpu_project_coarse_matches_reference_blocks():
         assert g.shape == r.shape
         assert np.abs(g - r).max() <= 1e-12 * np.abs(r).max(), k
     assert np.array_equal(cs.M11, cs.M11.T) and np.array_equal(cs.A22, cs.A22.T)
-    f1, f2 = P.project_load(space, z["b"], ops)
+    f1, f2 = P.project_load(space, z["b"])  # reference signature (no ops)
+    g1, g2 = P.project_load(space, z["b"], ops)  # round-1 signature still accepted
+    assert np.array_equal(f1, g1) and np.array_equal(f2, g2)
     np.testing.assert_allclose(f1, ref["f1"], rtol=1e-12, atol=1e-14 * np.abs(ref["f1"]).max())
     np.testing.assert_allclose(f2, ref["f2"], rtol=1e-12, atol=1e-14 * np.abs(ref["f2"]).max())
     # degenerate split (d2 = 0) and a bad basis

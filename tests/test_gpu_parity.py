@@ -480,47 +480,71 @@ def test_large_d_streaming_coarse_and_parareal():
         assert rel_rows(np.array(run.history), np.array(ref["history"])) < REL
 
 
-def _data(name):
+def _packed(name):
+    """A committed packed system / member set under data/ (never skipped: the reference-
+    built operators of configs 3 and 4 ship with the repository)."""
+    import os
+
+    from paper_2411_09244_b200.sysdata import load_system
+    from tests.conftest import ROOT
+
+    path = os.path.join(ROOT, "data", name)
+    assert os.path.exists(path), f"data/{name} is missing (oracle/build_cfg3.py, build_cfg4.py)"
+    return load_system(path)
+
+
+def _cfg4_members():
     import os
 
     from tests.conftest import ROOT
 
-    path = os.path.join(ROOT, "data", name)
-    if not os.path.exists(path):
-        pytest.skip(f"data/{name} not built (oracle/build_cfg3.py / build_cfg4.py)")
-    return np.load(path)
+    P = _pkg()
+    systems, loads, metas = [], [], []
+    for m in range(64):
+        b, f1, f2, meta = _packed(os.path.join("cfg4", f"m{m:02d}.npz"))
+        systems.append(P.CoarseSystem(**b))
+        loads.append(P.ConstantLoads(f1, f2))
+        metas.append(meta)
+    return systems, loads, metas, np.load(os.path.join(ROOT, "data", "cfg4", "runs.npz"))
 
 
 def test_config3_sampled_intervals():
-    """BASELINE config 3 (d = 4096+4096, J = 100): WR on sampled iteration-1 intervals with
-    a 3-sweep cap equals the CPU oracle (full reference runs are infeasible)."""
+    """BASELINE config 3 (d = 4096+4096, N = 128, J = 100): full waveform-relaxation solves
+    (reference stop logic, 400-sweep cap) on sampled intervals of iteration 1 and of later
+    parareal iterations, against the CPU oracle's full solves on the same inputs
+    (oracle/make_cfg3_golden.py; a full reference run is infeasible): finals
+    within 1e-10 relative L2, sweep counts and stop reasons as the oracle's except where
+    the oracle stopped on its round-off floor (documented in DESIGN.md §4)."""
     P = _pkg()
-    z = _data("sys_cfg3.npz")
+    blocks, f1, f2, meta = _packed("cfg3")
     gz = golden("cfg3_sample.npz")
-    s, ld = _system(z)
+    s, ld = P.CoarseSystem(**blocks), P.ConstantLoads(f1, f2)
     J, N, T = 100, 128, 2.0
-    wr = P.WaveformRelaxation(s, J, T / N, 0.1, ld, tol=1e-12, max_iter=int(gz["sweeps"]))
+    wr = P.WaveformRelaxation(s, J, T / N, 0.1, ld, tol=1e-12, max_iter=int(gz["max_iter"]))
     d1 = s.d1
-    states = [P.SplitState.fresh(gz[f"x_{n}"][:d1], gz[f"x_{n}"][d1:], n * T / N)
-              for n in gz["sample"]]
-    res = wr.solve_all(states)
-    for n, r in zip(gz["sample"], res):
-        assert r.iterations == int(gz["sweeps"]) and r.stop_reason == "max_iter"
-        assert rel_rows(r.trajectory.final.stacked(), gz[f"final_{n}"]) < REL
-        assert rel_rows(r.trajectory.U[5], gz[f"U5_{n}"]) < REL
-        np.testing.assert_allclose(r.residuals, gz[f"res_{n}"], rtol=1e-8)
+    keys = ["it1"] + [k[:-2] for k in gz.files if k.startswith("k") and k.endswith("_x")]
+    for key in keys:
+        X = gz[f"{key}_x"]
+        res = wr.solve_all([P.SplitState.fresh(x[:d1], x[d1:]) for x in X], trajectories=False)
+        for i, r in enumerate(res):
+            assert rel_rows(r.trajectory.final.stacked(), gz[f"{key}_final"][i]) < REL, (key, i)
+            ref_sw, ref_reason = int(gz[f"{key}_sweeps"][i]), str(gz[f"{key}_reasons"][i])
+            if ref_reason == "floor":
+                # the oracle's round-off floor (FFT + explicit complex inverses) sits just
+                # above tol; the modal sweep is more accurate and may run on to `tol`
+                assert r.stop_reason in ("floor", "tol") and abs(r.iterations - ref_sw) <= 0.25 * ref_sw
+            else:
+                assert (r.iterations, r.stop_reason) == (ref_sw, ref_reason), (key, i)
+                n = min(len(r.residuals), 50)
+                np.testing.assert_allclose(r.residuals[:n], gz[f"{key}_resid"][i][:n], rtol=1e-6)
 
 
 def test_config4_ensemble_iterations_and_histories():
     """BASELINE config 4: 64 members (contrast 1e2..1e8) in one batch; every member's
     parareal iteration count equals the reference's, four members' histories within 1e-10."""
     P = _pkg()
-    zm = _data("cfg4_members.npz")
-    zr = _data("cfg4_runs.npz")
-    E = zm["f1"].shape[0]
-    systems = [P.CoarseSystem(*(zm[k][m] for k in ("M11", "A11", "M12", "A12", "M22", "A22")))
-               for m in range(E)]
-    loads = [P.ConstantLoads(zm["f1"][m], zm["f2"][m]) for m in range(E)]
+    systems, loads, _, zr = _cfg4_members()
+    E = len(systems)
     d1, d2 = systems[0].d1, systems[0].d2
     cfg = P.ParerealConfig(time_grid=P.TimeGrid(1.0, 32, 32), alpha=0.1, epsilon=1e-8, k_max=32,
                            fine_kind="sequential", stop_rule="relative")
