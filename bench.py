@@ -39,9 +39,12 @@ FINE_TOL = 1e-12
 STOP_EPS = 1e-8  # relative-increment stop of BASELINE.json
 
 WORKLOADS = {
-    # BASELINE config 3; the reference's own 400-sweep WR cap (ParerealConfig.fine_max_iter)
+    # BASELINE config 3.  WR contracts at 0.943 per sweep here and needs ~502 sweeps to reach
+    # tol = 1e-12, so the reference's default 400-sweep cap (ParerealConfig.fine_max_iter)
+    # would stop every interval unconverged: the cap is raised to 600.
+    # Parareal itself needs ~50 iterations at this config, so the e2e leg runs a fixed 3.
     "cfg3-aao": dict(data="data/cfg3", T=2.0, N=128, J=100, kind="all-at-once", alpha=0.1,
-                     max_iter=400, golden="cfg3_sample.npz"),
+                     max_iter=600, golden="cfg3_sample.npz", e2e_iters=3),
     "cfg2-aao": dict(data="tests/golden/sys_cfg2.npz", T=1.0, N=64, J=64, kind="all-at-once",
                      alpha=0.1, max_iter=400, golden="run_cfg2_aao.npz"),
     "cfg2-seq": dict(data="tests/golden/sys_cfg2.npz", T=1.0, N=64, J=64, kind="sequential",
@@ -390,8 +393,9 @@ def parity_check(P, wl, ctx, system, loads, run_history, run_iterations, kind):
                         "run is infeasible at config 3 (SURVEY F7)",
                 "intervals": len(res), "max_rel_l2": max(res),
                 "sweeps_equal": f"{ok_sweeps}/{len(res)}",
-                "iterations_gpu": run_iterations,
-                "iterations_ref": None}
+                "iterations_gpu": None, "iterations_ref": None,
+                "iterations_note": "a full parareal run takes ~50 iterations of ~32 s on the GPU "
+                                   "(tools/cfg3_wr_probe.py) and is infeasible on the CPU"}
     if "history" in g and g["history"].ndim == 3:  # full reference run (cfg0/1/2)
         K = min(len(run_history), g["history"].shape[0])
         return {"what": "full parareal run vs the unmodified reference's run on the same inputs",
@@ -528,9 +532,12 @@ def gpu_arm(args, wl):
     step_avg = total_ms / args.steps
 
     # end to end through the public API: host initial state in, full host history out,
-    # run to the BASELINE stop rule (relative increment < 1e-8) -> the GPU iteration count
-    cfg = P.ParerealConfig(time_grid=P.TimeGrid(T, N, J), alpha=wl["alpha"], epsilon=STOP_EPS,
-                           k_max=min(N, 40), fine_kind=kind, fine_tol=FINE_TOL,
+    # run to the BASELINE stop rule (relative increment < 1e-8) -> the GPU iteration count;
+    # config 3 (~50 parareal iterations of ~32 s) runs a fixed number of iterations instead
+    fixed = wl.get("e2e_iters")
+    cfg = P.ParerealConfig(time_grid=P.TimeGrid(T, N, J), alpha=wl["alpha"],
+                           epsilon=0.0 if fixed else STOP_EPS,
+                           k_max=fixed or min(N, 40), fine_kind=kind, fine_tol=FINE_TOL,
                            fine_max_iter=max_iter, stop_rule="relative")
     zeros = P.SplitState.fresh(np.zeros(system.d1), np.zeros(system.d2))
     if dist:
@@ -541,13 +548,13 @@ def gpu_arm(args, wl):
 
         ops = LibpeShardOps(ctx, kind)
         t0 = time.perf_counter()
-        res = run_parareal_sharded(N, np.zeros(d), ops, cfg.k_max, STOP_EPS, "relative")
+        res = run_parareal_sharded(N, np.zeros(d), ops, cfg.k_max, cfg.epsilon, "relative")
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         K, hist = res["iterations"], list(res["history"])
         iters = K
         path = (f"paper_2411_09244_b200.run_parareal_sharded ({world} ranks, intervals sharded, "
-                "host arrays in/out, run to the relative 1e-8 stop)")
+                "host arrays in/out)")
     elif E == 1:
         props = P.SplitPropagators(system, loads)
         props._ctx[J] = ctx  # reuse the factorised context (setup stays out of e2e)
@@ -557,8 +564,7 @@ def gpu_arm(args, wl):
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         K, hist, iters = run.iterations, run.history, run.iterations
-        path = ("paper_2411_09244_b200.run_parareal (host arrays in/out, run to the relative "
-                "1e-8 stop)")
+        path = "paper_2411_09244_b200.run_parareal (host arrays in/out)"
     else:
         ens = P.ParerealEnsemble(cfg, systems, loads_l)  # setup stays out of e2e
         torch.cuda.synchronize()
@@ -574,7 +580,9 @@ def gpu_arm(args, wl):
     e2e = {"value": units * K / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": E * d * 8 / K,
            "d2h_bytes_per_step": E * ((K + 1) * (N + 1) * d * 8 + wr_bytes) / K,
-           "path": path, "iterations": K, "seconds": e2e_s}
+           "path": path, "iterations": K, "seconds": e2e_s,
+           "run": (f"fixed {fixed} iterations (epsilon 0)" if fixed else
+                   f"to the relative {STOP_EPS:g} stop")}
 
     line = None
     if rank == 0:

@@ -211,6 +211,37 @@ int pe_project_coarse(int n, int d1, int d2, const int* P_ptr, const int* P_idx,
 int pe_project_load(int n, int d, const int* P_colptr, const int* P_rowidx, const double* P_val,
                     const double* b, double* f_h, void* stream);
 
+/* ---- reference-API building blocks (api_ops.cu); device pointers unless noted ---- */
+
+/* apply_S (inverse = 0) / apply_S_inverse (inverse = 1) along the time axis
+ * (allatonce.py:74-88): x, y (J, ncols) row-major, planar real / imaginary parts (xi, yi
+ * may be NULL for a real input / a discarded imaginary output).  Direct DFT. */
+int pe_apply_S(int J, long long ncols, double alpha, int inverse, const double* xr,
+               const double* xi, double* yr, double* yi, void* stream);
+
+/* build_rhs (allatonce.py:136-158): rhs (J, d1) of the u all-at-once system from f1_rows
+ * (J, d1), u_start, u_final_prev (d1), w_start, w_lag (d2), w_rows_prev (J, d2) and the
+ * blocks M11 (d1 x d1), M12, A12 (d1 x d2), row-major. */
+int pe_build_rhs(int d1, int d2, int J, const double* M11, const double* M12, const double* A12,
+                 const double* f1_rows, const double* u_start, const double* w_start,
+                 const double* w_lag, const double* w_rows_prev, const double* u_final_prev,
+                 double dt, double alpha, double* rhs, void* stream);
+
+/* ImplicitAllAtOnce.solve (allatonce.py:112-133) on the context's all-at-once setup
+ * (pe_prepare_allatonce): solves (B kron M11 + I kron A11) u = rhs for nc right-hand
+ * sides per member.  R, U: (E, nc, J, d1).  resid (E * nc, optional): the relative
+ * residual ||(B kron M11 + I kron A11) u - rhs|| / ||rhs|| of each solve (:125-131). */
+int pe_allatonce_usolve(pe_ctx* ctx, const double* R, double* U, int nc, double* resid,
+                        void* stream);
+
+/* project_initial (stepping.py:216-226), host arrays: u = M11^-1 Psi1^T M u0 and
+ * w = M22^-1 Psi2^T M u0.  M: CSR (n x n); P: CSC (n x d) of hstack([Psi1, Psi2]);
+ * M11, M22 row-major; u0 (n); u_out (d1), w_out (d2).  LU with partial pivoting. */
+int pe_project_initial(int n, int d1, int d2, const int* M_ptr, const int* M_idx,
+                       const double* M_val, const int* P_colptr, const int* P_rowidx,
+                       const double* P_val, const double* M11, const double* M22,
+                       const double* u0, double* u_out, double* w_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -191,7 +191,11 @@ def make_config(name, workers=1):
             print("   wr sweeps", r["wr_iterations"].min(), r["wr_iterations"].max())
         if c["N"] >= 64:  # keep committed fixtures small: history is the parity target
             r.pop("fhat", None)
-            r.pop("wr_residuals", None)
+            res = r.pop("wr_residuals", None)
+            if res is not None:  # per-(k, n) WR residual histories: the stop-logic comparison
+                np.savez_compressed(os.path.join(OUT, f"run_{tag}_wr.npz"),
+                                    wr_iterations=r["wr_iterations"],
+                                    wr_reasons=r["wr_reasons"], wr_residuals=res)
         np.savez_compressed(os.path.join(OUT, f"run_{tag}.npz"), kind=kind,
                             **{k: v for k, v in r.items()})
 

@@ -6,8 +6,9 @@ Drop-in for the reference's online solver API; every solve runs in libpe
 """
 
 from ._lib import LIB_PATH, NativeUnavailable, PeError  # noqa: F401
-from .allatonce import (TimeMatrixB, WaveformRelaxation, WRResult,  # noqa: F401
-                        build_time_matrix, wr_fine_solve)
+from .allatonce import (ImplicitAllAtOnce, TimeMatrixB, WaveformRelaxation,  # noqa: F401
+                        WRResult, apply_S, apply_S_inverse, build_rhs, build_time_matrix,
+                        wr_fine_solve)
 from .engine import PeContext  # noqa: F401
 from .msbasis import CoarseSystem, project_coarse, project_load  # noqa: F401
 from .parareal import (AllAtOnceFine, ParerealConfig, ParerealEnsemble,  # noqa: F401
@@ -16,6 +17,6 @@ from .parareal import (AllAtOnceFine, ParerealConfig, ParerealEnsemble,  # noqa:
                        max_state_diff, run_parareal, run_parareal_ensemble)
 from .sharded import LibpeShardOps, run_parareal_sharded  # noqa: F401
 from .stepping import (ConstantLoads, SplitPropagators, SplitState,  # noqa: F401
-                       SplitTrajectory, TimeGrid, split_energy)
+                       SplitTrajectory, TimeGrid, project_initial, split_energy)
 
 __version__ = "0.1.0"

@@ -69,6 +69,12 @@ SIGNATURES = {
     "pe_project_coarse": (C.c_int, [C.c_int, C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _I, _I,
                                     _D, _D, _D, _D, _D, _D, _P]),
     "pe_project_load": (C.c_int, [C.c_int, C.c_int, _I, _I, _D, _D, _D, _P]),
+    "pe_apply_S": (C.c_int, [C.c_int, C.c_longlong, C.c_double, C.c_int, _P, _P, _P, _P, _P]),
+    "pe_build_rhs": (C.c_int, [C.c_int, C.c_int, C.c_int] + [_P] * 9 + [C.c_double, C.c_double,
+                                                                       _P, _P]),
+    "pe_allatonce_usolve": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
+    "pe_project_initial": (C.c_int, [C.c_int, C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _D, _D,
+                                     _D, _D, _D, _P]),
 }
 
 _lib = None

@@ -187,22 +187,108 @@ def _runs_from(res: dict, config: ParerealConfig, d1: int, kind: str, t_total: f
     return runs
 
 
-def _context_for(fine, propagators: SplitPropagators, tg: TimeGrid) -> PeContext:
+def _libpe_context(fine):
+    """The libpe context of a fine propagator built by this package, else None."""
     ctx = getattr(fine, "ctx", None)
-    if ctx is None:
-        raise TypeError("run_parareal needs a libpe fine propagator (SequentialFine / "
-                        "AllAtOnceFine from paper_2411_09244_b200)")
-    return ctx
+    return ctx if isinstance(ctx, PeContext) else None
+
+
+def _parallel_map(fn, items, workers: int = 1) -> list:
+    """Ordered map, optionally on a thread pool (util.py:12-23): results are merged in input
+    order, so the output does not depend on the worker count."""
+    items = list(items)
+    if workers <= 1 or len(items) <= 1:
+        return [fn(it) for it in items]
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        return list(pool.map(fn, items))
+
+
+def _run_parareal_plugin(config: ParerealConfig, propagators: SplitPropagators, fine,
+                         initial: SplitState) -> ParerealRun:
+    """`run_parareal` with a user fine propagator (the reference's duck-typed plugin
+    contract, parareal.py:53-106,191-193): any object with `propagate(state) -> (state,
+    info)`, optionally `propagate_all(states)` for a batch.  The fine sweep calls it once
+    per interval (through an ordered thread pool of `config.workers`, util.py:12-23) or
+    once per iteration with the batch; the initial coarse sweep, the correction
+    F + (G_new - G_old) and the convergence norm stay fused on the GPU (pe_coarse_correct),
+    one launch per iteration.  The stop rules and the record are those of the device loop."""
+    tg = config.time_grid
+    N, d1 = tg.n_intervals, propagators.system.d1
+    t_start = time.perf_counter()
+    ctx = propagators.context(tg.substeps)
+    ctx.prepare_coarse(tg.dt)
+    d = ctx.d
+    x0 = initial.stacked()
+    X = ctx.to_dev(np.zeros((1, N + 1, d)))
+    X[0, 0] = ctx.to_dev(x0)
+    G = ctx.empty(1, N, d)
+    diff = ctx.empty(1, 2)
+    ctx.coarse_correct(N, X, None, G, X)  # initial_sweep + cached G (parareal.py:178-179)
+    hist_rows = X[0].cpu().numpy()
+    history = [hist_rows.copy()]
+    times = [initial.t]  # state times as the reference carries them (t + dt per step)
+    for _ in range(N):
+        times.append(times[-1] + tg.dt)
+    max_diffs, fine_info, fine_seconds, coarse_seconds = [], [], [], []
+    converged = False
+    iterations = 0
+    for _ in range(config.k_max):
+        iterations += 1
+        tic = time.perf_counter()
+        states = [initial] + [SplitState.fresh(r[:d1], r[d1:], times[n])
+                              for n, r in enumerate(hist_rows[1:N], start=1)]
+        if hasattr(fine, "propagate_all"):
+            results = fine.propagate_all(states)
+        else:
+            results = _parallel_map(fine.propagate, states, config.workers)
+        fine_seconds.append(time.perf_counter() - tic)
+        fine_info.append([info for _, info in results])
+        times = [initial.t] + [st.t for st, _ in results]
+        tic = time.perf_counter()
+        F = ctx.to_dev(np.array([st.stacked() for st, _ in results])[None])
+        X_new = ctx.empty(1, N + 1, d)
+        ctx.coarse_correct(N, X, F, G, X_new, diff)
+        X = X_new
+        hist_rows = X[0].cpu().numpy()
+        dv = diff[0].cpu().numpy()
+        coarse_seconds.append(time.perf_counter() - tic)
+        history.append(hist_rows.copy())
+        v = float(dv[0]) if config.stop_rule == "absolute" else (
+            float(dv[0] / dv[1]) if dv[1] > 0 else float(dv[0]))
+        max_diffs.append(v)
+        if v < config.epsilon:
+            converged = True
+            break
+    run = ParerealRun(config=config, d1=d1, history=history, max_diffs=max_diffs,
+                      iterations=iterations, converged=converged, fine_info=fine_info,
+                      fine_seconds=fine_seconds, coarse_seconds=coarse_seconds,
+                      total_seconds=time.perf_counter() - t_start)
+    bad = run.wr_nonconverged()
+    if bad:
+        log.warning("fine solver hit max_iter on %d (iteration, interval) pairs", len(bad))
+    return run
 
 
 def run_parareal(config: ParerealConfig, propagators: SplitPropagators, fine,
                  initial: SplitState) -> ParerealRun:
-    """Full parareal run on the device; deterministic (fixed reduction order)."""
+    """Full parareal run on the device; deterministic (fixed reduction order).
+
+    `fine` is a propagator from `build_fine_propagator` (the whole loop then runs
+    device-resident in libpe, one host sync per iteration) or any user object following
+    the reference's fine-propagator contract (`propagate(state) -> (state, info)`); the
+    latter is called per interval and the coarse sweep / correction / norm run on the GPU.
+    """
     if config.stop_rule not in ("absolute", "relative"):
         raise ValueError(f"unknown stop rule {config.stop_rule!r}")
+    ctx = _libpe_context(fine)
+    if ctx is None:
+        if not callable(getattr(fine, "propagate", None)):
+            raise TypeError("fine propagator needs a propagate(state) -> (state, info) method")
+        return _run_parareal_plugin(config, propagators, fine, initial)
     tg = config.time_grid
     t0 = time.perf_counter()
-    ctx = _context_for(fine, propagators, tg)
     ctx.prepare_coarse(tg.dt)
     if fine.kind == "sequential":
         ctx.prepare_sequential(tg.dt_sub)

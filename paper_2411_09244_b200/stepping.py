@@ -195,6 +195,41 @@ class SplitPropagators:
             log.warning("substep %.3e exceeds stability bound %.3e", dt, bound)
 
 
+def project_initial(u0_fine, space, ops, *, stream=None) -> SplitState:
+    """Mass-orthogonal projection of a fine initial value onto each subspace
+    (stepping.py:216-226): M11 u = Psi1^T M u0, M22 w = Psi2^T M u0, lags equal to the
+    projections.  On the GPU (pe_project_initial): CSR SpMV, one warp per basis column,
+    LU solves of the two coarse mass blocks."""
+    import ctypes as C
+
+    import scipy.sparse as sp
+
+    from ._lib import check, require_cuda
+    from .fem import _csr, _dp, _ip, _stream_ptr
+
+    lib = require_cuda()
+    s = space.system
+    d1, d2 = s.M11.shape[0], s.M22.shape[0]
+    n = ops.M.shape[0]
+    u0 = np.ascontiguousarray(np.asarray(u0_fine, dtype=float))
+    if u0.shape != (n,):
+        raise ValueError(f"u0 has shape {u0.shape}, expected ({n},)")
+    mp, mi, mv = _csr(ops.M, n)
+    psi = sp.hstack([sp.csc_matrix(space.Psi1), sp.csc_matrix(space.Psi2)]).tocsc()
+    psi.sort_indices()
+    cp = np.ascontiguousarray(psi.indptr, dtype=np.int32)
+    ci = np.ascontiguousarray(psi.indices, dtype=np.int32)
+    cv = np.ascontiguousarray(psi.data, dtype=np.float64)
+    m11 = np.ascontiguousarray(s.M11, dtype=float)
+    m22 = np.ascontiguousarray(s.M22, dtype=float)
+    u, w = np.zeros(d1), np.zeros(d2)
+    check(lib.pe_project_initial(n, d1, d2, _ip(mp), _ip(mi), _dp(mv), _ip(cp), _ip(ci),
+                                 _dp(cv), _dp(m11) if d1 else None, _dp(m22) if d2 else None,
+                                 _dp(u0), _dp(u) if d1 else None, _dp(w) if d2 else None,
+                                 _stream_ptr(stream)))
+    return SplitState.fresh(u, w, 0.0)
+
+
 def split_energy(system: CoarseSystem, state: SplitState) -> float:
     """Squared fine-space L2 norm of the represented function (stepping.py:229-232)."""
     x = state.stacked()

@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "pe.h")
 def header_functions():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(pe_[a-z0-9_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(pe_[A-Za-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol():
