@@ -219,28 +219,104 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
 // active-interval count, so the device never waits on the host; the extra sweep after the
 // last interval stopped is fully masked.  `key` lists every pointer / value baked into the
 // nodes, so any reallocation or re-setup forces a recapture.
+//
+// Device loop (`loop_ok`: the body takes the conditional handle, modal path): the whole
+// solve is ONE graph launch, a conditional while-node around one captured sweep whose
+// decide kernel sets the condition to "some interval still iterating" -- no host round trip
+// per sweep and no speculative sweep after the last one.  Falls back to the pipelined host
+// loop if the driver rejects the conditional graph.
 template <class Body>
 static void run_sweeps(pe_ctx* c, int nc, int max_iter, const std::vector<const void*>& key,
-                       Body&& body, cudaStream_t st) {
+                       Body&& body, cudaStream_t st, bool loop_ok = false,
+                       const int* dev_sweeps = nullptr) {
   int* host_cnt = c->pinned_count;
   static const bool no_graphs = getenv("PE_NO_GRAPHS") != nullptr;
+  static const bool no_loop = getenv("PE_NO_DEVICE_LOOP") != nullptr;
   const bool graphs = c->use_graphs && !c->profiling && !no_graphs &&
                       getenv("PE_RECUR_TRACE") == nullptr;
   SweepGraphs* sg = nullptr;
-  if (graphs) {
+  if (graphs && loop_ok && c->device_loop && !no_loop) {
     sg = &c->sweep_graphs[nc];
-    if (sg->key != key) {
+    if (sg->key != key || !sg->loop) {
       for (auto& ex : sg->exec)
         if (ex) {
           cudaGraphExecDestroy(ex);
           ex = nullptr;
         }
+      if (sg->loop) {
+        cudaGraphExecDestroy(sg->loop);
+        sg->loop = nullptr;
+      }
+      const long long launches_before = g_launches;
+      bool ok = true;
+      cudaGraph_t g = nullptr;
+      try {
+        PE_CUDA_CHECK(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        PE_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        PE_CUDA_CHECK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+        cudaGraph_t bg = cp.conditional.phGraph_out[0];
+        PE_CUDA_CHECK(cudaStreamBeginCaptureToGraph(c->work, bg, nullptr, nullptr, 0,
+                                                    cudaStreamCaptureModeThreadLocal));
+        try {
+          body(0, c->work, h, 1);
+        } catch (...) {
+          cudaStreamEndCapture(c->work, &bg);
+          throw;
+        }
+        PE_CUDA_CHECK(cudaStreamEndCapture(c->work, &bg));
+        PE_CUDA_CHECK(cudaGraphInstantiate(&sg->loop, g, 0));
+      } catch (const Error&) {
+        ok = false;
+        cudaGetLastError();
+        if (sg->loop) cudaGraphExecDestroy(sg->loop);
+        sg->loop = nullptr;
+      }
+      if (g) cudaGraphDestroy(g);
+      sg->kernels = (int)(g_launches - launches_before);
+      g_launches = launches_before;
+      if (!ok) {
+        c->device_loop = false;  // this driver rejects it: pipelined host loop from now on
+        sg->key.clear();
+        run_sweeps(c, nc, max_iter, key, body, st, false, nullptr);
+        return;
+      }
+      sg->key = key;
+    }
+    PE_CUDA_CHECK(cudaGraphLaunch(sg->loop, st));
+    if (dev_sweeps) {  // launch evidence: kernels per sweep x sweeps run
+      PE_CUDA_CHECK(cudaMemcpyAsync(host_cnt, dev_sweeps, sizeof(int), cudaMemcpyDeviceToHost, st));
+      PE_CUDA_CHECK(cudaStreamSynchronize(st));
+      g_launches += (long long)sg->kernels * host_cnt[0];
+    } else {
+      PE_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    return;
+  }
+  if (graphs) {
+    sg = &c->sweep_graphs[nc];
+    if (sg->key != key || sg->loop) {
+      for (auto& ex : sg->exec)
+        if (ex) {
+          cudaGraphExecDestroy(ex);
+          ex = nullptr;
+        }
+      if (sg->loop) {
+        cudaGraphExecDestroy(sg->loop);
+        sg->loop = nullptr;
+      }
       const long long launches_before = g_launches;  // capture launches nothing
       for (int par = 0; par < 2; ++par) {
         cudaGraph_t g;
         PE_CUDA_CHECK(cudaStreamBeginCapture(c->work, cudaStreamCaptureModeThreadLocal));
         try {
-          body(par, c->work);
+          body(par, c->work, cudaGraphConditionalHandle(0), 0);
         } catch (...) {
           cudaStreamEndCapture(c->work, &g);
           throw;
@@ -262,7 +338,7 @@ static void run_sweeps(pe_ctx* c, int nc, int max_iter, const std::vector<const 
       PE_CUDA_CHECK(cudaGraphLaunch(sg->exec[sweep & 1], st));
       g_launches += c->graph_kernels;
     } else {
-      body(sweep & 1, st);
+      body(sweep & 1, st, cudaGraphConditionalHandle(0), 0);
     }
     PE_CUDA_CHECK(cudaEventRecord(ev[sweep & 1], st));
     collect_profile(c, st);
@@ -318,7 +394,7 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   c->Wx_new.ensure(sizeof(double) * E * (J + 2) * L2 + 8);
   c->colstate.ensure(sizeof(WrColumnState) * E * nc + 8);
   c->rhist.ensure(sizeof(double) * (size_t)E * nc * max_iter + 8);
-  c->counter.ensure(sizeof(int) * 2);
+  c->counter.ensure(sizeof(int) * 4);
   ensure_zeroed(c->wticket, sizeof(unsigned) * (size_t)E * nc + 8);  // self-resetting ticket
   c->colmax.ensure(sizeof(unsigned long long) * 2 * (size_t)E * nc + 8);
   PE_CUDA_CHECK(cudaMemsetAsync(c->colmax.p, 0, c->colmax.bytes, st));
@@ -434,7 +510,7 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     nu_m = nw_m = NJ;
   }
 
-  auto body = [&](int par, cudaStream_t s) {
+  auto body = [&](int par, cudaStream_t s, cudaGraphConditionalHandle h, int loop) {
     run_gemm(c, rhs_params(Zw), s);
     profiled_other(c, s, [&] {
       modal_uscan(E, nc, d1, J, dt, alpha, c->acoef.d(), c->cden.d(), Rb, Yw, Yw, DYb, EY, cs,
@@ -449,17 +525,19 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     profiled_other(c, s, [&] {
       modal_decide(E, nc, d1, d2, J, nu, nu_g, nu_m, nw, nw_g, nw_m,
                    (unsigned long long*)c->colmax.p, (unsigned*)c->wticket.p, cs, tol, max_iter,
-                   c->rhist.d(), cnt + par, 0, s);
+                   c->rhist.d(), cnt + par, 0, s, h, loop);
     });
-    PE_CUDA_CHECK(cudaMemcpyAsync(c->pinned_count + par, cnt + par, sizeof(int),
-                                  cudaMemcpyDeviceToHost, s));
+    if (!loop)
+      PE_CUDA_CHECK(cudaMemcpyAsync(c->pinned_count + par, cnt + par, sizeof(int),
+                                    cudaMemcpyDeviceToHost, s));
   };
   const std::vector<const void*> key = {
       (const void*)(intptr_t)4, c->Yb[0].p, c->Zb[0].p, c->R.p, c->DW.p, c->EYZ.p, c->nrmp.p, cs, c->rhist.p, cnt, c->pinned_count, c->RT.p,
       c->GT.p, c->f1t.p, c->cgt.p, c->acoef.p, c->cden.p, c->lam.p, c->Vcat.p, c->Ucat.p, c->colmax.p,
       c->wticket.p,
       (const void*)(intptr_t)max_iter, dkey(alpha), dkey(tol), dkey(dt)};
-  run_sweeps(c, nc, max_iter, key, body, st);
+  PE_CUDA_CHECK(cudaMemsetAsync(cnt + 2, 0, sizeof(int), st));
+  run_sweeps(c, nc, max_iter, key, body, st, true, cnt + 2);
 
   // final waveforms in the original bases: U = V1 Y, W = V2 Z from each interval's buffer
   basis_gemm(d1, c->Vcat.d(), Yw, d1, (J + 2) * L1, c->Ux_cur.d(), (J + 2) * L1,
@@ -689,7 +767,7 @@ static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc,
 
   // One sweep = ~10 launches (+ J GEMMs when the w recursion does not fit a cluster).
   int* host_cnt = c->pinned_count;
-  auto body = [&](int par, cudaStream_t s) {
+  auto body = [&](int par, cudaStream_t s, cudaGraphConditionalHandle, int) {
     PE_CUDA_CHECK(cudaMemsetAsync(cnt + par, 0, sizeof(int), s));
     for (auto& p : pre) run_gemm(c, p, s);
     if (d1) wr_diff_u(E, nc, d1, J, Un, c->DU.d(), s);
@@ -803,9 +881,11 @@ int pe_destroy(pe_ctx* c) {
   if (c->blas) cublasDestroy(c->blas);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->setup_stream) cudaStreamDestroy(c->setup_stream);
-  for (auto& kv : c->sweep_graphs)
+  for (auto& kv : c->sweep_graphs) {
     for (auto ex : kv.second.exec)
       if (ex) cudaGraphExecDestroy(ex);
+    if (kv.second.loop) cudaGraphExecDestroy(kv.second.loop);
+  }
   if (c->work) cudaStreamDestroy(c->work);
   if (c->pinned_count) cudaFreeHost(c->pinned_count);
   if (c->pinned_diff) cudaFreeHost(c->pinned_diff);

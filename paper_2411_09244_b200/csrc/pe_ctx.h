@@ -44,6 +44,7 @@ struct DevBuf {
 struct SweepGraphs {
   std::vector<const void*> key;
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  cudaGraphExec_t loop = nullptr;  // whole WR solve: one while-node around one sweep
   int kernels = 0;  // kernel launches recorded per captured sweep
 };
 
@@ -93,6 +94,7 @@ struct pe_ctx {
   pe::DevBuf partial, diff, Gc, active, hist_tmp, nrm, rhist, splitws;
   cudaStream_t work = nullptr;           // capture stream for the sweep graphs
   bool use_graphs = true;
+  bool device_loop = true;  // WR sweep loop as a conditional while-node (modal path)
   int graph_kernels = 0;   // kernels per captured sweep (launch accounting)
   std::map<int, pe::SweepGraphs> sweep_graphs;  // keyed by interval count
   int* pinned_count = nullptr;

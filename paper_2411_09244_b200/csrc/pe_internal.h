@@ -150,7 +150,7 @@ void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long l
                   long long nu_m, const double* nw, long long nw_g, long long nw_m,
                   unsigned long long* colmax, unsigned* ticket, WrColumnState* cs, double tol,
                   int max_iter, double* resid_hist, int* active_count, int par_new,
-                  cudaStream_t st);
+                  cudaStream_t st, cudaGraphConditionalHandle cond = 0, int use_cond = 0);
 
 void sub(long long n, const double* a, const double* b, double* out, cudaStream_t st);
 

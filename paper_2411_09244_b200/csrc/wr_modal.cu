@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(DECIDE_THREADS)
                         long long nu_g, long long nu_m, const double* __restrict__ nw,
                         long long nw_g, long long nw_m, unsigned long long* colmax,
                         unsigned* ticket, WrColumnState* cs, double tol, int max_iter,
-                        double* resid_hist, int* active_count, int par_new) {
+                        double* resid_hist, int* active_count, int par_new,
+                        cudaGraphConditionalHandle cond, int use_cond) {
   pdl_enter();
   const long long NJ = (long long)J * nc, per = (long long)E * NJ;
   const int gu = (d1 + 7) / 8, gw = (d2 + 7) / 8;
@@ -289,19 +290,27 @@ __global__ void __launch_bounds__(DECIDE_THREADS)
     }
     still += __syncthreads_count(go);
   }
-  if (threadIdx.x == 0) *active_count = still;
+  if (threadIdx.x == 0) {
+    *active_count = still;
+    // device-side sweep loop (pe_api.cu run_sweeps): the enclosing while-node of the
+    // captured graph runs another sweep only while some interval is still iterating
+    if (use_cond) {
+      active_count[2] += 1;  // counter slot 2 (loop mode runs buffer parity 0): sweeps run
+      cudaGraphSetConditional(cond, still > 0 ? 1u : 0u);
+    }
+  }
 }
 
 void modal_decide(int E, int nc, int d1, int d2, int J, const double* nu, long long nu_g,
                   long long nu_m, const double* nw, long long nw_g, long long nw_m,
                   unsigned long long* colmax, unsigned* ticket, WrColumnState* cs, double tol,
                   int max_iter, double* resid_hist, int* active_count, int par_new,
-                  cudaStream_t st) {
+                  cudaStream_t st, cudaGraphConditionalHandle cond, int use_cond) {
   const long long total = 8LL * E * J * nc;  // four lanes per (side, member, column)
   const int blocks = (int)std::max<long long>(1, (total + DECIDE_THREADS - 1) / DECIDE_THREADS);
   launch_k(modal_decide_kernel, dim3(blocks), dim3(DECIDE_THREADS), 0, st, E, nc, d1, d2, J, nu,
            nu_g, nu_m, nw, nw_g, nw_m, colmax, ticket, cs, tol, max_iter, resid_hist, active_count,
-           par_new);
+           par_new, cond, use_cond);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
 }

@@ -387,12 +387,15 @@ def test_baseline_config2(tag):
         assert abs(its.mean() - ref.mean()) / ref.mean() < 0.05
         assert np.abs(its - ref).max() <= 0.25 * ref.max()
         assert all(i["converged"] for sw in run.fine_info for i in sw)
-        # Per (iteration, interval): the residual histories agree (1e-3) on every sweep
-        # where the reference residual is above the floor band 1e3 * tol; every difference
-        # in sweep count or reason arises inside that band, where the stop is decided by
-        # round-off (reference: 'floor', two non-decreasing residuals <= 1e3 tol; GPU:
-        # usually 'tol', its residual keeps falling).  tools/wr_stop_compare.py writes the
-        # per-pair table (profiles/r02/wr_stop_cfg2.json).
+        # Per (iteration, interval), against the reference's own residual histories
+        # (run_cfg2_aao_wr.npz): every common sweep agrees to 1e-3 relative plus 1e-11
+        # absolute -- the reference's round-off floor here (its residual stalls at
+        # 5e-12 .. 1e-11: FFT + explicit complex inverses).  Every difference in sweep count
+        # or stop reason arises once both residuals are inside the floor band 1e3 * tol,
+        # where the stop is decided by round-off (reference: mostly 'floor', two
+        # non-decreasing residuals <= 1e3 tol; GPU: mostly 'tol', its residual keeps
+        # falling).  tools/wr_stop_compare.py writes the per-pair table
+        # (profiles/r02/wr_stop_cfg2.json).
         zw = golden("run_cfg2_aao_wr.npz")
         band = 1e3 * 1e-12
         for k, sw in enumerate(run.fine_info):
@@ -400,8 +403,7 @@ def test_baseline_config2(tag):
                 rr = zw["wr_residuals"][k, n, : int(zw["wr_iterations"][k, n])]
                 rg = np.array(info["residuals"])
                 m = min(len(rr), len(rg))
-                above = rr[:m] > band
-                np.testing.assert_allclose(rg[:m][above], rr[:m][above], rtol=1e-3,
+                np.testing.assert_allclose(rg[:m], rr[:m], rtol=1e-3, atol=1e-11,
                                            err_msg=f"k={k + 1} n={n}")
                 if info["iterations"] != len(rr) or info["stop_reason"] != \
                         ("tol", "diverged", "floor", "max_iter")[int(zw["wr_reasons"][k, n])]:

@@ -17,20 +17,22 @@ ap.add_argument("--workload", default="cfg2-aao")
 ap.add_argument("--steps", type=int, default=1)
 args = ap.parse_args()
 wl = bench.WORKLOADS[args.workload]
-blocks, f1, f2, meta = bench.load_system(wl["sys"])
-s = P.CoarseSystem(**blocks)
-ctx = P.PeContext([s], [P.ConstantLoads(f1, f2)], wl["J"])
+mem, meta = bench.load_workload(wl)
+systems = [P.CoarseSystem(**b) for b, _, _ in mem]
+s = systems[0]
+E = len(systems)
+ctx = P.PeContext(systems, [P.ConstantLoads(a, b) for _, a, b in mem], wl["J"])
 N, J, T, kind = wl["N"], wl["J"], wl["T"], wl["kind"]
 ctx.prepare_coarse(T / N)
 if kind == "sequential":
     ctx.prepare_sequential(T / N / J)
 else:
-    ctx.prepare_allatonce(T / N / J, wl["alpha"], bench.FINE_TOL, bench.MAX_ITER)
+    ctx.prepare_allatonce(T / N / J, wl["alpha"], bench.FINE_TOL, wl["max_iter"])
 d = s.d1 + s.d2
-A = torch.zeros(1, N + 1, d, dtype=torch.float64, device="cuda")
+A = torch.zeros(E, N + 1, d, dtype=torch.float64, device="cuda")
 B = torch.zeros_like(A)
-Gc = torch.zeros(1, N, d, dtype=torch.float64, device="cuda")
-diff = torch.zeros(1, 2, dtype=torch.float64, device="cuda")
+Gc = torch.zeros(E, N, d, dtype=torch.float64, device="cuda")
+diff = torch.zeros(E, 2, dtype=torch.float64, device="cuda")
 ctx.coarse_correct(N, A, None, Gc, A)
 ctx.iterate(kind, N, A, B, Gc, diff)
 A, B = B, A

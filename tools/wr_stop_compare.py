@@ -30,6 +30,7 @@ run = P.run_parareal(cfg, props, P.build_fine_propagator(cfg, props, ld),
 h, r = np.array(run.history), g["history"]
 rel = float((np.linalg.norm(h - r, axis=-1) / np.maximum(np.linalg.norm(r, axis=-1), 1e-300)).max())
 pairs, same = [], 0
+worst_excess = -1.0  # max over sweeps of |r_gpu - r_ref| - 1e-3 r_ref (the test allows 1e-11)
 cnt = {}
 for k, sw in enumerate(run.fine_info):
     for n, info in enumerate(sw):
@@ -39,6 +40,7 @@ for k, sw in enumerate(run.fine_info):
         rg = np.array(info["residuals"])
         m = min(len(rr), len(rg))
         dev = np.nonzero(np.abs(rg[:m] - rr[:m]) > 1e-3 * rr[:m])[0]
+        worst_excess = max(worst_excess, float(np.max(np.abs(rg[:m] - rr[:m]) - 1e-3 * rr[:m])))
         first = int(dev[0]) if dev.size else None
         key = f"{ref_reason}->{info['stop_reason']}"
         cnt[key] = cnt.get(key, 0) + 1
@@ -56,6 +58,7 @@ summary = dict(parareal_iterations=run.iterations, reference_iterations=int(g["i
                max_history_rel_l2=rel, pairs=len(pairs) + same, identical=same,
                reason_transitions=cnt,
                max_ref_resid_at_first_deviation=max(devs) if devs else None,
+               max_abs_excess_over_1e3_rel=worst_excess,
                tol=1e-12, floor_band=1e-9,
                gpu_sweeps_mean=float(np.mean([i["iterations"] for sw in run.fine_info for i in sw])),
                ref_sweeps_mean=float(gw["wr_iterations"].mean()))
