@@ -29,6 +29,13 @@ from scipy.linalg import cho_factor, cho_solve
 from oracle.pe_oracle import apply_S, apply_S_inverse, time_eigenvalues
 
 
+def _apply(A, X):
+    """A @ X[s] for every s of X (S, n, B) as ONE GEMM (A is read once, not S times)."""
+    S, n, B = X.shape
+    Y = A @ np.ascontiguousarray(X.transpose(1, 0, 2)).reshape(n, S * B)
+    return np.ascontiguousarray(Y.reshape(A.shape[0], S, B).transpose(1, 0, 2))
+
+
 class BatchWR:
     def __init__(self, s, J, dt_interval, alpha, tol=1e-12, max_iter=400, verbose=False):
         self.s, self.J, self.dt = s, J, dt_interval / J
@@ -71,8 +78,7 @@ class BatchWR:
             # build_rhs (allatonce.py:154-157): w_hist = [w_lag, w_start, W[:-1]]
             wh = np.concatenate([w0[None], w0[None], W[:-1]], axis=0)
             dw = (wh[1:] - wh[:-1]) / dt
-            rhs = f1[None] - np.einsum("ij,sjb->sib", s.M12, dw) \
-                - np.einsum("ij,sjb->sib", s.A12, wh[1:])
+            rhs = f1[None] - _apply(s.M12, dw) - _apply(s.A12, wh[1:])
             rhs[0] += s.M11 @ (u0 - al * ufp) / dt
             # u solve (allatonce.py:117-119): p = S^-1 rhs, q_k = inv_k p_k, u = Re(S q)
             p = apply_S_inverse(rhs, al)
@@ -83,8 +89,7 @@ class BatchWR:
             # w sweep (allatonce.py:222-229)
             uh = np.concatenate([u0[None], u0[None], Un[:-1]], axis=0)
             du = (uh[1:] - uh[:-1]) / dt
-            g = dt * np.einsum("sjb,jk->skb", f2[None] - np.einsum("ji,sjb->sib", s.M12, du)
-                               - np.einsum("ji,sjb->sib", s.A12, Un), self.m22_inv)
+            g = dt * _apply(self.m22_inv.T, f2[None] - _apply(s.M12.T, du) - _apply(s.A12.T, Un))
             Wn = np.empty_like(W)
             w = w0
             for i in range(J):

@@ -940,6 +940,216 @@ static void launch_tma_best(const GemmParams& p, cudaStream_t st) {
   }
 }
 
+// ----------------------------------------------------------------------------------------
+// Row-balanced persistent variant for batched skinny products (the ensemble fine step, cfg4:
+// E members x (d x 2d)(2d x nc), nc <= 32): the E * M rows are split in 8-row blocks into
+// one contiguous range per SM (max/mean 1.02 at cfg4, where 160-row tiles leave 40 SMs
+// with half the work of the others).  A range is processed as sub-segments that stay
+// inside one member and one side of `zero_rows` (rows below it have an exact-zero k-range
+// [zero_k0, zero_k1) of the second segment, segment-local k -- the composite step's
+// u x Du block -- whose k-tiles are neither loaded nor multiplied).  One producer warp streams, per k-tile, one
+// 8-row 128B-swizzled TMA box per m-block of A plus the sub-segment's member's B tile into
+// a STAGES-deep ring; 11 DMMA warps own the m-blocks w, w+11, ... (12 warps: 3 per SMSP,
+// 168 registers, no spills).  Same canonical k order and
+// epilogue as the other kernels, so a result differs from them only by the omitted +0 terms.
+constexpr int RB_WARPS = 11, RB_FM = 3, RB_FN = 4, RB_STAGES = 5;
+constexpr int RB_MAXB = RB_WARPS * RB_FM;  // m-blocks per CTA range (33 = 264 rows)
+constexpr int RB_A_BYTES = RB_MAXB * 1024, RB_B_BYTES = 8 * RB_FN * 128;
+constexpr int RB_STAGE = RB_A_BYTES + RB_B_BYTES;
+constexpr size_t RB_SMEM = (size_t)RB_STAGES * RB_STAGE + 1024 + 2 * RB_STAGES * 8;
+
+struct alignas(64) RowBalArgs {
+  CUtensorMap ta[2];  // A segment maps {K_s, E * M} (box 16 x 8 rows)
+  CUtensorMap tb[2];  // B segment maps {K_s, E * N} (box 16 x 8 FN rows)
+  GemmParams p;
+  int blocks;         // E * M / 8
+  int zero_rows, zk0, zk1;
+};
+
+__global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
+    gemm_rowbal_kernel(const __grid_constant__ RowBalArgs a) {
+  extern __shared__ unsigned char smraw[];
+  const unsigned sbase = (smem_u32(smraw) + 1023u) & ~1023u;
+  const unsigned char* sgen = smraw + (sbase - smem_u32(smraw));
+  const unsigned bar_full = sbase + RB_STAGES * RB_STAGE;
+  const unsigned bar_empty = bar_full + RB_STAGES * 8;
+  const GemmParams& p = a.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mb = p.M / 8;  // m-blocks per member
+  const long long b0 = (long long)a.blocks * blockIdx.x / gridDim.x;
+  const long long b1 = (long long)a.blocks * (blockIdx.x + 1) / gridDim.x;
+  const int kt0 = (p.seg[0].K + 15) / 16, kt1 = p.nseg > 1 ? (p.seg[1].K + 15) / 16 : 0;
+  // k-tiles of the last segment entirely inside its zero k-range [zk0, zk1) (segment-local
+  // k), as indices into the concatenated k-tile sequence
+  const int kz = kt0;
+  const int zt0 = p.nseg > 1 ? kz + (a.zk0 + 15) / 16 : 0;
+  const int zt1 = p.nseg > 1 ? kz + a.zk1 / 16 : 0;
+  const int zr_blocks = a.zero_rows / 8;  // member-local m-blocks entirely below zero_rows
+
+  if (tid == 0) {
+    for (int s = 0; s < RB_STAGES; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, RB_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_enter();
+
+  // sub-segment walk shared by producer and consumers: [sb, se) member-local blocks of e
+  auto next_sub = [&](long long& b, int& e, int& sb, int& se, bool& skip) {
+    e = (int)(b / mb);
+    sb = (int)(b - (long long)e * mb);
+    int lim = mb;
+    if (zt1 > zt0 && sb < zr_blocks) lim = zr_blocks;  // split at the zero-row boundary
+    const long long rem = b1 - (long long)e * mb;
+    se = (int)(rem < lim ? rem : (long long)lim);
+    skip = zt1 > zt0 && se <= zr_blocks;
+    b = (long long)e * mb + se;
+  };
+  const int ktot = kt0 + kt1;
+
+  if (warp == RB_WARPS) {  // producer
+    if (lane == 0) {
+      int t = 0;
+      for (long long b = b0; b < b1;) {
+        int e, sb, se;
+        bool skip;
+        next_sub(b, e, sb, se, skip);
+        const int nb = se - sb;
+        for (int g = 0; g < ktot; ++g) {
+          if (skip && g >= zt0 && g < zt1) continue;
+          const int st = t % RB_STAGES;
+          if (t >= RB_STAGES) mbar_wait_cta(bar_empty + 8 * st, ((t / RB_STAGES) - 1) & 1);
+          const int s = g < kt0 ? 0 : 1;
+          const int kk = (s ? g - kt0 : g) * 16;
+          const unsigned full = bar_full + 8 * st;
+          mbar_expect_tx(full, nb * 1024 + RB_B_BYTES);
+          const unsigned dA = sbase + st * RB_STAGE;
+          for (int x = 0; x < nb; ++x)
+            tma_load_4d(dA + x * 1024, &a.ta[s], kk, e * p.M + (sb + x) * 8, 0, 0, full);
+          tma_load_4d(dA + RB_A_BYTES, &a.tb[s], kk, e * p.N, 0, 0, full);
+          ++t;
+        }
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 2, t4 = lane & 3;
+  const unsigned ko0 = swz(g, 4 * t4), ko1 = swz(g, 4 * t4 + 2);
+  int t = 0;
+  for (long long b = b0; b < b1;) {
+    int e, sb, se;
+    bool skip;
+    next_sub(b, e, sb, se, skip);
+    const int nb = se - sb;
+    const int nmine = nb > warp ? (nb - 1 - warp) / RB_WARPS + 1 : 0;  // my m-blocks
+    double acc[RB_FM][RB_FN][2];
+#pragma unroll
+    for (int x = 0; x < RB_FM; ++x)
+#pragma unroll
+      for (int y = 0; y < RB_FN; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int gk = 0; gk < ktot; ++gk) {
+      if (skip && gk >= zt0 && gk < zt1) continue;
+      const int st = t % RB_STAGES;
+      mbar_wait_cta(bar_full + 8 * st, (t / RB_STAGES) & 1);
+      const unsigned char* sa = sgen + st * RB_STAGE;
+      const unsigned char* sbp = sa + RB_A_BYTES;
+      double af[RB_FM][4], bf[RB_FN][4];
+#pragma unroll
+      for (int x = 0; x < RB_FM; ++x)
+        if (x < nmine) {
+          const unsigned char* r = sa + (warp + x * RB_WARPS) * 1024;
+          const double2 u = *reinterpret_cast<const double2*>(r + ko0);
+          const double2 v = *reinterpret_cast<const double2*>(r + ko1);
+          af[x][0] = u.x; af[x][1] = u.y; af[x][2] = v.x; af[x][3] = v.y;
+        }
+#pragma unroll
+      for (int y = 0; y < RB_FN; ++y) {
+        const double2 u = *reinterpret_cast<const double2*>(sbp + y * 8 * 128 + ko0);
+        const double2 v = *reinterpret_cast<const double2*>(sbp + y * 8 * 128 + ko1);
+        bf[y][0] = u.x; bf[y][1] = u.y; bf[y][2] = v.x; bf[y][3] = v.y;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_empty + 8 * st);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int x = 0; x < RB_FM; ++x)
+          if (x < nmine)
+#pragma unroll
+            for (int y = 0; y < RB_FN; ++y)
+              dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x][q], bf[y][q]);
+      ++t;
+    }
+#pragma unroll
+    for (int x = 0; x < RB_FM; ++x)
+      if (x < nmine)
+        gemm_epilogue<1, RB_FN>(p, e, 0, (sb + warp + x * RB_WARPS) * 8 + g, 2 * t4,
+                                reinterpret_cast<const double(&)[1][RB_FN][2]>(acc[x]));
+  }
+}
+
+// Eligibility: batch over nb1 >= 2 only, M % 8 == 0, N <= 32, 1-2 k-contiguous segments whose A
+// rows share one stride and batch stride M * stride (a dense member-major stack, as T),
+// B columns k-contiguous with batch stride N * column stride, TMA alignment.
+static int num_sms() {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    PE_CUDA_CHECK(cudaGetDevice(&dev));
+    PE_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return nsm;
+}
+
+bool gemm_rowbalanced_eligible(const GemmParams& p) {
+  static const bool off = getenv("PE_GEMM_NO_ROWBAL") != nullptr;
+  if (off || p.nb2 != 1 || p.nb1 < 2 || p.M % 8 || p.N > 8 * RB_FN || p.N < 1 || p.nseg < 1 ||
+      p.nseg > 2 || p.nrm || p.Cin || !tma_ok(p))
+    return false;
+  for (int s = 0; s < p.nseg; ++s) {
+    const Operand& A = p.seg[s].A;
+    const Operand& B = p.seg[s].B;
+    if (A.b1 != (long long)p.M * A.s0 || B.b1 != (long long)p.N * B.s1) return false;
+  }
+  const long long blocks = (long long)p.nb1 * (p.M / 8);
+  const int grid = (int)std::min<long long>(num_sms(), blocks);
+  return blocks <= INT32_MAX && (blocks + grid - 1) / grid <= RB_MAXB;
+}
+
+void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int zero_k1,
+                          cudaStream_t st) {
+  if (!gemm_rowbalanced_eligible(p)) throw Error{PE_ERR_ARG, "rowbalanced: shape not eligible"};
+  const long long blocks = (long long)p.nb1 * (p.M / 8);
+  static bool attr = false;
+  if (!attr) {
+    PE_CUDA_CHECK(cudaFuncSetAttribute(gemm_rowbal_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_SMEM));
+    attr = true;
+  }
+  RowBalArgs a;
+  memset(static_cast<void*>(&a), 0, sizeof(a));
+  a.p = p;
+  a.p.ksplit = 1;
+  for (int s = 0; s < p.nseg; ++s) {
+    const GemmSeg& g = p.seg[s];
+    int use[2];
+    // rows of all members as one 2-D extent (member-major stack)
+    encode_operand(&a.ta[s], use, g.A.p, g.K, p.M * p.nb1, g.A.s0, 0, 1, 0, 1, 8);
+    encode_operand(&a.tb[s], use, g.B.p, g.K, p.N * p.nb1, g.B.s1, 0, 1, 0, 1, 8 * RB_FN);
+  }
+  a.blocks = (int)blocks;
+  a.zero_rows = zero_rows;
+  a.zk0 = zero_k0;
+  a.zk1 = zero_k1;
+  const int grid = (int)std::min<long long>(num_sms(), blocks);
+  launch_k(gemm_rowbal_kernel, dim3(grid), dim3((RB_WARPS + 1) * 32), RB_SMEM, st, a);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+}
+
 void gemm_f64(const GemmParams& p, cudaStream_t st) {
   if (p.M <= 0 || p.N <= 0 || p.nb1 * p.nb2 <= 0) return;
   bool ak = true, bk = true;

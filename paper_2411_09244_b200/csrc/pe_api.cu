@@ -204,7 +204,17 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
         p.D = Dn;
         p.Xp = Xs;
       }
-      run_gemm(c, p, st);
+      // ensembles: one row-balanced persistent launch per step, skipping T's exact-zero
+      // u x Du block (rows < d1, D-segment columns < d1); else the tiled kernels
+      if (gemm_rowbalanced_eligible(p)) {
+        // algorithmic flops: the skipped u x Du block is a structural zero
+        const double zero = Ds ? 2.0 * ec * nc * (double)c->d1 * c->d1 : 0.0;
+        profiled(c, gemm_flops(p) - zero, st, [&] {
+          gemm_f64_rowbalanced(p, Ds ? c->d1 : 0, 0, Ds ? c->d1 : 0, st);
+        });
+      } else {
+        run_gemm(c, p, st);
+      }
       Xs = Xn;
       Ds = Dn;
     }
