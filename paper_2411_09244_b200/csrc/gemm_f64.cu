@@ -17,6 +17,7 @@
 #include <cstring>
 #include <string>
 #include <stdexcept>
+#include <type_traits>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -942,20 +943,21 @@ static void launch_tma_best(const GemmParams& p, cudaStream_t st) {
 
 // ----------------------------------------------------------------------------------------
 // Row-balanced persistent variant for batched skinny products (the ensemble fine step, cfg4:
-// E members x (d x 2d)(2d x nc), nc <= 32): the E * M rows are split in 8-row blocks into
+// E members x (d x 2d)(2d x nc), nc <= 32).  The E * M rows are split in 8-row blocks into
 // one contiguous range per SM (max/mean 1.02 at cfg4, where 160-row tiles leave 40 SMs
-// with half the work of the others).  A range is processed as sub-segments that stay
-// inside one member and one side of `zero_rows` (rows below it have an exact-zero k-range
-// [zero_k0, zero_k1) of the second segment, segment-local k -- the composite step's
-// u x Du block -- whose k-tiles are neither loaded nor multiplied).  One producer warp streams, per k-tile, one
-// 8-row 128B-swizzled TMA box per m-block of A plus the sub-segment's member's B tile into
-// a STAGES-deep ring; 11 DMMA warps own the m-blocks w, w+11, ... (12 warps: 3 per SMSP,
-// 168 registers, no spills).  Same canonical k order and
-// epilogue as the other kernels, so a result differs from them only by the omitted +0 terms.
-constexpr int RB_WARPS = 11, RB_FM = 3, RB_FN = 4, RB_STAGES = 5;
-constexpr int RB_MAXB = RB_WARPS * RB_FM;  // m-blocks per CTA range (33 = 264 rows)
+// with half the work of the others).  A range covers at most two members (a "part" each);
+// both parts run through ONE k-loop: every consumer warp owns 4 consecutive m-blocks
+// (32 rows) of one part, and each stage holds the part's A blocks plus one B tile per part.
+// Rows below `zero_rows` have an exact-zero k-range [zero_k0, zero_k1) of the second
+// segment (segment-local k; the composite step's u x Du block): a warp whose four blocks
+// all lie below it neither loads nor multiplies those k-tiles.  One producer warp issues
+// one 8-row 128B-swizzled TMA box per loaded m-block and one box per B tile.  Same
+// canonical k order and epilogue as the other kernels, so a result differs from theirs only
+// by the omitted +0 terms.
+constexpr int RB_WARPS = 10, RB_FM = 4, RB_FN = 4, RB_STAGES = 5;  // 11 warps: <= 3 per SMSP
+constexpr int RB_MAXB = 33;  // m-blocks per CTA range (264 rows): ceil(a/4)+ceil(b/4) <= 10
 constexpr int RB_A_BYTES = RB_MAXB * 1024, RB_B_BYTES = 8 * RB_FN * 128;
-constexpr int RB_STAGE = RB_A_BYTES + RB_B_BYTES;
+constexpr int RB_STAGE = RB_A_BYTES + 2 * RB_B_BYTES;
 constexpr size_t RB_SMEM = (size_t)RB_STAGES * RB_STAGE + 1024 + 2 * RB_STAGES * 8;
 
 struct alignas(64) RowBalArgs {
@@ -966,6 +968,28 @@ struct alignas(64) RowBalArgs {
   int zero_rows, zk0, zk1;
 };
 
+// CTA range -> up to two parts (member, first member-local block, block count) and the
+// warp layout: part 0 takes warps [0, w0), part 1 [w0, w0 + w1), 4 blocks per warp.
+struct RbPlan {
+  int e[2], sb[2], nb[2], w0, nw;
+};
+__device__ __forceinline__ RbPlan rb_plan(const RowBalArgs& a) {
+  const int mb = a.p.M / 8;
+  const long long b0 = (long long)a.blocks * blockIdx.x / gridDim.x;
+  const long long b1 = (long long)a.blocks * (blockIdx.x + 1) / gridDim.x;
+  RbPlan r;
+  r.e[0] = (int)(b0 / mb);
+  r.sb[0] = (int)(b0 - (long long)r.e[0] * mb);
+  const long long end0 = (long long)(r.e[0] + 1) * mb;
+  r.nb[0] = (int)((b1 < end0 ? b1 : end0) - b0);
+  r.e[1] = r.e[0] + 1;
+  r.sb[1] = 0;
+  r.nb[1] = b1 > end0 ? (int)(b1 - end0) : 0;
+  r.w0 = (r.nb[0] + RB_FM - 1) / RB_FM;
+  r.nw = r.w0 + (r.nb[1] + RB_FM - 1) / RB_FM;
+  return r;
+}
+
 __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
     gemm_rowbal_kernel(const __grid_constant__ RowBalArgs a) {
   extern __shared__ unsigned char smraw[];
@@ -975,96 +999,99 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   const unsigned bar_empty = bar_full + RB_STAGES * 8;
   const GemmParams& p = a.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int mb = p.M / 8;  // m-blocks per member
-  const long long b0 = (long long)a.blocks * blockIdx.x / gridDim.x;
-  const long long b1 = (long long)a.blocks * (blockIdx.x + 1) / gridDim.x;
+  const RbPlan pl = rb_plan(a);
   const int kt0 = (p.seg[0].K + 15) / 16, kt1 = p.nseg > 1 ? (p.seg[1].K + 15) / 16 : 0;
-  // k-tiles of the last segment entirely inside its zero k-range [zk0, zk1) (segment-local
-  // k), as indices into the concatenated k-tile sequence
-  const int kz = kt0;
-  const int zt0 = p.nseg > 1 ? kz + (a.zk0 + 15) / 16 : 0;
-  const int zt1 = p.nseg > 1 ? kz + a.zk1 / 16 : 0;
-  const int zr_blocks = a.zero_rows / 8;  // member-local m-blocks entirely below zero_rows
+  const int ktot = kt0 + kt1;
+  // k-tiles of the second segment entirely inside its zero k-range, as concatenated indices
+  const int zt0 = p.nseg > 1 ? kt0 + (a.zk0 + 15) / 16 : 0;
+  const int zt1 = p.nseg > 1 ? kt0 + a.zk1 / 16 : 0;
+  const int zr_blocks = a.zero_rows / 8;  // member-local blocks entirely below zero_rows
+  // warp w's part, first block (member-local) and block count
+  auto wplace = [&](int w, int& part, int& fb, int& cnt) {
+    part = w < pl.w0 ? 0 : 1;
+    const int q = part ? w - pl.w0 : w;
+    fb = pl.sb[part] + q * RB_FM;
+    const int left = pl.nb[part] - q * RB_FM;
+    cnt = left < RB_FM ? left : RB_FM;
+  };
+  auto skips = [&](int fb, int cnt, int g) {  // warp's blocks all exact zero on k-tile g
+    return g >= zt0 && g < zt1 && fb + cnt <= zr_blocks;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < RB_STAGES; ++s) {
       mbar_init(bar_full + 8 * s, 1);
-      mbar_init(bar_empty + 8 * s, RB_WARPS);
+      mbar_init(bar_empty + 8 * s, pl.nw);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   pdl_enter();
-
-  // sub-segment walk shared by producer and consumers: [sb, se) member-local blocks of e
-  auto next_sub = [&](long long& b, int& e, int& sb, int& se, bool& skip) {
-    e = (int)(b / mb);
-    sb = (int)(b - (long long)e * mb);
-    int lim = mb;
-    if (zt1 > zt0 && sb < zr_blocks) lim = zr_blocks;  // split at the zero-row boundary
-    const long long rem = b1 - (long long)e * mb;
-    se = (int)(rem < lim ? rem : (long long)lim);
-    skip = zt1 > zt0 && se <= zr_blocks;
-    b = (long long)e * mb + se;
-  };
-  const int ktot = kt0 + kt1;
+  if (pl.nw == 0) return;
 
   if (warp == RB_WARPS) {  // producer
     if (lane == 0) {
-      int t = 0;
-      for (long long b = b0; b < b1;) {
-        int e, sb, se;
-        bool skip;
-        next_sub(b, e, sb, se, skip);
-        const int nb = se - sb;
-        for (int g = 0; g < ktot; ++g) {
-          if (skip && g >= zt0 && g < zt1) continue;
-          const int st = t % RB_STAGES;
-          if (t >= RB_STAGES) mbar_wait_cta(bar_empty + 8 * st, ((t / RB_STAGES) - 1) & 1);
-          const int s = g < kt0 ? 0 : 1;
-          const int kk = (s ? g - kt0 : g) * 16;
-          const unsigned full = bar_full + 8 * st;
-          mbar_expect_tx(full, nb * 1024 + RB_B_BYTES);
-          const unsigned dA = sbase + st * RB_STAGE;
-          for (int x = 0; x < nb; ++x)
-            tma_load_4d(dA + x * 1024, &a.ta[s], kk, e * p.M + (sb + x) * 8, 0, 0, full);
-          tma_load_4d(dA + RB_A_BYTES, &a.tb[s], kk, e * p.N, 0, 0, full);
-          ++t;
+      for (int gk = 0; gk < ktot; ++gk) {
+        const int st = gk % RB_STAGES;
+        if (gk >= RB_STAGES) mbar_wait_cta(bar_empty + 8 * st, ((gk / RB_STAGES) - 1) & 1);
+        const int s = gk < kt0 ? 0 : 1;
+        const int kk = (s ? gk - kt0 : gk) * 16;
+        const unsigned full = bar_full + 8 * st;
+        int boxes = 0;
+        for (int w = 0; w < pl.nw; ++w) {
+          int part, fb, cnt;
+          wplace(w, part, fb, cnt);
+          if (!skips(fb, cnt, gk)) boxes += cnt;
         }
+        mbar_expect_tx(full, boxes * 1024 + (pl.nb[1] ? 2 : 1) * RB_B_BYTES);
+        const unsigned dA = sbase + st * RB_STAGE;
+        for (int w = 0; w < pl.nw; ++w) {
+          int part, fb, cnt;
+          wplace(w, part, fb, cnt);
+          if (skips(fb, cnt, gk)) continue;
+          const int slot0 = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);  // compact A slots
+          for (int x = 0; x < cnt; ++x)
+            tma_load_4d(dA + (slot0 + x) * 1024, &a.ta[s], kk,
+                        pl.e[part] * p.M + (fb + x) * 8, 0, 0, full);
+        }
+        for (int part = 0; part < (pl.nb[1] ? 2 : 1); ++part)
+          tma_load_4d(dA + RB_A_BYTES + part * RB_B_BYTES, &a.tb[s], kk, pl.e[part] * p.N, 0, 0,
+                      full);
       }
     }
     return;
   }
+  if (warp >= pl.nw) return;  // no blocks for this warp
 
+  int part, fb, cnt;
+  wplace(warp, part, fb, cnt);
+  const int slot0 = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);
   const int g = lane >> 2, t4 = lane & 3;
   const unsigned ko0 = swz(g, 4 * t4), ko1 = swz(g, 4 * t4 + 2);
-  int t = 0;
-  for (long long b = b0; b < b1;) {
-    int e, sb, se;
-    bool skip;
-    next_sub(b, e, sb, se, skip);
-    const int nb = se - sb;
-    const int nmine = nb > warp ? (nb - 1 - warp) / RB_WARPS + 1 : 0;  // my m-blocks
-    double acc[RB_FM][RB_FN][2];
+  double acc[RB_FM][RB_FN][2];
 #pragma unroll
-    for (int x = 0; x < RB_FM; ++x)
+  for (int x = 0; x < RB_FM; ++x)
 #pragma unroll
-      for (int y = 0; y < RB_FN; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int y = 0; y < RB_FN; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  auto kloop = [&](auto FMC) {  // FMC: this warp's block count, compile-time
+    constexpr int F = decltype(FMC)::value;
     for (int gk = 0; gk < ktot; ++gk) {
-      if (skip && gk >= zt0 && gk < zt1) continue;
-      const int st = t % RB_STAGES;
-      mbar_wait_cta(bar_full + 8 * st, (t / RB_STAGES) & 1);
-      const unsigned char* sa = sgen + st * RB_STAGE;
-      const unsigned char* sbp = sa + RB_A_BYTES;
-      double af[RB_FM][4], bf[RB_FN][4];
+      const int st = gk % RB_STAGES;
+      mbar_wait_cta(bar_full + 8 * st, (gk / RB_STAGES) & 1);
+      if (skips(fb, cnt, gk)) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_empty + 8 * st);
+        continue;
+      }
+      const unsigned char* sa = sgen + st * RB_STAGE + slot0 * 1024;
+      const unsigned char* sbp = sgen + st * RB_STAGE + RB_A_BYTES + part * RB_B_BYTES;
+      double af[F][4], bf[RB_FN][4];
 #pragma unroll
-      for (int x = 0; x < RB_FM; ++x)
-        if (x < nmine) {
-          const unsigned char* r = sa + (warp + x * RB_WARPS) * 1024;
-          const double2 u = *reinterpret_cast<const double2*>(r + ko0);
-          const double2 v = *reinterpret_cast<const double2*>(r + ko1);
-          af[x][0] = u.x; af[x][1] = u.y; af[x][2] = v.x; af[x][3] = v.y;
-        }
+      for (int x = 0; x < F; ++x) {
+        const double2 u = *reinterpret_cast<const double2*>(sa + x * 1024 + ko0);
+        const double2 v = *reinterpret_cast<const double2*>(sa + x * 1024 + ko1);
+        af[x][0] = u.x; af[x][1] = u.y; af[x][2] = v.x; af[x][3] = v.y;
+      }
 #pragma unroll
       for (int y = 0; y < RB_FN; ++y) {
         const double2 u = *reinterpret_cast<const double2*>(sbp + y * 8 * 128 + ko0);
@@ -1076,24 +1103,30 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int x = 0; x < RB_FM; ++x)
-          if (x < nmine)
+        for (int x = 0; x < F; ++x)
 #pragma unroll
-            for (int y = 0; y < RB_FN; ++y)
-              dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x][q], bf[y][q]);
-      ++t;
+          for (int y = 0; y < RB_FN; ++y)
+            dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x][q], bf[y][q]);
     }
-#pragma unroll
-    for (int x = 0; x < RB_FM; ++x)
-      if (x < nmine)
-        gemm_epilogue<1, RB_FN>(p, e, 0, (sb + warp + x * RB_WARPS) * 8 + g, 2 * t4,
-                                reinterpret_cast<const double(&)[1][RB_FN][2]>(acc[x]));
+  };
+  switch (cnt) {
+    case 4: kloop(std::integral_constant<int, 4>{}); break;
+    case 3: kloop(std::integral_constant<int, 3>{}); break;
+    case 2: kloop(std::integral_constant<int, 2>{}); break;
+    default: kloop(std::integral_constant<int, 1>{}); break;
   }
+  // rows fb*8 .. (fb+cnt)*8 of member pl.e[part]; blocks past cnt hold zeros, not stored
+#pragma unroll
+  for (int x = 0; x < RB_FM; ++x)
+    if (x < cnt)
+      gemm_epilogue<1, RB_FN>(p, pl.e[part], 0, (fb + x) * 8 + g, 2 * t4,
+                              reinterpret_cast<const double(&)[1][RB_FN][2]>(acc[x]));
 }
 
-// Eligibility: batch over nb1 >= 2 only, M % 8 == 0, N <= 32, 1-2 k-contiguous segments whose A
-// rows share one stride and batch stride M * stride (a dense member-major stack, as T),
-// B columns k-contiguous with batch stride N * column stride, TMA alignment.
+// Eligibility: batch over nb1 >= 2 only, M % 8 == 0, N <= 32, 1-2 k-contiguous segments
+// whose A rows share one stride and batch stride M * stride (a dense member-major stack,
+// as T), B columns k-contiguous with batch stride N * column stride, TMA alignment, and at
+// most RB_MAXB (< M / 8) blocks per SM so that a range spans at most two members.
 static int num_sms() {
   static int nsm = 0;
   if (!nsm) {
@@ -1116,7 +1149,8 @@ bool gemm_rowbalanced_eligible(const GemmParams& p) {
   }
   const long long blocks = (long long)p.nb1 * (p.M / 8);
   const int grid = (int)std::min<long long>(num_sms(), blocks);
-  return blocks <= INT32_MAX && (blocks + grid - 1) / grid <= RB_MAXB;
+  const long long per = (blocks + grid - 1) / grid;
+  return blocks <= INT32_MAX && per <= RB_MAXB && per <= p.M / 8;
 }
 
 void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int zero_k1,
