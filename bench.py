@@ -181,6 +181,55 @@ def fp64_peak_tflops(torch):
     return 2.0 * n ** 3 / best / 1e9
 
 
+class CudaBackend:
+    """The real arm: libpe on one GPU per rank, NCCL, CUDA events on the launch stream."""
+
+    name = "cuda"
+    dist_backend = "nccl"
+
+    def __init__(self, local):
+        import torch
+
+        self.torch = torch
+        torch.cuda.set_device(local)
+        self.local = local
+        self.device = torch.device("cuda", local)
+
+    def init_dist(self, dist):
+        dist.init_process_group("nccl", device_id=self.device)
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+
+    def event(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def make_context(self, P, systems, loads, J):
+        return P.PeContext(systems, loads, J, self.local)
+
+    def clocks(self):
+        return ClockSampler(self.local)
+
+    def flush_buffer(self):
+        return self.torch.empty(320 * 1024 * 1024 // 8, dtype=self.torch.float64,
+                                device=self.device)
+
+    def fp64_peak(self):
+        return fp64_peak_tflops(self.torch)
+
+
+def make_backend(local):
+    """CudaBackend, or (dry runs of the multi-process logic from the tests only) the class
+    named by PE_BENCH_BACKEND=module:attr, constructed with the local rank."""
+    spec = os.environ.get("PE_BENCH_BACKEND")
+    if not spec:
+        return CudaBackend(local)
+    import importlib
+
+    mod, attr = spec.split(":")
+    return getattr(importlib.import_module(mod), attr)(local)
+
+
 # ---------------------------------------------------------------------- CPU arms
 
 def _osys(blocks, f1, f2):
@@ -416,12 +465,14 @@ def gpu_arm(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    be = make_backend(local)
+    be.workload = args.workload
+    dev = be.device
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        be.init_dist(dist)
     import paper_2411_09244_b200 as P
 
     mem, meta = load_workload(wl)
@@ -434,27 +485,27 @@ def gpu_arm(args, wl):
     max_iter = wl["max_iter"]
     d = system.d1 + system.d2
     units = E * d * N * J  # per replica / per problem
-    torch.cuda.synchronize()
+    be.sync()
     t_setup = time.perf_counter()
-    ctx = P.PeContext(systems, loads_l, J, local)
-    torch.cuda.synchronize()
+    ctx = be.make_context(P, systems, loads_l, J)
+    be.sync()
     t_upload = time.perf_counter() - t_setup
     ctx.prepare_coarse(T / N)
     if kind == "sequential":
         ctx.prepare_sequential(T / N / J)
     else:
         ctx.prepare_allatonce(T / N / J, wl["alpha"], FINE_TOL, max_iter)
-    torch.cuda.synchronize()
+    be.sync()
     t_setup = time.perf_counter() - t_setup
     modal = ctx.modal_level() if kind == "all-at-once" else None
 
-    A = torch.zeros(E, N + 1, d, dtype=torch.float64, device="cuda")
+    A = torch.zeros(E, N + 1, d, dtype=torch.float64, device=dev)
     B = torch.zeros_like(A)
-    Gc = torch.zeros(E, N, d, dtype=torch.float64, device="cuda")
-    diff = torch.zeros(E, 2, dtype=torch.float64, device="cuda")
+    Gc = torch.zeros(E, N, d, dtype=torch.float64, device=dev)
+    diff = torch.zeros(E, 2, dtype=torch.float64, device=dev)
     ctx.coarse_correct(N, A, None, Gc, A)  # initial coarse sweep (x_0 = 0, u0 = 0 projection)
-    flush = torch.empty(320 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    sweeps_buf = torch.zeros(E, N, dtype=torch.int32, device="cuda") if kind != "sequential" \
+    flush = be.flush_buffer()
+    sweeps_buf = torch.zeros(E, N, dtype=torch.int32, device=dev) if kind != "sequential" \
         else None
     sweeps_seen = []
 
@@ -464,7 +515,7 @@ def gpu_arm(args, wl):
         ranges = [shard_members(N, r, world) for r in range(world)]
         mine = ranges[rank]
         m_loc = max(len(r) for r in ranges)
-        F_loc = torch.zeros(E, m_loc, d, dtype=torch.float64, device="cuda")
+        F_loc = torch.zeros(E, m_loc, d, dtype=torch.float64, device=dev)
         parts = [torch.empty_like(F_loc) for _ in range(world)]
 
         def step(x_old, x_new):
@@ -488,15 +539,15 @@ def gpu_arm(args, wl):
     for _ in range(args.warmup):
         step(A, B)
         A, B = B, A
-    torch.cuda.synchronize()
+    be.sync()
     sweeps_seen.clear()
     if dist:
         dist.barrier()
     launches0 = ctx.launch_count()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
+    starts = [be.event() for _ in range(args.steps)]
+    ends = [be.event() for _ in range(args.steps)]
+    with be.clocks() as clk:
+        be.sync()
         t_wall = time.perf_counter()
         for i in range(args.steps):
             flush.fill_(float(i))  # evict L2 (320 MB > 126 MB) between timed steps
@@ -504,7 +555,7 @@ def gpu_arm(args, wl):
             step(A, B)
             ends[i].record()
             A, B = B, A
-        torch.cuda.synchronize()
+        be.sync()
         t_wall = time.perf_counter() - t_wall
     if dist:
         dist.barrier()
@@ -512,7 +563,7 @@ def gpu_arm(args, wl):
     launches = ctx.launch_count() - launches0
     total_ms = float(sum(step_ms))
     if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     # whole job: one problem (sharded) or `world` replicas
@@ -524,10 +575,10 @@ def gpu_arm(args, wl):
     ctx.set_profiling(True)
     flush.fill_(0.0)
     step(A, B)
-    torch.cuda.synchronize()
+    be.sync()
     st = ctx.fine_stats()
     ctx.set_profiling(False)
-    peak = fp64_peak_tflops(torch)
+    peak = be.fp64_peak()
     achieved = st["gemm_flops"] / (st["gemm_ms"] / 1e3) / 1e12 if st["gemm_ms"] > 0 else 0.0
     step_avg = total_ms / args.steps
 
@@ -542,14 +593,14 @@ def gpu_arm(args, wl):
     zeros = P.SplitState.fresh(np.zeros(system.d1), np.zeros(system.d2))
     if dist:
         dist.barrier()
-    torch.cuda.synchronize()
+    be.sync()
     if shard:
         from paper_2411_09244_b200.sharded import LibpeShardOps, run_parareal_sharded
 
         ops = LibpeShardOps(ctx, kind)
         t0 = time.perf_counter()
         res = run_parareal_sharded(N, np.zeros(d), ops, cfg.k_max, cfg.epsilon, "relative")
-        torch.cuda.synchronize()
+        be.sync()
         e2e_s = time.perf_counter() - t0
         K, hist = res["iterations"], list(res["history"])
         iters = K
@@ -561,16 +612,16 @@ def gpu_arm(args, wl):
         fine = P.build_fine_propagator(cfg, props, loads)
         t0 = time.perf_counter()
         run = P.run_parareal(cfg, props, fine, zeros)
-        torch.cuda.synchronize()
+        be.sync()
         e2e_s = time.perf_counter() - t0
         K, hist, iters = run.iterations, run.history, run.iterations
         path = "paper_2411_09244_b200.run_parareal (host arrays in/out)"
     else:
         ens = P.ParerealEnsemble(cfg, systems, loads_l)  # setup stays out of e2e
-        torch.cuda.synchronize()
+        be.sync()
         t0 = time.perf_counter()
         runs = ens.run([zeros] * E)
-        torch.cuda.synchronize()
+        be.sync()
         e2e_s = time.perf_counter() - t0
         K = max(r.iterations for r in runs)
         iters = [r.iterations for r in runs]
@@ -586,9 +637,10 @@ def gpu_arm(args, wl):
 
     line = None
     if rank == 0:
-        parity = parity_check(P, wl, ctx, system, loads, hist, iters, kind)
+        parity = (parity_check(P, wl, ctx, system, loads, hist, iters, kind) if be.name == "cuda"
+                  else {"status": f"dry run ({be.name} backend): no parity check"})
         cpu = None
-        if world == 1 and not args.no_cpu:
+        if world == 1 and not args.no_cpu and be.name == "cuda":
             blocks, f1, f2 = mem[0]
             sampler = CpuSampler(wl, blocks, f1, f2, len(os.sched_getaffinity(0)))
             t_iter, t_meas, info = sampler.sample()

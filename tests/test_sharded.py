@@ -129,3 +129,30 @@ def test_sharded_driver_rejects_unknown_rule():
     with pytest.raises(ValueError):
         run_parareal_sharded(4, np.zeros(s.d1 + s.d2), OracleOps(s, 1.0, 4, 10, "sequential"),
                              k_max=1, epsilon=0.0, rule="bogus")
+
+
+def test_bench_two_rank_dry_run_reports_the_job(tmp_path):
+    """`bench.py --gpus 2` re-executes itself under torchrun (one process per device), shards
+    the intervals, all-gathers the fine endpoints once per iteration and prints ONE line from
+    rank 0 with n_gpus 2 and the strong-scaling tag -- here on CPU under gloo with the oracle
+    stand-in context (PE_BENCH_BACKEND), so only the multi-process logic is exercised."""
+    import json
+    import subprocess
+    import sys
+
+    from tests.conftest import ROOT
+
+    env = dict(os.environ, PE_BENCH_BACKEND="tests.bench_cpu_backend:CpuBackend",
+               PYTHONPATH=ROOT, OMP_NUM_THREADS="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--workload", "cfg0-seq", "--steps", "2", "--warmup", "3"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["steps"] == 2
+    assert d["parallelism"].startswith("intervals sharded over 2 ranks")
+    assert d["config"]["workload"] == "cfg0-seq" and d["value"] > 0
+    assert d["e2e"]["iterations"] >= 1
