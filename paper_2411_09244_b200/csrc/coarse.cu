@@ -493,15 +493,19 @@ static void coarse_correct_stream(int E, int d, int N, const double* Phi, const 
     attr = true;
   }
   if (smem > 200 * 1024) throw Error{PE_ERR_ARG, "coarse state too large for one SM"};
-  // Members are independent: when all Phi exceed the L2 budget (cfg4: 64 x 2.9 MB) run
-  // member chunks through all N steps, so a chunk's Phi is read from HBM once and from L2
-  // for its other N - 1 steps (same arithmetic, per member).  One member larger than the
-  // budget (cfg3: 537 MB) streams each step.
+  // Members are independent: member chunks can run through all N steps so that a chunk's
+  // Phi is read from HBM once and from L2 afterwards (same arithmetic, per member).
+  // Measured at cfg4 (64 x 2.9 MB): chunks of 20 members through all 32 steps took 128 x
+  // 29.7 us against 32 x 43.7 us for the one-pass stream of all members (the chunk's 58 MB
+  // did not come back from L2 faster than a full HBM stream), so chunking is off unless
+  // PE_COARSE_CHUNK_MB sets a budget.
+  static const double budget = getenv("PE_COARSE_CHUNK_MB") ? atof(getenv("PE_COARSE_CHUNK_MB")) * 1e6
+                                                            : 0.0;
   const double phi_bytes = 8.0 * d * d;
-  const double budget = 60e6;
-  const int ec = (N > 1 && phi_bytes <= budget) ? std::max(1, std::min(E, (int)(budget / phi_bytes)))
-                                                : E;
-  const bool keep = ec < E || (N > 1 && phi_bytes * E <= budget);
+  const int ec = (budget > 0 && N > 1 && phi_bytes <= budget)
+                     ? std::max(1, std::min(E, (int)(budget / phi_bytes)))
+                     : E;
+  const bool keep = budget > 0 && (ec < E || (N > 1 && phi_bytes * E <= budget));
   for (int e0 = 0; e0 < E; e0 += ec) {
     const int m = std::min(ec, E - e0);
     for (int n = 0; n < N; ++n) {

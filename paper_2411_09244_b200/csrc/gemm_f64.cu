@@ -962,6 +962,7 @@ constexpr size_t RB_SMEM = (size_t)RB_STAGES * RB_STAGE + 1024 + 2 * RB_STAGES *
 
 struct alignas(64) RowBalArgs {
   CUtensorMap ta[2];  // A segment maps {K_s, E * M} (box 16 x 8 rows)
+  CUtensorMap ta4[2];  // the same with 32-row boxes (a full warp's four blocks, one TMA)
   CUtensorMap tb[2];  // B segment maps {K_s, E * N} (box 16 x 8 FN rows)
   GemmParams p;
   int blocks;         // E * M / 8
@@ -1031,30 +1032,42 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
 
   if (warp == RB_WARPS) {  // producer
     if (lane == 0) {
+      // per consumer warp: global first row, block count, compact smem slot, all-zero flag
+      int wrow[RB_WARPS], wcnt[RB_WARPS], wslot[RB_WARPS];
+      bool wz[RB_WARPS];
+      int bytes_all = 0, bytes_nz = 0;
+#pragma unroll
+      for (int w = 0; w < RB_WARPS; ++w) {
+        int part = 0, fb = 0, cnt = 0;
+        if (w < pl.nw) wplace(w, part, fb, cnt);
+        wrow[w] = pl.e[part] * p.M + fb * 8;
+        wcnt[w] = cnt;
+        wslot[w] = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);
+        wz[w] = fb + cnt <= zr_blocks;
+        bytes_all += cnt * 1024;
+        if (!wz[w]) bytes_nz += cnt * 1024;
+      }
+      const int nparts = pl.nb[1] ? 2 : 1;
       for (int gk = 0; gk < ktot; ++gk) {
         const int st = gk % RB_STAGES;
         if (gk >= RB_STAGES) mbar_wait_cta(bar_empty + 8 * st, ((gk / RB_STAGES) - 1) & 1);
         const int s = gk < kt0 ? 0 : 1;
         const int kk = (s ? gk - kt0 : gk) * 16;
+        const bool zt = gk >= zt0 && gk < zt1;
         const unsigned full = bar_full + 8 * st;
-        int boxes = 0;
-        for (int w = 0; w < pl.nw; ++w) {
-          int part, fb, cnt;
-          wplace(w, part, fb, cnt);
-          if (!skips(fb, cnt, gk)) boxes += cnt;
-        }
-        mbar_expect_tx(full, boxes * 1024 + (pl.nb[1] ? 2 : 1) * RB_B_BYTES);
+        mbar_expect_tx(full, (zt ? bytes_nz : bytes_all) + nparts * RB_B_BYTES);
         const unsigned dA = sbase + st * RB_STAGE;
-        for (int w = 0; w < pl.nw; ++w) {
-          int part, fb, cnt;
-          wplace(w, part, fb, cnt);
-          if (skips(fb, cnt, gk)) continue;
-          const int slot0 = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);  // compact A slots
-          for (int x = 0; x < cnt; ++x)
-            tma_load_4d(dA + (slot0 + x) * 1024, &a.ta[s], kk,
-                        pl.e[part] * p.M + (fb + x) * 8, 0, 0, full);
+#pragma unroll
+        for (int w = 0; w < RB_WARPS; ++w) {
+          if (wcnt[w] == 0 || (zt && wz[w])) continue;
+          if (wcnt[w] == RB_FM) {
+            tma_load_4d(dA + wslot[w] * 1024, &a.ta4[s], kk, wrow[w], 0, 0, full);
+          } else {
+            for (int x = 0; x < wcnt[w]; ++x)
+              tma_load_4d(dA + (wslot[w] + x) * 1024, &a.ta[s], kk, wrow[w] + 8 * x, 0, 0, full);
+          }
         }
-        for (int part = 0; part < (pl.nb[1] ? 2 : 1); ++part)
+        for (int part = 0; part < nparts; ++part)
           tma_load_4d(dA + RB_A_BYTES + part * RB_B_BYTES, &a.tb[s], kk, pl.e[part] * p.N, 0, 0,
                       full);
       }
@@ -1172,6 +1185,7 @@ void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int z
     int use[2];
     // rows of all members as one 2-D extent (member-major stack)
     encode_operand(&a.ta[s], use, g.A.p, g.K, p.M * p.nb1, g.A.s0, 0, 1, 0, 1, 8);
+    encode_operand(&a.ta4[s], use, g.A.p, g.K, p.M * p.nb1, g.A.s0, 0, 1, 0, 1, 8 * RB_FM);
     encode_operand(&a.tb[s], use, g.B.p, g.K, p.N * p.nb1, g.B.s1, 0, 1, 0, 1, 8 * RB_FN);
   }
   a.blocks = (int)blocks;
