@@ -346,18 +346,12 @@ __global__ void __launch_bounds__(COARSE_THREADS, 1) coarse_kernel(const __grid_
 constexpr int CS_THREADS = 256;
 constexpr int CS_WARPS = CS_THREADS / 32;
 
-template <bool KEEP>
-__device__ __forceinline__ double ld_phi(const double* p) {
-  return KEEP ? __ldcg(p) : __ldcs(p);  // L2-resident member chunk vs one-pass stream
-}
-
-template <bool KEEP>
 __global__ void __launch_bounds__(CS_THREADS)
-    coarse_step_stream_kernel(int d, int n, int N, int e0, const double* __restrict__ Phi,
+    coarse_step_stream_kernel(int d, int n, int N, const double* __restrict__ Phi,
                               const double* __restrict__ gvec, const double* X_old,
                               const double* F_hat, double* G_cache, double* X_new,
                               double* partial, const int* active) {
-  const int e = e0 + blockIdx.y;
+  const int e = blockIdx.y;
   if (active && active[e] == 0) {
     if (n == 0) {  // frozen member: copy the whole iterate once
       const double* xo = X_old + (long long)e * (N + 1) * d;
@@ -391,7 +385,7 @@ __global__ void __launch_bounds__(CS_THREADS)
     for (; k + 224 < d; k += 256) {
       double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = ld_phi<KEEP>(row + k + 32 * u);
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(row + k + 32 * u);
       a0 = fma(v[0], xs[k], a0);
       a1 = fma(v[1], xs[k + 32], a1);
       a2 = fma(v[2], xs[k + 64], a2);
@@ -402,12 +396,12 @@ __global__ void __launch_bounds__(CS_THREADS)
       a3 = fma(v[7], xs[k + 224], a3);
     }
     for (; k + 96 < d; k += 128) {
-      a0 = fma(ld_phi<KEEP>(row + k), xs[k], a0);
-      a1 = fma(ld_phi<KEEP>(row + k + 32), xs[k + 32], a1);
-      a2 = fma(ld_phi<KEEP>(row + k + 64), xs[k + 64], a2);
-      a3 = fma(ld_phi<KEEP>(row + k + 96), xs[k + 96], a3);
+      a0 = fma(__ldcs(row + k), xs[k], a0);
+      a1 = fma(__ldcs(row + k + 32), xs[k + 32], a1);
+      a2 = fma(__ldcs(row + k + 64), xs[k + 64], a2);
+      a3 = fma(__ldcs(row + k + 96), xs[k + 96], a3);
     }
-    for (; k < d; k += 32) a0 = fma(ld_phi<KEEP>(row + k), xs[k], a0);
+    for (; k < d; k += 32) a0 = fma(__ldcs(row + k), xs[k], a0);
     double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -486,38 +480,16 @@ static void coarse_correct_stream(int E, int d, int N, const double* Phi, const 
   const size_t smem = sizeof(double) * d;
   static bool attr = false;
   if (!attr) {
-    PE_CUDA_CHECK(cudaFuncSetAttribute(coarse_step_stream_kernel<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    PE_CUDA_CHECK(cudaFuncSetAttribute(coarse_step_stream_kernel<true>,
+    PE_CUDA_CHECK(cudaFuncSetAttribute(coarse_step_stream_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
   if (smem > 200 * 1024) throw Error{PE_ERR_ARG, "coarse state too large for one SM"};
-  // Members are independent: member chunks can run through all N steps so that a chunk's
-  // Phi is read from HBM once and from L2 afterwards (same arithmetic, per member).
-  // Measured at cfg4 (64 x 2.9 MB): chunks of 20 members through all 32 steps took 128 x
-  // 29.7 us against 32 x 43.7 us for the one-pass stream of all members (the chunk's 58 MB
-  // did not come back from L2 faster than a full HBM stream), so chunking is off unless
-  // PE_COARSE_CHUNK_MB sets a budget.
-  static const double budget = getenv("PE_COARSE_CHUNK_MB") ? atof(getenv("PE_COARSE_CHUNK_MB")) * 1e6
-                                                            : 0.0;
-  const double phi_bytes = 8.0 * d * d;
-  const int ec = (budget > 0 && N > 1 && phi_bytes <= budget)
-                     ? std::max(1, std::min(E, (int)(budget / phi_bytes)))
-                     : E;
-  const bool keep = budget > 0 && (ec < E || (N > 1 && phi_bytes * E <= budget));
-  for (int e0 = 0; e0 < E; e0 += ec) {
-    const int m = std::min(ec, E - e0);
-    for (int n = 0; n < N; ++n) {
-      if (keep)
-        coarse_step_stream_kernel<true><<<dim3(nb, m), CS_THREADS, smem, st>>>(
-            d, n, N, e0, Phi, gvec, X_old, F_hat, G_cache, X_new, partial, active);
-      else
-        coarse_step_stream_kernel<false><<<dim3(nb, m), CS_THREADS, smem, st>>>(
-            d, n, N, e0, Phi, gvec, X_old, F_hat, G_cache, X_new, partial, active);
-      ++g_launches;
-      PE_CUDA_CHECK(cudaGetLastError());
-    }
+  for (int n = 0; n < N; ++n) {
+    coarse_step_stream_kernel<<<dim3(nb, E), CS_THREADS, smem, st>>>(
+        d, n, N, Phi, gvec, X_old, F_hat, G_cache, X_new, partial, active);
+    ++g_launches;
+    PE_CUDA_CHECK(cudaGetLastError());
   }
   if (diff) {
     coarse_norm_reduce_kernel<<<E, 256, 0, st>>>(N, nb, partial, diff, active);
