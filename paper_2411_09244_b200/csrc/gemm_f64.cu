@@ -954,8 +954,8 @@ static void launch_tma_best(const GemmParams& p, cudaStream_t st) {
 // one 8-row 128B-swizzled TMA box per loaded m-block and one box per B tile.  Same
 // canonical k order and epilogue as the other kernels, so a result differs from theirs only
 // by the omitted +0 terms.
-constexpr int RB_WARPS = 10, RB_FM = 4, RB_FN = 4, RB_STAGES = 5;  // 11 warps: <= 3 per SMSP
-constexpr int RB_MAXB = 33;  // m-blocks per CTA range (264 rows): ceil(a/4)+ceil(b/4) <= 10
+constexpr int RB_WARPS = 11, RB_FM = 4, RB_FN = 4, RB_STAGES = 4;  // 12 warps: 3 per SMSP
+constexpr int RB_MAXB = 40;  // m-blocks per CTA range: ceil(a/4) + ceil(b/4) <= 11
 constexpr int RB_A_BYTES = RB_MAXB * 1024, RB_B_BYTES = 8 * RB_FN * 128;
 constexpr int RB_STAGE = RB_A_BYTES + 2 * RB_B_BYTES;
 constexpr size_t RB_SMEM = (size_t)RB_STAGES * RB_STAGE + 1024 + 2 * RB_STAGES * 8;
@@ -967,6 +967,9 @@ struct alignas(64) RowBalArgs {
   GemmParams p;
   int blocks;         // E * M / 8
   int zero_rows, zk0, zk1;
+  // work-weighted split: a member-local block below zero_rows / 8 weighs wu k-tiles (its
+  // zero k-tiles are skipped), any other block ww; CTA c starts at weight W c / grid
+  int wu, ww, zrb;
 };
 
 // CTA range -> up to two parts (member, first member-local block, block count) and the
@@ -974,10 +977,26 @@ struct alignas(64) RowBalArgs {
 struct RbPlan {
   int e[2], sb[2], nb[2], w0, nw;
 };
+// first block whose cumulative weight reaches w (blocks in member-major order)
+__device__ __forceinline__ long long rb_block_at(const RowBalArgs& a, long long w) {
+  const int mb = a.p.M / 8;
+  const long long wm = (long long)a.zrb * a.wu + (long long)(mb - a.zrb) * a.ww;
+  const long long e = w / wm;
+  long long r = w - e * wm;
+  long long b;
+  if (r < (long long)a.zrb * a.wu)
+    b = (r + a.wu - 1) / a.wu;
+  else
+    b = a.zrb + (r - (long long)a.zrb * a.wu + a.ww - 1) / a.ww;
+  return e * mb + b;
+}
 __device__ __forceinline__ RbPlan rb_plan(const RowBalArgs& a) {
   const int mb = a.p.M / 8;
-  const long long b0 = (long long)a.blocks * blockIdx.x / gridDim.x;
-  const long long b1 = (long long)a.blocks * (blockIdx.x + 1) / gridDim.x;
+  const long long E = a.blocks / mb;
+  const long long W = E * ((long long)a.zrb * a.wu + (long long)(mb - a.zrb) * a.ww);
+  const long long b0 = blockIdx.x == 0 ? 0 : rb_block_at(a, W * blockIdx.x / gridDim.x);
+  const long long b1 = blockIdx.x + 1 == gridDim.x ? a.blocks
+                                                   : rb_block_at(a, W * (blockIdx.x + 1) / gridDim.x);
   RbPlan r;
   r.e[0] = (int)(b0 / mb);
   r.sb[0] = (int)(b0 - (long long)r.e[0] * mb);
@@ -1150,7 +1169,17 @@ static int num_sms() {
   return nsm;
 }
 
-bool gemm_rowbalanced_eligible(const GemmParams& p) {
+// work weights of the two block kinds (k-tiles multiplied): wu below zero_rows, ww above
+static void rb_weights(const GemmParams& p, int zero_rows, int zero_k0, int zero_k1, int& wu,
+                       int& ww, int& zrb) {
+  const int kt0 = (p.seg[0].K + 15) / 16, kt1 = p.nseg > 1 ? (p.seg[1].K + 15) / 16 : 0;
+  const int nz = p.nseg > 1 ? std::max(0, zero_k1 / 16 - (zero_k0 + 15) / 16) : 0;
+  ww = kt0 + kt1;
+  wu = std::max(1, ww - nz);
+  zrb = p.nseg > 1 ? std::min(std::max(zero_rows, 0) / 8, p.M / 8) : 0;
+}
+
+bool gemm_rowbalanced_eligible(const GemmParams& p, int zero_rows, int zero_k0, int zero_k1) {
   static const bool off = getenv("PE_GEMM_NO_ROWBAL") != nullptr;
   if (off || p.nb2 != 1 || p.nb1 < 2 || p.M % 8 || p.N > 8 * RB_FN || p.N < 1 || p.nseg < 1 ||
       p.nseg > 2 || p.nrm || p.Cin || !tma_ok(p))
@@ -1161,14 +1190,21 @@ bool gemm_rowbalanced_eligible(const GemmParams& p) {
     if (A.b1 != (long long)p.M * A.s0 || B.b1 != (long long)p.N * B.s1) return false;
   }
   const long long blocks = (long long)p.nb1 * (p.M / 8);
+  if (blocks > INT32_MAX) return false;
+  int wu, ww, zrb;
+  rb_weights(p, zero_rows, zero_k0, zero_k1, wu, ww, zrb);
+  const int mb = p.M / 8;
+  const long long W = (long long)p.nb1 * ((long long)zrb * wu + (long long)(mb - zrb) * ww);
   const int grid = (int)std::min<long long>(num_sms(), blocks);
-  const long long per = (blocks + grid - 1) / grid;
-  return blocks <= INT32_MAX && per <= RB_MAXB && per <= p.M / 8;
+  // longest possible range: all of it in the cheaper kind, +2 for the rounding at both ends
+  const double per = (double)W / grid / std::min(wu, ww) + 2.0;
+  return per <= RB_MAXB && per <= mb;
 }
 
 void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int zero_k1,
                           cudaStream_t st) {
-  if (!gemm_rowbalanced_eligible(p)) throw Error{PE_ERR_ARG, "rowbalanced: shape not eligible"};
+  if (!gemm_rowbalanced_eligible(p, zero_rows, zero_k0, zero_k1))
+    throw Error{PE_ERR_ARG, "rowbalanced: shape not eligible"};
   const long long blocks = (long long)p.nb1 * (p.M / 8);
   static bool attr = false;
   if (!attr) {
@@ -1192,6 +1228,7 @@ void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int z
   a.zero_rows = zero_rows;
   a.zk0 = zero_k0;
   a.zk1 = zero_k1;
+  rb_weights(p, zero_rows, zero_k0, zero_k1, a.wu, a.ww, a.zrb);
   const int grid = (int)std::min<long long>(num_sms(), blocks);
   launch_k(gemm_rowbal_kernel, dim3(grid), dim3((RB_WARPS + 1) * 32), RB_SMEM, st, a);
   ++g_launches;

@@ -206,7 +206,7 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
       }
       // ensembles: one row-balanced persistent launch per step, skipping T's exact-zero
       // u x Du block (rows < d1, D-segment columns < d1); else the tiled kernels
-      if (gemm_rowbalanced_eligible(p)) {
+      if (gemm_rowbalanced_eligible(p, Ds ? c->d1 : 0, 0, Ds ? c->d1 : 0)) {
         // algorithmic flops: the skipped u x Du block is a structural zero
         const double zero = Ds ? 2.0 * ec * nc * (double)c->d1 * c->d1 : 0.0;
         profiled(c, gemm_flops(p) - zero, st, [&] {

@@ -106,7 +106,7 @@ void gemm_f64(const GemmParams& p, cudaStream_t st);
 // Row-balanced persistent launch for batched skinny products (ensemble fine step); rows
 // below zero_rows have exact zeros in the second segment's k-range [zero_k0, zero_k1)
 // (segment-local), skipped.  Only for shapes with gemm_rowbalanced_eligible(p).
-bool gemm_rowbalanced_eligible(const GemmParams& p);
+bool gemm_rowbalanced_eligible(const GemmParams& p, int zero_rows, int zero_k0, int zero_k1);
 void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int zero_k1,
                           cudaStream_t st);
 // Flop count of one launch (2*M*N*sumK*batch), for the roofline bookkeeping.
