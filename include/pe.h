@@ -242,6 +242,14 @@ int pe_project_initial(int n, int d1, int d2, const int* M_ptr, const int* M_idx
                        const double* P_val, const double* M11, const double* M22,
                        const double* u0, double* u_out, double* w_out, void* stream);
 
+/* SplitPropagators.stability_max_step (stepping.py:191-207) for one member of the context:
+ * power iteration on M22^-1 A22 with the reference's Rayleigh quotient and stopping rule
+ * (|lam_new - lam| <= tol |lam_new|, at most max_iter iterations).  bound = 2 / lam
+ * (INFINITY when d2 = 0 or A22 = 0); iterations (optional) = the count, negative when
+ * max_iter was hit (the reference warns and returns the last bound). */
+int pe_stability_max_step(pe_ctx* ctx, int member, double tol, int max_iter, double* bound,
+                          int* iterations, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

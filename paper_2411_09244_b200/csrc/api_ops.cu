@@ -231,6 +231,108 @@ __global__ void k_csc_tdot(int d, const int* __restrict__ cp, const int* __restr
   if (lane == 0) f[j] = s;
 }
 
+// ------------------------------------------------------------------ stability bound
+// Power iteration of stepping.py:191-207 on P = M22^-1 A22: z = P v / ||P v||,
+// lam = (z^T A22 z) / (z^T M22 z), stop when |lam_new - lam| <= tol |lam_new|.  One warp per
+// row for the three products, block partials summed in a fixed order by one thread; every
+// kernel returns at once when st[0] (done) is set, so batches of iterations can be enqueued.
+struct PowerState {
+  double lam, lam_new;
+  int done, iters;
+};
+
+__global__ void k_pw_gemv(int n, const double* __restrict__ P, const double* __restrict__ v,
+                          double* __restrict__ y, double* __restrict__ part,
+                          const PowerState* ps) {
+  if (ps->done) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double wp[8];
+  double acc2 = 0.0;
+  for (int r = blockIdx.x * 8 + warp; r < n; r += gridDim.x * 8) {
+    double a = 0.0;
+    for (int k = lane; k < n; k += 32) a = fma(P[(long long)r * n + k], v[k], a);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) {
+      y[r] = a;
+      acc2 = fma(a, a, acc2);
+    }
+  }
+  if (lane == 0) wp[warp] = acc2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += wp[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_pw_rq(int n, const double* __restrict__ A, const double* __restrict__ M,
+                        const double* __restrict__ y, const double* __restrict__ ypart, int nb,
+                        double* __restrict__ z, double* __restrict__ part, const PowerState* ps) {
+  if (ps->done) return;
+  // every block recomputes ||y|| from the same partials in the same order (identical bits)
+  __shared__ double nrm;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < nb; ++b) t += ypart[b];
+    nrm = sqrt(t);
+  }
+  __syncthreads();
+  const double inv = nrm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double wa[8], wm[8];
+  double sa = 0.0, sm = 0.0;
+  for (int r = blockIdx.x * 8 + warp; r < n; r += gridDim.x * 8) {
+    double a = 0.0, m = 0.0;
+    for (int k = lane; k < n; k += 32) {
+      const double zk = y[k] / inv;
+      a = fma(A[(long long)r * n + k], zk, a);
+      m = fma(M[(long long)r * n + k], zk, m);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      m += __shfl_xor_sync(0xffffffffu, m, o);
+    }
+    if (lane == 0) {
+      const double zr = y[r] / inv;
+      z[r] = zr;
+      sa = fma(zr, a, sa);
+      sm = fma(zr, m, sm);
+    }
+  }
+  if (lane == 0) {
+    wa[warp] = sa;
+    wm[warp] = sm;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ta = 0.0, tm = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      ta += wa[w];
+      tm += wm[w];
+    }
+    part[2 * blockIdx.x] = ta;
+    part[2 * blockIdx.x + 1] = tm;
+  }
+}
+
+__global__ void k_pw_finish(int nb, const double* __restrict__ part, double tol, int max_iter,
+                            PowerState* ps) {
+  if (ps->done) return;
+  double ta = 0.0, tm = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    ta += part[2 * b];
+    tm += part[2 * b + 1];
+  }
+  const double lam_new = ta / tm;
+  const bool done = fabs(lam_new - ps->lam) <= tol * fabs(lam_new);
+  ps->lam = lam_new;
+  ps->iters += 1;
+  if (done || ps->iters >= max_iter) ps->done = done ? 1 : 2;
+}
+
 int grid_for(long long n, int threads) {
   long long g = (n + threads - 1) / threads;
   return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 32));
@@ -491,5 +593,109 @@ extern "C" int pe_project_initial(int n, int d1, int d2, const int* M_ptr, const
     solve(d1, M11, b.p, u_out);
     solve(d2, M22, b.p + d1, w_out);
     PE_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+extern "C" int pe_stability_max_step(pe_ctx* c, int member, double tol, int max_iter,
+                                     double* bound, int* iterations, void* stream) {
+  return api_guard("pe_stability_max_step", [&] {
+    require_arg(c && bound && member >= 0 && member < c->E && max_iter >= 1 && tol > 0,
+                "need a context, a member index, tol > 0, max_iter >= 1 and an output");
+    PE_CUDA_CHECK(cudaSetDevice(c->device));
+    const int n = c->d2;
+    if (iterations) *iterations = 0;
+    const double* A22 = c->A22.d() + (size_t)member * n * n;
+    const double* M22 = c->M22.d() + (size_t)member * n * n;
+    if (n == 0) {
+      *bound = INFINITY;
+      return;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    // A22 == 0 (stepping.py:194): infinite bound
+    {
+      std::vector<double> h((size_t)n * n);
+      PE_CUDA_CHECK(cudaMemcpyAsync(h.data(), A22, sizeof(double) * h.size(),
+                                    cudaMemcpyDeviceToHost, st));
+      PE_CUDA_CHECK(cudaStreamSynchronize(st));
+      double mx = 0.0;
+      for (double x : h) mx = std::max(mx, std::fabs(x));
+      if (mx == 0.0) {
+        *bound = INFINITY;
+        return;
+      }
+    }
+    // P = M22^-1 A22 by Cholesky (cho_solve, stepping.py:199): potrs on the column-major
+    // copies (M22 is symmetric, so its row-major storage is its column-major storage; A22 is
+    // transposed into column-major on the host), then P back to row-major for the GEMV
+    Dev<double> L((size_t)n * n), P((size_t)n * n), v(n), y(n), z(n), part(3 * 512);
+    Dev<int> info(2);
+    Dev<PowerState> ps(1);
+    PE_CUDA_CHECK(cudaMemcpyAsync(L.p, M22, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
+    {
+      std::vector<double> h((size_t)n * n);
+      PE_CUDA_CHECK(cudaMemcpyAsync(h.data(), A22, sizeof(double) * h.size(),
+                                    cudaMemcpyDeviceToHost, st));
+      PE_CUDA_CHECK(cudaStreamSynchronize(st));
+      std::vector<double> t((size_t)n * n);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) t[(size_t)j * n + i] = h[(size_t)i * n + j];
+      PE_CUDA_CHECK(cudaMemcpyAsync(P.p, t.data(), sizeof(double) * t.size(),
+                                    cudaMemcpyHostToDevice, st));
+      cusolverDnHandle_t h2 = nullptr;
+      if (cusolverDnCreate(&h2) != CUSOLVER_STATUS_SUCCESS)
+        throw Error{PE_ERR_SOLVER, "cusolverDnCreate failed"};
+      struct HG {
+        cusolverDnHandle_t h;
+        ~HG() { cusolverDnDestroy(h); }
+      } hg{h2};
+      cusolverDnSetStream(h2, st);
+      int lw = 0;
+      cusolverDnDpotrf_bufferSize(h2, CUBLAS_FILL_MODE_LOWER, n, L.p, n, &lw);
+      Dev<double> work(lw > 0 ? lw : 1);
+      if (cusolverDnDpotrf(h2, CUBLAS_FILL_MODE_LOWER, n, L.p, n, work.p, lw, info.p) !=
+              CUSOLVER_STATUS_SUCCESS ||
+          cusolverDnDpotrs(h2, CUBLAS_FILL_MODE_LOWER, n, n, L.p, n, P.p, n, info.p + 1) !=
+              CUSOLVER_STATUS_SUCCESS)
+        throw Error{PE_ERR_SOLVER, "potrf/potrs failed"};
+      int hi[2] = {0, 0};
+      PE_CUDA_CHECK(cudaMemcpyAsync(hi, info.p, sizeof(hi), cudaMemcpyDeviceToHost, st));
+      PE_CUDA_CHECK(cudaStreamSynchronize(st));
+      if (hi[0] != 0) throw Error{PE_ERR_SOLVER, "M22 is not positive definite"};
+      // X (column-major) = M22^-1 A22 = P: to row-major
+      PE_CUDA_CHECK(cudaMemcpyAsync(t.data(), P.p, sizeof(double) * t.size(),
+                                    cudaMemcpyDeviceToHost, st));
+      PE_CUDA_CHECK(cudaStreamSynchronize(st));
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) h[(size_t)i * n + j] = t[(size_t)j * n + i];
+      PE_CUDA_CHECK(cudaMemcpyAsync(P.p, h.data(), sizeof(double) * h.size(),
+                                    cudaMemcpyHostToDevice, st));
+    }
+    {
+      std::vector<double> v0(n, 1.0 / std::sqrt((double)n));
+      PE_CUDA_CHECK(cudaMemcpyAsync(v.p, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      PowerState p0{0.0, 0.0, 0, 0};
+      PE_CUDA_CHECK(cudaMemcpyAsync(ps.p, &p0, sizeof(p0), cudaMemcpyHostToDevice, st));
+    }
+    const int nb = std::min(512, (n + 7) / 8);
+    PowerState hp{};
+    double* bufs[2] = {v.p, z.p};
+    int it = 0;
+    while (it < max_iter) {
+      const int chunk = std::min(64, max_iter - it);
+      for (int q = 0; q < chunk; ++q, ++it) {
+        double* vin = bufs[it & 1];
+        double* vout = bufs[(it + 1) & 1];
+        k_pw_gemv<<<nb, 256, 0, st>>>(n, P.p, vin, y.p, part.p, ps.p);
+        k_pw_rq<<<nb, 256, 0, st>>>(n, A22, M22, y.p, part.p, nb, vout, part.p + nb, ps.p);
+        k_pw_finish<<<1, 1, 0, st>>>(nb, part.p + nb, tol, max_iter, ps.p);
+        g_launches += 3;
+      }
+      PE_CUDA_CHECK(cudaGetLastError());
+      PE_CUDA_CHECK(cudaMemcpyAsync(&hp, ps.p, sizeof(hp), cudaMemcpyDeviceToHost, st));
+      PE_CUDA_CHECK(cudaStreamSynchronize(st));
+      if (hp.done) break;
+    }
+    *bound = 2.0 / hp.lam;
+    if (iterations) *iterations = hp.done == 1 ? hp.iters : -hp.iters;  // < 0: hit max_iter
   });
 }

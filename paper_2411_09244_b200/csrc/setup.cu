@@ -165,21 +165,19 @@ static void inverse(pe_ctx* c, int n, const double* A, double* Ainv) {
   PE_CUDA_CHECK(cudaStreamSynchronize(st));
 }
 
+// (d_k M11 + A11)^-1 by LU + solve against I, enqueued without a host round trip: the
+// factorisation status goes to info[slot] (checked once per setup, after every mode).
 static void zinverse(pe_ctx* c, int n, cuDoubleComplex* S, cuDoubleComplex* Sinv, DevBuf& ipiv,
-                     DevBuf& info, DevBuf& work) {
+                     int* info_slot, DevBuf& work) {
   cudaStream_t st = c->setup_stream;
   int lwork = 0;
   SOLVER_CHECK(cusolverDnZgetrf_bufferSize(c->solver, n, n, S, n, &lwork));
   work.ensure(sizeof(cuDoubleComplex) * std::max(lwork, 1));
   ipiv.ensure(sizeof(int) * n);
-  info.ensure(sizeof(int));
-  SOLVER_CHECK(cusolverDnZgetrf(c->solver, n, n, S, n, (cuDoubleComplex*)work.p, ipiv.i(), info.i()));
-  int h_info = 0;
-  PE_CUDA_CHECK(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  PE_CUDA_CHECK(cudaStreamSynchronize(st));
-  if (h_info != 0) throw Error{PE_ERR_SOLVER, "singular shifted matrix d_k M11 + A11 (zgetrf info " + std::to_string(h_info) + ")"};
+  SOLVER_CHECK(cusolverDnZgetrf(c->solver, n, n, S, n, (cuDoubleComplex*)work.p, ipiv.i(), info_slot));
   zidentity_kernel<<<grid_for((long long)n * n), 256, 0, st>>>(n, Sinv);
-  SOLVER_CHECK(cusolverDnZgetrs(c->solver, CUBLAS_OP_N, n, n, S, n, ipiv.i(), Sinv, n, info.i()));
+  SOLVER_CHECK(cusolverDnZgetrs(c->solver, CUBLAS_OP_N, n, n, S, n, ipiv.i(), Sinv, n,
+                                info_slot + 1));
 }
 
 void setup_sequential(pe_ctx* c, double dt) {
@@ -606,6 +604,8 @@ static void setup_allatonce_general(pe_ctx* c, double dt, double alpha, int npm,
   Sinv.ensure(sizeof(cuDoubleComplex) * (size_t)d1 * d1 + 16);
   M22inv.ensure(sizeof(double) * (size_t)d2 * d2 + 8);
   const double om_r = std::pow(alpha, 1.0 / J);
+  info.ensure(sizeof(int) * 2 * (size_t)E * (J / 2 + 1) + 8);
+  PE_CUDA_CHECK(cudaMemsetAsync(info.p, 0, info.bytes, st));
   for (int e = 0; e < E; ++e) {
     const double* M11 = c->M11.d() + (size_t)e * d1 * d1;
     const double* A11 = c->A11.d() + (size_t)e * d1 * d1;
@@ -624,7 +624,8 @@ static void setup_allatonce_general(pe_ctx* c, double dt, double alpha, int npm,
         const double dim = (-om_r * std::sin(ang)) / dt;
         shifted_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
             d1, dre, dim, M11, A11, (cuDoubleComplex*)S.p);
-        zinverse(c, d1, (cuDoubleComplex*)S.p, (cuDoubleComplex*)Sinv.p, ipiv, info, work);
+        zinverse(c, d1, (cuDoubleComplex*)S.p, (cuDoubleComplex*)Sinv.p, ipiv,
+                 info.i() + 2 * ((size_t)e * (J / 2 + 1) + k), work);
         if (k == 0 || (even && 2 * k == J))  // real modes: diagonal block of pseudo-mode 0
           real_block_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
               d1, (const cuDoubleComplex*)Sinv.p, Bk0, k == 0 ? 0 : 1);
@@ -655,6 +656,18 @@ static void setup_allatonce_general(pe_ctx* c, double dt, double alpha, int npm,
         rm_gemm(h, true, true, d2, d1, d2, -1.0, M22inv.d(), d2, M12, d2, 0.0, GW + d1, 2 * d1);
       }
     }
+  }
+  if (d1) {  // one host round trip for every mode's factorisation status
+    std::vector<int> h_info(2 * (size_t)E * (J / 2 + 1));
+    PE_CUDA_CHECK(cudaMemcpyAsync(h_info.data(), info.p, sizeof(int) * h_info.size(),
+                                  cudaMemcpyDeviceToHost, st));
+    PE_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (size_t q = 0; q < h_info.size(); ++q)
+      if (h_info[q] != 0)
+        throw Error{PE_ERR_SOLVER, "singular shifted matrix d_k M11 + A11 (member " +
+                                       std::to_string(q / 2 / (J / 2 + 1)) + ", mode " +
+                                       std::to_string((q / 2) % (J / 2 + 1)) + ", info " +
+                                       std::to_string(h_info[q]) + ")"};
   }
   if (wr_tiny_eligible(d1, d2, J, npm)) {  // transposed Bk for the fused small-problem path
     c->BkT.ensure(sizeof(double) * (size_t)E * npm * 4 * d1 * d1 + 8);

@@ -163,31 +163,23 @@ class SplitPropagators:
         return SplitTrajectory(times, traj[:, :d1].copy(), traj[:, d1:].copy(), cur)
 
     def stability_max_step(self, tol: float = 1e-10, max_iter: int = 10000) -> float:
-        """2 / lambda_max(M22^{-1} A22) by power iteration (stepping.py:191-207).
+        """2 / lambda_max(M22^{-1} A22) by power iteration (stepping.py:191-207), in libpe
+        (pe_stability_max_step: the reference's start vector, Rayleigh quotient and stop)."""
+        import ctypes as C
 
-        Setup-time helper; runs in FP64 on the GPU through torch.
-        """
+        from ._lib import check
+
         s = self.system
-        if s.d2 == 0 or np.abs(s.A22).max() == 0.0:
+        if s.d2 == 0:
             return np.inf
-        dev = torch.device("cuda", self.device if self.device is not None
-                           else torch.cuda.current_device())
-        m22 = torch.as_tensor(s.M22, dtype=torch.float64, device=dev)
-        a22 = torch.as_tensor(s.A22, dtype=torch.float64, device=dev)
-        chol = torch.linalg.cholesky(m22)
-        v = torch.full((s.d2, 1), 1.0 / np.sqrt(s.d2), dtype=torch.float64, device=dev)
-        lam = 0.0
-        for _ in range(max_iter):
-            z = torch.cholesky_solve(a22 @ v, chol)
-            z = z / torch.linalg.norm(z)
-            new = float((z.T @ (a22 @ z)) / (z.T @ (m22 @ z)))
-            done = abs(new - lam) <= tol * abs(new)
-            v, lam = z, new
-            if done:
-                return 2.0 / lam
-        log.warning("stability power iteration hit %d iterations, last rayleigh %.6e",
-                    max_iter, lam)
-        return 2.0 / lam
+        ctx = self.context(1)
+        out, its = C.c_double(0.0), C.c_int(0)
+        check(ctx.lib.pe_stability_max_step(ctx.ptr, 0, float(tol), int(max_iter),
+                                            C.byref(out), C.byref(its), ctx.stream()))
+        if its.value < 0:
+            log.warning("stability power iteration hit %d iterations, last rayleigh %.6e",
+                        max_iter, 2.0 / out.value)
+        return float(out.value)
 
     def check_substep(self, dt: float) -> None:
         bound = self.stability_max_step()

@@ -266,3 +266,29 @@ def test_example1_iteration_counts():
         if c != r:
             assert abs(c - r) == 1, (n, c, r)
             assert g[f"diffs_{n}"][min(c, r) - 1] < 2 * eps, (n, c, r)
+
+
+@pytest.mark.parametrize("name", ["sys_cfg0.npz", "sys_cfg2.npz"])
+def test_stability_max_step_matches_oracle(name):
+    """SplitPropagators.stability_max_step (stepping.py:191-207) in libpe against the
+    oracle's power iteration (same start vector, Rayleigh quotient and stop rule): 1e-9."""
+    P = _pkg()
+    from oracle import pe_oracle as po
+
+    z = golden(name)
+    blocks = [z[k] for k in ("M11", "A11", "M12", "A12", "M22", "A22")]
+    props = P.SplitPropagators(P.CoarseSystem(*blocks), P.ConstantLoads(z["f1"], z["f2"]))
+    ref = po.OracleSplit(po.OSystem(*blocks, z["f1"], z["f2"])).stability_max_step()
+    got = props.stability_max_step()
+    assert abs(got - ref) <= 1e-9 * ref, (got, ref)
+
+
+def test_stability_max_step_degenerate_blocks():
+    """d2 = 0 and A22 = 0 give an infinite bound (stepping.py:194-195)."""
+    P = _pkg()
+    u_only = P.CoarseSystem(np.eye(2), np.eye(2), np.zeros((2, 0)), np.zeros((2, 0)),
+                            np.zeros((0, 0)), np.zeros((0, 0)))
+    assert P.SplitPropagators(u_only, P.ConstantLoads.zero(u_only)).stability_max_step() == np.inf
+    w_free = P.CoarseSystem(np.eye(1), np.eye(1), np.zeros((1, 2)), np.zeros((1, 2)),
+                            np.eye(2), np.zeros((2, 2)))
+    assert P.SplitPropagators(w_free, P.ConstantLoads.zero(w_free)).stability_max_step() == np.inf
