@@ -250,6 +250,19 @@ int pe_project_initial(int n, int d1, int d2, const int* M_ptr, const int* M_idx
 int pe_stability_max_step(pe_ctx* ctx, int member, double tol, int max_iter, double* bound,
                           int* iterations, void* stream);
 
+/* CEM-GMsFEM basis of a uniform nx x nx Q1 grid cut into nb x nb blocks (
+ * msbasis.py:296-394 aux_eigen_cem + build_cem_basis for every block), host arrays:
+ * kappa (nx * nx cells, row-major), kt_scale (aux weight kt = kappa * kt_scale; nb^2 for
+ * the reference's "kappa_h2").  values: per block b the n_eig basis columns on the
+ * patch-interior nodes of b (row-major node order, layers rings of blocks, zero
+ * Dirichlet rim), column-major, starting at offsets[b] (offsets: nb^2 + 1 entries);
+ * eigenvalues (optional): nb^2 x n_eig aux eigenvalues; worst (optional): the largest
+ * constraint residual |C phi - e|.  pe_cem_basis_size gives the values length. */
+int pe_cem_basis(int nx, int nb, int layers, int n_eig, const double* kappa, double kt_scale,
+                 double* values, long long* offsets, double* eigenvalues, double* worst,
+                 void* stream);
+long long pe_cem_basis_size(int nx, int nb, int layers, int n_eig);
+
 #ifdef __cplusplus
 }
 #endif

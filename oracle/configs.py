@@ -123,3 +123,48 @@ def corner_load(nx, f_cells):
     ix = np.arange(1, nx)
     interior = (ix[:, None] * n1 + ix[None, :]).ravel()
     return b[interior]
+
+
+def kappa_field(name, member=0, background=1.0):
+    """Cell-wise coefficient of a config (generate_field, fem.py:150-162): background
+    everywhere, background * contrast on every channel / inclusion rectangle (half-open cell
+    ranges, row-major cells)."""
+    nx = CONFIGS[name]["nx"]
+    rects, contrast, _ = rectangles(name, member)
+    k = np.full((nx, nx), background)
+    for x0, x1, y0, y1 in rects:
+        k[y0:y1, x0:x1] = background * contrast
+    return k.ravel()
+
+
+Q1_STIFF = np.array([[4.0, -1.0, -2.0, -1.0], [-1.0, 4.0, -1.0, -2.0],
+                     [-2.0, -1.0, 4.0, -1.0], [-1.0, -2.0, -1.0, 4.0]]) / 6.0
+Q1_MASS = np.array([[4.0, 2.0, 1.0, 2.0], [2.0, 4.0, 2.0, 1.0],
+                    [1.0, 2.0, 4.0, 2.0], [2.0, 1.0, 2.0, 4.0]]) / 36.0
+
+
+def assemble_fine(nx, kappa):
+    """Interior-node Q1 mass and stiffness (fem.py:196-206, 277-289): element matrices
+    summed over cells (nodes SW, SE, NE, NW), symmetrised as (X + X^T) / 2, boundary rows
+    and columns removed.  Returns scipy CSR (M, A)."""
+    import scipy.sparse as sp
+
+    n1 = nx + 1
+    cells = np.arange(nx * nx)
+    cx, cy = cells % nx, cells // nx
+    n00 = cy * n1 + cx
+    conn = np.stack([n00, n00 + 1, n00 + n1 + 1, n00 + n1], axis=1)
+    rows = np.broadcast_to(conn[:, :, None], (nx * nx, 4, 4)).ravel()
+    cols = np.broadcast_to(conn[:, None, :], (nx * nx, 4, 4)).ravel()
+
+    def asm(data_cells, ref):
+        data = (data_cells[:, None, None] * ref[None]).ravel()
+        m = sp.coo_matrix((data, (rows, cols)), shape=(n1 * n1, n1 * n1)).tocsr()
+        return (m + m.T) * 0.5
+
+    h = 1.0 / nx
+    full_m = asm(np.full(nx * nx, h * h), Q1_MASS)
+    full_a = asm(np.asarray(kappa, dtype=float), Q1_STIFF)
+    ix = np.arange(1, nx)
+    idx = (ix[:, None] * n1 + ix[None, :]).ravel()
+    return full_m[idx][:, idx].tocsr(), full_a[idx][:, idx].tocsr()

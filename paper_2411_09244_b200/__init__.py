@@ -10,7 +10,8 @@ from .allatonce import (ImplicitAllAtOnce, TimeMatrixB, WaveformRelaxation,  # n
                         WRResult, apply_S, apply_S_inverse, build_rhs, build_time_matrix,
                         wr_fine_solve)
 from .engine import PeContext  # noqa: F401
-from .msbasis import CoarseSystem, project_coarse, project_load  # noqa: F401
+from .msbasis import (CemSpace, CoarseSystem, build_cem_space, project_coarse,  # noqa: F401
+                      project_load)
 from .parareal import (AllAtOnceFine, ParerealConfig, ParerealEnsemble,  # noqa: F401
                        ParerealRun,
                        SequentialFine, build_fine_propagator, check_stop, initial_sweep,

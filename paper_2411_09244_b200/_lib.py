@@ -76,6 +76,9 @@ SIGNATURES = {
     "pe_project_initial": (C.c_int, [C.c_int, C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _D, _D,
                                      _D, _D, _D, _P]),
     "pe_stability_max_step": (C.c_int, [_P, C.c_int, C.c_double, C.c_int, _D, _I, _P]),
+    "pe_cem_basis": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _D, C.c_double, _D,
+                               C.POINTER(C.c_longlong), _D, _D, _P]),
+    "pe_cem_basis_size": (C.c_longlong, [C.c_int, C.c_int, C.c_int, C.c_int]),
 }
 
 _lib = None

@@ -144,3 +144,24 @@ def test_config_runs_match_reference(run_name):
     if kind == "all-at-once":
         its = np.array([[i["iterations"] for i in sw] for sw in r["fine_info"]])
         np.testing.assert_array_equal(its, z["wr_iterations"])
+
+
+def test_config_kappa_and_fine_assembly_pinned():
+    """The harness's kappa generator and Q1 assembly (oracle/configs.py) reproduce the
+    reference's fine operators of config 0 (fine_cfg0.npz: M and the kappa-rescaled A)."""
+    import json
+
+    import scipy.sparse as sp
+
+    from oracle.configs import assemble_fine, kappa_field
+
+    z = golden("fine_cfg0.npz")
+    scale = json.loads(str(golden("sys_cfg0.npz")["meta"]))["kappa_scale"]
+    M, A = assemble_fine(40, kappa_field("cfg0"))
+
+    def ref(prefix):
+        return sp.csr_matrix((z[prefix + "_val"], z[prefix + "_idx"], z[prefix + "_ptr"]),
+                             shape=tuple(z[prefix + "_shape"]))
+
+    assert abs(M - ref("M")).max() <= 1e-15 * abs(ref("M")).max()
+    assert abs(A * scale - ref("A")).max() <= 1e-14 * abs(ref("A")).max()
