@@ -185,16 +185,18 @@ class ImplicitAllAtOnce:
                              f"{self.system.d1})")
         ctx = self.ctx
         nc = rhs.shape[0]
-        R = ctx.to_dev(rhs[None])
-        U = ctx.empty(1, nc, tm.substeps, self.system.d1)
-        res = ctx.empty(nc)
-        check(ctx.lib.pe_allatonce_usolve(ctx.ptr, C.c_void_p(R.data_ptr()),
-                                          C.c_void_p(U.data_ptr()), nc,
-                                          C.c_void_p(res.data_ptr()), ctx.stream()))
-        self.last_residual = float(res[-1].item())
+        with ctx.lock:
+            R = ctx.to_dev(rhs[None])
+            U = ctx.empty(1, nc, tm.substeps, self.system.d1)
+            res = ctx.empty(nc)
+            check(ctx.lib.pe_allatonce_usolve(ctx.ptr, C.c_void_p(R.data_ptr()),
+                                              C.c_void_p(U.data_ptr()), nc,
+                                              C.c_void_p(res.data_ptr()), ctx.stream()))
+            self.last_residual = float(res[-1].item())
+            U = U[0].cpu().numpy()
         self.last_imag_residue = 0.0
         log.debug("all-at-once residual %.3e", self.last_residual)
-        return U[0].cpu().numpy()
+        return U
 
 
 @dataclass
@@ -234,19 +236,20 @@ class WaveformRelaxation:
 
     def solve_all(self, states, trajectories: bool = True) -> list:
         ctx = self.ctx
-        ctx.prepare_allatonce(self.dt, self.alpha, self.tol, self.max_iter)
-        X = ctx.to_dev(np.array([s.stacked() for s in states])[None])
-        Y, sw, rs, rh = ctx.fine_allatonce(X)
         nc = len(states)
-        Y = Y[0].cpu().numpy()
-        sw = sw[0].cpu().numpy()
-        rs = rs[0].cpu().numpy()
-        rh = rh[0].cpu().numpy()
+        with ctx.lock:
+            ctx.prepare_allatonce(self.dt, self.alpha, self.tol, self.max_iter)
+            X = ctx.to_dev(np.array([s.stacked() for s in states])[None])
+            Y, sw, rs, rh = ctx.fine_allatonce(X)
+            Y = Y[0].cpu().numpy()
+            sw = sw[0].cpu().numpy()
+            rs = rs[0].cpu().numpy()
+            rh = rh[0].cpu().numpy()
+            if trajectories:
+                U, W = ctx.wr_waveforms(nc)
+                U = U[0].cpu().numpy()
+                W = W[0].cpu().numpy()
         d1 = self.system.d1
-        if trajectories:
-            U, W = ctx.wr_waveforms(nc)
-            U = U[0].cpu().numpy()
-            W = W[0].cpu().numpy()
         out = []
         for n, s in enumerate(states):
             it = int(sw[n])

@@ -5,6 +5,7 @@ operators in HBM, with torch tensors as the device buffers passed across the C A
 from __future__ import annotations
 
 import ctypes as C
+import threading
 
 import numpy as np
 import torch
@@ -41,6 +42,10 @@ class PeContext:
         check(self.lib.pe_create(C.byref(ptr), self.E, self.d1, self.d2, 1 << 24, self.J,
                                  device))
         self.ptr = ptr
+        # one libpe context is not thread-safe (shared work buffers); the reference lets
+        # callers invoke propagators from a thread pool (parareal.py:191-193), so every
+        # host-side use of the context is serialised (the GPU work is ordered anyway)
+        self.lock = threading.RLock()
         self._keep = []
         for m, (s, ld) in enumerate(zip(systems, loads)):
             if (s.d1, s.d2) != (self.d1, self.d2):

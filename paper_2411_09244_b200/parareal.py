@@ -63,9 +63,10 @@ class SequentialFine:
 
     def propagate_all(self, states):
         ctx = self.ctx
-        ctx.prepare_sequential(self.time_grid.dt_sub)
-        X = ctx.to_dev(np.array([s.stacked() for s in states])[None])
-        Y = ctx.fine_sequential(X)[0].cpu().numpy()
+        with ctx.lock:
+            ctx.prepare_sequential(self.time_grid.dt_sub)
+            X = ctx.to_dev(np.array([s.stacked() for s in states])[None])
+            Y = ctx.fine_sequential(X)[0].cpu().numpy()
         d1 = self.propagators.system.d1
         return [(SplitState.fresh(y[:d1], y[d1:], s.t + self.time_grid.dt), {"converged": True})
                 for y, s in zip(Y, states)]

@@ -122,10 +122,11 @@ class SplitPropagators:
     def split_step(self, state: SplitState, dt: float) -> SplitState:
         """One substep of the partially explicit scheme (stepping.py:122-147)."""
         ctx = self.context(1)
-        ctx.prepare_sequential(dt)
-        x = ctx.to_dev(state.stacked()[None, None])
-        xp = ctx.to_dev(np.concatenate([state.u_prev, state.w_prev])[None, None])
-        y = ctx.split_step(x, xp)[0, 0].cpu().numpy()
+        with ctx.lock:
+            ctx.prepare_sequential(dt)
+            x = ctx.to_dev(state.stacked()[None, None])
+            xp = ctx.to_dev(np.concatenate([state.u_prev, state.w_prev])[None, None])
+            y = ctx.split_step(x, xp)[0, 0].cpu().numpy()
         d1 = self.system.d1
         return SplitState(y[:d1].copy(), y[d1:].copy(), state.u.copy(), state.w.copy(),
                           state.t + dt)
@@ -136,8 +137,9 @@ class SplitPropagators:
 
     def coarse_step_all(self, states, dt: float):
         ctx = self.context(1)
-        ctx.prepare_coarse(dt)
-        y = ctx.coarse_apply(ctx.to_dev(_stack_states(states)[None]))[0].cpu().numpy()
+        with ctx.lock:
+            ctx.prepare_coarse(dt)
+            y = ctx.coarse_apply(ctx.to_dev(_stack_states(states)[None]))[0].cpu().numpy()
         d1 = self.system.d1
         return [SplitState(r[:d1].copy(), r[d1:].copy(), s.u.copy(), s.w.copy(), s.t + dt)
                 for r, s in zip(y, states)]
@@ -147,16 +149,17 @@ class SplitPropagators:
         """`substeps` split steps with lags reset (stepping.py:178-189), full trajectory."""
         ctx = self.context(1)
         dt = dt_interval / substeps
-        ctx.prepare_sequential(dt)
         d1 = self.system.d1
-        x = ctx.to_dev(state.stacked()[None, None])
-        xp = x.clone()
-        rows = [x[0, 0]]
-        for _ in range(substeps):
-            y = ctx.split_step(x, xp)
-            xp, x = x, y
-            rows.append(y[0, 0])
-        traj = torch.stack(rows).cpu().numpy()
+        with ctx.lock:
+            ctx.prepare_sequential(dt)
+            x = ctx.to_dev(state.stacked()[None, None])
+            xp = x.clone()
+            rows = [x[0, 0]]
+            for _ in range(substeps):
+                y = ctx.split_step(x, xp)
+                xp, x = x, y
+                rows.append(y[0, 0])
+            traj = torch.stack(rows).cpu().numpy()
         cur = SplitState(traj[-1, :d1].copy(), traj[-1, d1:].copy(), traj[-2, :d1].copy(),
                          traj[-2, d1:].copy(), state.t + dt * substeps)
         times = state.t + dt * np.arange(substeps + 1)
@@ -174,8 +177,9 @@ class SplitPropagators:
             return np.inf
         ctx = self.context(1)
         out, its = C.c_double(0.0), C.c_int(0)
-        check(ctx.lib.pe_stability_max_step(ctx.ptr, 0, float(tol), int(max_iter),
-                                            C.byref(out), C.byref(its), ctx.stream()))
+        with ctx.lock:
+            check(ctx.lib.pe_stability_max_step(ctx.ptr, 0, float(tol), int(max_iter),
+                                                C.byref(out), C.byref(its), ctx.stream()))
         if its.value < 0:
             log.warning("stability power iteration hit %d iterations, last rayleigh %.6e",
                         max_iter, 2.0 / out.value)
