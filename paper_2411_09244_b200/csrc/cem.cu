@@ -6,8 +6,10 @@
 //     rectangle's nodes minus the global Dirichlet boundary; natural on the block edges)
 //       a(psi, v) = lambda s(psi, v),  a = sum_cells kappa K_ref,  s = sum_cells kt h^2 M_ref,
 //     kt = kappa nb^2 (the "kappa_h2" weight, msbasis.py:266-268).  Dense per block, padded
-//     to (s+1)^2 with a decoupled (pad I, I) block: S = L L^T (batched potrf),
-//     C = L^-1 A L^-T (batched trsm), C = Y diag(w) Y^T (batched syev, ascending), V = L^-T Y
+//     to (s+1)^2 with a decoupled (I, I) block: S = L L^T (batched potrf),
+//     C = L^-1 A L^-T (batched trsm; the padded diagonal then set just above a Gershgorin
+//     bound of the real part, so the padding sorts last without inflating ||C||),
+//     C = Y diag(w) Y^T (batched syev, ascending), V = L^-T Y
 //     (s-orthonormal), the first n_eig columns with the reference's sign (largest-magnitude
 //     entry positive, first such entry).
 //  2. Constraint functions W_j = s_j V_j on each block's free nodes (batched GEMM).
@@ -133,6 +135,29 @@ __global__ void k_aux_assemble(CemGeom g, const double* __restrict__ kappa,
     S[o] = m;
     S_keep[o] = m;
   }
+}
+
+// After the reduction C = L^-1 A L^-T: the padded (decoupled) diagonal is set just above a
+// Gershgorin bound of the block's real part, so the padded eigenvalues sort after every real
+// one while ||C|| -- and with it the eigensolver's absolute error -- stays at the real scale.
+__global__ void k_aux_pad(CemGeom g, double* C) {
+  const int b = blockIdx.x, n = g.n, nf = block_free_count(g, b);
+  double* c = C + (long long)b * n * n;
+  __shared__ double red[256];
+  double m = 0.0;
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+    double r = 0.0;
+    for (int j = 0; j < nf; ++j) r += fabs(c[(long long)j * n + i]);
+    m = fmax(m, r);
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  const double pad = 2.0 * red[0] + 1.0;
+  for (int i = nf + threadIdx.x; i < n; i += blockDim.x) c[(long long)i * n + i] = pad;
 }
 
 // sign convention (msbasis.py:321-324): per column k < n_eig, the first entry of largest
@@ -317,9 +342,7 @@ static void cem_impl(CemArgs& a) {
   const double one = 1.0, zero = 0.0;
   {  // aux work buffers (freed before the patch solves)
   Dv<double> A(nn * nblk), S(nn * nblk), Sk(nn * nblk);
-  double amax = 0.0;
-  for (size_t c = 0; c < cells; ++c) amax = std::max(amax, a.kappa[c]);
-  const double pad = 1e12 * std::max(amax, 1.0) * a.nx * a.nx;  // far above every eigenvalue
+  const double pad = 1.0;  // placeholder; k_aux_pad sets the padded eigenvalues after reduction
   k_aux_assemble<<<dim3(std::max(1, std::min(64, (int)((nn + 255) / 256))), nblk), 256, 0, st>>>(
       g, kap.p, kt.p, pad, A.p, S.p, Sk.p);
   ++g_launches;
@@ -347,6 +370,9 @@ static void cem_impl(CemArgs& a) {
                               CUBLAS_DIAG_NON_UNIT, n, n, &one, dS.p, n, dA.p, n, nblk));
   CEM_BLAS(cublasDtrsmBatched(bl, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
                               CUBLAS_DIAG_NON_UNIT, n, n, &one, dS.p, n, dA.p, n, nblk));
+  k_aux_pad<<<nblk, 256, 0, st>>>(g, A.p);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
   {
     cusolverDnParams_t prm;
     CEM_SOLVER(cusolverDnCreateParams(&prm));
