@@ -45,6 +45,21 @@ cs = P.project_coarse(space.Psi1, space.Psi2, ops)
 t_proj = time.perf_counter() - t0
 dev = {k: float(np.abs(getattr(cs, k) - blocks[k]).max() / np.abs(blocks[k]).max())
        for k in blocks}
+
+
+def invariants(s, f1, f2):
+    """Unchanged by orthogonal transforms within Psi1 / Psi2 (eigenvector sign ties and
+    repeated eigenvalues of the aux problems, tests/test_gpu_cem.py)."""
+    import scipy.linalg as sla
+
+    out = {"eig11": np.sort(sla.eigh(s["A11"], s["M11"], eigvals_only=True)),
+           "eig22": np.sort(sla.eigh(s["A22"], s["M22"], eigvals_only=True))}
+    l1, l2 = np.linalg.cholesky(s["M11"]), np.linalg.cholesky(s["M22"])
+    cm = sla.solve_triangular(l1, sla.solve_triangular(l2, s["M12"].T, lower=True).T, lower=True)
+    out["mass_angles"] = np.linalg.svd(cm, compute_uv=False)
+    out["f1"] = np.array([f1 @ np.linalg.solve(s["M11"], f1)])
+    out["f2"] = np.array([f2 @ np.linalg.solve(s["M22"], f2)])
+    return out
 _, _, src = rectangles(name)
 if src == "constant":
     fc = np.ones(c["nx"] * c["nx"])
@@ -53,7 +68,13 @@ else:
 g1, g2 = P.project_load(space, corner_load(c["nx"], fc))
 load_dev = max(float(np.abs(g1 - f1).max() / np.abs(f1).max()),
                float(np.abs(g2 - f2).max() / np.abs(f2).max()))
+t0 = time.perf_counter()
+mine = invariants({k: getattr(cs, k) for k in blocks}, g1, g2)
+ref = invariants(blocks, f1, f2)
+inv_dev = {k: float(np.abs(mine[k] - ref[k]).max() / np.abs(ref[k]).max()) for k in ref}
+t_inv = time.perf_counter() - t0
 out = dict(config=name, basis_seconds=t_basis, projection_seconds=t_proj,
+           invariant_rel_dev=inv_dev, invariant_seconds=t_inv,
            host_assembly_seconds=t_asm, constraint_residual=space.constraint_residual,
            max_block_rel_dev=max(dev.values()), block_rel_dev=dev, load_rel_dev=load_dev,
            d1=space.Psi1.shape[1], d2=space.Psi2.shape[1], basis_nnz=int(space.Psi1.nnz + space.Psi2.nnz),
