@@ -17,8 +17,9 @@
 //     zero Dirichlet rim): min a(phi, phi) subject to C phi = e_t, with the rows of C the
 //     restrictions of W_j (j over the patch blocks, ascending, n_eig each).  The KKT system
 //     [[A, C^T], [C, 0]] (solved by sparse LU in the reference) is solved by its Schur
-//     complement: A = L L^T, Y = A^-1 C^T, G = C Y, phi = Y G^-1 E_t for the n_eig targets.
-//     Dense per block (patch <= 55^2 nodes at config 3), cuSOLVER potrf / potrs.
+//     complement: A = L L^T, Y = A^-1 C^T, G = C Y, phi = Y G^-1 E_t for the n_eig targets,
+//     then two steps of iterative refinement on the full KKT system.  Dense per block (patch
+//     <= 55^2 nodes at config 3), cuSOLVER potrf / potrs.
 //
 // Output: per block, the n_eig basis columns on its patch-interior nodes (row-major
 // node order), plus the worst constraint residual |C phi - e|.
@@ -421,9 +422,10 @@ static void cem_impl(CemArgs& a) {
     nl_max = std::max(nl_max, p.n);
     m_max = std::max(m_max, (p.jb1x - p.jb0x) * (p.jb1y - p.jb0y) * ne);
   }
-  Dv<double> Al((size_t)nl_max * nl_max), Ct((size_t)nl_max * m_max), Y((size_t)nl_max * m_max),
-      G((size_t)m_max * m_max), E((size_t)m_max * ne), Phi((size_t)nl_max * ne),
-      R((size_t)m_max * ne);
+  Dv<double> Al((size_t)nl_max * nl_max), A0((size_t)nl_max * nl_max), Ct((size_t)nl_max * m_max),
+      Y((size_t)nl_max * m_max), G((size_t)m_max * m_max), E((size_t)m_max * ne),
+      Phi((size_t)nl_max * ne), R((size_t)m_max * ne), Z((size_t)nl_max * ne),
+      T1((size_t)m_max * ne);
   cusolverDnParams_t prm;
   CEM_SOLVER(cusolverDnCreateParams(&prm));
   struct HP {
@@ -458,6 +460,7 @@ static void cem_impl(CemArgs& a) {
     k_constraints<<<dim3((nl + 255) / 256, m), 256, 0, st>>>(g, p, ne, W.p, Ct.p);
     g_launches += 2;
     PE_CUDA_CHECK(cudaGetLastError());
+    PE_CUDA_CHECK(cudaMemcpyAsync(A0.p, Al.p, sizeof(double) * nl * nl, cudaMemcpyDeviceToDevice, st));
     CEM_SOLVER(cusolverDnXpotrf(sol, prm, CUBLAS_FILL_MODE_LOWER, nl, CUDA_R_64F, Al.p, nl,
                                 CUDA_R_64F, work.p, wd_max, hwork.data(), wh_max, dinfo.p + 2 * b));
     PE_CUDA_CHECK(cudaMemcpyAsync(Y.p, Ct.p, sizeof(double) * nl * m, cudaMemcpyDeviceToDevice, st));
@@ -483,6 +486,34 @@ static void cem_impl(CemArgs& a) {
     const double mone = -1.0;
     CEM_BLAS(cublasDgemm(bl, CUBLAS_OP_T, CUBLAS_OP_N, m, ne, nl, &one, Ct.p, nl, Phi.p, nl, &mone,
                          R.p, m));
+    // Two steps of iterative refinement on the full KKT system [[A, C^T], [C, 0]]
+    // [phi; lambda] = [0; E] (lambda = -mu): the Schur complement G = C A^-1 C^T squares the
+    // saddle point's conditioning, the refinement brings phi back to the KKT's own accuracy.
+    for (int it = 0; it < 2; ++it) {
+      // r1 = C^T mu - A phi  -> Z ;  r2 = E - C phi = -R
+      CEM_BLAS(cublasDgemm(bl, CUBLAS_OP_N, CUBLAS_OP_N, nl, ne, m, &one, Ct.p, nl, E.p, m, &zero,
+                           Z.p, nl));
+      CEM_BLAS(cublasDgemm(bl, CUBLAS_OP_N, CUBLAS_OP_N, nl, ne, nl, &mone, A0.p, nl, Phi.p, nl,
+                           &one, Z.p, nl));
+      // z = A^-1 r1
+      CEM_SOLVER(cusolverDnXpotrs(sol, prm, CUBLAS_FILL_MODE_LOWER, nl, ne, CUDA_R_64F, Al.p, nl,
+                                  CUDA_R_64F, Z.p, nl, dinfo.p + 2 * b + 1));
+      // dlambda = G^-1 (C z - r2) = G^-1 (C z + R)
+      PE_CUDA_CHECK(cudaMemcpyAsync(T1.p, R.p, sizeof(double) * m * ne, cudaMemcpyDeviceToDevice, st));
+      CEM_BLAS(cublasDgemm(bl, CUBLAS_OP_T, CUBLAS_OP_N, m, ne, nl, &one, Ct.p, nl, Z.p, nl, &one,
+                           T1.p, m));
+      CEM_SOLVER(cusolverDnXpotrs(sol, prm, CUBLAS_FILL_MODE_LOWER, m, ne, CUDA_R_64F, G.p, m,
+                                  CUDA_R_64F, T1.p, m, dinfo.p + 2 * b + 1));
+      // phi += z - Y dlambda ;  mu -= dlambda
+      CEM_BLAS(cublasDgemm(bl, CUBLAS_OP_N, CUBLAS_OP_N, nl, ne, m, &mone, Y.p, nl, T1.p, m, &one,
+                           Z.p, nl));
+      CEM_BLAS(cublasDaxpy(bl, nl * ne, &one, Z.p, 1, Phi.p, 1));
+      CEM_BLAS(cublasDaxpy(bl, m * ne, &mone, T1.p, 1, E.p, 1));
+      // R = C phi - E_t
+      PE_CUDA_CHECK(cudaMemcpyAsync(R.p, he.data(), he.size() * 8, cudaMemcpyHostToDevice, st));
+      CEM_BLAS(cublasDgemm(bl, CUBLAS_OP_T, CUBLAS_OP_N, m, ne, nl, &one, Ct.p, nl, Phi.p, nl,
+                           &mone, R.p, m));
+    }
     PE_CUDA_CHECK(cudaMemcpyAsync(hphi.data(), Phi.p, sizeof(double) * nl * ne,
                                   cudaMemcpyDeviceToHost, st));
     PE_CUDA_CHECK(cudaMemcpyAsync(hres.data(), R.p, sizeof(double) * m * ne,
