@@ -263,6 +263,25 @@ int pe_cem_basis(int nx, int nb, int layers, int n_eig, const double* kappa, dou
                  void* stream);
 long long pe_cem_basis_size(int nx, int nb, int layers, int n_eig);
 
+/* ---- time-dependent loads (the reference's `loads.at(t)`, stepping.py:125,164 and
+ * allatonce.py:212-218).  F: device (E, nc, J, d) = [f1(t); f2(t)] for every member,
+ * interval column and substep s at the time the reference evaluates it (substep end);
+ * Fc: device (E, N, d) = [f1; f2](t_n + Dt) per coarse step.  Same results as the
+ * constant-load entry points when every row equals (f1, f2).  The all-at-once variant needs
+ * the modal sweep (symmetric-definite pencils, d1, d2 > 0): PE_ERR_ARG otherwise. */
+int pe_fine_sequential_loads(pe_ctx* ctx, const double* X_in, double* X_out, int nc,
+                             const double* F, void* stream);
+int pe_split_step_loads(pe_ctx* ctx, const double* X_in, const double* X_prev, double* X_out,
+                        int nc, const double* F, void* stream); /* F: (E, nc, 1, d) */
+int pe_fine_allatonce_loads(pe_ctx* ctx, const double* X_in, double* X_out, int nc,
+                            const double* F, int* sweeps, int* reasons, double* resid_hist,
+                            void* stream);
+int pe_coarse_correct_loads(pe_ctx* ctx, int N, const double* X_old, const double* F_hat,
+                            double* G_cache, double* X_new, double* diff, const int* active,
+                            const double* Fc, void* stream);
+int pe_coarse_apply_loads(pe_ctx* ctx, const double* X_in, double* X_out, int nc,
+                          const double* Fc, void* stream); /* Fc: (E, nc, d), one per state */
+
 #ifdef __cplusplus
 }
 #endif

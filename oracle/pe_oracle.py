@@ -44,6 +44,12 @@ class OSystem:
     A22: np.ndarray
     f1: np.ndarray
     f2: np.ndarray
+    # time-dependent loads (stepping.py:125,164 `loads.at(t + dt)`; allatonce.py:212-218):
+    # t -> (f1(t), f2(t)); None = the constant pair (f1, f2)
+    loads_at: object = None
+
+    def f_at(self, t):
+        return (self.f1, self.f2) if self.loads_at is None else self.loads_at(t)
 
     @property
     def d1(self) -> int:
@@ -78,33 +84,39 @@ class OracleSplit:
             self._kchol[dt] = cho_factor(self.s.M11 / dt + self.s.A11)
         return self._kchol[dt]
 
-    def split_step(self, u, w, up, wp, dt):
+    def split_step(self, u, w, up, wp, dt, t=0.0):
+        """One substep from time t (loads at t + dt, stepping.py:125)."""
         s = self.s
+        f1, f2 = s.f_at(t + dt)
         if s.d1:
-            r = s.M11 @ u / dt - s.M12 @ (w - wp) / dt - s.A12 @ w + s.f1
+            r = s.M11 @ u / dt - s.M12 @ (w - wp) / dt - s.A12 @ w + f1
             un = cho_solve(self._k(dt), r)
         else:
             un = u.copy()
         if s.d2:
             r = (s.M22 @ w / dt - s.M12.T @ (u - up) / dt - s.A12.T @ un
-                 - s.A22 @ w + s.f2)
+                 - s.A22 @ w + f2)
             wn = cho_solve(self._m22, dt * r)
         else:
             wn = w.copy()
         return un, wn
 
-    def fine_interval(self, u, w, dt_interval, substeps):
-        """Returns (U, W) trajectories of shape (J+1, d1), (J+1, d2); lags reset."""
+    def fine_interval(self, u, w, dt_interval, substeps, t=0.0, return_t=False):
+        """Returns (U, W) trajectories of shape (J+1, d1), (J+1, d2); lags reset.
+        The substep time accumulates as the reference's SplitState.t (stepping.py:147)."""
         dt = dt_interval / substeps
         u = np.array(u, dtype=float)
         w = np.array(w, dtype=float)
         up, wp = u.copy(), w.copy()
         us, ws = [u.copy()], [w.copy()]
         for _ in range(substeps):
-            un, wn = self.split_step(u, w, up, wp, dt)
+            un, wn = self.split_step(u, w, up, wp, dt, t)
             up, wp, u, w = u, w, un, wn
+            t = t + dt
             us.append(u.copy())
             ws.append(w.copy())
+        if return_t:
+            return np.array(us), np.array(ws), t
         return np.array(us), np.array(ws)
 
     def _g(self, dt):
@@ -115,12 +127,14 @@ class OracleSplit:
             self._glu[dt] = lu_factor(k)
         return self._glu[dt]
 
-    def coarse_step(self, x, dt):
+    def coarse_step(self, x, dt, t=0.0):
+        """G from time t (loads at t + dt, stepping.py:164)."""
         s = self.s
+        f1, f2 = s.f_at(t + dt)
         u, w = x[: s.d1], x[s.d1:]
         rhs = np.concatenate([
-            s.f1 + s.M11 @ u / dt + s.M12 @ w / dt - s.A12 @ w,
-            s.f2 + s.M12.T @ u / dt + s.M22 @ w / dt - s.A22 @ w,
+            f1 + s.M11 @ u / dt + s.M12 @ w / dt - s.A12 @ w,
+            f2 + s.M12.T @ u / dt + s.M22 @ w / dt - s.A22 @ w,
         ])
         return lu_solve(self._g(dt), rhs)
 
@@ -230,10 +244,15 @@ class OracleWR:
             out[i] = w
         return out
 
-    def solve(self, u0, w0):
+    def solve(self, u0, w0, t0=0.0):
         s, J = self.s, self.J
-        f1_rows = np.tile(s.f1, (J, 1))
-        f2_rows = np.tile(s.f2, (J, 1))
+        if s.loads_at is None:
+            f1_rows = np.tile(s.f1, (J, 1))
+            f2_rows = np.tile(s.f2, (J, 1))
+        else:  # _load_rows (allatonce.py:212-218)
+            pairs = [s.loads_at(t) for t in t0 + self.dt * np.arange(1, J + 1)]
+            f1_rows = np.array([q[0] for q in pairs])
+            f2_rows = np.array([q[1] for q in pairs])
         U = np.tile(u0, (J, 1))
         W = np.tile(w0, (J, 1))
         ufp = np.array(u0, dtype=float).copy()
@@ -293,7 +312,7 @@ def resolved_fine_tol(epsilon, fine_tol=None):
 
 def run_parareal(s: OSystem, x0, t_end, n_intervals, substeps, *, kind="sequential",
                  alpha=0.5, epsilon=1e-14, k_max=100, stop="absolute", fine_tol=None,
-                 fine_max_iter=400, workers=1):
+                 fine_max_iter=400, workers=1, t0=0.0):
     """Algorithm 1 (parareal.py:160-236) with the stop rule selectable.
 
     stop="absolute" is the reference check_stop (parareal.py:145-147);
@@ -307,27 +326,31 @@ def run_parareal(s: OSystem, x0, t_end, n_intervals, substeps, *, kind="sequenti
     dt = t_end / n_intervals
     sp_ = OracleSplit(s)
     if kind == "sequential":
-        def fine(x):
-            U, W = sp_.fine_interval(x[:d1], x[d1:], dt, substeps)
-            return np.concatenate([U[-1], W[-1]]), {"converged": True}
+        def fine(xt):
+            x, t = xt
+            U, W, t1 = sp_.fine_interval(x[:d1], x[d1:], dt, substeps, t, return_t=True)
+            return np.concatenate([U[-1], W[-1]]), {"converged": True}, t1
     elif kind == "all-at-once":
         wr = OracleWR(s, substeps, dt, alpha, tol=resolved_fine_tol(epsilon, fine_tol),
                       max_iter=fine_max_iter)
 
-        def fine(x):
-            r = wr.solve(x[:d1], x[d1:])
+        def fine(xt):
+            x, t = xt
+            r = wr.solve(x[:d1], x[d1:], t)
             return np.concatenate([r["U"][-1], r["W"][-1]]), {
                 "converged": r["converged"], "iterations": r["iterations"],
-                "residuals": r["residuals"], "stop_reason": r["stop_reason"]}
+                "residuals": r["residuals"], "stop_reason": r["stop_reason"]}, t + dt
     else:
         raise ValueError(f"unknown fine propagator kind {kind!r}")
     check = rel_state_diff if stop == "relative" else max_state_diff
 
     x0 = np.asarray(x0, dtype=float)
     states = [x0.copy()]
+    times = [float(t0)]  # SplitState.t of each state (parareal.py:150-157, 210)
     for _ in range(n_intervals):
-        states.append(sp_.coarse_step(states[-1], dt))
-    gold = [sp_.coarse_step(x, dt) for x in states[:-1]]
+        states.append(sp_.coarse_step(states[-1], dt, times[-1]))
+        times.append(times[-1] + dt)
+    gold = [sp_.coarse_step(x, dt, t) for x, t in zip(states[:-1], times[:-1])]
     history = [np.array(states)]
     max_diffs, fine_info, fsec, csec = [], [], [], []
     converged, iterations = False, 0
@@ -336,19 +359,21 @@ def run_parareal(s: OSystem, x0, t_end, n_intervals, substeps, *, kind="sequenti
         for _ in range(k_max):
             iterations += 1
             tic = time.perf_counter()
+            args = [(states[n], times[n]) for n in range(n_intervals)]
             if pool is None:
-                fr = [fine(states[n]) for n in range(n_intervals)]
+                fr = [fine(a) for a in args]
             else:
-                fr = list(pool.map(fine, [states[n] for n in range(n_intervals)]))
+                fr = list(pool.map(fine, args))
             fsec.append(time.perf_counter() - tic)
-            fine_info.append([info for _, info in fr])
+            fine_info.append([info for _, info, _ in fr])
             tic = time.perf_counter()
             new = [x0.copy()]
             gnew = []
             for n in range(n_intervals):
-                g = sp_.coarse_step(new[n], dt)
+                g = sp_.coarse_step(new[n], dt, times[n])
                 gnew.append(g)
                 new.append(fr[n][0] + (g - gold[n]))
+            times = [float(t0)] + [fr[n][2] for n in range(n_intervals)]
             csec.append(time.perf_counter() - tic)
             history.append(np.array(new))
             diff = check(history[-2], history[-1])

@@ -79,6 +79,11 @@ SIGNATURES = {
     "pe_cem_basis": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _D, C.c_double, _D,
                                C.POINTER(C.c_longlong), _D, _D, _P]),
     "pe_cem_basis_size": (C.c_longlong, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "pe_fine_sequential_loads": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
+    "pe_split_step_loads": (C.c_int, [_P, _P, _P, _P, C.c_int, _P, _P]),
+    "pe_fine_allatonce_loads": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, _P, _P]),
+    "pe_coarse_correct_loads": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "pe_coarse_apply_loads": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
 }
 
 _lib = None

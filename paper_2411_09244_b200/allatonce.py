@@ -217,8 +217,7 @@ class WaveformRelaxation:
                  loads: ConstantLoads, tol: float = 1e-12, max_iter: int = 50,
                  device: int | None = None, context: PeContext | None = None):
         TimeMatrixB(substeps, dt_interval / substeps if dt_interval > 0 else -1.0, alpha)
-        if not getattr(loads, "constant", False):
-            raise NotImplementedError("libpe supports time-constant loads (ConstantLoads)")
+        self.constant_loads = bool(getattr(loads, "constant", False))
         self.system = system
         self.substeps = substeps
         self.dt_interval = dt_interval
@@ -227,7 +226,9 @@ class WaveformRelaxation:
         self.loads = loads
         self.tol = tol
         self.max_iter = max_iter
-        self.ctx = context or PeContext([system], [loads], substeps, device)
+        self.ctx = context or PeContext(
+            [system], [loads if self.constant_loads else ConstantLoads.zero(system)], substeps,
+            device)
         self.ctx.prepare_allatonce(self.dt, alpha, tol, max_iter)
 
     def solve(self, state: SplitState) -> WRResult:
@@ -237,10 +238,22 @@ class WaveformRelaxation:
     def solve_all(self, states, trajectories: bool = True) -> list:
         ctx = self.ctx
         nc = len(states)
+        F = None
+        if not self.constant_loads:  # _load_rows: t0 + dt (1..J) (allatonce.py:212-218)
+            rows = []
+            for s in states:
+                pairs = [self.loads.at(float(t))
+                         for t in s.t + self.dt * np.arange(1, self.substeps + 1)]
+                rows.append(np.array([np.concatenate([np.ravel(a), np.ravel(b)])
+                                      for a, b in pairs]))
+            F = np.array(rows)
         with ctx.lock:
             ctx.prepare_allatonce(self.dt, self.alpha, self.tol, self.max_iter)
             X = ctx.to_dev(np.array([s.stacked() for s in states])[None])
-            Y, sw, rs, rh = ctx.fine_allatonce(X)
+            if F is None:
+                Y, sw, rs, rh = ctx.fine_allatonce(X)
+            else:
+                Y, sw, rs, rh = ctx.fine_allatonce_loads(X, ctx.to_dev(F[None]))
             Y = Y[0].cpu().numpy()
             sw = sw[0].cpu().numpy()
             rs = rs[0].cpu().numpy()

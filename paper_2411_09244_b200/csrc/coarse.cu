@@ -41,7 +41,8 @@ struct CoarseArgs {
   int d, N, cs;
   int phi_in_smem;
   const double* Phi;   // (E, d, d) row-major
-  const double* gvec;  // (E, d)
+  const double* gvec;  // (E, d); with a load series (E, N, d): member stride ge, step stride gn
+  long long ge, gn;
   const double* X_old; // (E, N+1, d)
   const double* F_hat; // (E, N, d) or null (initial sweep)
   double* G_cache;     // (E, N, d)
@@ -105,7 +106,7 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
   const double* X_old = a.X_old + (long long)e * (N + 1) * d;
   double* X_new = a.X_new + (long long)e * (N + 1) * d;
   const double* Phi = a.Phi + (long long)e * d * d;
-  const double* gv = a.gvec + (long long)e * d;
+  const double* gv = a.gvec + (long long)e * a.ge;
   const double* F = a.F_hat ? a.F_hat + (long long)e * N * d : nullptr;
   double* Gc = a.G_cache + (long long)e * N * d;
   const double* rowp[RPW];
@@ -125,7 +126,7 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
   auto prefetch = [&](int n) {
     if (n < N && mine) {
       const long long o = (long long)n * d + r0 + myrr;
-      nf_b = gv[r0 + myrr];
+      nf_b = gv[(long long)n * a.gn + r0 + myrr];
       nf_o = X_old[o + d];
       if (F) {
         nf_f = F[o];
@@ -348,7 +349,8 @@ constexpr int CS_WARPS = CS_THREADS / 32;
 
 __global__ void __launch_bounds__(CS_THREADS)
     coarse_step_stream_kernel(int d, int n, int N, const double* __restrict__ Phi,
-                              const double* __restrict__ gvec, const double* X_old,
+                              const double* __restrict__ gvec, long long ge, long long gn,
+                              const double* X_old,
                               const double* F_hat, double* G_cache, double* X_new,
                               double* partial, const int* active) {
   const int e = blockIdx.y;
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(CS_THREADS)
       Xn[r] = Xo[r];
   __syncthreads();
   const double* Pm = Phi + (long long)e * d * d;
-  const double* gv = gvec + (long long)e * d;
+  const double* gv = gvec + (long long)e * ge + (long long)n * gn;
   const double* F = F_hat ? F_hat + (long long)e * N * d : nullptr;
   double* Gc = G_cache + (long long)e * N * d;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -473,11 +475,17 @@ __global__ void coarse_norm_reduce_kernel(int N, int nblocks, const double* part
 int coarse_stream_blocks(int d) { return std::min(296, (d + CS_WARPS - 1) / CS_WARPS); }
 
 static void coarse_correct_stream(int E, int d, int N, const double* Phi, const double* gvec,
+                                  long long ge, long long gn,
                                   const double* X_old, const double* F_hat, double* G_cache,
                                   double* X_new, double* partial, double* diff,
                                   const int* active, cudaStream_t st) {
   const int nb = coarse_stream_blocks(d);
-  const size_t smem = sizeof(double) * d;
+  // at most 4 CTAs (32 warps) per SM: measured at cfg4, the same stream with 5 CTAs per SM
+  // (48 instead of 64 registers after an unrelated code change) ran 2.3x slower; the
+  // dynamic shared memory request pins the occupancy independently of register allocation
+  static const size_t pad_smem = getenv("PE_COARSE_STREAM_SMEM")
+                                     ? (size_t)atol(getenv("PE_COARSE_STREAM_SMEM")) : 50 * 1024;
+  const size_t smem = std::max(sizeof(double) * d, pad_smem);
   static bool attr = false;
   if (!attr) {
     PE_CUDA_CHECK(cudaFuncSetAttribute(coarse_step_stream_kernel,
@@ -487,7 +495,7 @@ static void coarse_correct_stream(int E, int d, int N, const double* Phi, const 
   if (smem > 200 * 1024) throw Error{PE_ERR_ARG, "coarse state too large for one SM"};
   for (int n = 0; n < N; ++n) {
     coarse_step_stream_kernel<<<dim3(nb, E), CS_THREADS, smem, st>>>(
-        d, n, N, Phi, gvec, X_old, F_hat, G_cache, X_new, partial, active);
+        d, n, N, Phi, gvec, ge, gn, X_old, F_hat, G_cache, X_new, partial, active);
     ++g_launches;
     PE_CUDA_CHECK(cudaGetLastError());
   }
@@ -507,7 +515,11 @@ int coarse_cluster_size(int d) {
 
 void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
                     const double* X_old, const double* F_hat, double* G_cache, double* X_new,
-                    double* partial, double* diff, const int* active, cudaStream_t st) {
+                    double* partial, double* diff, const int* active, cudaStream_t st,
+                    const double* gseries) {
+  // gseries (E, N, d): per-step load terms K_G^-1 f(t_n + Dt) (time-dependent loads)
+  const long long ge = gseries ? (long long)N * d : d, gn = gseries ? d : 0;
+  if (gseries) gvec = gseries;
   if (N <= 0 || d <= 0) return;
   CoarseArgs a;
   a.d = d;
@@ -521,13 +533,15 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   // Large d (Phi not smem-resident) or many members (more member clusters than fit at
   // once, ~9 clusters of 16): stream Phi from HBM, all SMs per step.
   if (!a.phi_in_smem || (long long)E * a.cs > 148) {
-    coarse_correct_stream(E, d, N, Phi, gvec, X_old, F_hat, G_cache, X_new, partial, diff,
+    coarse_correct_stream(E, d, N, Phi, gvec, ge, gn, X_old, F_hat, G_cache, X_new, partial, diff,
                           active, st);
     return;
   }
   size_t smem = a.phi_in_smem ? with_phi : base;
   a.Phi = Phi;
   a.gvec = gvec;
+  a.ge = ge;
+  a.gn = gn;
   a.X_old = X_old;
   a.F_hat = F_hat;
   a.G_cache = G_cache;

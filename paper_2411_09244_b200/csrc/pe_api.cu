@@ -114,9 +114,86 @@ static void collect_profile(pe_ctx* c, cudaStream_t st) {
 // X_in/X_out: (E, nc, d) == per member a column-major d x nc matrix.
 // With X_prev == nullptr the lags are reset (D_0 = 0, interval start); otherwise
 // D_0 = X_in - X_prev (a single split_step with explicit lags, stepping.py:122-147).
+// ------------------------------------------------------------------ time-dependent loads
+// The reference evaluates loads at each step's end time (stepping.py:125,164;
+// allatonce.py:212-218).  A call with a load series F (E, nc, J, d) -- [f1(t); f2(t)] per
+// (member, interval column, substep) -- turns the constant bias vectors into per-column
+// terms: the sequential step's Lf F (Lf from setup_sequential), the WR rhs term V1^T F1 and
+// h term dt V2^T F2, the coarse step's K_G^-1 F.
+__global__ void k_perm_seni(long long E, int nc, int J, int d, int k0, int dk,
+                            const double* __restrict__ src, double* __restrict__ dst,
+                            int step_major) {
+  // src [e][n][s][k] (row length d) -> dst rows of dk: step_major ? [s][e][n] : [e][s][n]
+  const long long total = E * nc * J * (long long)dk;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(q % dk);
+    long long r = q / dk;
+    const int s = (int)(r % J);
+    r /= J;
+    const int n = (int)(r % nc);
+    const long long e = r / nc;
+    const long long o = step_major ? (((long long)s * E + e) * nc + n) * dk + k
+                                   : ((e * J + s) * nc + n) * dk + k;
+    dst[o] = src[q / dk * d + k0 + k];
+  }
+}
+
+static int loads_grid(long long n) {
+  return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 16));
+}
+
+// LB [s][e][n][d] = Lf F (the sequential step's per-column bias series)
+static double* seq_load_terms(pe_ctx* c, int nc, int J, const double* F, cudaStream_t st) {
+  const int d = c->d, E = c->E;
+  const size_t n = (size_t)E * nc * J * d;
+  c->LF1.ensure(sizeof(double) * n + 8);
+  c->LB.ensure(sizeof(double) * n + 8);
+  GemmParams p;  // tmp (E, nc, J, d) = Lf F, columns (n, s) contiguous
+  p.M = d;
+  p.N = nc * J;
+  p.nb1 = E;
+  p.nseg = 1;
+  p.seg[0].A = Operand{c->Lf.d(), d, 1, (long long)d * d, 0};
+  p.seg[0].B = Operand{F, 1, d, (long long)nc * J * d, 0};
+  p.seg[0].K = d;
+  p.C = c->LF1.d();
+  p.c_i = 1;
+  p.c_j = d;
+  p.c_b1 = (long long)nc * J * d;
+  run_gemm(c, p, st);
+  k_perm_seni<<<loads_grid((long long)n), 256, 0, st>>>(E, nc, J, d, 0, d, c->LF1.d(), c->LB.d(), 1);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+  return c->LB.d();
+}
+
+// LGs (E, N, d) = K_G^-1 Fc  (the coarse step's per-interval load terms)
+static double* coarse_load_terms(pe_ctx* c, int N, const double* Fc, cudaStream_t st) {
+  const int d = c->d, E = c->E;
+  c->LGs.ensure(sizeof(double) * (size_t)E * N * d + 8);
+  GemmParams p;
+  p.M = d;
+  p.N = N;
+  p.nb1 = E;
+  p.nseg = 1;
+  p.seg[0].A = Operand{c->LG.d(), d, 1, (long long)d * d, 0};
+  p.seg[0].B = Operand{Fc, 1, d, (long long)N * d, 0};
+  p.seg[0].K = d;
+  p.C = c->LGs.d();
+  p.c_i = 1;
+  p.c_j = d;
+  p.c_b1 = (long long)N * d;
+  run_gemm(c, p, st);
+  return c->LGs.d();
+}
+
 static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc,
-                            cudaStream_t st, const double* X_prev = nullptr, int steps = -1) {
+                            cudaStream_t st, const double* X_prev = nullptr, int steps = -1,
+                            const double* Fload = nullptr) {
   const int d = c->d, E = c->E, J = steps < 0 ? c->J : steps;
+  // time-dependent loads: per-(step, column) bias terms, per-step GEMMs only
+  const double* LB = Fload ? seq_load_terms(c, nc, J, Fload, st) : nullptr;
   const size_t n = (size_t)E * nc * d;
   c->Xa.ensure(sizeof(double) * n + 8);
   c->Xb.ensure(sizeof(double) * n + 8);
@@ -132,7 +209,7 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
     c->Xin.ensure(sizeof(double) * n + 8);
     sub((long long)n, X_in, X_prev, c->Xin.d(), st);
     Ds = c->Xin.d();
-  } else {
+  } else if (!LB) {
     int rpc_, cs_;
     size_t sm_;
     // algorithmic flops of J split steps: u rows contract [X; Dw], w rows [X; Dw; Du]
@@ -200,6 +277,11 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
       p.ws_doubles = c->splitws.bytes / sizeof(double);
       p.bias = c->cvec.d() + (long long)e0 * d;
       p.bias_b1 = d;
+      if (LB) {  // C = T [X; D] + LB[s]  (per-column load terms replace the bias)
+        p.bias = nullptr;
+        p.Cin = LB + ((size_t)s * E + e0) * (size_t)nc * d;
+        p.beta = 1.0;
+      }
       if (Dn) {
         p.D = Dn;
         p.Xp = Xs;
@@ -368,7 +450,8 @@ static void run_sweeps(pe_ctx* c, int nc, int max_iter, const std::vector<const 
 // The modal sweep (wr_modal.cu; setup_modal_full): per sweep the rhs GEMM, the u scan, the
 // g GEMM, the w scan, the residual-norm GEMM(s) and the stop decision.
 static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, int nc,
-                                 int* sweeps, int* reasons, double* resid_hist, cudaStream_t st) {
+                                 int* sweeps, int* reasons, double* resid_hist, cudaStream_t st,
+                                 const double* Fload = nullptr) {
   const int d1 = c->d1, d2 = c->d2, d = c->d, E = c->E, J = c->J;
   const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
   const double alpha = c->wr_alpha, tol = c->wr_tol, dt = c->wr_dt;
@@ -434,6 +517,41 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
   basis_gemm(d2, c->Vicat.d() + (long long)d1 * d1, X_in + d1, d, (long long)nc * d, c->Z0.d(), L2, nc);
   modal_seed(E, nc, d1, d2, J, c->Y0m.d(), c->Z0.d(), Yw, nullptr, Zw, nullptr, DZ, st);
 
+  // time-dependent loads: per-(substep, interval) rhs / h load terms replace V1^T f1 and
+  // dt V2^T f2 (allatonce.py:212-218 load rows; build_rhs :156, _w_sweep :224)
+  const double* LB1 = nullptr;
+  const double* LB2 = nullptr;
+  if (Fload) {
+    const size_t n1 = (size_t)E * NJ * d1, n2 = (size_t)E * NJ * d2;
+    c->LF1.ensure(sizeof(double) * n1 + 8);
+    c->LF2.ensure(sizeof(double) * n2 + 8);
+    c->LB1.ensure(sizeof(double) * n1 + 8);
+    c->LB2.ensure(sizeof(double) * n2 + 8);
+    k_perm_seni<<<loads_grid((long long)n1), 256, 0, st>>>(E, nc, J, d, 0, d1, Fload, c->LF1.d(), 0);
+    k_perm_seni<<<loads_grid((long long)n2), 256, 0, st>>>(E, nc, J, d, d1, d2, Fload, c->LF2.d(), 0);
+    g_launches += 2;
+    PE_CUDA_CHECK(cudaGetLastError());
+    auto tgemm = [&](int M, const double* V, const double* B, double* C, double alpha_) {
+      GemmParams p;  // C = alpha V^T B over all (s, n) columns, V row-major M x M
+      p.M = M;
+      p.N = (int)NJ;
+      p.nb1 = E;
+      p.nseg = 1;
+      p.alpha = alpha_;
+      p.seg[0].A = Operand{V, 1, M, vstride, 0};
+      p.seg[0].B = Operand{B, 1, M, NJ * M, 0};
+      p.seg[0].K = M;
+      p.C = C;
+      p.c_i = 1;
+      p.c_j = M;
+      p.c_b1 = NJ * M;
+      run_gemm(c, p, st);
+    };
+    tgemm(d1, c->Vcat.d(), c->LF1.d(), c->LB1.d(), 1.0);
+    tgemm(d2, c->Vcat.d() + (long long)d1 * d1, c->LF2.d(), c->LB2.d(), dt);
+    LB1 = c->LB1.d();
+    LB2 = c->LB2.d();
+  }
   // loop-invariant GEMM parameter blocks (buffer parity fills in the B / C pointers)
   auto rhs_params = [&](const double* Zcur) {
     GemmParams r;  // r~ = [A~ | M~][Z_s; DZ_s] + V1^T f1   (build_rhs, allatonce.py:136-158)
@@ -453,6 +571,11 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     r.c_b1 = J * L1;
     r.bias = c->f1t.d();
     r.bias_b1 = d1;
+    if (LB1) {
+      r.bias = nullptr;
+      r.Cin = LB1;
+      r.beta = 1.0;
+    }
     return r;
   };
   auto g_params = [&](const double* Ynew) {
@@ -473,6 +596,11 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
     g.c_b1 = J * L2;
     g.bias = c->cgt.d();
     g.bias_b1 = d2;
+    if (LB2) {
+      g.bias = nullptr;
+      g.Cin = LB2;
+      g.beta = 1.0;
+    }
     return g;
   };
   // residual norms ||V1 EY_s|| = ||U1 EY_s|| (U1 upper-triangular, setup.cu norm_factor),
@@ -545,7 +673,7 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
       (const void*)(intptr_t)4, c->Yb[0].p, c->Zb[0].p, c->R.p, c->DW.p, c->EYZ.p, c->nrmp.p, cs, c->rhist.p, cnt, c->pinned_count, c->RT.p,
       c->GT.p, c->f1t.p, c->cgt.p, c->acoef.p, c->cden.p, c->lam.p, c->Vcat.p, c->Ucat.p, c->colmax.p,
       c->wticket.p,
-      (const void*)(intptr_t)max_iter, dkey(alpha), dkey(tol), dkey(dt)};
+      (const void*)(intptr_t)max_iter, dkey(alpha), dkey(tol), dkey(dt), LB1, LB2};
   PE_CUDA_CHECK(cudaMemsetAsync(cnt + 2, 0, sizeof(int), st));
   run_sweeps(c, nc, max_iter, key, body, st, true, cnt + 2);
 
@@ -562,7 +690,15 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
 }
 
 static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc, int* sweeps,
-                           int* reasons, double* resid_hist, cudaStream_t st) {
+                           int* reasons, double* resid_hist, cudaStream_t st,
+                           const double* Fload = nullptr) {
+  if (Fload) {
+    require(c->wr_modal_avail, PE_ERR_ARG,
+            "time-dependent loads in the all-at-once solver need symmetric-definite pencils "
+            "(A11, M11), (A22, M22) with d1, d2 > 0 (the modal sweep)");
+    fine_allatonce_modal(c, X_in, X_out, nc, sweeps, reasons, resid_hist, st, Fload);
+    return;
+  }
   if (c->wr_modal_full) {
     fine_allatonce_modal(c, X_in, X_out, nc, sweeps, reasons, resid_hist, st);
     return;
@@ -996,6 +1132,83 @@ int pe_coarse_correct(pe_ctx* c, int N, const double* X_old, const double* F_hat
     c->partial.ensure(sizeof(double) * (size_t)c->E * N * 296 * 2 + 8);
     coarse_correct(c->E, c->d, N, c->Phi.d(), c->gG.d(), X_old, F_hat, G_cache, X_new,
                    c->partial.d(), diff, active, (cudaStream_t)stream);
+  });
+}
+
+int pe_fine_sequential_loads(pe_ctx* c, const double* X_in, double* X_out, int nc,
+                             const double* F, void* stream) {
+  return guarded([&] {
+    require(c && X_in && X_out && F && nc >= 1, PE_ERR_ARG, "bad fine_sequential_loads arguments");
+    require(c->seq_dt > 0, PE_ERR_STATE, "pe_prepare_sequential not called");
+    bind(c);
+    fine_sequential(c, X_in, X_out, nc, (cudaStream_t)stream, nullptr, -1, F);
+  });
+}
+
+int pe_split_step_loads(pe_ctx* c, const double* X_in, const double* X_prev, double* X_out,
+                        int nc, const double* F, void* stream) {
+  return guarded([&] {
+    require(c && X_in && X_prev && X_out && F && nc >= 1, PE_ERR_ARG, "bad split_step_loads arguments");
+    require(c->seq_dt > 0, PE_ERR_STATE, "pe_prepare_sequential not called");
+    bind(c);
+    fine_sequential(c, X_in, X_out, nc, (cudaStream_t)stream, X_prev, 1, F);
+  });
+}
+
+int pe_fine_allatonce_loads(pe_ctx* c, const double* X_in, double* X_out, int nc,
+                            const double* F, int* sweeps, int* reasons, double* resid_hist,
+                            void* stream) {
+  return guarded([&] {
+    require(c && X_in && X_out && F && nc >= 1 && nc <= c->maxc, PE_ERR_ARG,
+            "bad fine_allatonce_loads arguments");
+    require(c->wr_ready, PE_ERR_STATE, "pe_prepare_allatonce not called");
+    bind(c);
+    fine_allatonce(c, X_in, X_out, nc, sweeps, reasons, resid_hist, (cudaStream_t)stream, F);
+  });
+}
+
+int pe_coarse_correct_loads(pe_ctx* c, int N, const double* X_old, const double* F_hat,
+                            double* G_cache, double* X_new, double* diff, const int* active,
+                            const double* Fc, void* stream) {
+  return guarded([&] {
+    require(c && X_old && X_new && G_cache && Fc && N >= 1, PE_ERR_ARG,
+            "bad coarse_correct_loads arguments");
+    require(c->coarse_dt > 0, PE_ERR_STATE, "pe_prepare_coarse not called");
+    bind(c);
+    cudaStream_t st = (cudaStream_t)stream;
+    c->partial.ensure(sizeof(double) * (size_t)c->E * N * 296 * 2 + 8);
+    const double* gs = coarse_load_terms(c, N, Fc, st);
+    coarse_correct(c->E, c->d, N, c->Phi.d(), c->gG.d(), X_old, F_hat, G_cache, X_new,
+                   c->partial.d(), diff, active, st, gs);
+  });
+}
+
+int pe_coarse_apply_loads(pe_ctx* c, const double* X_in, double* X_out, int nc,
+                          const double* Fc, void* stream) {
+  return guarded([&] {
+    require(c && X_in && X_out && Fc && nc >= 1, PE_ERR_ARG, "bad coarse_apply_loads arguments");
+    require(c->coarse_dt > 0, PE_ERR_STATE, "pe_prepare_coarse not called");
+    bind(c);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int d = c->d, E = c->E;
+    c->hist_tmp.ensure(sizeof(double) * (size_t)E * 2 * d + 8);
+    c->Gc.ensure(sizeof(double) * (size_t)E * d + 8);
+    c->partial.ensure(sizeof(double) * (size_t)E * 296 * 2 + 8);
+    const double* gs = coarse_load_terms(c, nc, Fc, st);  // (E, nc, d): one term per state
+    c->Xs.ensure(sizeof(double) * (size_t)E * d + 8);
+    for (int n = 0; n < nc; ++n) {
+      PE_CUDA_CHECK(cudaMemcpy2DAsync(c->hist_tmp.d(), sizeof(double) * 2 * d, X_in + (size_t)n * d,
+                                      sizeof(double) * nc * d, sizeof(double) * d, E,
+                                      cudaMemcpyDeviceToDevice, st));
+      PE_CUDA_CHECK(cudaMemcpy2DAsync(c->Xs.d(), sizeof(double) * d, gs + (size_t)n * d,
+                                      sizeof(double) * nc * d, sizeof(double) * d, E,
+                                      cudaMemcpyDeviceToDevice, st));
+      coarse_correct(E, d, 1, c->Phi.d(), c->gG.d(), c->hist_tmp.d(), nullptr, c->Gc.d(),
+                     c->hist_tmp.d(), c->partial.d(), nullptr, nullptr, st, c->Xs.d());
+      PE_CUDA_CHECK(cudaMemcpy2DAsync(X_out + (size_t)n * d, sizeof(double) * nc * d,
+                                      c->hist_tmp.d() + d, sizeof(double) * 2 * d,
+                                      sizeof(double) * d, E, cudaMemcpyDeviceToDevice, st));
+    }
   });
 }
 

@@ -67,12 +67,15 @@ struct pe_ctx {
   pe::DevBuf M11, A11, M12, A12, M22, A22, f1, f2;
   std::vector<char> member_set;
 
-  // sequential fine: X_{s+1} = T [X_s; D_s] + cvec   (T: E x d x 2d)
+  // sequential fine: X_{s+1} = T [X_s; D_s] + cvec   (T: E x d x 2d); cvec = Lf [f1; f2]
   double seq_dt = -1.0;
-  pe::DevBuf T, cvec;
-  // coarse: G(x) = Phi x + gG                         (Phi: E x d x d)
+  pe::DevBuf T, cvec, Lf;
+  // coarse: G(x) = Phi x + gG                         (Phi: E x d x d); gG = LG [f1; f2]
   double coarse_dt = -1.0;
-  pe::DevBuf Phi, gG;
+  pe::DevBuf Phi, gG, LG;
+  // time-dependent loads: per-call load-term series (sequential bias, WR rhs / h terms,
+  // coarse terms) and their permuted inputs
+  pe::DevBuf LB, LF1, LF2, LB1, LB2, LGs;
   // all-at-once
   bool wr_ready = false;
   double wr_dt = 0, wr_alpha = 0, wr_tol = 0;
@@ -85,6 +88,7 @@ struct pe_ctx {
   pe::DevBuf Vm, Vinv, lam, GZ, cgz, Z0, Hz;
   // full modal sweep (setup_modal_full, wr_modal.cu): both pencils diagonalised
   bool wr_modal_full = false;
+  bool wr_modal_avail = false;  // modal operators built (also when the tiny kernel is used)
   pe::DevBuf Vcat, Vicat, Ucat, RT, GT, f1t, cgt, acoef, cden;
   pe::DevBuf Yb[2], Zb[2], DYm, EYZ, Y0m, nrmp, colmax;
 

@@ -191,7 +191,7 @@ void wr_tiny(const TinyArgsPublic& p, cudaStream_t st);
 // Row-partitioned cluster kernel; see coarse.cu.
 void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
                     const double* X_old, const double* F_hat, double* G_cache, double* X_new,
-                    double* partial, double* diff, const int* active, cudaStream_t st);
+                    double* partial, double* diff, const int* active, cudaStream_t st, const double* gseries = nullptr);
 int coarse_cluster_size(int d);
 
 extern long long g_launches;  // kernel launches issued by libpe in this process

@@ -186,6 +186,7 @@ void setup_sequential(pe_ctx* c, double dt) {
   cublasHandle_t h = c->blas;
   c->T.ensure(sizeof(double) * (size_t)c->E * d * 2 * d + 8);
   c->cvec.ensure(sizeof(double) * (size_t)c->E * d + 8);
+  c->Lf.ensure(sizeof(double) * (size_t)c->E * d * d + 8);
   DevBuf K, Kinv, M22inv, Ew, Qd, Qu, cw;
   K.ensure(sizeof(double) * d1 * (size_t)d1 + 8);
   Kinv.ensure(sizeof(double) * d1 * (size_t)d1 + 8);
@@ -206,6 +207,10 @@ void setup_sequential(pe_ctx* c, double dt) {
     const double* f2 = c->f2.d() + (size_t)e * d2;
     double* T = c->T.d() + (size_t)e * d * ldT;
     double* cv = c->cvec.d() + (size_t)e * d;
+    // load map: bias = Lf [f1; f2], Lf = [[K^-1, 0], [Qu K^-1, dt M22^-1]] (the loads'
+    // path through split_step, stepping.py:125-146), for time-dependent loads
+    double* Lf = c->Lf.d() + (size_t)e * d * d;
+    zero_block_kernel<<<grid_for((long long)d * d), 256, 0, st>>>(d, d, Lf, d);
     zero_block_kernel<<<grid_for((long long)d * ldT), 256, 0, st>>>(d, ldT, T, ldT);
     if (d1) {
       rm_geam(h, false, false, d1, d1, 1.0 / dt, M11, d1, 1.0, A11, d1, K.d(), d1);
@@ -217,6 +222,7 @@ void setup_sequential(pe_ctx* c, double dt) {
                 T + d + d1, ldT);  // Pd
       }
       rm_gemm(h, false, false, d1, 1, d1, 1.0, Kinv.d(), d1, f1, 1, 0.0, cv, 1);  // cu
+      rm_geam(h, false, false, d1, d1, 1.0, Kinv.d(), d1, 0.0, Kinv.d(), d1, Lf, d);
     }
     if (d2) {
       inverse(c, d2, M22, M22inv.d());
@@ -225,6 +231,8 @@ void setup_sequential(pe_ctx* c, double dt) {
       set_identity(d2, Tw + d1, ldT, 1.0, st);
       rm_gemm(h, false, false, d2, d2, d2, -dt, M22inv.d(), d2, A22, d2, 1.0, Tw + d1, ldT);
       rm_gemm(h, false, false, d2, 1, d2, dt, M22inv.d(), d2, f2, 1, 0.0, cv + d1, 1);  // cw
+      rm_geam(h, false, false, d2, d2, dt, M22inv.d(), d2, 0.0, M22inv.d(), d2,
+              Lf + (size_t)d1 * d + d1, d);
       if (d1) {
         rm_gemm(h, false, true, d2, d1, d2, -1.0, M22inv.d(), d2, M12, d2, 0.0, Tw + d, ldT);  // Qd
         rm_gemm(h, false, true, d2, d1, d2, -dt, M22inv.d(), d2, A12, d2, 0.0, Qu.d(), d1);   // Qu
@@ -234,6 +242,8 @@ void setup_sequential(pe_ctx* c, double dt) {
         rm_gemm(h, false, false, d2, d2, d1, 1.0, Qu.d(), d1, T + d + d1, ldT, 0.0,
                 Tw + d + d1, ldT);
         rm_gemm(h, false, false, d2, 1, d1, 1.0, Qu.d(), d1, cv, 1, 1.0, cv + d1, 1);
+        rm_gemm(h, false, false, d2, d1, d1, 1.0, Qu.d(), d1, Kinv.d(), d1, 0.0,
+                Lf + (size_t)d1 * d, d);
       }
     }
   }
@@ -277,6 +287,7 @@ void setup_coarse(pe_ctx* c, double dt) {
   cudaStream_t st = c->setup_stream;
   c->Phi.ensure(sizeof(double) * (size_t)c->E * d * d + 8);
   c->gG.ensure(sizeof(double) * (size_t)c->E * d + 8);
+  c->LG.ensure(sizeof(double) * (size_t)c->E * d * d + 8);  // K_G^-1 (time-dependent loads)
   DevBuf KG, RG, KGinv, f;
   KG.ensure(sizeof(double) * (size_t)d * d);
   RG.ensure(sizeof(double) * (size_t)d * d);
@@ -295,6 +306,8 @@ void setup_coarse(pe_ctx* c, double dt) {
             c->Phi.d() + (size_t)e * d * d, d);
     rm_gemm(c->blas, false, false, d, 1, d, 1.0, KGinv.d(), d, f.d(), 1, 0.0,
             c->gG.d() + (size_t)e * d, 1);
+    PE_CUDA_CHECK(cudaMemcpyAsync(c->LG.d() + (size_t)e * d * d, KGinv.d(),
+                                  sizeof(double) * (size_t)d * d, cudaMemcpyDeviceToDevice, st));
   }
   PE_CUDA_CHECK(cudaStreamSynchronize(st));
   c->coarse_dt = dt;
@@ -577,7 +590,8 @@ void setup_allatonce(pe_ctx* c, double dt, double alpha, double tol, int max_ite
   }
   // modal sweep when both pencils diagonalise (wr_modal.cu); otherwise the general path
   c->wr_modal = false;
-  c->wr_modal_full = c->use_modal && !wr_tiny_eligible(d1, d2, J, npm) && setup_modal_full(c, dt, alpha);
+  c->wr_modal_avail = c->use_modal && setup_modal_full(c, dt, alpha);
+  c->wr_modal_full = c->wr_modal_avail && !wr_tiny_eligible(d1, d2, J, npm);
   if (!c->wr_modal_full) setup_allatonce_general(c, dt, alpha, npm, even);
   PE_CUDA_CHECK(cudaStreamSynchronize(st));
   c->wr_ready = true;

@@ -117,6 +117,44 @@ class PeContext:
                                          _ptr(rh), self.stream()))
         return Y, sw, rs, rh
 
+    # ------------------------------------------------------------------ time-dependent loads
+    def fine_sequential_loads(self, X: torch.Tensor, F: torch.Tensor) -> torch.Tensor:
+        """F: (E, nc, J, d) loads [f1; f2] at each substep's end time."""
+        nc = X.shape[1]
+        Y = self.empty(self.E, nc, self.d)
+        check(self.lib.pe_fine_sequential_loads(self.ptr, _ptr(X), _ptr(Y), nc, _ptr(F),
+                                                self.stream()))
+        return Y
+
+    def split_step_loads(self, X, Xp, F) -> torch.Tensor:
+        nc = X.shape[1]
+        Y = self.empty(self.E, nc, self.d)
+        check(self.lib.pe_split_step_loads(self.ptr, _ptr(X), _ptr(Xp), _ptr(Y), nc, _ptr(F),
+                                           self.stream()))
+        return Y
+
+    def fine_allatonce_loads(self, X: torch.Tensor, F: torch.Tensor, record: bool = True):
+        nc = X.shape[1]
+        Y = self.empty(self.E, nc, self.d)
+        sw = self.empty(self.E, nc, dtype=torch.int32)
+        rs = self.empty(self.E, nc, dtype=torch.int32)
+        rh = self.empty(self.E, nc, self.max_iter) if record else None
+        check(self.lib.pe_fine_allatonce_loads(self.ptr, _ptr(X), _ptr(Y), nc, _ptr(F),
+                                               _ptr(sw), _ptr(rs), _ptr(rh), self.stream()))
+        return Y, sw, rs, rh
+
+    def coarse_correct_loads(self, N, X_old, F_hat, G_cache, X_new, Fc, diff=None, active=None):
+        check(self.lib.pe_coarse_correct_loads(self.ptr, N, _ptr(X_old), _ptr(F_hat),
+                                               _ptr(G_cache), _ptr(X_new), _ptr(diff),
+                                               _ptr(active), _ptr(Fc), self.stream()))
+
+    def coarse_apply_loads(self, X: torch.Tensor, Fc: torch.Tensor) -> torch.Tensor:
+        nc = X.shape[1]
+        Y = self.empty(self.E, nc, self.d)
+        check(self.lib.pe_coarse_apply_loads(self.ptr, _ptr(X), _ptr(Y), nc, _ptr(Fc),
+                                             self.stream()))
+        return Y
+
     def wr_waveforms(self, nc: int):
         U = self.empty(self.E, nc, self.J + 1, self.d1)
         W = self.empty(self.E, nc, self.J + 1, self.d2)

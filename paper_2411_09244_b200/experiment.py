@@ -122,12 +122,9 @@ def run_single(pipe, n: int, *, stop_rule: str = "absolute") -> RunResult:
     tg = cfg.time_grid(n)
     tg = TimeGrid(tg.t_end, tg.n_intervals, tg.substeps)
     loads = pipe.loads
-    if not getattr(loads, "constant", False):
-        # the reference's Pipeline loads are ConstantLoads; anything time-dependent goes
-        # through the same check as SplitPropagators / WaveformRelaxation
-        raise NotImplementedError("run_single: libpe supports time-constant loads "
-                                  "(ConstantLoads); got %r" % type(loads).__name__)
-    loads = ConstantLoads(*loads.at(0.0))
+    if getattr(loads, "constant", False):
+        loads = ConstantLoads(*loads.at(0.0))
+    # otherwise a time-dependent provider with at(t), used as given (stepping.py:125,164)
     if getattr(cfg, "compute_reference", False):
         from .fem import check_reference_size
 

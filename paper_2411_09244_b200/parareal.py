@@ -63,13 +63,25 @@ class SequentialFine:
 
     def propagate_all(self, states):
         ctx = self.ctx
+        tg = self.time_grid
+        props = self.propagators
+        F = (None if props.constant_loads else
+             props.fine_load_series([s.t for s in states], tg.dt_sub, tg.substeps))
         with ctx.lock:
-            ctx.prepare_sequential(self.time_grid.dt_sub)
+            ctx.prepare_sequential(tg.dt_sub)
             X = ctx.to_dev(np.array([s.stacked() for s in states])[None])
-            Y = ctx.fine_sequential(X)[0].cpu().numpy()
-        d1 = self.propagators.system.d1
-        return [(SplitState.fresh(y[:d1], y[d1:], s.t + self.time_grid.dt), {"converged": True})
-                for y, s in zip(Y, states)]
+            if F is None:
+                Y = ctx.fine_sequential(X)[0].cpu().numpy()
+            else:
+                Y = ctx.fine_sequential_loads(X, ctx.to_dev(F[None]))[0].cpu().numpy()
+        d1 = props.system.d1
+        out = []
+        for y, s in zip(Y, states):
+            t = s.t
+            for _ in range(tg.substeps):  # the reference's accumulated SplitState.t
+                t = t + tg.dt_sub
+            out.append((SplitState.fresh(y[:d1], y[d1:], t), {"converged": True}))
+        return out
 
 
 class AllAtOnceFine:
@@ -221,17 +233,26 @@ def _run_parareal_plugin(config: ParerealConfig, propagators: SplitPropagators, 
     ctx = propagators.context(tg.substeps)
     ctx.prepare_coarse(tg.dt)
     d = ctx.d
+    const = propagators.constant_loads
     x0 = initial.stacked()
     X = ctx.to_dev(np.zeros((1, N + 1, d)))
     X[0, 0] = ctx.to_dev(x0)
     G = ctx.empty(1, N, d)
     diff = ctx.empty(1, 2)
-    ctx.coarse_correct(N, X, None, G, X)  # initial_sweep + cached G (parareal.py:178-179)
-    hist_rows = X[0].cpu().numpy()
-    history = [hist_rows.copy()]
     times = [initial.t]  # state times as the reference carries them (t + dt per step)
     for _ in range(N):
         times.append(times[-1] + tg.dt)
+
+    def coarse(X_old, F_hat, X_new, dif):
+        if const:
+            ctx.coarse_correct(N, X_old, F_hat, G, X_new, dif)
+        else:  # G from state n at times[n]: loads at times[n] + dt (stepping.py:164)
+            Fc = ctx.to_dev(propagators.load_rows([times[n] + tg.dt for n in range(N)])[None])
+            ctx.coarse_correct_loads(N, X_old, F_hat, G, X_new, Fc, dif)
+
+    coarse(X, None, X, None)  # initial_sweep + cached G (parareal.py:178-179)
+    hist_rows = X[0].cpu().numpy()
+    history = [hist_rows.copy()]
     max_diffs, fine_info, fine_seconds, coarse_seconds = [], [], [], []
     converged = False
     iterations = 0
@@ -250,7 +271,7 @@ def _run_parareal_plugin(config: ParerealConfig, propagators: SplitPropagators, 
         tic = time.perf_counter()
         F = ctx.to_dev(np.array([st.stacked() for st, _ in results])[None])
         X_new = ctx.empty(1, N + 1, d)
-        ctx.coarse_correct(N, X, F, G, X_new, diff)
+        coarse(X, F, X_new, diff)
         X = X_new
         hist_rows = X[0].cpu().numpy()
         dv = diff[0].cpu().numpy()
@@ -284,7 +305,9 @@ def run_parareal(config: ParerealConfig, propagators: SplitPropagators, fine,
     if config.stop_rule not in ("absolute", "relative"):
         raise ValueError(f"unknown stop rule {config.stop_rule!r}")
     ctx = _libpe_context(fine)
-    if ctx is None:
+    if ctx is None or not propagators.constant_loads:
+        # user propagators, and time-dependent loads (whose per-iteration load series come
+        # from the host): host loop over iterations, fine + coarse on the GPU
         if not callable(getattr(fine, "propagate", None)):
             raise TypeError("fine propagator needs a propagate(state) -> (state, info) method")
         return _run_parareal_plugin(config, propagators, fine, initial)

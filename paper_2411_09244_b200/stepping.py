@@ -105,18 +105,43 @@ class SplitPropagators:
     context, built once per step size.
     """
 
-    def __init__(self, system: CoarseSystem, loads: ConstantLoads, device: int | None = None):
-        if not getattr(loads, "constant", False):
-            raise NotImplementedError("libpe supports time-constant loads (ConstantLoads)")
+    def __init__(self, system: CoarseSystem, loads, device: int | None = None):
         self.system = system
         self.loads = loads
         self.device = device
         self._ctx: dict[int, PeContext] = {}
 
+    @property
+    def constant_loads(self) -> bool:
+        return bool(getattr(self.loads, "constant", False))
+
     def context(self, substeps: int) -> PeContext:
         if substeps not in self._ctx:
-            self._ctx[substeps] = PeContext([self.system], [self.loads], substeps, self.device)
+            base = self.loads if self.constant_loads else ConstantLoads.zero(self.system)
+            self._ctx[substeps] = PeContext([self.system], [base], substeps, self.device)
         return self._ctx[substeps]
+
+    def load_rows(self, times) -> np.ndarray:
+        """[f1(t); f2(t)] for every t (the reference's `loads.at`), shape (len(times), d)."""
+        rows = []
+        for t in times:
+            f1, f2 = self.loads.at(float(t))
+            rows.append(np.concatenate([np.asarray(f1, dtype=float).ravel(),
+                                        np.asarray(f2, dtype=float).ravel()]))
+        return np.array(rows).reshape(len(rows), self.system.d1 + self.system.d2)
+
+    def fine_load_series(self, starts, dt: float, substeps: int) -> np.ndarray:
+        """Loads of a sequential fine interval from each start time: substep s at the
+        reference's accumulated SplitState.t + dt (stepping.py:125,147), (nc, J, d)."""
+        out = []
+        for t in starts:
+            times = []
+            tt = float(t)
+            for _ in range(substeps):
+                times.append(tt + dt)
+                tt = tt + dt
+            out.append(self.load_rows(times))
+        return np.array(out)
 
     # ------------------------------------------------------------------ reference API
     def split_step(self, state: SplitState, dt: float) -> SplitState:
@@ -126,7 +151,11 @@ class SplitPropagators:
             ctx.prepare_sequential(dt)
             x = ctx.to_dev(state.stacked()[None, None])
             xp = ctx.to_dev(np.concatenate([state.u_prev, state.w_prev])[None, None])
-            y = ctx.split_step(x, xp)[0, 0].cpu().numpy()
+            if self.constant_loads:
+                y = ctx.split_step(x, xp)[0, 0].cpu().numpy()
+            else:  # loads at state.t + dt (stepping.py:125)
+                F = ctx.to_dev(self.load_rows([state.t + dt])[None, None])
+                y = ctx.split_step_loads(x, xp, F)[0, 0].cpu().numpy()
         d1 = self.system.d1
         return SplitState(y[:d1].copy(), y[d1:].copy(), state.u.copy(), state.w.copy(),
                           state.t + dt)
@@ -139,7 +168,12 @@ class SplitPropagators:
         ctx = self.context(1)
         with ctx.lock:
             ctx.prepare_coarse(dt)
-            y = ctx.coarse_apply(ctx.to_dev(_stack_states(states)[None]))[0].cpu().numpy()
+            X = ctx.to_dev(_stack_states(states)[None])
+            if self.constant_loads:
+                y = ctx.coarse_apply(X)[0].cpu().numpy()
+            else:  # loads at state.t + dt (stepping.py:164)
+                Fc = ctx.to_dev(self.load_rows([s.t + dt for s in states])[None])
+                y = ctx.coarse_apply_loads(X, Fc)[0].cpu().numpy()
         d1 = self.system.d1
         return [SplitState(r[:d1].copy(), r[d1:].copy(), s.u.copy(), s.w.copy(), s.t + dt)
                 for r, s in zip(y, states)]
@@ -150,18 +184,25 @@ class SplitPropagators:
         ctx = self.context(1)
         dt = dt_interval / substeps
         d1 = self.system.d1
+        Fs = None if self.constant_loads else self.fine_load_series([state.t], dt, substeps)[0]
         with ctx.lock:
             ctx.prepare_sequential(dt)
             x = ctx.to_dev(state.stacked()[None, None])
             xp = x.clone()
             rows = [x[0, 0]]
-            for _ in range(substeps):
-                y = ctx.split_step(x, xp)
+            for s in range(substeps):
+                if Fs is None:
+                    y = ctx.split_step(x, xp)
+                else:
+                    y = ctx.split_step_loads(x, xp, ctx.to_dev(Fs[s][None, None]))
                 xp, x = x, y
                 rows.append(y[0, 0])
             traj = torch.stack(rows).cpu().numpy()
+        t_end = state.t
+        for _ in range(substeps):  # SplitState.t accumulates per substep (stepping.py:147)
+            t_end = t_end + dt
         cur = SplitState(traj[-1, :d1].copy(), traj[-1, d1:].copy(), traj[-2, :d1].copy(),
-                         traj[-2, d1:].copy(), state.t + dt * substeps)
+                         traj[-2, d1:].copy(), t_end)
         times = state.t + dt * np.arange(substeps + 1)
         return SplitTrajectory(times, traj[:, :d1].copy(), traj[:, d1:].copy(), cur)
 

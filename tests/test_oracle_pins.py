@@ -165,3 +165,40 @@ def test_config_kappa_and_fine_assembly_pinned():
 
     assert abs(M - ref("M")).max() <= 1e-15 * abs(ref("M")).max()
     assert abs(A * scale - ref("A")).max() <= 1e-14 * abs(ref("A")).max()
+
+
+def _wave(z):
+    f1, f2 = z["f1"], z["f2"]
+    return lambda t: (f1 * (1.0 + 0.5 * np.sin(2.0 * np.pi * t)),
+                      f2 * (1.0 - 0.3 * np.cos(2.0 * np.pi * t)) + 0.01 * t)
+
+
+def test_oracle_time_dependent_loads_pinned():
+    """The oracle's time-dependent-load paths (loads at t + dt in the split / coarse steps,
+    at t0 + s dt in the WR rows, state times carried through parareal) against the
+    unmodified reference (tests/golden/tv_loads.npz, oracle/make_tv_golden.py)."""
+    import dataclasses
+
+    g = golden("tv_loads.npz")
+    z = golden("sys_cfg0.npz")
+    s = dataclasses.replace(_sys(z), loads_at=_wave(z))
+    o = po.OracleSplit(s)
+    x = g["x"]
+    d1 = s.d1
+    un, wn = o.split_step(x[:d1], x[d1:], x[:d1] * 0.9, x[d1:] * 1.1, 0.01, 0.37)
+    np.testing.assert_allclose(np.concatenate([un, wn]), g["split"], rtol=1e-12, atol=1e-18)
+    # coarse_step reads the current state only
+    np.testing.assert_allclose(o.coarse_step(x, 0.1, 0.37), g["coarse"], rtol=1e-12, atol=1e-18)
+    U, W, t1 = o.fine_interval(x[:d1], x[d1:], 0.1, 10, 0.37, return_t=True)
+    np.testing.assert_allclose(U, g["fine_U"], rtol=1e-12, atol=1e-18)
+    np.testing.assert_allclose(W, g["fine_W"], rtol=1e-12, atol=1e-18)
+    assert t1 == float(g["fine_t"])
+    r = po.OracleWR(s, 10, 0.1, 0.1, tol=1e-12, max_iter=400).solve(x[:d1], x[d1:], 0.37)
+    assert r["iterations"] == int(g["wr_meta"][0])
+    np.testing.assert_allclose(r["U"], g["wr_U"], rtol=1e-10, atol=1e-16)
+    for kind, tag in (("sequential", "seq"), ("all-at-once", "aao")):
+        ref = po.run_parareal(s, np.zeros(s.d1 + s.d2), 1.0, 10, 10, kind=kind, alpha=0.1,
+                              epsilon=1e-8, k_max=10, stop="relative", fine_tol=1e-12)
+        assert ref["iterations"] == int(g[f"{tag}_iters"])
+        h = np.array(ref["history"])
+        assert np.abs(h - g[f"{tag}_hist"]).max() <= 1e-10 * np.abs(g[f"{tag}_hist"]).max()

@@ -10,9 +10,10 @@ def summarize(path, top=12, by_grid=False):
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     gi = h.index("Grid Size")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         name = r[ki]
         base = name.split("(")[0]
