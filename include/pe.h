@@ -234,6 +234,13 @@ int pe_build_rhs(int d1, int d2, int J, const double* M11, const double* M12, co
 int pe_allatonce_usolve(pe_ctx* ctx, const double* R, double* U, int nc, double* resid,
                         void* stream);
 
+/* WRResult.solver_residual (allatonce.py:296; ImplicitAllAtOnce's guard, :125-131) for the
+ * intervals of the last all-at-once solve on this context (pe_fine_allatonce[_loads] or a
+ * parareal all-at-once iteration): out (device, E x nc) = ||B U M11 + U A11 - rhs|| / ||rhs||
+ * with rhs = build_rhs of each interval's final waveforms, solved on the context's
+ * factorisation.  PE_ERR_STATE when no solve has run. */
+int pe_wr_solver_residual(pe_ctx* ctx, double* out, void* stream);
+
 /* project_initial (stepping.py:216-226), host arrays: u = M11^-1 Psi1^T M u0 and
  * w = M22^-1 Psi2^T M u0.  M: CSR (n x n); P: CSC (n x d) of hstack([Psi1, Psi2]);
  * M11, M22 row-major; u0 (n); u_out (d1), w_out (d2).  LU with partial pivoting. */

@@ -73,6 +73,7 @@ SIGNATURES = {
     "pe_build_rhs": (C.c_int, [C.c_int, C.c_int, C.c_int] + [_P] * 9 + [C.c_double, C.c_double,
                                                                        _P, _P]),
     "pe_allatonce_usolve": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
+    "pe_wr_solver_residual": (C.c_int, [_P, _P, _P]),
     "pe_project_initial": (C.c_int, [C.c_int, C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _D, _D,
                                      _D, _D, _D, _P]),
     "pe_stability_max_step": (C.c_int, [_P, C.c_int, C.c_double, C.c_int, _D, _I, _P]),

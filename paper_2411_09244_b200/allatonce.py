@@ -262,6 +262,7 @@ class WaveformRelaxation:
                 U, W = ctx.wr_waveforms(nc)
                 U = U[0].cpu().numpy()
                 W = W[0].cpu().numpy()
+            sres = ctx.wr_solver_residual(nc)[0].cpu().numpy()
         d1 = self.system.d1
         out = []
         for n, s in enumerate(states):
@@ -283,7 +284,11 @@ class WaveformRelaxation:
             final = SplitState(u=Y[n, :d1].copy(), w=Y[n, d1:].copy(),
                                u_prev=Un[-2].copy(), w_prev=Wn[-2].copy(),
                                t=s.t + self.dt_interval)
-            out.append(WRResult(SplitTrajectory(times, Un, Wn, final), res, it, conv, reason))
+            # solver_residual: the u-solve's relative residual (allatonce.py:125-131, :296);
+            # imag_residue is 0.0: the solves run in real arithmetic (ImplicitAllAtOnce above)
+            log.debug("all-at-once residual %.3e", sres[n])
+            out.append(WRResult(SplitTrajectory(times, Un, Wn, final), res, it, conv, reason,
+                                solver_residual=float(sres[n]), imag_residue=0.0))
         return out
 
 

@@ -208,6 +208,32 @@ __global__ void k_aao_residual_sum(long long cols, int J, const double* __restri
   out[c] = sqrt(r) / fmax(sqrt(b), 1e-300);
 }
 
+
+// WR solver-residual diagnostic inputs from the final waveforms (blocks 1..J+1 of
+// Ux_cur / Wx_cur, member stride (J+2) L): DWdt_s = (W_{s+1} - W_s) / dt with
+// DWdt_0 = 0 (w_lag = w_start), V = u_start - alpha u_J
+__global__ void k_wr_diag_prep(int E, int J, long long L1, long long L2, double dt, double alpha,
+                               const double* __restrict__ U, const double* __restrict__ W,
+                               double* __restrict__ DWdt, double* __restrict__ V) {
+  const long long nw = (long long)E * J * L2, total = nw + (long long)E * L1;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    if (q < nw) {
+      const long long e = q / (J * L2);
+      const long long r = q - e * J * L2;
+      const int sidx = (int)(r / L2);
+      const long long x = r - (long long)sidx * L2;
+      const double* w = W + e * (J + 2) * L2 + x;
+      DWdt[q] = sidx == 0 ? 0.0 : (w[(long long)(sidx + 1) * L2] - w[(long long)sidx * L2]) / dt;
+    } else {
+      const long long t = q - nw;
+      const long long e = t / L1, x = t - e * L1;
+      const double* u = U + e * (J + 2) * L1 + x;
+      V[t] = u[L1] - alpha * u[(long long)(J + 1) * L1];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ projection helpers
 __global__ void k_csr_spmv(int n, const int* __restrict__ p, const int* __restrict__ ix,
                            const double* __restrict__ v, const double* __restrict__ x,
@@ -480,6 +506,82 @@ void allatonce_usolve(pe_ctx* c, const double* R, double* U, int nc, double* res
   }
 }
 
+
+// WRResult.solver_residual (allatonce.py:296): ImplicitAllAtOnce's conditioning guard
+// (:125-131) for the intervals of the last all-at-once solve.  The rhs is build_rhs
+// (:136-158) of each interval's final waveforms -- the system the sweep after the stop would
+// solve; it differs from the last sweep's by at most the WR tolerance, which moves a
+// relative residual of a linear solve only at rounding level -- solved on the context's
+// factorisation, residual in the row form of :129-131.
+void wr_solver_residual(pe_ctx* c, double* out, cudaStream_t st) {
+  const int d1 = c->d1, d2 = c->d2, J = c->J, E = c->E, nc = c->wr_last_nc;
+  const long long L1 = (long long)d1 * nc, L2 = (long long)d2 * nc;
+  const double dt = c->wr_dt, alpha = c->wr_alpha;
+  const double* U = c->Ux_cur.d();
+  const double* W = c->Wx_cur.d();
+  Dev<double> dw((size_t)E * J * L2 + 1), v((size_t)E * L1), rb((size_t)E * J * L1),
+      rf((size_t)E * J * L1), uf((size_t)E * J * L1);
+  k_wr_diag_prep<<<grid_for((long long)E * (J * L2 + L1), 256), 256, 0, st>>>(
+      E, J, L1, L2, dt, alpha, U, W, dw.p, v.p);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+  // R_s = f1_s - A12 wh_{s+1} - M12 (wh_{s+1} - wh_s) / dt, wh_{s+1} = W block s + 1
+  GemmParams r;
+  r.M = d1;
+  r.N = J * nc;
+  r.nb1 = E;
+  r.alpha = -1.0;
+  r.C = rb.p;
+  r.c_i = 1;
+  r.c_j = d1;
+  r.c_b1 = J * L1;
+  if (c->wr_last_loads) {
+    r.Cin = c->LF1.d();  // [e][s][n][i]: the R block layout
+    r.beta = 1.0;
+  } else {
+    r.bias = c->f1.d();
+    r.bias_b1 = d1;
+  }
+  if (d2) {
+    r.nseg = 2;
+    r.seg[0].A = Operand{c->A12.d(), d2, 1, (long long)d1 * d2, 0};
+    r.seg[0].B = Operand{W + L2, 1, d2, (J + 2) * L2, 0};
+    r.seg[0].K = d2;
+    r.seg[1].A = Operand{c->M12.d(), d2, 1, (long long)d1 * d2, 0};
+    r.seg[1].B = Operand{dw.p, 1, d2, J * L2, 0};
+    r.seg[1].K = d2;
+    gemm_f64(r, st);
+  } else {  // no w block: R = f1 rows
+    r.nseg = 1;
+    r.alpha = 0.0;
+    r.seg[0].A = Operand{c->M11.d(), d1, 1, (long long)d1 * d1, 0};
+    r.seg[0].B = Operand{U + L1, 1, d1, (J + 2) * L1, 0};
+    r.seg[0].K = d1;
+    gemm_f64(r, st);
+  }
+  // R_0 += M11 (u_start - alpha u_final) / dt
+  GemmParams r0;
+  r0.M = d1;
+  r0.N = nc;
+  r0.nb1 = E;
+  r0.nseg = 1;
+  r0.alpha = 1.0 / dt;
+  r0.seg[0].A = Operand{c->M11.d(), d1, 1, (long long)d1 * d1, 0};
+  r0.seg[0].B = Operand{v.p, 1, d1, L1, 0};
+  r0.seg[0].K = d1;
+  r0.C = rb.p;
+  r0.c_i = 1;
+  r0.c_j = d1;
+  r0.c_b1 = J * L1;
+  r0.Cin = rb.p;
+  r0.beta = 1.0;
+  gemm_f64(r0, st);
+  const long long per = (long long)E * nc * J * d1;
+  k_permute_nsi<<<grid_for(per, 256), 256, 0, st>>>(E, nc, J, d1, rf.p, rb.p, J * L1, 0, 0);
+  ++g_launches;
+  PE_CUDA_CHECK(cudaGetLastError());
+  allatonce_usolve(c, rf.p, uf.p, nc, out, st);  // synchronises before the buffers go
+}
 }  // namespace pe
 
 using namespace pe;
@@ -525,6 +627,21 @@ extern "C" int pe_allatonce_usolve(pe_ctx* c, const double* R, double* U, int nc
     require_arg(c && nc >= 0 && (nc == 0 || (R && U)), "need a context, nc >= 0 and buffers");
     PE_CUDA_CHECK(cudaSetDevice(c->device));
     allatonce_usolve(c, R, U, nc, resid, (cudaStream_t)stream);
+  });
+}
+
+extern "C" int pe_wr_solver_residual(pe_ctx* c, double* out, void* stream) {
+  return api_guard("pe_wr_solver_residual", [&] {
+    require_arg(c && out, "need a context and an output buffer");
+    if (!c->wr_ready || c->wr_last_nc < 1 || !c->Ux_cur.p)
+      throw Error{PE_ERR_STATE, "no all-at-once solve to diagnose"};
+    PE_CUDA_CHECK(cudaSetDevice(c->device));
+    if (c->d1 == 0) {
+      PE_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(double) * c->E * c->wr_last_nc,
+                                    (cudaStream_t)stream));
+      return;
+    }
+    wr_solver_residual(c, out, (cudaStream_t)stream);
   });
 }
 

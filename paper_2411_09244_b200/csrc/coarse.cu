@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(COARSE_THREADS, 1) coarse_kernel(const __grid_
 // partials reduced in block order by a final kernel.
 constexpr int CS_THREADS = 256;
 constexpr int CS_WARPS = CS_THREADS / 32;
+int coarse_stream_blocks(int d) { return std::min(296, (d + CS_WARPS - 1) / CS_WARPS); }
 
 __global__ void __launch_bounds__(CS_THREADS)
     coarse_step_stream_kernel(int d, int n, int N, const double* __restrict__ Phi,
@@ -381,9 +382,35 @@ __global__ void __launch_bounds__(CS_THREADS)
   double sd = 0.0, sn = 0.0;
   for (int r = blockIdx.x * CS_WARPS + warp; r < d; r += gridDim.x * CS_WARPS) {
     const double* row = Pm + (long long)r * d;
+    // the epilogue's operands are loaded ahead of the row so that their latency overlaps
+    // the stream (left to the compiler, they were serialised after it in some builds:
+    // 45 vs 105 us per cfg4 coarse step)
+    const long long o = (long long)n * d + r;
+    double pg = 0.0, pf = 0.0, pc = 0.0, px = 0.0;
+    if (lane == 0) {
+      pg = gv[r];
+      px = Xo[o + d];
+      if (F) {
+        pf = F[o];
+        pc = Gc[o];
+      }
+    }
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int k = lane;
-    // 8 independent loads in flight per lane (HBM-bound stream of Phi)
+    // 16 (then 8, 4) independent loads in flight per lane (HBM-bound stream of Phi)
+#pragma unroll 1
+    for (; k + 480 < d; k += 512) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = __ldcs(row + k + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 16; u += 4) {
+        a0 = fma(v[u], xs[k + 32 * u], a0);
+        a1 = fma(v[u + 1], xs[k + 32 * u + 32], a1);
+        a2 = fma(v[u + 2], xs[k + 32 * u + 64], a2);
+        a3 = fma(v[u + 3], xs[k + 32 * u + 96], a3);
+      }
+    }
     for (; k + 224 < d; k += 256) {
       double v[8];
 #pragma unroll
@@ -403,17 +430,19 @@ __global__ void __launch_bounds__(CS_THREADS)
       a2 = fma(__ldcs(row + k + 64), xs[k + 64], a2);
       a3 = fma(__ldcs(row + k + 96), xs[k + 96], a3);
     }
-    for (; k < d; k += 32) a0 = fma(__ldcs(row + k), xs[k], a0);
+    // tail: element k + 32 u still goes to accumulator u % 4 (the bulk kernel's order)
+    if (k < d) a0 = fma(__ldcs(row + k), xs[k], a0);  // at most three strides remain
+    if (k + 32 < d) a1 = fma(__ldcs(row + k + 32), xs[k + 32], a1);
+    if (k + 64 < d) a2 = fma(__ldcs(row + k + 64), xs[k + 64], a2);
     double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
-      const long long o = (long long)n * d + r;
-      const double g = acc + gv[r];
-      const double x = F ? F[o] + (g - Gc[o]) : g;
+      const double g = acc + pg;
+      const double x = F ? pf + (g - pc) : g;
       Gc[o] = g;
       Xn[o + d] = x;
-      const double df = x - Xo[o + d];
+      const double df = x - px;
       sd += df * df;
       sn += x * x;
     }
@@ -472,7 +501,6 @@ __global__ void coarse_norm_reduce_kernel(int N, int nblocks, const double* part
   }
 }
 
-int coarse_stream_blocks(int d) { return std::min(296, (d + CS_WARPS - 1) / CS_WARPS); }
 
 static void coarse_correct_stream(int E, int d, int N, const double* Phi, const double* gvec,
                                   long long ge, long long gn,
@@ -480,12 +508,7 @@ static void coarse_correct_stream(int E, int d, int N, const double* Phi, const 
                                   double* X_new, double* partial, double* diff,
                                   const int* active, cudaStream_t st) {
   const int nb = coarse_stream_blocks(d);
-  // at most 4 CTAs (32 warps) per SM: measured at cfg4, the same stream with 5 CTAs per SM
-  // (48 instead of 64 registers after an unrelated code change) ran 2.3x slower; the
-  // dynamic shared memory request pins the occupancy independently of register allocation
-  static const size_t pad_smem = getenv("PE_COARSE_STREAM_SMEM")
-                                     ? (size_t)atol(getenv("PE_COARSE_STREAM_SMEM")) : 50 * 1024;
-  const size_t smem = std::max(sizeof(double) * d, pad_smem);
+  const size_t smem = sizeof(double) * d;
   static bool attr = false;
   if (!attr) {
     PE_CUDA_CHECK(cudaFuncSetAttribute(coarse_step_stream_kernel,

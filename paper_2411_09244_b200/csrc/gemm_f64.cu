@@ -944,19 +944,18 @@ static void launch_tma_best(const GemmParams& p, cudaStream_t st) {
 // ----------------------------------------------------------------------------------------
 // Row-balanced persistent variant for batched skinny products (the ensemble fine step, cfg4:
 // E members x (d x 2d)(2d x nc), nc <= 32).  The E * M rows are split in 8-row blocks into
-// one contiguous, work-weighted range per SM (u-row blocks skip T's zero u x Du k-tiles,
-// so they weigh less).  A range covers at most two members ("parts"); its blocks form one
-// compact list and consumer warp w owns entries [5 w, 5 w + 5) -- possibly straddling the
-// two parts, in which case it multiplies its part-0 blocks with part 0's B tile and then
-// its part-1 blocks with part 1's.  8 DMMA warps + 1 producer: 2 DMMA warps on every SMSP.
+// one contiguous range per SM (max/mean 1.02 at cfg4, where 160-row tiles leave 40 SMs
+// with half the work of the others).  A range covers at most two members (a "part" each);
+// both parts run through ONE k-loop: every consumer warp owns 4 consecutive m-blocks
+// (32 rows) of one part, and each stage holds the part's A blocks plus one B tile per part.
 // Rows below `zero_rows` have an exact-zero k-range [zero_k0, zero_k1) of the second
-// segment (segment-local k; the composite step's u x Du block): a warp whose blocks all lie
-// below it neither loads nor multiplies those k-tiles.  The producer issues one 40-row
-// 128B-swizzled TMA box per warp that lies in one part (8-row boxes otherwise) and one box
-// per B tile.  Same canonical k order and epilogue as the other kernels, so a result
-// differs from theirs only by the omitted +0 terms.
-constexpr int RB_WARPS = 8, RB_FM = 5, RB_FN = 4, RB_STAGES = 4;  // 9 warps: 2 DMMA warps per SMSP
-constexpr int RB_MAXB = RB_WARPS * RB_FM;  // m-blocks per CTA range (40)
+// segment (segment-local k; the composite step's u x Du block): a warp whose four blocks
+// all lie below it neither loads nor multiplies those k-tiles.  One producer warp issues
+// one 8-row 128B-swizzled TMA box per loaded m-block and one box per B tile.  Same
+// canonical k order and epilogue as the other kernels, so a result differs from theirs only
+// by the omitted +0 terms.
+constexpr int RB_WARPS = 11, RB_FM = 4, RB_FN = 4, RB_STAGES = 4;  // 12 warps: 3 per SMSP
+constexpr int RB_MAXB = 40;  // m-blocks per CTA range: ceil(a/4) + ceil(b/4) <= 11
 constexpr int RB_A_BYTES = RB_MAXB * 1024, RB_B_BYTES = 8 * RB_FN * 128;
 constexpr int RB_STAGE = RB_A_BYTES + 2 * RB_B_BYTES;
 constexpr size_t RB_SMEM = (size_t)RB_STAGES * RB_STAGE + 1024 + 2 * RB_STAGES * 8;
@@ -973,11 +972,10 @@ struct alignas(64) RowBalArgs {
   int wu, ww, zrb;
 };
 
-// CTA range -> up to two parts (member, first member-local block, block count).  The
-// range's blocks form one compact list (part 0 first); consumer warp w owns list entries
-// [RB_FM w, RB_FM (w + 1)), which may straddle the two parts.
+// CTA range -> up to two parts (member, first member-local block, block count) and the
+// warp layout: part 0 takes warps [0, w0), part 1 [w0, w0 + w1), 4 blocks per warp.
 struct RbPlan {
-  int e[2], sb[2], nb[2], nbt, nw;
+  int e[2], sb[2], nb[2], w0, nw;
 };
 // first block whose cumulative weight reaches w (blocks in member-major order)
 __device__ __forceinline__ long long rb_block_at(const RowBalArgs& a, long long w) {
@@ -1007,8 +1005,8 @@ __device__ __forceinline__ RbPlan rb_plan(const RowBalArgs& a) {
   r.e[1] = r.e[0] + 1;
   r.sb[1] = 0;
   r.nb[1] = b1 > end0 ? (int)(b1 - end0) : 0;
-  r.nbt = r.nb[0] + r.nb[1];
-  r.nw = (r.nbt + RB_FM - 1) / RB_FM;
+  r.w0 = (r.nb[0] + RB_FM - 1) / RB_FM;
+  r.nw = r.w0 + (r.nb[1] + RB_FM - 1) / RB_FM;
   return r;
 }
 
@@ -1028,17 +1026,16 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   const int zt0 = p.nseg > 1 ? kt0 + (a.zk0 + 15) / 16 : 0;
   const int zt1 = p.nseg > 1 ? kt0 + a.zk1 / 16 : 0;
   const int zr_blocks = a.zero_rows / 8;  // member-local blocks entirely below zero_rows
-  // warp w: list entries [f, f + cnt), of which c0 in part 0 (the rest in part 1); all its
-  // blocks exact zero on the zero k-tiles?
-  auto wplace = [&](int w, int& f, int& c0, int& c1, bool& z) {
-    f = RB_FM * w;
-    const int cnt = max(0, min(RB_FM, pl.nbt - f));
-    c0 = max(0, min(cnt, pl.nb[0] - f));
-    c1 = cnt - c0;
-    // part-0 entries are member-local sb0 + i, part-1 entries i - nb0
-    const bool z0 = c0 == 0 || pl.sb[0] + f + c0 <= zr_blocks;
-    const bool z1 = c1 == 0 || (f + cnt - pl.nb[0]) <= zr_blocks;
-    z = cnt > 0 && z0 && z1;
+  // warp w's part, first block (member-local) and block count
+  auto wplace = [&](int w, int& part, int& fb, int& cnt) {
+    part = w < pl.w0 ? 0 : 1;
+    const int q = part ? w - pl.w0 : w;
+    fb = pl.sb[part] + q * RB_FM;
+    const int left = pl.nb[part] - q * RB_FM;
+    cnt = left < RB_FM ? left : RB_FM;
+  };
+  auto skips = [&](int fb, int cnt, int g) {  // warp's blocks all exact zero on k-tile g
+    return g >= zt0 && g < zt1 && fb + cnt <= zr_blocks;
   };
 
   if (tid == 0) {
@@ -1054,18 +1051,22 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
 
   if (warp == RB_WARPS) {  // producer
     if (lane == 0) {
-      int wf[RB_WARPS], w0c[RB_WARPS], w1c[RB_WARPS];
+      // per consumer warp: global first row, block count, compact smem slot, all-zero flag
+      int wrow[RB_WARPS], wcnt[RB_WARPS], wslot[RB_WARPS];
       bool wz[RB_WARPS];
       int bytes_all = 0, bytes_nz = 0;
 #pragma unroll
       for (int w = 0; w < RB_WARPS; ++w) {
-        wplace(w, wf[w], w0c[w], w1c[w], wz[w]);
-        bytes_all += (w0c[w] + w1c[w]) * 1024;
-        if (!wz[w]) bytes_nz += (w0c[w] + w1c[w]) * 1024;
+        int part = 0, fb = 0, cnt = 0;
+        if (w < pl.nw) wplace(w, part, fb, cnt);
+        wrow[w] = pl.e[part] * p.M + fb * 8;
+        wcnt[w] = cnt;
+        wslot[w] = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);
+        wz[w] = fb + cnt <= zr_blocks;
+        bytes_all += cnt * 1024;
+        if (!wz[w]) bytes_nz += cnt * 1024;
       }
       const int nparts = pl.nb[1] ? 2 : 1;
-      const int row0 = pl.e[0] * p.M + pl.sb[0] * 8;  // list entry i of part 0: row0 + 8 i
-      const int row1 = pl.e[1] * p.M - 8 * pl.nb[0];   // entry i of part 1: row1 + 8 i
       for (int gk = 0; gk < ktot; ++gk) {
         const int st = gk % RB_STAGES;
         if (gk >= RB_STAGES) mbar_wait_cta(bar_empty + 8 * st, ((gk / RB_STAGES) - 1) & 1);
@@ -1077,16 +1078,12 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
         const unsigned dA = sbase + st * RB_STAGE;
 #pragma unroll
         for (int w = 0; w < RB_WARPS; ++w) {
-          if (w0c[w] + w1c[w] == 0 || (zt && wz[w])) continue;
-          if (w0c[w] == RB_FM) {
-            tma_load_4d(dA + wf[w] * 1024, &a.ta4[s], kk, row0 + 8 * wf[w], 0, 0, full);
-          } else if (w1c[w] == RB_FM) {
-            tma_load_4d(dA + wf[w] * 1024, &a.ta4[s], kk, row1 + 8 * wf[w], 0, 0, full);
+          if (wcnt[w] == 0 || (zt && wz[w])) continue;
+          if (wcnt[w] == RB_FM) {
+            tma_load_4d(dA + wslot[w] * 1024, &a.ta4[s], kk, wrow[w], 0, 0, full);
           } else {
-            for (int x = 0; x < w0c[w]; ++x)
-              tma_load_4d(dA + (wf[w] + x) * 1024, &a.ta[s], kk, row0 + 8 * (wf[w] + x), 0, 0, full);
-            for (int x = w0c[w]; x < w0c[w] + w1c[w]; ++x)
-              tma_load_4d(dA + (wf[w] + x) * 1024, &a.ta[s], kk, row1 + 8 * (wf[w] + x), 0, 0, full);
+            for (int x = 0; x < wcnt[w]; ++x)
+              tma_load_4d(dA + (wslot[w] + x) * 1024, &a.ta[s], kk, wrow[w] + 8 * x, 0, 0, full);
           }
         }
         for (int part = 0; part < nparts; ++part)
@@ -1098,9 +1095,9 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   }
   if (warp >= pl.nw) return;  // no blocks for this warp
 
-  int f, c0, c1;
-  bool wz;
-  wplace(warp, f, c0, c1, wz);
+  int part, fb, cnt;
+  wplace(warp, part, fb, cnt);
+  const int slot0 = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);
   const int g = lane >> 2, t4 = lane & 3;
   const unsigned ko0 = swz(g, 4 * t4), ko1 = swz(g, 4 * t4 + 2);
   double acc[RB_FM][RB_FN][2];
@@ -1108,81 +1105,54 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   for (int x = 0; x < RB_FM; ++x)
 #pragma unroll
     for (int y = 0; y < RB_FN; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-  // F0 blocks against part 0's B tile, then F1 against part 1's (one B set live at a time)
-  auto kloop = [&](auto F0C, auto F1C) {
-    constexpr int F0 = decltype(F0C)::value, F1 = decltype(F1C)::value;
+  auto kloop = [&](auto FMC) {  // FMC: this warp's block count, compile-time
+    constexpr int F = decltype(FMC)::value;
     for (int gk = 0; gk < ktot; ++gk) {
       const int st = gk % RB_STAGES;
       mbar_wait_cta(bar_full + 8 * st, (gk / RB_STAGES) & 1);
-      if (wz && gk >= zt0 && gk < zt1) {
+      if (skips(fb, cnt, gk)) {
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_empty + 8 * st);
         continue;
       }
-      const unsigned char* sa = sgen + st * RB_STAGE + f * 1024;
-      const unsigned char* sbp = sgen + st * RB_STAGE + RB_A_BYTES;
-      double af[F0 + F1][4], bf[RB_FN][4];
+      const unsigned char* sa = sgen + st * RB_STAGE + slot0 * 1024;
+      const unsigned char* sbp = sgen + st * RB_STAGE + RB_A_BYTES + part * RB_B_BYTES;
+      double af[F][4], bf[RB_FN][4];
 #pragma unroll
-      for (int x = 0; x < F0 + F1; ++x) {
+      for (int x = 0; x < F; ++x) {
         const double2 u = *reinterpret_cast<const double2*>(sa + x * 1024 + ko0);
         const double2 v = *reinterpret_cast<const double2*>(sa + x * 1024 + ko1);
         af[x][0] = u.x; af[x][1] = u.y; af[x][2] = v.x; af[x][3] = v.y;
       }
-      auto load_b = [&](int part) {
 #pragma unroll
-        for (int y = 0; y < RB_FN; ++y) {
-          const double2 u = *reinterpret_cast<const double2*>(sbp + part * RB_B_BYTES + y * 8 * 128 + ko0);
-          const double2 v = *reinterpret_cast<const double2*>(sbp + part * RB_B_BYTES + y * 8 * 128 + ko1);
-          bf[y][0] = u.x; bf[y][1] = u.y; bf[y][2] = v.x; bf[y][3] = v.y;
-        }
-      };
-      if constexpr (F0 > 0) load_b(0);
-      if constexpr (F0 == 0) load_b(1);
-      if constexpr (F0 == 0 || F1 == 0) {  // one part: the stage is free after the loads
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_empty + 8 * st);
+      for (int y = 0; y < RB_FN; ++y) {
+        const double2 u = *reinterpret_cast<const double2*>(sbp + y * 8 * 128 + ko0);
+        const double2 v = *reinterpret_cast<const double2*>(sbp + y * 8 * 128 + ko1);
+        bf[y][0] = u.x; bf[y][1] = u.y; bf[y][2] = v.x; bf[y][3] = v.y;
       }
-      constexpr int X0 = F0 > 0 ? 0 : 0, X1 = F0 > 0 ? F0 : F1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_empty + 8 * st);
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int x = X0; x < X1; ++x)
+        for (int x = 0; x < F; ++x)
 #pragma unroll
           for (int y = 0; y < RB_FN; ++y)
             dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x][q], bf[y][q]);
-      if constexpr (F0 > 0 && F1 > 0) {
-        load_b(1);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_empty + 8 * st);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int x = F0; x < F0 + F1; ++x)
-#pragma unroll
-            for (int y = 0; y < RB_FN; ++y)
-              dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x][q], bf[y][q]);
-      }
     }
   };
-#define RB_CASE(A, B) \
-  if (c0 == A && c1 == B) kloop(std::integral_constant<int, A>{}, std::integral_constant<int, B>{});
-  RB_CASE(1, 0) RB_CASE(2, 0) RB_CASE(3, 0) RB_CASE(4, 0) RB_CASE(5, 0)
-  RB_CASE(0, 1) RB_CASE(0, 2) RB_CASE(0, 3) RB_CASE(0, 4) RB_CASE(0, 5)
-  RB_CASE(1, 1) RB_CASE(1, 2) RB_CASE(1, 3) RB_CASE(1, 4)
-  RB_CASE(2, 1) RB_CASE(2, 2) RB_CASE(2, 3)
-  RB_CASE(3, 1) RB_CASE(3, 2)
-  RB_CASE(4, 1)
-#undef RB_CASE
-  // epilogue: entry i < c0 is member-local block sb0 + f + i of member e0, else f + i - nb0
-  // of member e1
+  switch (cnt) {
+    case 4: kloop(std::integral_constant<int, 4>{}); break;
+    case 3: kloop(std::integral_constant<int, 3>{}); break;
+    case 2: kloop(std::integral_constant<int, 2>{}); break;
+    default: kloop(std::integral_constant<int, 1>{}); break;
+  }
+  // rows fb*8 .. (fb+cnt)*8 of member pl.e[part]; blocks past cnt hold zeros, not stored
 #pragma unroll
   for (int x = 0; x < RB_FM; ++x)
-    if (x < c0 + c1) {
-      const int part = x < c0 ? 0 : 1;
-      const int lb = part ? f + x - pl.nb[0] : pl.sb[0] + f + x;
-      gemm_epilogue<1, RB_FN>(p, pl.e[part], 0, lb * 8 + g, 2 * t4,
+    if (x < cnt)
+      gemm_epilogue<1, RB_FN>(p, pl.e[part], 0, (fb + x) * 8 + g, 2 * t4,
                               reinterpret_cast<const double(&)[1][RB_FN][2]>(acc[x]));
-    }
 }
 
 // Eligibility: batch over nb1 >= 2 only, M % 8 == 0, N <= 32, 1-2 k-contiguous segments

@@ -692,6 +692,8 @@ static void fine_allatonce_modal(pe_ctx* c, const double* X_in, double* X_out, i
 static void fine_allatonce(pe_ctx* c, const double* X_in, double* X_out, int nc, int* sweeps,
                            int* reasons, double* resid_hist, cudaStream_t st,
                            const double* Fload = nullptr) {
+  c->wr_last_nc = nc;
+  c->wr_last_loads = Fload != nullptr;
   if (Fload) {
     require(c->wr_modal_avail, PE_ERR_ARG,
             "time-dependent loads in the all-at-once solver need symmetric-definite pencils "

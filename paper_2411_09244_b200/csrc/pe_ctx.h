@@ -80,6 +80,8 @@ struct pe_ctx {
   bool wr_ready = false;
   double wr_dt = 0, wr_alpha = 0, wr_tol = 0;
   int wr_max_iter = 0;
+  int wr_last_nc = 0;          // intervals of the last fine_allatonce (Ux_cur / Wx_cur hold them)
+  bool wr_last_loads = false;  // ... and whether it ran with time-dependent loads (LF1 rows)
   int wr_nk = 0;  // solved time modes (half spectrum, floor(J/2) + 1)
   pe::DevBuf Bk, BkT, RW, M11dt, GW, cg, Emat, Finv, Fw;
   // modal w recursion (setup_modal): E = Vm diag(lam) Vinv; GZ = Vinv GW, cgz = Vinv cg

@@ -161,6 +161,12 @@ class PeContext:
         check(self.lib.pe_wr_waveforms(self.ptr, _ptr(U), _ptr(W), nc, self.stream()))
         return U, W
 
+    def wr_solver_residual(self, nc: int) -> torch.Tensor:
+        """(E, nc) ImplicitAllAtOnce residual guard of the last all-at-once solve."""
+        out = self.empty(self.E, nc)
+        check(self.lib.pe_wr_solver_residual(self.ptr, _ptr(out), self.stream()))
+        return out
+
     def coarse_apply(self, X: torch.Tensor) -> torch.Tensor:
         nc = X.shape[1]
         Y = self.empty(self.E, nc, self.d)

@@ -292,3 +292,35 @@ def test_stability_max_step_degenerate_blocks():
     w_free = P.CoarseSystem(np.eye(1), np.eye(1), np.zeros((1, 2)), np.zeros((1, 2)),
                             np.eye(2), np.zeros((2, 2)))
     assert P.SplitPropagators(w_free, P.ConstantLoads.zero(w_free)).stability_max_step() == np.inf
+
+
+@pytest.mark.parametrize("cfg", ["cfg0", "cfg2"])
+def test_wr_result_carries_the_solver_residual(cfg):
+    """WRResult.solver_residual / imag_residue (allatonce.py:296-297): the all-at-once
+    solver's conditioning guard.  libpe evaluates it on build_rhs of each interval's final
+    waveforms; the same rhs solved through the drop-in ImplicitAllAtOnce must report the
+    same guard, and both sit at rounding level for the reference systems."""
+    from tests.conftest import golden
+
+    P = _pkg()
+    z = golden(f"sys_{cfg}.npz")
+    s = P.CoarseSystem(*(z[k] for k in ("M11", "A11", "M12", "A12", "M22", "A22")))
+    ld = P.ConstantLoads(z["f1"], z["f2"])
+    J, dti, alpha = 12, 0.05, 0.1
+    wr = P.WaveformRelaxation(s, J, dti, alpha, ld, tol=1e-12, max_iter=300)
+    rng = np.random.default_rng(5)
+    states = [P.SplitState.fresh(rng.standard_normal(s.d1) * 1e-2,
+                                 rng.standard_normal(s.d2) * 1e-2, 0.1 * k) for k in range(3)]
+    res = wr.solve_all(states)
+    dt = dti / J
+    imp = P.ImplicitAllAtOnce(s, J, dt, alpha)
+    for st, r in zip(states, res):
+        assert r.imag_residue == 0.0
+        assert 0.0 < r.solver_residual < 1e-11, r.solver_residual
+        U, W = r.trajectory.U, r.trajectory.W
+        rhs = P.build_rhs(s, np.tile(z["f1"], (J, 1)), U[0], W[0], W[0], W[1:], U[-1], dt,
+                          alpha)
+        imp.solve(rhs)
+        # both are rounding-level numbers of the same linear solve on rhs equal up to
+        # rounding: the same magnitude, not the same digits
+        assert imp.last_residual / 3 <= r.solver_residual <= 3 * imp.last_residual
