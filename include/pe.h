@@ -289,6 +289,21 @@ int pe_coarse_correct_loads(pe_ctx* ctx, int N, const double* X_old, const doubl
 int pe_coarse_apply_loads(pe_ctx* ctx, const double* X_in, double* X_out, int nc,
                           const double* Fc, void* stream); /* Fc: (E, nc, d), one per state */
 
+/* ---- batched factor / solve (SURVEY kernel K3; batchlu.cu) ---------------------------
+ * Ainv[b] = A[b]^-1 for `batch` row-major n x n matrices (device pointers, batch stride
+ * n*n; A is not modified): libpe's recursive blocked LU with partial pivoting, every
+ * matrix of the batch in the same launches.  info (host, batch ints): 0, or the 1-based
+ * index of the first exactly-zero pivot of that matrix (its inverse is then undefined). */
+int pe_batched_inverse(int n, int batch, const double* A, double* Ainv, int* info,
+                       void* stream);
+/* ImplicitAllAtOnce.__init__'s per-mode inverses (allatonce.py:100-110): for every time mode
+ * k = 0 .. J-1, inv(d_k M11 + A11) with d_k = (1 - alpha^(1/J) e^(-2 pi i k / J)) / dt, all
+ * modes in one batched pass.  M11, A11: device, row-major d1 x d1.  inv_re / inv_im:
+ * device (J, d1, d1) planar real / imaginary parts.  Only modes 0 .. J/2 are factored; the
+ * rest are their complex conjugates (real M11, A11).  PE_ERR_SOLVER on a zero pivot. */
+int pe_shifted_inverses(int d1, int J, double dt, double alpha, const double* M11,
+                        const double* A11, double* inv_re, double* inv_im, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

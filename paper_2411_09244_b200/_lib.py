@@ -85,6 +85,9 @@ SIGNATURES = {
     "pe_fine_allatonce_loads": (C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, _P, _P]),
     "pe_coarse_correct_loads": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pe_coarse_apply_loads": (C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
+    "pe_batched_inverse": (C.c_int, [C.c_int, C.c_int, _P, _P, _I, _P]),
+    "pe_shifted_inverses": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, _P, _P, _P, _P,
+                                      _P]),
 }
 
 _lib = None

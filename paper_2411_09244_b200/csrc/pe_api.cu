@@ -1415,6 +1415,34 @@ int pe_gemm_f64(int M, int N, int K, int batch, const double* A, long long a_i, 
   });
 }
 
+int pe_batched_inverse(int n, int batch, const double* A, double* Ainv, int* info,
+                       void* stream) {
+  return guarded([&] {
+    require(n >= 1 && batch >= 1 && A && Ainv, PE_ERR_ARG, "bad batched-inverse arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t tot = (size_t)batch * n * n;
+    DevBuf lu, piv, dinfo;
+    lu.ensure(sizeof(double) * tot);
+    piv.ensure(sizeof(int) * (size_t)batch * n);
+    dinfo.ensure(sizeof(int) * (size_t)batch);
+    PE_CUDA_CHECK(cudaMemcpyAsync(lu.p, A, sizeof(double) * tot, cudaMemcpyDeviceToDevice, st));
+    batched_lu_inverse(n, batch, lu.d(), Ainv, piv.i(), dinfo.i(), st);
+    std::vector<int> h((size_t)batch);
+    PE_CUDA_CHECK(cudaMemcpyAsync(h.data(), dinfo.p, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+    PE_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (info) std::copy(h.begin(), h.end(), info);
+  });
+}
+
+int pe_shifted_inverses(int d1, int J, double dt, double alpha, const double* M11,
+                        const double* A11, double* inv_re, double* inv_im, void* stream) {
+  return guarded([&] {
+    require(d1 >= 1 && J >= 1 && dt > 0 && alpha > 0 && M11 && A11 && inv_re && inv_im,
+            PE_ERR_ARG, "bad shifted-inverse arguments");
+    shifted_inverses(d1, J, dt, alpha, M11, A11, inv_re, inv_im, (cudaStream_t)stream);
+  });
+}
+
 long long pe_launch_count(pe_ctx* c) { return c ? g_launches - c->launches_at_create : g_launches; }
 
 int pe_last_fine_other_ms(pe_ctx* c, double* other_ms) {

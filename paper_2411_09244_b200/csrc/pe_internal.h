@@ -112,6 +112,16 @@ void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int z
 // Flop count of one launch (2*M*N*sumK*batch), for the roofline bookkeeping.
 double gemm_flops(const GemmParams& p);
 
+// ---------------------------------------------------------------- batched inversion (batchlu.cu)
+// Ainv[b] = A[b]^-1 for `batch` row-major n x n matrices (batch stride n*n).  A is
+// overwritten by its LU factors; piv: batch*n ints; info: batch ints (device), 0 or the
+// 1-based index of the first zero pivot.  Enqueued on st, no host synchronisation.
+void batched_lu_inverse(int n, int batch, double* A, double* Ainv, int* piv, int* info,
+                        cudaStream_t st);
+// inv(d_k M11 + A11) for every time mode, planar (J, d1, d1) outputs (allatonce.py:100-110)
+void shifted_inverses(int d1, int J, double dt, double alpha, const double* M11,
+                      const double* A11, double* inv_re, double* inv_im, cudaStream_t st);
+
 // ---------------------------------------------------------------- WR helpers
 struct WrColumnState {
   int active;

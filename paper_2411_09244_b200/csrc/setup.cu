@@ -88,38 +88,38 @@ __global__ void zero_block_kernel(int m, int n, double* X, int ld) {
     X[(t / n) * ld + (t % n)] = 0.0;
 }
 
-// S = dk * M11 + A11 (complex, row-major d1 x d1)
-__global__ void shifted_kernel(int n, double dre, double dim, const double* M, const double* A,
-                               cuDoubleComplex* S) {
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  for (; t < (long long)n * n; t += (long long)gridDim.x * blockDim.x)
-    S[t] = make_cuDoubleComplex(dre * M[t] + A[t], dim * M[t]);
-}
-__global__ void zidentity_kernel(int n, cuDoubleComplex* X) {
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  for (; t < (long long)n * n; t += (long long)gridDim.x * blockDim.x)
-    X[t] = make_cuDoubleComplex((t / n) == (t % n) ? 1.0 : 0.0, 0.0);
-}
-// Bk (2n x 2n row-major, planar blocks) = [[Re, -Im], [Im, Re]] of inv (row-major n x n)
-__global__ void realify_kernel(int n, const cuDoubleComplex* inv, double* B) {
+// The shifted matrix d_k M11 + A11 in its real block form [[Re, -Im], [Im, Re]] (2n x 2n
+// row-major): its inverse is the block form of the complex inverse, i.e. the operator the
+// sweep applies to the planar (re, im) transformed right-hand sides.
+__global__ void shifted_blockform_kernel(int n, double dre, double dim, const double* M,
+                                         const double* A, double* S) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long n2 = 2LL * n;
   for (; t < (long long)n * n; t += (long long)gridDim.x * blockDim.x) {
     const long long i = t / n, j = t % n;
-    const double re = cuCreal(inv[t]), im = cuCimag(inv[t]);
-    B[i * n2 + j] = re;
-    B[i * n2 + n + j] = -im;
-    B[(i + n) * n2 + j] = im;
-    B[(i + n) * n2 + n + j] = re;
+    const double re = dre * M[t] + A[t], im = dim * M[t];
+    S[i * n2 + j] = re;
+    S[i * n2 + n + j] = -im;
+    S[(i + n) * n2 + j] = im;
+    S[(i + n) * n2 + n + j] = re;
   }
 }
-
-// Re(inv) into diagonal block `which` of a (2n x 2n) row-major block matrix (real modes)
-__global__ void real_block_kernel(int n, const cuDoubleComplex* inv, double* B, int which) {
+// The real modes k = 0 and (J even) k = J/2 share pseudo-mode 0 as a block diagonal;
+// a missing second mode (J odd) is an identity block, cleared again after the inversion.
+__global__ void shifted_real_block_kernel(int n, double dre, const double* M, const double* A,
+                                          double* S, int which, int identity) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long n2 = 2LL * n, o = (long long)which * n;
+  for (; t < (long long)n * n; t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / n, j = t % n;
+    S[(i + o) * n2 + o + j] = identity ? (i == j ? 1.0 : 0.0) : dre * M[t] + A[t];
+  }
+}
+__global__ void clear_block_kernel(int n, double* S, int which) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long n2 = 2LL * n, o = (long long)which * n;
   for (; t < (long long)n * n; t += (long long)gridDim.x * blockDim.x)
-    B[(t / n + o) * n2 + o + t % n] = cuCreal(inv[t]);
+    S[(t / n + o) * n2 + o + t % n] = 0.0;
 }
 
 __global__ void transpose_blocks_kernel(int nblocks, int n, const double* src, double* dst) {
@@ -142,42 +142,20 @@ void transpose_blocks(int nblocks, int n, const double* src, double* dst, cudaSt
 
 static int grid_for(long long n) { return (int)std::max<long long>(1, std::min<long long>(4096, (n + 255) / 256)); }
 
-// Ainv = A^{-1} for a row-major n x n buffer (inv(A^T) = inv(A)^T, so the
-// column-major solver view is harmless).
+// Ainv = A^{-1} for a row-major n x n buffer: libpe's own blocked LU (batchlu.cu).
 static void inverse(pe_ctx* c, int n, const double* A, double* Ainv) {
   if (n == 0) return;
   cudaStream_t st = c->setup_stream;
-  DevBuf lu, ipiv, info, work;
+  DevBuf lu, ipiv, info;
   lu.ensure(sizeof(double) * n * (size_t)n);
   ipiv.ensure(sizeof(int) * n);
   info.ensure(sizeof(int));
   PE_CUDA_CHECK(cudaMemcpyAsync(lu.p, A, sizeof(double) * n * (size_t)n, cudaMemcpyDeviceToDevice, st));
-  int lwork = 0;
-  SOLVER_CHECK(cusolverDnDgetrf_bufferSize(c->solver, n, n, lu.d(), n, &lwork));
-  work.ensure(sizeof(double) * std::max(lwork, 1));
-  SOLVER_CHECK(cusolverDnDgetrf(c->solver, n, n, lu.d(), n, work.d(), ipiv.i(), info.i()));
+  batched_lu_inverse(n, 1, lu.d(), Ainv, ipiv.i(), info.i(), st);
   int h_info = 0;
   PE_CUDA_CHECK(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   PE_CUDA_CHECK(cudaStreamSynchronize(st));
-  if (h_info != 0) throw Error{PE_ERR_SOLVER, "singular matrix in setup factorisation (getrf info " + std::to_string(h_info) + ")"};
-  set_identity(n, Ainv, n, 1.0, st);
-  SOLVER_CHECK(cusolverDnDgetrs(c->solver, CUBLAS_OP_N, n, n, lu.d(), n, ipiv.i(), Ainv, n, info.i()));
-  PE_CUDA_CHECK(cudaStreamSynchronize(st));
-}
-
-// (d_k M11 + A11)^-1 by LU + solve against I, enqueued without a host round trip: the
-// factorisation status goes to info[slot] (checked once per setup, after every mode).
-static void zinverse(pe_ctx* c, int n, cuDoubleComplex* S, cuDoubleComplex* Sinv, DevBuf& ipiv,
-                     int* info_slot, DevBuf& work) {
-  cudaStream_t st = c->setup_stream;
-  int lwork = 0;
-  SOLVER_CHECK(cusolverDnZgetrf_bufferSize(c->solver, n, n, S, n, &lwork));
-  work.ensure(sizeof(cuDoubleComplex) * std::max(lwork, 1));
-  ipiv.ensure(sizeof(int) * n);
-  SOLVER_CHECK(cusolverDnZgetrf(c->solver, n, n, S, n, (cuDoubleComplex*)work.p, ipiv.i(), info_slot));
-  zidentity_kernel<<<grid_for((long long)n * n), 256, 0, st>>>(n, Sinv);
-  SOLVER_CHECK(cusolverDnZgetrs(c->solver, CUBLAS_OP_N, n, n, S, n, ipiv.i(), Sinv, n,
-                                info_slot + 1));
+  if (h_info != 0) throw Error{PE_ERR_SOLVER, "singular matrix in setup factorisation (zero pivot " + std::to_string(h_info) + ")"};
 }
 
 void setup_sequential(pe_ctx* c, double dt) {
@@ -613,13 +591,18 @@ static void setup_allatonce_general(pe_ctx* c, double dt, double alpha, int npm,
   c->GW.ensure(sizeof(double) * (size_t)E * d2 * 2 * d1 + 8);
   c->cg.ensure(sizeof(double) * (size_t)E * d2 + 8);
   c->Emat.ensure(sizeof(double) * (size_t)E * d2 * d2 + 8);
-  DevBuf S, Sinv, ipiv, info, work, M22inv;
-  S.ensure(sizeof(cuDoubleComplex) * (size_t)d1 * d1 + 16);
-  Sinv.ensure(sizeof(cuDoubleComplex) * (size_t)d1 * d1 + 16);
+  // Every member's and every mode's shifted matrix in real block form, inverted in one
+  // batched LU pass (batchlu.cu); slot 0 of a member holds the real modes k = 0 and J/2.
+  DevBuf S, ipiv, info, M22inv;
+  const size_t n2 = 2 * (size_t)d1, per = n2 * n2;
+  const int nmat = E * npm;
+  if (d1) {
+    S.ensure(sizeof(double) * (size_t)nmat * per + 16);
+    ipiv.ensure(sizeof(int) * (size_t)nmat * n2 + 16);
+    info.ensure(sizeof(int) * (size_t)nmat + 16);
+  }
   M22inv.ensure(sizeof(double) * (size_t)d2 * d2 + 8);
   const double om_r = std::pow(alpha, 1.0 / J);
-  info.ensure(sizeof(int) * 2 * (size_t)E * (J / 2 + 1) + 8);
-  PE_CUDA_CHECK(cudaMemsetAsync(info.p, 0, info.bytes, st));
   for (int e = 0; e < E; ++e) {
     const double* M11 = c->M11.d() + (size_t)e * d1 * d1;
     const double* A11 = c->A11.d() + (size_t)e * d1 * d1;
@@ -629,23 +612,22 @@ static void setup_allatonce_general(pe_ctx* c, double dt, double alpha, int npm,
     const double* A22 = c->A22.d() + (size_t)e * d2 * d2;
     const double* f2 = c->f2.d() + (size_t)e * d2;
     if (d1) {
-      double* Bk0 = c->Bk.d() + (size_t)e * npm * 4 * d1 * d1;
-      PE_CUDA_CHECK(cudaMemsetAsync(Bk0, 0, sizeof(double) * 4 * d1 * d1, st));
+      double* S0 = S.d() + (size_t)e * npm * per;
+      PE_CUDA_CHECK(cudaMemsetAsync(S0, 0, sizeof(double) * per, st));
+      if (!even)
+        shifted_real_block_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
+            d1, 0.0, M11, A11, S0, 1, 1);
       for (int k = 0; k <= J / 2; ++k) {
         // d_k = (1 - alpha^{1/J} e^{-2 pi i k/J}) / dt   (allatonce.py:58-62)
         const double ang = -6.283185307179586476925286766559 * (double)k / J;
         const double dre = (1.0 - om_r * std::cos(ang)) / dt;
         const double dim = (-om_r * std::sin(ang)) / dt;
-        shifted_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
-            d1, dre, dim, M11, A11, (cuDoubleComplex*)S.p);
-        zinverse(c, d1, (cuDoubleComplex*)S.p, (cuDoubleComplex*)Sinv.p, ipiv,
-                 info.i() + 2 * ((size_t)e * (J / 2 + 1) + k), work);
         if (k == 0 || (even && 2 * k == J))  // real modes: diagonal block of pseudo-mode 0
-          real_block_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
-              d1, (const cuDoubleComplex*)Sinv.p, Bk0, k == 0 ? 0 : 1);
+          shifted_real_block_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
+              d1, dre, M11, A11, S0, k == 0 ? 0 : 1, 0);
         else
-          realify_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
-              d1, (const cuDoubleComplex*)Sinv.p, c->Bk.d() + ((size_t)e * npm + k) * 4 * d1 * d1);
+          shifted_blockform_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
+              d1, dre, dim, M11, A11, S0 + (size_t)k * per);
         PE_CUDA_CHECK(cudaGetLastError());
       }
       double* RW = c->RW.d() + (size_t)e * d1 * 2 * d2;
@@ -671,16 +653,22 @@ static void setup_allatonce_general(pe_ctx* c, double dt, double alpha, int npm,
       }
     }
   }
-  if (d1) {  // one host round trip for every mode's factorisation status
-    std::vector<int> h_info(2 * (size_t)E * (J / 2 + 1));
+  if (d1) {
+    batched_lu_inverse((int)n2, nmat, S.d(), c->Bk.d(), ipiv.i(), info.i(), st);
+    if (!even)
+      for (int e = 0; e < E; ++e)
+        clear_block_kernel<<<grid_for((long long)d1 * d1), 256, 0, st>>>(
+            d1, c->Bk.d() + (size_t)e * npm * per, 1);
+    // one host round trip for every mode's factorisation status
+    std::vector<int> h_info((size_t)nmat);
     PE_CUDA_CHECK(cudaMemcpyAsync(h_info.data(), info.p, sizeof(int) * h_info.size(),
                                   cudaMemcpyDeviceToHost, st));
     PE_CUDA_CHECK(cudaStreamSynchronize(st));
     for (size_t q = 0; q < h_info.size(); ++q)
       if (h_info[q] != 0)
         throw Error{PE_ERR_SOLVER, "singular shifted matrix d_k M11 + A11 (member " +
-                                       std::to_string(q / 2 / (J / 2 + 1)) + ", mode " +
-                                       std::to_string((q / 2) % (J / 2 + 1)) + ", info " +
+                                       std::to_string(q / npm) + ", pseudo-mode " +
+                                       std::to_string(q % npm) + ", zero pivot " +
                                        std::to_string(h_info[q]) + ")"};
   }
   if (wr_tiny_eligible(d1, d2, J, npm)) {  // transposed Bk for the fused small-problem path
