@@ -20,8 +20,11 @@
 //
 // Deterministic: fixed reduction orders, first-maximum pivot rule (as LAPACK's idamax).
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -29,6 +32,8 @@
 #include "pe_internal.h"
 
 namespace pe {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -136,6 +141,127 @@ __global__ void __launch_bounds__(PANEL_T) lu_panel_kernel(int n, int j0, int nb
       const int r = (int)(q / nb), c = (int)(q - (long long)r * nb);
       Ab[(long long)r * n + c] = P[r * ld + c];
     }
+  }
+}
+
+// The same panel for tall matrices: a thread-block cluster per matrix, the panel's rows
+// split in contiguous ranges over the cluster's CTAs and held in their shared memory.
+// Per column: local pivot candidates, one cluster barrier, every CTA reads all candidates
+// through distributed shared memory and picks the same winner; the pivot row is pulled
+// from its owner by every CTA (and the displaced row jj by the owner), a second cluster
+// barrier, then the owners write the swapped rows and every CTA updates its own rows.
+__global__ void __launch_bounds__(PANEL_T) lu_panel_cluster_kernel(int n, int j0, int nb, double* A,
+                                                                   long long sA, int* piv,
+                                                                   int* info) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int b = blockIdx.x / CS;
+  extern __shared__ double sm[];
+  __shared__ double prow[LEAF], tmp[LEAF];
+  __shared__ double cand_v;
+  __shared__ int cand_i;
+  __shared__ double red_v[PANEL_T / 32];
+  __shared__ int red_i[PANEL_T / 32];
+  __shared__ int s_p;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int rows = n - j0;
+  const int rp = (rows + CS - 1) / CS;  // >= nb: row jj always lives in CTA 0
+  const int r_lo = min(rows, rank * rp), r_hi = min(rows, r_lo + rp);
+  const int ld = nb + 1;
+  double* Ab = A + b * sA + (long long)j0 * n + j0;
+  int* pv = piv + (long long)b * n + j0;
+  double* P = sm;
+  for (long long q = tid; q < (long long)(r_hi - r_lo) * nb; q += PANEL_T) {
+    const int r = (int)(q / nb), c = (int)(q - (long long)r * nb);
+    P[r * ld + c] = Ab[(long long)(r_lo + r) * n + c];
+  }
+  __syncthreads();
+  for (int jj = 0; jj < nb; ++jj) {
+    double best = -1.0;
+    int bi = rows;
+    for (int i = max(jj, r_lo) + tid; i < r_hi; i += PANEL_T) {
+      const double v = fabs(P[(i - r_lo) * ld + jj]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      red_v[wid] = best;
+      red_i[wid] = bi;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      best = lane < PANEL_T / 32 ? red_v[lane] : -1.0;
+      bi = lane < PANEL_T / 32 ? red_i[lane] : rows;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+          best = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        cand_v = best;
+        cand_i = bi;
+      }
+    }
+    cl.sync();
+    if (tid == 0) {
+      best = -1.0;
+      bi = rows;
+      for (int q = 0; q < CS; ++q) {
+        const double ov = *cl.map_shared_rank(&cand_v, q);
+        const int oi = *cl.map_shared_rank(&cand_i, q);
+        if (ov > best || (ov == best && oi < bi)) {
+          best = ov;
+          bi = oi;
+        }
+      }
+      if (bi >= rows) bi = jj;
+      s_p = bi;
+      if (rank == 0) {
+        pv[jj] = j0 + bi;
+        if (!(best > 0.0) && info[b] == 0) info[b] = j0 + jj + 1;
+      }
+    }
+    __syncthreads();
+    const int p = s_p, owner = p / rp;
+    if (tid < nb) {
+      prow[tid] = cl.map_shared_rank(sm, owner)[(p - owner * rp) * ld + tid];
+      if (rank == owner) tmp[tid] = cl.map_shared_rank(sm, 0)[jj * ld + tid];
+    }
+    cl.sync();
+    if (tid < nb) {
+      if (rank == 0) P[jj * ld + tid] = prow[tid];
+      if (rank == owner && p != jj) P[(p - r_lo) * ld + tid] = tmp[tid];
+    }
+    __syncthreads();
+    const double pvt = prow[jj];
+    if (pvt != 0.0) {
+      for (int i = max(jj + 1, r_lo) + tid; i < r_hi; i += PANEL_T) {
+        double* r = P + (i - r_lo) * ld;
+        const double l = r[jj] / pvt;
+        r[jj] = l;
+        for (int c = jj + 1; c < nb; ++c) r[c] = fma(-l, prow[c], r[c]);
+      }
+    }
+    __syncthreads();
+  }
+  for (long long q = tid; q < (long long)(r_hi - r_lo) * nb; q += PANEL_T) {
+    const int r = (int)(q / nb), c = (int)(q - (long long)r * nb);
+    Ab[(long long)(r_lo + r) * n + c] = P[r * ld + c];
   }
 }
 
@@ -258,7 +384,7 @@ struct Lu {
   int* piv;
   int* info;
   cudaStream_t st;
-  bool smem_ok;
+  int max_cluster;  // largest cluster size of the tall-panel kernel (0: none)
 
   static int split(int w) {
     int w1 = ((w / 2 + LEAF - 1) / LEAF) * LEAF;
@@ -327,13 +453,35 @@ struct Lu {
   }
 
   void panel(int j0, int nb) const {
-    const size_t need = sizeof(double) * (size_t)(n - j0) * (nb + 1);
-    if (smem_ok && need <= PANEL_SMEM_MAX)
-      lu_panel_kernel<true><<<batch, PANEL_T, need, st>>>(n, j0, nb, A, sA, piv, info);
-    else
-      lu_panel_kernel<false><<<batch, PANEL_T, 0, st>>>(n, j0, nb, A, sA, piv, info);
-    PE_CUDA_CHECK(cudaGetLastError());
+    const int rows = n - j0;
+    const size_t need = sizeof(double) * (size_t)rows * (nb + 1);
     ++g_launches;
+    if (need <= PANEL_SMEM_MAX) {
+      lu_panel_kernel<true><<<batch, PANEL_T, need, st>>>(n, j0, nb, A, sA, piv, info);
+      PE_CUDA_CHECK(cudaGetLastError());
+      return;
+    }
+    for (int cs = 2; cs <= max_cluster; cs *= 2) {
+      const int rp = (rows + cs - 1) / cs;
+      const size_t sm = sizeof(double) * (size_t)rp * (nb + 1);
+      if (sm > PANEL_SMEM_MAX) continue;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(batch * cs);
+      cfg.blockDim = dim3(PANEL_T);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = st;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      PE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, lu_panel_cluster_kernel, n, j0, nb, A, sA, piv, info));
+      return;
+    }
+    lu_panel_kernel<false><<<batch, PANEL_T, 0, st>>>(n, j0, nb, A, sA, piv, info);
+    PE_CUDA_CHECK(cudaGetLastError());
   }
 
   // factor columns [j0, j0+w) of rows [j0, n); interchanges applied within those columns
@@ -351,6 +499,12 @@ struct Lu {
 
 }  // namespace
 
+// PE_LU_CLUSTER caps the tall-panel cluster size (tests: 0 forces the global-memory panel)
+static int panel_max_cluster() {
+  const char* e = std::getenv("PE_LU_CLUSTER");
+  return e ? std::atoi(e) : 16;
+}
+
 void batched_lu_inverse(int n, int batch, double* A, double* Ainv, int* piv, int* info,
                         cudaStream_t st) {
   if (n <= 0 || batch <= 0) return;
@@ -362,6 +516,11 @@ void batched_lu_inverse(int n, int batch, double* A, double* Ainv, int* piv, int
     PE_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_kernel<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)PANEL_SMEM_MAX));
+    PE_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_cluster_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)PANEL_SMEM_MAX));
+    PE_CUDA_CHECK(cudaFuncSetAttribute(lu_panel_cluster_kernel,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     PE_CUDA_CHECK(cudaFuncSetAttribute(lu_perm_identity_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)PANEL_SMEM_MAX));
@@ -378,7 +537,7 @@ void batched_lu_inverse(int n, int batch, double* A, double* Ainv, int* piv, int
   lu_transpose_inplace_kernel<<<tgrid, tblock, 0, st>>>(n, A, sA);
   PE_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
-  Lu lu{n, batch, A, sA, piv, info, st, true};
+  Lu lu{n, batch, A, sA, piv, info, st, panel_max_cluster()};
   lu.factor(0, n);
   lu_perm_identity_kernel<<<dim3(batch, std::max(1, std::min(64, n / 64))), 1024,
                             sizeof(int) * (size_t)n, st>>>(n, piv, Ainv, sA);

@@ -30,7 +30,8 @@ def _inverse(A):
 
 
 @pytest.mark.parametrize("n,batch", [(1, 1), (2, 3), (5, 2), (31, 2), (32, 1), (33, 3), (64, 2),
-                                     (97, 3), (300, 4), (600, 5), (801, 2), (1500, 2)])
+                                     (97, 3), (300, 4), (600, 5), (801, 2), (1500, 2), (3100, 2),
+                                     (6500, 1)])
 def test_batched_inverse_matches_lapack(n, batch):
     """General (non-symmetric, pivoting-needed) matrices: residual at round-off and the
     inverse within cond * eps of numpy's (LAPACK getrf / getri)."""
@@ -61,6 +62,21 @@ def test_batched_inverse_is_deterministic_and_batch_invariant():
     assert np.array_equal(X1, X2)
     Xs, _ = _inverse(A[2:3])
     assert np.array_equal(Xs[0], X1[2])
+
+
+def test_tall_panel_cluster_kernel_equals_single_cta_panel(monkeypatch):
+    """Panels too tall for one CTA's shared memory run on a thread-block cluster (rows
+    split over the CTAs, pivot exchange through distributed shared memory); the
+    global-memory single-CTA panel does the same arithmetic: equal bits."""
+    rng = np.random.default_rng(8)
+    A = rng.standard_normal((3, 1700, 1700))
+    X1, i1 = _inverse(A)
+    monkeypatch.setenv("PE_LU_CLUSTER", "0")
+    X0, i0 = _inverse(A)
+    monkeypatch.setenv("PE_LU_CLUSTER", "4")
+    X4, _ = _inverse(A)
+    assert np.array_equal(X0, X1) and np.array_equal(X4, X1)
+    assert np.all(i0 == 0) and np.all(i1 == 0)
 
 
 def test_batched_inverse_reports_singular_matrices():
