@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "pe.h"
+#include "finescale.h"
 #include "mbar.cuh"
 #include "pe_internal.h"
 
@@ -418,22 +419,19 @@ static int fs_guard(const char* what, void (*fn)(void*), void* arg) {
   }
 }
 
-struct RefSolveArgs {
-  int n;
-  const int *mp, *mi, *ap, *ai;
-  const double *mv, *av, *b, *u0;
-  double t_end;
-  int n_steps;
-  double* states_h;
-  int keep;
-  cudaStream_t st;
-  float* step_ms;
-};
+void fine_rhs(int n, const int* mp, const int* mi, const double* mv, double inv_dt,
+              const double* u, const double* b, double* v, cudaStream_t st) {
+  k_rhs<<<(n + 255) / 256, 256, 0, st>>>(n, mp, mi, mv, inv_dt, u, b, v);
+}
 
 static void ref_solve_impl(void* vp) {
   RefSolveArgs& a = *static_cast<RefSolveArgs*>(vp);
   const int n = a.n;
-  if (n > 65535) throw Error{PE_ERR_ARG, "fine problems above 65535 interior nodes are not supported"};
+  // large banded operators: the block-tridiagonal chain solver (finechain.cu)
+  if (fine_chain_applicable(n, a.mp, a.mi, a.ap, a.ai)) return fine_chain_solve(a);
+  if (n > 65535)
+    throw Error{PE_ERR_ARG, "fine problems above 65535 interior nodes need a banded operator "
+                            "(half-bandwidth <= 512) for the chain solver"};
   const double dt = a.t_end / a.n_steps;
   const double inv_dt = 1.0 / dt;
   const long long ld = padded_ld(n);

@@ -292,7 +292,19 @@ __global__ void __launch_bounds__(WGM * WGN * 32)
   const int zt = blockIdx.z;
   const int sp = zt % p.ksplit, z = zt / p.ksplit;
   const int z1 = z / p.nb2, z2 = z - (z / p.nb2) * p.nb2;
-  const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
+  // Grouped rasterisation for multi-wave grids: CTAs are dispatched in linear block order,
+  // so walking `raster` row tiles down before stepping one column tile keeps a wave on a
+  // near-square patch of C (its A and B panels are shared through L2 by the co-running
+  // CTAs) instead of two full rows of tiles that re-stream all of B for every row tile.
+  int ty = blockIdx.y, tx = blockIdx.x;
+  if (p.raster > 1) {
+    const int pid = blockIdx.y * gridDim.x + blockIdx.x, gsz = p.raster * gridDim.x;
+    const int g = pid / gsz, first = g * p.raster, r = pid - g * gsz;
+    const int gm = min(p.raster, (int)gridDim.y - first);
+    ty = first + r % gm;
+    tx = r / gm;
+  }
+  const int i0 = ty * BM, j0 = tx * BN;
   const int tid = threadIdx.x;
 
   int kt0 = 0, kt1 = 0, kt2 = 0;
@@ -561,9 +573,14 @@ static int fast_occupancy() {
 template <int WGM, int WGN, int FM, int FN, int BK, int STAGES, bool BJC, bool PRE = false>
 static void launch_fast(const GemmParams& p, cudaStream_t st) {
   using Cfg = FastCfg<WGM, WGN, FM, FN, BK, STAGES, BJC>;
-  fast_occupancy<WGM, WGN, FM, FN, BK, STAGES, BJC, PRE>();
+  const int occ = fast_occupancy<WGM, WGN, FM, FN, BK, STAGES, BJC, PRE>();
   dim3 grid((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM, p.nb1 * p.nb2 * p.ksplit);
-  launch_k(gemm_fast_kernel<WGM, WGN, FM, FN, BK, STAGES, BJC, PRE>, grid, dim3(Cfg::NT), Cfg::SMEM, st, p);
+  GemmParams q = p;
+  // more than two waves per batch slice and enough row tiles to group
+  static const int raster_env = std::getenv("PE_GEMM_RASTER") ? std::atoi(std::getenv("PE_GEMM_RASTER")) : 16;
+  if (raster_env > 1 && grid.y >= 4 && (long long)grid.x * grid.y > 2LL * 148 * std::max(1, occ))
+    q.raster = std::min<int>(raster_env, grid.y);
+  launch_k(gemm_fast_kernel<WGM, WGN, FM, FN, BK, STAGES, BJC, PRE>, grid, dim3(Cfg::NT), Cfg::SMEM, st, q);
   ++g_launches;
 }
 
@@ -1278,7 +1295,8 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
   // TMA pipeline: measured faster than the cp.async kernels only for many skinny batched
   // products (the shifted solves: N <= 128 per batch, long K); slower on the wide rhs / g /
   // norm / ensemble-step shapes (tools/gemm_bench.py, profiles/r01/README.md)
-  const bool tma_shape = batch >= 16 && p.N <= 128 && p.seg[0].K >= 512;
+  static const bool tma_all = getenv("PE_GEMM_TMA_ALL") != nullptr;  // tuning only
+  const bool tma_shape = (batch >= 16 && p.N <= 128 && p.seg[0].K >= 512) || (tma_all && !p.nrm);
   if (lay == 0 && (tiles64 >= 96 || tiles_n32 >= 96) && tma_shape && tma_ok(p)) {
     launch_tma_best(p, st);
   } else if (lay >= 0 && (tiles64 >= 96 || tiles_n32 >= 96)) {

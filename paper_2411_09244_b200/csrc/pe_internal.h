@@ -99,6 +99,7 @@ struct GemmParams {
   double* ws = nullptr;
   size_t ws_doubles = 0;
   int ksplit = 1;  // set by gemm_f64
+  int raster = 0;  // set by gemm_f64: grouped tile rasterisation (row tiles per group)
 };
 
 // Launch; chooses tile shape and the k-/j-contiguous loader variant from strides.

@@ -128,7 +128,7 @@ def run_single(pipe, n: int, *, stop_rule: str = "absolute") -> RunResult:
     if getattr(cfg, "compute_reference", False):
         from .fem import check_reference_size
 
-        check_reference_size(pipe.ops.M.shape[0])
+        check_reference_size(pipe.ops)
     props = SplitPropagators(pipe.space.system, loads)
     bound = props.stability_max_step()
     if tg.dt_sub > bound:

@@ -64,16 +64,29 @@ def _load_vector(ops, source, n):
     return b
 
 
-MAX_REFERENCE_NODES = 65535  # dense K^-1 formulation limit (finescale.cu)
+MAX_DENSE_NODES = 65535      # dense (packed) K^-1 formulation limit (finescale.cu)
+MAX_CHAIN_BANDWIDTH = 512    # block-tridiagonal chain solver limit (finechain.cu)
 
 
-def check_reference_size(n: int) -> None:
-    """The GPU fine reference solve keeps a dense (packed) K^-1: above 65535 interior nodes
-    it would not fit.  Raised before any work, so `run_single` fails before its parareal run
-    rather than after it."""
-    if n > MAX_REFERENCE_NODES:
-        raise ValueError(f"fine reference solve supports at most {MAX_REFERENCE_NODES} interior "
-                         f"nodes (dense K^-1 formulation); this grid has {n}")
+def _half_bandwidth(A) -> int:
+    A = A.tocsr()
+    rows = np.repeat(np.arange(A.shape[0]), np.diff(A.indptr))
+    return int(np.abs(A.indices - rows).max()) if A.nnz else 0
+
+
+def check_reference_size(ops) -> None:
+    """Up to 65535 interior nodes the GPU fine reference solve can keep a dense (packed)
+    K^-1; larger grids need a banded operator (half-bandwidth <= 512: the chain solver of
+    finechain.cu, which any row-ordered Q1 grid up to 511^2 nodes satisfies).  Raised before
+    any work, so `run_single` fails before its parareal run rather than after it."""
+    n = ops.M.shape[0]
+    if n <= MAX_DENSE_NODES:
+        return
+    w = max(_half_bandwidth(ops.M), _half_bandwidth(ops.A))
+    if w > MAX_CHAIN_BANDWIDTH:
+        raise ValueError(f"fine reference solve: {n} interior nodes exceed the dense K^-1 limit "
+                         f"({MAX_DENSE_NODES}) and the operator's half-bandwidth {w} exceeds the "
+                         f"chain solver's ({MAX_CHAIN_BANDWIDTH})")
 
 
 def reference_solve(ops, source, t_end: float, n_steps: int, u0=None,
@@ -85,7 +98,7 @@ def reference_solve(ops, source, t_end: float, n_steps: int, u0=None,
     times = [0, t_end].  `timing`, if given, receives the device time of the step loop.
     """
     n = ops.M.shape[0]
-    check_reference_size(n)
+    check_reference_size(ops)
     lib = require_cuda()
     if n_steps <= 0 or not t_end > 0:
         raise ValueError("need n_steps > 0 and t_end > 0")

@@ -170,6 +170,46 @@ def test_gpu_reference_solve_packed_symmetric_path(m, monkeypatch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("m,steps", [(20, 5), (63, 6), (64, 4), (100, 7), (150, 3)])
+def test_gpu_reference_solve_chain_solver(m, steps, monkeypatch):
+    """The block-tridiagonal chain solver (finechain.cu; default above 16384 nodes, forced
+    here): block sizes 64 .. 192, partial last block, one and several ring chunks, against
+    the oracle's splu (fem.py:292-318) and the dense path."""
+    from paper_2411_09244_b200 import fem
+
+    M, A, u0 = _fem_like(m, 100 + m)
+    b = np.full(m * m, 1.0 / (m + 1) ** 2)
+    ops = types.SimpleNamespace(M=M, A=A)
+    ref = po.fine_reference_solve(M, A, b, 0.02, steps, u0=u0)
+    monkeypatch.setenv("PE_FINE_CHAIN", "1")
+    tm = {}
+    _, got = fem.reference_solve(ops, b, 0.02, steps, u0=u0, timing=tm)
+    assert got.shape == ref.shape and tm["step_ms"] > 0
+    for r, g in zip(got, ref):
+        assert _rel(r, g) < 1e-11, (m, steps)
+    _, ends = fem.reference_solve(ops, b, 0.02, steps, u0=u0, keep_trajectory=False)
+    assert np.array_equal(ends[0], u0) and np.array_equal(ends[1], got[-1])
+    monkeypatch.setenv("PE_FINE_CHAIN", "0")
+    _, dense = fem.reference_solve(ops, b, 0.02, steps, u0=u0)
+    assert _rel(dense[-1], got[-1]) < 1e-11
+
+
+@pytest.mark.gpu
+def test_gpu_reference_solve_chain_solver_is_default_for_large_grids():
+    """n = 150^2 = 22500 > 16384 takes the chain solver without any switch, and a grid
+    above the dense path's 65535-node cap (257^2) runs at all."""
+    from paper_2411_09244_b200 import fem
+
+    for m, steps in ((150, 2), (257, 2)):
+        M, A, u0 = _fem_like(m, 7)
+        b = np.full(m * m, 1.0 / (m + 1) ** 2)
+        ops = types.SimpleNamespace(M=M, A=A)
+        ref = po.fine_reference_solve(M, A, b, 0.01, steps, u0=u0)
+        _, got = fem.reference_solve(ops, b, 0.01, steps, u0=u0)
+        assert _rel(got[-1], ref[-1]) < 1e-11, m
+
+
+@pytest.mark.gpu
 def test_gpu_error_series_matches_reference():
     from paper_2411_09244_b200 import fem
 

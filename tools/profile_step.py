@@ -15,6 +15,8 @@ import paper_2411_09244_b200 as P  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="cfg2-aao")
 ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--max-iter", type=int, default=0,
+                help="cap the WR sweeps per solve (shares of a sweep do not depend on it)")
 args = ap.parse_args()
 wl = bench.WORKLOADS[args.workload]
 mem, meta = bench.load_workload(wl)
@@ -27,7 +29,8 @@ ctx.prepare_coarse(T / N)
 if kind == "sequential":
     ctx.prepare_sequential(T / N / J)
 else:
-    ctx.prepare_allatonce(T / N / J, wl["alpha"], bench.FINE_TOL, wl["max_iter"])
+    ctx.prepare_allatonce(T / N / J, wl["alpha"], bench.FINE_TOL,
+                          args.max_iter or wl["max_iter"])
 d = s.d1 + s.d2
 A = torch.zeros(E, N + 1, d, dtype=torch.float64, device="cuda")
 B = torch.zeros_like(A)
