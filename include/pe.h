@@ -171,6 +171,13 @@ int pe_last_fine_other_ms(pe_ctx* ctx, double* other_ms);
 
 /* ---- Fine-scale accuracy path (host buffers in and out) ---------- */
 
+/* Which formulation pe_fine_reference_solve takes for this operator: 0 = one fused dense
+ * GEMV (n < 4096), 1 = packed symmetric K^-1 tiles, 2 = block-tridiagonal chain solver
+ * (banded operators from 16384 nodes, finechain.cu; PE_FINE_CHAIN=1 / 0 forces / disables
+ * it); *block (optional) = the chain solver's block size.  Host CSR index arrays. */
+int pe_fine_solver_kind(int n, const int* M_ptr, const int* M_idx, const int* A_ptr,
+                        const int* A_idx, int* block);
+
 /* Backward Euler on the fine interior nodes, (M/dt + A) u_{s+1} = M u_s / dt + b with
  * dt = t_end / n_steps (fem.py:292-318 reference_solve).  M, A: host CSR (int32 indptr /
  * indices, FP64 values) of the n x n interior mass and stiffness (FineOperators.M/.A,

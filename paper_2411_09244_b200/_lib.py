@@ -64,6 +64,7 @@ SIGNATURES = {
     "pe_last_fine_stats": (C.c_int, [_P, _D, _D, _I]),
     "pe_fine_reference_solve": (C.c_int, [C.c_int, _I, _I, _D, _I, _I, _D, _D, _D, C.c_double,
                                           C.c_int, C.c_int, _D, _F, _P]),
+    "pe_fine_solver_kind": (C.c_int, [C.c_int, _I, _I, _I, _I, _I]),
     "pe_relative_error_series": (C.c_int, [C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _D,
                                            C.c_int, _D, _D, _P]),
     "pe_project_coarse": (C.c_int, [C.c_int, C.c_int, C.c_int, _I, _I, _D, _I, _I, _D, _I, _I,

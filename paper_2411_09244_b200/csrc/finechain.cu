@@ -18,8 +18,9 @@
 // full sparse vector y_i (or U_i x_{i+1}) redundantly from the previous step's broadcast
 // vector, (2) dots its own rows of P_i -- streamed by cp.async.bulk into a shared-memory
 // ring that runs several block steps ahead -- with it, (3) writes its rpc results into
-// every peer's receive buffer through distributed shared memory and (4) passes one
-// cluster barrier.  z_i stays in the owner's shared memory for the backward sweep.
+// every peer's receive buffer by st.async, completing on the receiver's mbarrier: the
+// chain has no cluster barrier (the double-buffered receive is ordered by the data flow
+// itself).  z_i stays in the owner's shared memory for the backward sweep.
 //
 // The block inverses come from libpe's own LU (batchlu.cu).  Deterministic: fixed-order
 // dot products and shuffles.
@@ -82,6 +83,13 @@ __device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigne
       : "memory");
 }
 
+__device__ __forceinline__ void st_async_b64(unsigned remote_addr, double x, unsigned remote_bar) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                   remote_addr),
+               "l"(__double_as_longlong(x)), "r"(remote_bar)
+               : "memory");
+}
+
 __global__ void __launch_bounds__(CH_T, 1) fine_chain_kernel(const __grid_constant__ ChainArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
@@ -93,8 +101,11 @@ __global__ void __launch_bounds__(CH_T, 1) fine_chain_kernel(const __grid_consta
   double* full = recv + 2 * bs;                                       // bs (this step's vector)
   double* zloc = full + bs;                                           // nb x rpc
   __shared__ __align__(8) unsigned long long bar[8];
+  __shared__ __align__(8) unsigned long long rbar[2];  // receive barriers, by step parity
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) mbar_init(smem_u32(&bar[s]), 1);
+    mbar_init(smem_u32(&rbar[0]), 1);
+    mbar_init(smem_u32(&rbar[1]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -143,8 +154,11 @@ __global__ void __launch_bounds__(CH_T, 1) fine_chain_kernel(const __grid_consta
     const int blk = block_of(step);
     const double* prev = recv + (size_t)((step + 1) & 1) * bs;  // written during step - 1
     double* next = recv + (size_t)(step & 1) * bs;
+    // this step's receive barrier: bs doubles from the 16 CTAs (own rows included)
+    if (tid == 0) mbar_expect_tx(smem_u32(&rbar[step & 1]), (unsigned)(bs * sizeof(double)));
     // (1) full vector: y_i = v_i - L_i z_{i-1}  or  t_i = U_i x_{i+1}
     const bool has_prev = step > 0;
+    if (has_prev) mbar_wait(smem_u32(&rbar[(step + 1) & 1]), ((step - 1) >> 1) & 1);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int r = tid + h * CH_T;
@@ -159,34 +173,50 @@ __global__ void __launch_bounds__(CH_T, 1) fine_chain_kernel(const __grid_consta
       }
     }
     if (step + 1 < steps) prefetch(step + 1);
-    __syncthreads();
-    // (2) own rows of P_i times the full vector, chunk by chunk; (3) broadcast
+    __syncthreads();  // full[] complete; every warp is past the previous step's ring chunk
+    if (npc == 1 && tid == 0 && step > 0 && g - 1 + ST < G) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(g - 1 + ST);
+    }
+    // (2) own rows of P_i times the full vector, chunk by chunk; (3) broadcast.  No cluster
+    // barrier: a peer's step s+2 stores into the buffer this CTA reads in step s+1 only
+    // after it received this CTA's step s+1 rows, i.e. after that read.
+    const unsigned next_u32 = smem_u32(next), rbar_u32 = smem_u32(&rbar[step & 1]);
     for (int part = 0; part < npc; ++part, ++g) {
       mbar_wait_cta(smem_u32(&bar[g % ST]), (g / ST) & 1);
       const double* tile = ring + (size_t)(g % ST) * rc * bs;
-      for (int rr = warp; rr < rc; rr += CH_W) {
-        const double2* row = reinterpret_cast<const double2*>(tile + (size_t)rr * bs);
+      // two rows per warp pass, one per half-warp (16 lanes x 16-byte loads: conflict free)
+      const int half = lane >> 4, hl = lane & 15;
+      for (int r2 = 2 * warp; r2 < rc; r2 += 2 * CH_W) {
+        const int rr = r2 + half;
+        const bool live = rr < rc;
+        const double2* row = reinterpret_cast<const double2*>(tile + (size_t)(live ? rr : r2) * bs);
         const double2* f2 = reinterpret_cast<const double2*>(full);
-        double s0 = 0.0, s1 = 0.0;
-        for (int k = lane; k < bs / 2; k += 32) {
-          const double2 p = row[k], f = f2[k];
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        for (int k = hl; k < bs / 2; k += 32) {  // bs % 64 == 0: both strides in range
+          const double2 p = row[k], f = f2[k], q = row[k + 16], h2 = f2[k + 16];
           s0 = fma(p.x, f.x, s0);
           s1 = fma(p.y, f.y, s1);
+          s2 = fma(q.x, h2.x, s2);
+          s3 = fma(q.y, h2.y, s3);
         }
-        double s = s0 + s1;
+        double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        const int lr = part * rc + rr;  // local row
+        for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const int lr = part * rc + (live ? rr : r2);  // local row
         double val;
         if (fwd) {
           val = s;  // z_i
-          if (lane == 0) zloc[(size_t)blk * rpc + lr] = val;
+          if (hl == 0 && live) zloc[(size_t)blk * rpc + lr] = val;
         } else {
           val = zloc[(size_t)blk * rpc + lr] - s;  // x_i
         }
-        if (lane < CH_CS) cl.map_shared_rank(next, lane)[rank * rpc + lr] = val;
+        // each half-warp's 16 lanes store its row to the 16 CTAs
+        if (live)
+          st_async_b64(map_rank(next_u32 + (unsigned)((rank * rpc + lr) * sizeof(double)), hl), val,
+                       map_rank(rbar_u32, hl));
         const int grow = blk * bs + rank * rpc + lr;
-        if (lane == 0 && grow < a.n && (!fwd || blk == nb - 1)) a.x[grow] = val;
+        if (hl == 0 && live && grow < a.n && (!fwd || blk == nb - 1)) a.x[grow] = val;
       }
       if (npc > 1) {
         __syncthreads();  // chunk fully read
@@ -196,13 +226,10 @@ __global__ void __launch_bounds__(CH_T, 1) fine_chain_kernel(const __grid_consta
         }
       }
     }
-    // (4) everyone's rows of this step have landed everywhere
-    cl.sync();
-    if (npc == 1 && tid == 0 && g - 1 + ST < G) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(g - 1 + ST);
-    }
   }
+  // the last step's rows: nobody exits while a peer may still store into its buffers
+  mbar_wait(smem_u32(&rbar[(steps - 1) & 1]), ((steps - 1) >> 1) & 1);
+  cl.sync();
 }
 
 // dense diagonal blocks (row-major, identity on the padding rows) from the merged CSR of K
@@ -251,7 +278,8 @@ __global__ void chain_schur(int bs, const int* cidx, const double* cval, const d
 
 }  // namespace
 
-bool fine_chain_applicable(int n, const int* mp, const int* mi, const int* ap, const int* ai) {
+bool fine_chain_applicable(int n, const int* mp, const int* mi, const int* ap, const int* ai,
+                           int* block) {
   const char* env = std::getenv("PE_FINE_CHAIN");
   if (env && std::atoi(env) == 0) return false;
   const bool forced = env && std::atoi(env) != 0;
@@ -264,6 +292,7 @@ bool fine_chain_applicable(int n, const int* mp, const int* mi, const int* ap, c
   const long long bs = std::max<long long>(64, (w + 63) / 64 * 64);
   if (bs > 512) return false;                  // a ring chunk holds >= 8 rows
   if (!forced && bs * 8 > n) return false;     // not banded enough to pay
+  if (block) *block = (int)bs;
   return true;
 }
 

@@ -626,6 +626,17 @@ extern "C" int pe_fine_reference_solve(int n, const int* M_ptr, const int* M_idx
   return pe::fs_guard("pe_fine_reference_solve", pe::ref_solve_impl, &a);
 }
 
+extern "C" int pe_fine_solver_kind(int n, const int* M_ptr, const int* M_idx, const int* A_ptr,
+                                   const int* A_idx, int* block) {
+  if (n <= 0 || !M_ptr || !A_ptr) {
+    pe::set_error("pe_fine_solver_kind: need n > 0 and CSR index arrays");
+    return -1;
+  }
+  if (block) *block = 0;
+  if (pe::fine_chain_applicable(n, M_ptr, M_idx, A_ptr, A_idx, block)) return 2;
+  return (n >= pe::kSymMin && !getenv("PE_FINE_NO_SYM")) ? 1 : 0;
+}
+
 extern "C" int pe_relative_error_series(int n, int d, const int* P_ptr, const int* P_idx,
                                         const double* P_val, const int* M_ptr,
                                         const int* M_idx, const double* M_val,

@@ -23,7 +23,8 @@ void fine_rhs(int n, const int* mp, const int* mi, const double* mv, double inv_
               const double* u, const double* b, double* v, cudaStream_t st);
 
 // Banded operator, large enough (or PE_FINE_CHAIN=1): the chain solver applies
-bool fine_chain_applicable(int n, const int* mp, const int* mi, const int* ap, const int* ai);
+bool fine_chain_applicable(int n, const int* mp, const int* mi, const int* ap, const int* ai,
+                           int* block = nullptr);
 void fine_chain_solve(RefSolveArgs& a);
 
 }  // namespace pe

@@ -119,8 +119,20 @@ def reference_solve(ops, source, t_end: float, n_steps: int, u0=None,
         timing["step_ms"] = float(ms.value)
         # algorithmic HBM bytes per step: R once + u, c, u' (n < 4096); from n = 4096 on the
         # lower triangle of the symmetric K^-1 once + M, u, b, v, u' (finescale.cu)
-        timing["bytes_per_step"] = (8.0 * n * (n + 2) if n < SYM_MIN
-                                    else 8.0 * (n * (n + 1) / 2 + 4 * n) + 12.0 * ops.M.nnz)
+        blk = C.c_int(0)
+        kind = lib.pe_fine_solver_kind(n, _ip(mp), _ip(mi), _ip(ap), _ip(ai), C.byref(blk))
+        timing["solver"] = {0: "dense-gemv", 1: "packed-tiles", 2: "block-chain"}.get(kind, "?")
+        if kind == 2:
+            # chain solver: the nb dense block inverses twice (forward and backward sweep,
+            # the last block once) + the sparse couplings and vectors (finechain.cu)
+            bs = blk.value
+            nblk = -(-n // bs)
+            timing["block"] = bs
+            timing["bytes_per_step"] = (8.0 * (2 * nblk - 1) * bs * bs + 12.0 * ops.M.nnz
+                                        + 12.0 * (ops.M.nnz + ops.A.nnz) / 2 + 8.0 * 5 * n)
+        else:
+            timing["bytes_per_step"] = (8.0 * n * (n + 2) if n < SYM_MIN
+                                        else 8.0 * (n * (n + 1) / 2 + 4 * n) + 12.0 * ops.M.nnz)
     times = np.linspace(0.0, t_end, n_steps + 1) if keep_trajectory else np.array([0.0, t_end])
     return times, states
 

@@ -83,7 +83,8 @@ def main():
         _, chk = fem.reference_solve(ops, b, 1.0 * args.cpu_steps / args.steps, args.cpu_steps,
                                      keep_trajectory=False)
         rel = float(np.linalg.norm(chk[1] - ref[1]) / np.linalg.norm(ref[1]))
-        print(json.dumps(dict(nx=nx, n=n, steps=args.steps, step_ms=step_ms, hbm_gbs=gbs,
+        print(json.dumps(dict(nx=nx, n=n, solver=tm.get("solver"), block=tm.get("block"),
+                              steps=args.steps, step_ms=step_ms, hbm_gbs=gbs,
                               peak_gbs=peak, frac=(gbs / peak if peak else None),
                               bytes_per_step=tm["bytes_per_step"], wall_s_incl_setup=wall,
                               cpu_splu_step_ms=cpu_ms, speedup_per_step=cpu_ms / step_ms,
