@@ -751,7 +751,15 @@ __global__ void __launch_bounds__((WGM * WGN + 1) * 32)
   const GemmParams& p = a.p;
   const int z = blockIdx.z;
   const int z1 = z / p.nb2, z2 = z - (z / p.nb2) * p.nb2;
-  const int i0 = blockIdx.y * Cfg::BM, j0 = blockIdx.x * Cfg::BN;
+  int ty = blockIdx.y, tx = blockIdx.x;
+  if (p.raster > 1) {  // grouped rasterisation, as gemm_fast_kernel
+    const int pid = blockIdx.y * gridDim.x + blockIdx.x, gsz = p.raster * gridDim.x;
+    const int gq = pid / gsz, first = gq * p.raster, r = pid - gq * gsz;
+    const int gm = min(p.raster, (int)gridDim.y - first);
+    ty = first + r % gm;
+    tx = r / gm;
+  }
+  const int i0 = ty * Cfg::BM, j0 = tx * Cfg::BN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   int kt[3] = {0, 0, 0};
@@ -901,6 +909,9 @@ static void launch_tma(const GemmParams& p, cudaStream_t st) {
     encode_operand(&a.tb[s], a.zb[s], g.B.p, g.K, p.N, g.B.s1, g.B.b1, p.nb1, g.B.b2, p.nb2, Cfg::BN);
   }
   dim3 grid((p.N + Cfg::BN - 1) / Cfg::BN, (p.M + Cfg::BM - 1) / Cfg::BM, p.nb1 * p.nb2);
+  static const int raster_env = std::getenv("PE_GEMM_RASTER") ? std::atoi(std::getenv("PE_GEMM_RASTER")) : 16;
+  if (raster_env > 1 && grid.y >= 4 && (long long)grid.x * grid.y > 6LL * 148)
+    a.p.raster = std::min<int>(raster_env, grid.y);
   launch_k(kern, grid, dim3(Cfg::NT), Cfg::SMEM, st, a);
   ++g_launches;
 }
@@ -1296,8 +1307,18 @@ void gemm_f64(const GemmParams& p, cudaStream_t st) {
   // products (the shifted solves: N <= 128 per batch, long K); slower on the wide rhs / g /
   // norm / ensemble-step shapes (tools/gemm_bench.py, profiles/r01/README.md)
   static const bool tma_all = getenv("PE_GEMM_TMA_ALL") != nullptr;  // tuning only
-  const bool tma_shape = (batch >= 16 && p.N <= 128 && p.seg[0].K >= 512) || (tma_all && !p.nrm);
-  if (lay == 0 && (tiles64 >= 96 || tiles_n32 >= 96) && tma_shape && tma_ok(p)) {
+  static const bool no_big_tma = getenv("PE_GEMM_NO_BIG_TMA") != nullptr;
+  const bool tma_shape = (batch >= 16 && p.N <= 128 && p.seg[0].K >= 512) || tma_all;
+  // Many-wave products with a long K (the config-3 rhs / h / norm products: 12800 tiles of
+  // 64 x 64, K = 8192): the TMA producer pipeline with 64 x 64 tiles measured 35.7 TF/s
+  // against 34.5 for the cp.async kernel (cuBLAS 36.0, tools/gemm_bench.py); the wide
+  // medium-size modal shapes of config 2 (285 tiles, one wave) stay on cp.async.
+  int ktiles16 = 0;
+  for (int sgi = 0; sgi < p.nseg; ++sgi) ktiles16 += (p.seg[sgi].K + 15) / 16;
+  const bool big = !no_big_tma && p.M >= 256 && p.N >= 256 && tiles64 >= 8 * 148 && ktiles16 >= 128;
+  if (lay == 0 && big && tma_ok(p)) {
+    launch_tma<2, 2, 4, 4, 4>(p, st);
+  } else if (lay == 0 && (tiles64 >= 96 || tiles_n32 >= 96) && tma_shape && tma_ok(p)) {
     launch_tma_best(p, st);
   } else if (lay >= 0 && (tiles64 >= 96 || tiles_n32 >= 96)) {
     // pick the tile / pipeline variant with the best wave-quantised cost; the choice is a
