@@ -23,12 +23,18 @@ def num(k):
     return float(d[k].replace(",", ""))
 
 
-rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
-unit_r = rows[1][h.index("dram__bytes_read.sum")]
-scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1.0)
-dur = num("gpu__time_duration.sum")
-dur_unit = rows[1][h.index("gpu__time_duration.sum")]
-dscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(dur_unit, 1e-9)
+BYTES = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+SECONDS = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0,
+           "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
+
+
+def scaled(k, table):
+    return num(k) * table[rows[1][h.index(k)]]
+
+
+rd, wr = scaled("dram__bytes_read.sum", BYTES), scaled("dram__bytes_write.sum", BYTES)
+scale = 1.0
+dur, dscale = scaled("gpu__time_duration.sum", SECONDS), 1.0
 entry = {"kernel": d["Kernel Name"][:200], "grid": d.get("Grid Size"), "block": d.get("Block Size"),
          "dram_bytes_per_launch": (rd + wr) * scale, "dram_read_bytes": rd * scale,
          "dram_write_bytes": wr * scale, "algorithmic_bytes_per_launch": alg,
