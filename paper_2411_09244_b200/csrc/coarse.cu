@@ -84,13 +84,12 @@ __device__ __forceinline__ void cs_wait(unsigned bar, unsigned parity) {
       "@!p bra W_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
 }
 
-// x_{n+1} rows travel as one bulk DSMEM copy per peer: each CTA stages its new rows in a
-// double-buffered smem block and copies it into every peer's next x buffer, completing on
-// the peer's mbarrier (same protocol as recur.cu); a CTA waits only on its own mbarrier.
-// Rows are dealt in pairs so every copy is 16-byte aligned and sized (an odd d pads one
-// trailing zero).  Each warp computes all of its rows together (independent accumulators
-// sharing the x loads), and the per-warp norm partials go straight to global memory, so a
-// step has one CTA barrier (before the copies).
+// x_{n+1} rows travel by st.async: the lane that finished a row stores it into every peer's
+// next x buffer, completing on the peer's mbarrier; a CTA waits only on its own mbarrier
+// and a step has no CTA barrier (round 2; round 1 staged the rows and issued one bulk
+// DSMEM copy per peer behind a CTA barrier: 3.2 us per step at d = 600).  Each warp
+// computes all of its rows together (independent accumulators sharing the x loads), and
+// the per-warp norm partials go straight to global memory.
 __device__ __forceinline__ void cs_fence_proxy() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -118,6 +117,18 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
     rv[j] = rr < nrows;
     rowp[j] = PHIS ? phis + (long long)(rv[j] ? rr : 0) * d
                    : Phi + (long long)(r0 + (rv[j] ? rr : 0)) * d;
+  }
+  // Warps without rows neither read x nor send: they leave (with no CTA barrier in the
+  // step loop a lagging idle warp could miss a whole phase of the receive barrier).  Warp 0
+  // stays: its thread 0 arms the barrier and its own wait keeps it in step.
+  if (wrows == 0 && warp != 0) {
+    if (lane == 0)  // its norm partials are zeros
+      for (int n = 0; n < N; ++n) {
+        double* p = a.partial + ((((long long)e * N + n) * a.cs + rank) * COARSE_WARPS + warp) * 2;
+        p[0] = 0.0;
+        p[1] = 0.0;
+      }
+    return;
   }
   // lane j < RPW owns row warp + 8 j: its operands for step n are fetched one step ahead
   const int myrr = warp + COARSE_WARPS * lane;
@@ -192,17 +203,31 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
     const double pf_f = nf_f, pf_g = nf_g, pf_b = nf_b, pf_o = nf_o;
     prefetch(n + 1);
     double sd = 0.0, sn = 0.0;
-    double* ybuf = ybuf2 + (size_t)cur * ncopy;
+    double x = 0.0;
     if (mine) {
       const long long o = (long long)n * d + r0 + myrr;
       const double g = mya + pf_b;
-      const double x = F ? pf_f + (g - pf_g) : g;  // grouping kept exactly (parareal.py:209)
+      x = F ? pf_f + (g - pf_g) : g;  // grouping kept exactly (parareal.py:209)
       Gc[o] = g;
       X_new[o + d] = x;
       const double df = x - pf_o;
       sd = df * df;
       sn = x * x;
-      ybuf[myrr] = x;
+    }
+    // x_{n+1}: row (warp + 8 j) goes from lane j to every CTA's next x buffer, lane q
+    // storing to peer q (st.async completing on the peer's mbarrier).  No staging, no CTA
+    // barrier: a peer's step n+2 stores into the buffer read here in step n+1 only after it
+    // has received this warp's step n+1 rows, i.e. after this warp's dot products.
+    if (n + 1 < N) {
+      const unsigned nbar = cs_map_rank(bar0 + 8 * ((n + 1) & 1), lane < a.cs ? lane : 0);
+      const unsigned dstb =
+          cs_map_rank(xs_base + (unsigned)((((n + 1) & 1) * xsd + r0) * 8), lane < a.cs ? lane : 0);
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) {
+        const double v = __shfl_sync(0xffffffffu, x, j);
+        const int rr = warp + COARSE_WARPS * j;
+        if (rr < nrows && lane < a.cs) cs_st_async(dstb + (unsigned)(rr * 8), v, nbar);
+      }
     }
     // per-warp norm partials, summed later in (rank, warp) order
 #pragma unroll
@@ -216,25 +241,7 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
       p[1] = sn;
     }
     CS_TRACE(3 + 3 * n)
-    if (n + 1 < N) {
-      // copies issued last step read the other ybuf parity; wait before it is rewritten next
-      if ((int)threadIdx.x < a.cs) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      cs_fence_proxy();
-      __syncthreads();
-      if ((int)threadIdx.x < a.cs) {
-        const int q = threadIdx.x;
-        const unsigned nbar = cs_map_rank(bar0 + 8 * ((n + 1) & 1), q);
-        const unsigned dst =
-            cs_map_rank(xs_base + (unsigned)((((n + 1) & 1) * xsd + r0) * 8), q);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(dst), "r"(yb_base + (unsigned)(cur * ncopy * 8)), "r"((unsigned)(ncopy * 8)), "r"(nbar)
-            : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    }
   }
-  if ((int)threadIdx.x < a.cs) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 __global__ void __launch_bounds__(COARSE_THREADS, 1) coarse_kernel(const __grid_constant__ CoarseArgs a) {
@@ -273,7 +280,7 @@ __global__ void __launch_bounds__(COARSE_THREADS, 1) coarse_kernel(const __grid_
   for (int k = threadIdx.x; k < 2 * xsd; k += COARSE_THREADS) xs2[k] = (k < d) ? X_old[k] : 0.0;
   for (int k = threadIdx.x; k < 2 * ncmax; k += COARSE_THREADS) ybuf2[k] = 0.0;  // pad rows
   for (int r = r0 + threadIdx.x; r < r1; r += COARSE_THREADS) X_new[r] = X_old[r];
-  const unsigned bytes = (unsigned)(2 * half * 8);  // all CTAs' copies of one step
+  const unsigned bytes = (unsigned)(d * 8);  // every row of x_{n+1}, from all CTAs
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cs_smem_u32(&mbar[0])) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cs_smem_u32(&mbar[1])) : "memory");
