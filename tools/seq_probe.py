@@ -11,7 +11,8 @@ import bench  # noqa: E402
 import paper_2411_09244_b200 as P  # noqa: E402
 
 wl = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "cfg2-seq"]
-blocks, f1, f2, meta = bench.load_system(wl["sys"])
+mem, meta = bench.load_workload(wl)
+blocks, f1, f2 = mem[0]
 s = P.CoarseSystem(**blocks)
 ctx = P.PeContext([s], [P.ConstantLoads(f1, f2)], wl["J"])
 N, J, T = wl["N"], wl["J"], wl["T"]
