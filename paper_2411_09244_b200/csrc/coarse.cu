@@ -514,7 +514,14 @@ static void coarse_correct_stream(int E, int d, int N, const double* Phi, const 
                                   const double* X_old, const double* F_hat, double* G_cache,
                                   double* X_new, double* partial, double* diff,
                                   const int* active, cudaStream_t st) {
-  const int nb = coarse_stream_blocks(d);
+  // Ensembles: about one resident wave of CTAs (8 per SM) over all members, several rows
+  // per warp.  One row per warp in 4800 short-lived CTAs reloaded the member's state for 8
+  // rows each: 43.7 us per cfg4 coarse step, 5.21 ms per iteration; measured per blocks
+  // per member (tools sweep, PE_CS_BLOCKS): 38: 5.12, 25: 5.06, 19: 4.99, 15: 5.16,
+  // 13: 4.94, 10: 5.13 ms
+  int nb = coarse_stream_blocks(d);
+  if (E > 1) nb = std::min(nb, std::max(1, (148 * 8 + E / 2) / E));  // one resident wave
+  if (getenv("PE_CS_BLOCKS")) nb = std::max(1, std::min(296, atoi(getenv("PE_CS_BLOCKS"))));
   const size_t smem = sizeof(double) * d;
   static bool attr = false;
   if (!attr) {
