@@ -44,11 +44,23 @@
 
 namespace pe {
 
-constexpr int SG_CWARPS = 8;   // compute warps: two per SMSP (one cannot hide LDS + pipeline overhead)
+// Build-time knobs of the measured variants (cfg2-seq, us per chain step, B200):
+//   8 warps x 16-k chunks x 4 stages 5.32 (kept) | 8 x 8 6.68 | 12 x 8 5.87 | 8 x 24 x 3 5.47 |
+//   8 x 32 x 2 5.33 | 8 x 16 x 3 5.33.  The critical warp runs ~49 cycles per DMMA whatever
+//   the chunk size: two warps per SMSP share the DMMA pipe (16 cycles each) and the
+//   shared-memory pipe, which moves T slice + Z reads + Z writes = 292 KB per sub-step
+//   (84 % of the 128 B/clk x 1.42 us the DMMAs need).
+#ifndef SG_CWARPS_N
+#define SG_CWARPS_N 8
+#endif
+#ifndef SG_KCH_N
+#define SG_KCH_N 16
+#endif
+constexpr int SG_CWARPS = SG_CWARPS_N;  // compute warps (one per SMSP cannot hide LDS + pipeline overhead)
 constexpr int SG_CTHREADS = SG_CWARPS * 32;
 constexpr int SG_THREADS = SG_CTHREADS + 64;  // + the admit warp and the publish warp
 constexpr int SG_WARPS = SG_CWARPS;
-constexpr int SG_KCH = 16;     // k per pipeline chunk
+constexpr int SG_KCH = SG_KCH_N;  // k per pipeline chunk
 constexpr int SG_MAXR = 148;   // row tiles per column range (<= SMs)
 constexpr int SG_MT = 3;       // max m8 tiles (rows / 8) per CTA
 constexpr int SG_MAXH = 4;     // chain groups per CTA
@@ -104,11 +116,7 @@ __device__ __forceinline__ bool sg_mbar_test(unsigned bar, unsigned parity) {
   asm volatile(  // try_wait suspends the thread for a while instead of spinning on the issue port
       "{\n"
       ".reg .pred p;\n"
-#ifdef SG_TESTWAIT
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-#else
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-#endif
       "selp.u32 %0, 1, 0, p;\n"
       "}\n"
       : "=r"(ok)
@@ -257,11 +265,11 @@ __global__ void __launch_bounds__(SG_THREADS, 1) seqgrid_kernel(const __grid_con
   auto load_chunk = [&](const double* Zp, int ncol, int ch, int slot) {
     double* dst = myring + (size_t)slot * CT * ZS;
     const int k0 = ch * SG_KCH;
-    // CT columns x 16 k = CT x 8 sixteen-byte pieces; 32 lanes
+    // CT columns x KCH k = CT x KCH/2 sixteen-byte pieces; 32 lanes
 #pragma unroll
-    for (int q0 = 0; q0 < CT * 8; q0 += 32) {
+    for (int q0 = 0; q0 < CT * (SG_KCH / 2); q0 += 32) {
       const int q = lane + q0;
-      const int col = q >> 3, kk = (q & 7) * 2;
+      const int col = q / (SG_KCH / 2), kk = (q % (SG_KCH / 2)) * 2;
       const int k = k0 + kk;
       const bool ok = col < ncol && k < KT;
       const double* src = ok ? Zp + (size_t)col * D2 + k : Zp;
