@@ -1006,7 +1006,8 @@ struct RbPlan {
   int e[2], sb[2], nb[2], w0, nw;
 };
 // first block whose cumulative weight reaches w (blocks in member-major order)
-__device__ __forceinline__ long long rb_block_at(const RowBalArgs& a, long long w) {
+template <class Args>
+__device__ __forceinline__ long long rb_block_at(const Args& a, long long w) {
   const int mb = a.p.M / 8;
   const long long wm = (long long)a.zrb * a.wu + (long long)(mb - a.zrb) * a.ww;
   const long long e = w / wm;
@@ -1018,13 +1019,20 @@ __device__ __forceinline__ long long rb_block_at(const RowBalArgs& a, long long 
     b = a.zrb + (r - (long long)a.zrb * a.wu + a.ww - 1) / a.ww;
   return e * mb + b;
 }
-__device__ __forceinline__ RbPlan rb_plan(const RowBalArgs& a) {
+// block range [b0, b1) of CTA c
+template <class Args>
+__device__ __forceinline__ void rb_range(const Args& a, int c, long long& b0, long long& b1) {
   const int mb = a.p.M / 8;
   const long long E = a.blocks / mb;
   const long long W = E * ((long long)a.zrb * a.wu + (long long)(mb - a.zrb) * a.ww);
-  const long long b0 = blockIdx.x == 0 ? 0 : rb_block_at(a, W * blockIdx.x / gridDim.x);
-  const long long b1 = blockIdx.x + 1 == gridDim.x ? a.blocks
-                                                   : rb_block_at(a, W * (blockIdx.x + 1) / gridDim.x);
+  b0 = c == 0 ? 0 : rb_block_at(a, W * c / gridDim.x);
+  b1 = c + 1 == (int)gridDim.x ? a.blocks : rb_block_at(a, W * (c + 1) / gridDim.x);
+}
+template <class Args>
+__device__ __forceinline__ RbPlan rb_plan(const Args& a) {
+  const int mb = a.p.M / 8;
+  long long b0, b1;
+  rb_range(a, (int)blockIdx.x, b0, b1);
   RbPlan r;
   r.e[0] = (int)(b0 / mb);
   r.sb[0] = (int)(b0 - (long long)r.e[0] * mb);
@@ -1261,6 +1269,340 @@ void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int z
   launch_k(gemm_rowbal_kernel, dim3(grid), dim3((RB_WARPS + 1) * 32), RB_SMEM, st, a);
   ++g_launches;
   PE_CUDA_CHECK(cudaGetLastError());
+}
+
+// ----------------------------------------------------------------------------------------
+// The same row-balanced step, J times in ONE cooperative launch (the ensemble fine chain):
+//     X_{s+1} = T [X_s ; D_s] + c,   D_{s+1} = X_{s+1} - X_s
+// Every CTA keeps its row range for all steps.  A range's B operand is the full state of its
+// (at most two) members, written by the two or three CTAs that cover the member: after its
+// epilogue a CTA's last consumer warp release-increments a per-member counter, and the
+// producer lane admits step s+1's B tiles once the counters of its members show s+1 complete
+// covers (then a proxy fence: the TMA engine reads what other SMs stored).  The producer
+// streams step s+1's T tiles while the consumers are still in step s's epilogue, so T keeps
+// coming from HBM across the step boundary; a launch per step left every SM idle for ~15 %
+// of the step (CTA launch, pipeline fill, tail).  Ring phases run on across steps.
+struct alignas(64) RowBalChainArgs {
+  CUtensorMap ta[2], ta4[2];  // T segments, 8-row and 32-row boxes
+  CUtensorMap tbx[3];         // X_in, bufX[0], bufX[1]
+  CUtensorMap tbd[3];         // D_in (when present), bufD[0], bufD[1]
+  GemmParams p;               // epilogue template: M, N, strides, bias
+  int blocks;
+  int zero_rows, zk0, zk1;
+  int wu, ww, zrb;
+  int J, has_d0;
+  const double* X_in;
+  double* X_out;
+  double* bufX[2];
+  double* bufD[2];
+  unsigned* cnt;              // per member: covers that finished a step (zeroed before launch)
+};
+
+constexpr unsigned RB_SPIN_LIMIT = 1u << 26;
+
+__global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
+    gemm_rowbal_chain_kernel(const __grid_constant__ RowBalChainArgs a) {
+  extern __shared__ unsigned char smraw[];
+  const unsigned sbase = (smem_u32(smraw) + 1023u) & ~1023u;
+  const unsigned char* sgen = smraw + (sbase - smem_u32(smraw));
+  const unsigned bar_full = sbase + RB_STAGES * RB_STAGE;
+  const unsigned bar_empty = bar_full + RB_STAGES * 8;
+  __shared__ unsigned done_tickets;
+  __shared__ int ncov_s[2];
+  const GemmParams& p = a.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const RbPlan pl = rb_plan(a);
+  const int kt0 = (p.seg[0].K + 15) / 16, kt1 = (p.seg[1].K + 15) / 16;
+  const int zt0 = kt0 + (a.zk0 + 15) / 16, zt1 = kt0 + a.zk1 / 16;
+  const int zr_blocks = a.zero_rows / 8;
+  const int mb = p.M / 8;
+  auto wplace = [&](int w, int& part, int& fb, int& cnt) {
+    part = w < pl.w0 ? 0 : 1;
+    const int q = part ? w - pl.w0 : w;
+    fb = pl.sb[part] + q * RB_FM;
+    const int left = pl.nb[part] - q * RB_FM;
+    cnt = left < RB_FM ? left : RB_FM;
+  };
+  auto skips = [&](int fb, int cnt, int g) {
+    return g >= zt0 && g < zt1 && fb + cnt <= zr_blocks;
+  };
+  const int nparts = pl.nb[1] ? 2 : 1;
+
+  if (tid == 0) {
+    for (int s = 0; s < RB_STAGES; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, pl.nw);
+    }
+    done_tickets = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    // covers of this range's members: CTAs whose (non-empty) range meets the member's blocks
+    for (int part = 0; part < 2; ++part) {
+      const long long m0 = (long long)pl.e[part] * mb, m1 = m0 + mb;
+      int n = 0;
+      for (int c0 = 0; c0 < (int)gridDim.x; c0 += 32) {  // small ensembles: many covers
+        const int c = c0 + lane;
+        bool hit = false;
+        if (c < (int)gridDim.x) {
+          long long b0, b1;
+          rb_range(a, c, b0, b1);
+          hit = b1 > b0 && b0 < m1 && b1 > m0;
+        }
+        n += __popc(__ballot_sync(0xffffffffu, hit));
+      }
+      if (lane == 0) ncov_s[part] = n;
+    }
+  }
+  __syncthreads();
+  if (pl.nw == 0) return;
+  const int J = a.J;
+
+  if (warp == RB_WARPS) {  // producer
+    if (lane == 0) {
+      int wrow[RB_WARPS], wcnt[RB_WARPS], wslot[RB_WARPS];
+      bool wz[RB_WARPS];
+      int bytes_all = 0, bytes_nz = 0;
+#pragma unroll
+      for (int w = 0; w < RB_WARPS; ++w) {
+        int part = 0, fb = 0, cnt = 0;
+        if (w < pl.nw) wplace(w, part, fb, cnt);
+        wrow[w] = pl.e[part] * p.M + fb * 8;
+        wcnt[w] = cnt;
+        wslot[w] = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);
+        wz[w] = fb + cnt <= zr_blocks;
+        bytes_all += cnt * 1024;
+        if (!wz[w]) bytes_nz += cnt * 1024;
+      }
+      const unsigned need0 = (unsigned)ncov_s[0], need1 = (unsigned)ncov_s[1];
+      int gidx = 0;  // k-tiles issued so far, over all steps
+      for (int s = 0; s < J; ++s) {
+        const bool two = s > 0 || a.has_d0;
+        const int ktot = two ? kt0 + kt1 : kt0;
+        const int bsel = s == 0 ? 0 : 1 + ((s - 1) & 1);
+        bool admitted = s == 0;
+        for (int gk = 0; gk < ktot; ++gk, ++gidx) {
+          const int st = gidx % RB_STAGES;
+          if (gidx >= RB_STAGES) mbar_wait_cta(bar_empty + 8 * st, ((gidx / RB_STAGES) - 1) & 1);
+          const int sg = gk < kt0 ? 0 : 1;
+          const int kk = (sg ? gk - kt0 : gk) * 16;
+          const bool zt = gk >= zt0 && gk < zt1;
+          const unsigned full = bar_full + 8 * st;
+          mbar_expect_tx(full, (zt ? bytes_nz : bytes_all) + nparts * RB_B_BYTES);
+          const unsigned dA = sbase + st * RB_STAGE;
+#pragma unroll
+          for (int w = 0; w < RB_WARPS; ++w) {
+            if (wcnt[w] == 0 || (zt && wz[w])) continue;
+            if (wcnt[w] == RB_FM) {
+              tma_load_4d(dA + wslot[w] * 1024, &a.ta4[sg], kk, wrow[w], 0, 0, full);
+            } else {
+              for (int x = 0; x < wcnt[w]; ++x)
+                tma_load_4d(dA + (wslot[w] + x) * 1024, &a.ta[sg], kk, wrow[w] + 8 * x, 0, 0, full);
+            }
+          }
+          if (!admitted) {
+            // every cover of both members has stored step s - 1 (T tiles above did not wait)
+            unsigned spins = 0;
+            for (;;) {
+              unsigned c0v, c1v = 0xffffffffu;
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c0v) : "l"(a.cnt + pl.e[0]) : "memory");
+              if (nparts > 1)
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c1v) : "l"(a.cnt + pl.e[1]) : "memory");
+              if (c0v >= (unsigned)s * need0 && (nparts < 2 || c1v >= (unsigned)s * need1)) break;
+              if (++spins > RB_SPIN_LIMIT) __trap();
+            }
+            asm volatile("fence.proxy.async;" ::: "memory");  // generic-proxy stores -> TMA reads
+            admitted = true;
+          }
+          const CUtensorMap* tb = sg ? &a.tbd[bsel] : &a.tbx[bsel];
+          for (int part = 0; part < nparts; ++part)
+            tma_load_4d(dA + RB_A_BYTES + part * RB_B_BYTES, tb, kk, pl.e[part] * p.N, 0, 0, full);
+        }
+      }
+    }
+    return;
+  }
+  if (warp >= pl.nw) return;  // no blocks for this warp
+
+  int part, fb, cnt;
+  wplace(warp, part, fb, cnt);
+  const int slot0 = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);
+  const int g = lane >> 2, t4 = lane & 3;
+  const unsigned ko0 = swz(g, 4 * t4), ko1 = swz(g, 4 * t4 + 2);
+  int gbase = 0;
+  for (int s = 0; s < J; ++s) {
+    const bool two = s > 0 || a.has_d0;
+    const int ktot = two ? kt0 + kt1 : kt0;
+    const bool last = s == J - 1;
+    double acc[RB_FM][RB_FN][2];
+#pragma unroll
+    for (int x = 0; x < RB_FM; ++x)
+#pragma unroll
+      for (int y = 0; y < RB_FN; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    auto kloop = [&](auto FMC) {  // FMC: this warp's block count, compile-time
+      constexpr int F = decltype(FMC)::value;
+      for (int gk = 0; gk < ktot; ++gk) {
+        const int gidx = gbase + gk;
+        const int st = gidx % RB_STAGES;
+        mbar_wait_cta(bar_full + 8 * st, (gidx / RB_STAGES) & 1);
+        if (skips(fb, cnt, gk)) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_empty + 8 * st);
+          continue;
+        }
+        const unsigned char* sa = sgen + st * RB_STAGE + slot0 * 1024;
+        const unsigned char* sbp = sgen + st * RB_STAGE + RB_A_BYTES + part * RB_B_BYTES;
+        double af[F][4], bf[RB_FN][4];
+#pragma unroll
+        for (int x = 0; x < F; ++x) {
+          const double2 u = *reinterpret_cast<const double2*>(sa + x * 1024 + ko0);
+          const double2 v = *reinterpret_cast<const double2*>(sa + x * 1024 + ko1);
+          af[x][0] = u.x; af[x][1] = u.y; af[x][2] = v.x; af[x][3] = v.y;
+        }
+#pragma unroll
+        for (int y = 0; y < RB_FN; ++y) {
+          const double2 u = *reinterpret_cast<const double2*>(sbp + y * 8 * 128 + ko0);
+          const double2 v = *reinterpret_cast<const double2*>(sbp + y * 8 * 128 + ko1);
+          bf[y][0] = u.x; bf[y][1] = u.y; bf[y][2] = v.x; bf[y][3] = v.y;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_empty + 8 * st);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+          for (int x = 0; x < F; ++x)
+#pragma unroll
+            for (int y = 0; y < RB_FN; ++y)
+              dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x][qq], bf[y][qq]);
+      }
+    };
+    switch (cnt) {
+      case 4: kloop(std::integral_constant<int, 4>{}); break;
+      case 3: kloop(std::integral_constant<int, 3>{}); break;
+      case 2: kloop(std::integral_constant<int, 2>{}); break;
+      default: kloop(std::integral_constant<int, 1>{}); break;
+    }
+    gbase += ktot;
+    // epilogue (gemm_epilogue's arithmetic for alpha = 1, no Cin): C = acc + bias,
+    // D = C - X_s; only the three pointers change from step to step
+    {
+      const long long cb = (long long)pl.e[part] * p.c_b1;
+      double* C = (last ? a.X_out : a.bufX[s & 1]) + cb;
+      double* D = last ? nullptr : a.bufD[s & 1] + cb;
+      const double* Xp = last ? nullptr : (s == 0 ? a.X_in : a.bufX[(s - 1) & 1]) + cb;
+      const double* bias = p.bias ? p.bias + (long long)pl.e[part] * p.bias_b1 : nullptr;
+#pragma unroll
+      for (int x = 0; x < RB_FM; ++x) {
+        if (x >= cnt) continue;
+        const int gi = (fb + x) * 8 + g;
+        const long long ro = gi * p.c_i;
+        double pre[RB_FN][2];
+#pragma unroll
+        for (int b = 0; b < RB_FN; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gj = 2 * t4 + b * 8 + h;
+            pre[b][h] = (Xp && gj < p.N) ? Xp[ro + gj * p.c_j] : 0.0;
+          }
+        const double bv = bias ? bias[gi] : 0.0;
+#pragma unroll
+        for (int b = 0; b < RB_FN; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gj = 2 * t4 + b * 8 + h;
+            if (gj >= p.N) continue;
+            const long long off = ro + gj * p.c_j;
+            double v = acc[x][b][h];
+            if (bias) v = __dadd_rn(v, bv);
+            C[off] = v;
+            if (D) D[off] = __dsub_rn(v, pre[b][h]);
+          }
+      }
+    }
+    if (!last) {
+      // the last consumer warp to finish publishes the step for both members (its release at
+      // gpu scope is cumulative over the other warps' cta-scope releases)
+      __syncwarp();
+      if (lane == 0) {
+        unsigned t;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(t) : "r"(smem_u32(&done_tickets)) : "memory");
+        if (t + 1 == (unsigned)pl.nw * (unsigned)(s + 1)) {
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + pl.e[0]) : "memory");
+          if (nparts > 1)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + pl.e[1]) : "memory");
+        }
+      }
+    }
+  }
+}
+
+bool gemm_rowbalanced_chain_eligible(const GemmParams& p2, int zero_rows, int zero_k0, int zero_k1) {
+  static const bool off = getenv("PE_ROWBAL_NO_CHAIN") != nullptr;
+  if (off || p2.nseg != 2 || p2.alpha != 1.0 || p2.Cin) return false;
+  // the range split of the two-segment step is used for every step (also a one-segment
+  // first step), and the whole grid must be co-resident
+  const long long blocks = (long long)p2.nb1 * (p2.M / 8);
+  return gemm_rowbalanced_eligible(p2, zero_rows, zero_k0, zero_k1) && blocks >= num_sms();
+}
+
+void gemm_f64_rowbalanced_chain(const GemmParams& p2, int zero_rows, int zero_k0, int zero_k1, int J,
+                                const double* X_in, const double* D_in, double* const bufX[2],
+                                double* const bufD[2], double* X_out, unsigned* cnt,
+                                cudaStream_t st) {
+  if (!gemm_rowbalanced_chain_eligible(p2, zero_rows, zero_k0, zero_k1))
+    throw Error{PE_ERR_ARG, "rowbalanced chain: shape not eligible"};
+  const long long blocks = (long long)p2.nb1 * (p2.M / 8);
+  static bool attr = false;
+  if (!attr) {
+    PE_CUDA_CHECK(cudaFuncSetAttribute(gemm_rowbal_chain_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_SMEM));
+    attr = true;
+  }
+  RowBalChainArgs a;
+  memset(static_cast<void*>(&a), 0, sizeof(a));
+  a.p = p2;
+  a.p.ksplit = 1;
+  int use[2];
+  for (int s = 0; s < 2; ++s) {
+    const GemmSeg& g = p2.seg[s];
+    encode_operand(&a.ta[s], use, g.A.p, g.K, p2.M * p2.nb1, g.A.s0, 0, 1, 0, 1, 8);
+    encode_operand(&a.ta4[s], use, g.A.p, g.K, p2.M * p2.nb1, g.A.s0, 0, 1, 0, 1, 8 * RB_FM);
+  }
+  const long long bs1 = p2.seg[0].B.s1;
+  const double* bx[3] = {X_in, bufX[0], bufX[1]};
+  const double* bd[3] = {D_in ? D_in : bufD[0], bufD[0], bufD[1]};
+  for (int i = 0; i < 3; ++i) {
+    encode_operand(&a.tbx[i], use, bx[i], p2.seg[0].K, p2.N * p2.nb1, bs1, 0, 1, 0, 1, 8 * RB_FN);
+    encode_operand(&a.tbd[i], use, bd[i], p2.seg[1].K, p2.N * p2.nb1, bs1, 0, 1, 0, 1, 8 * RB_FN);
+  }
+  a.blocks = (int)blocks;
+  a.zero_rows = zero_rows;
+  a.zk0 = zero_k0;
+  a.zk1 = zero_k1;
+  rb_weights(p2, zero_rows, zero_k0, zero_k1, a.wu, a.ww, a.zrb);
+  a.J = J;
+  a.has_d0 = D_in != nullptr;
+  a.X_in = X_in;
+  a.X_out = X_out;
+  a.bufX[0] = bufX[0];
+  a.bufX[1] = bufX[1];
+  a.bufD[0] = bufD[0];
+  a.bufD[1] = bufD[1];
+  a.cnt = cnt;
+  PE_CUDA_CHECK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * p2.nb1, st));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms());
+  cfg.blockDim = dim3((RB_WARPS + 1) * 32);
+  cfg.dynamicSmemBytes = RB_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // CTAs wait on each other: all co-resident
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  PE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_rowbal_chain_kernel, a));
+  ++g_launches;
 }
 
 void gemm_f64(const GemmParams& p, cudaStream_t st) {

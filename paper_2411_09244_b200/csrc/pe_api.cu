@@ -252,6 +252,41 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
     const long long xo = e0 * xs;
     Xs = X0 + xo;
     Ds = D0 ? D0 + xo : nullptr;
+    if (!LB && J >= 2) {
+      // ensembles: all J steps in one cooperative row-balanced launch (per-member counters
+      // order the steps; T streams on across the step boundaries)
+      GemmParams p2;
+      p2.M = d;
+      p2.N = nc;
+      p2.nb1 = ec;
+      p2.nseg = 2;
+      p2.seg[0].A = Operand{c->T.d() + e0 * 2LL * d * d, 2LL * d, 1, 2LL * d * d, 0};
+      p2.seg[0].B = Operand{Xs, 1, d, xs, 0};
+      p2.seg[0].K = d;
+      p2.seg[1].A = Operand{c->T.d() + e0 * 2LL * d * d + d, 2LL * d, 1, 2LL * d * d, 0};
+      p2.seg[1].B = Operand{bufD[0] + xo, 1, d, xs, 0};
+      p2.seg[1].K = d;
+      p2.C = bufX[0] + xo;
+      p2.c_i = 1;
+      p2.c_j = d;
+      p2.c_b1 = xs;
+      p2.bias = c->cvec.d() + (long long)e0 * d;
+      p2.bias_b1 = d;
+      if (gemm_rowbalanced_chain_eligible(p2, c->d1, 0, c->d1)) {
+        double* bx[2] = {bufX[0] + xo, bufX[1] + xo};
+        double* bd[2] = {bufD[0] + xo, bufD[1] + xo};
+        c->gcnt.ensure(sizeof(unsigned) * ((size_t)ec + 8));
+        // algorithmic flops: the u x Du block is a structural zero; D_0 = 0 has no product
+        const double per2 = 2.0 * ec * nc * ((double)d * 2 * d - (double)c->d1 * c->d1);
+        const double per1 = 2.0 * ec * nc * (double)d * d;
+        const double flops = (Ds ? per2 : per1) + (J - 1) * per2;
+        profiled(c, flops, st, [&] {
+          gemm_f64_rowbalanced_chain(p2, c->d1, 0, c->d1, J, Xs, Ds, bx, bd, X_out + xo,
+                                     (unsigned*)c->gcnt.p, st);
+        });
+        continue;
+      }
+    }
     for (int s = 0; s < J; ++s) {
       const bool last = (s == J - 1);
       double* Xn = (last ? X_out : bufX[s & 1]) + xo;
