@@ -1283,7 +1283,7 @@ void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int z
 // coming from HBM across the step boundary; a launch per step left every SM idle for ~15 %
 // of the step (CTA launch, pipeline fill, tail).  Ring phases run on across steps.
 struct alignas(64) RowBalChainArgs {
-  CUtensorMap ta[2], ta4[2];  // T segments, 8-row and 32-row boxes
+  CUtensorMap ta[2][RB_FM];   // T segments, boxes of 8, 16, 24, 32 rows (a warp's blocks: one TMA)
   CUtensorMap tbx[3];         // X_in, bufX[0], bufX[1]
   CUtensorMap tbd[3];         // D_in (when present), bufD[0], bufD[1]
   GemmParams p;               // epilogue template: M, N, strides, bias
@@ -1309,6 +1309,13 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   const unsigned bar_empty = bar_full + RB_STAGES * 8;
   __shared__ unsigned done_tickets;
   __shared__ int ncov_s[2];
+  // warp -> (part, first member-local block, block count).  The blocks of a part are spread
+  // evenly over its share of the 11 consumer warps (3 or 4 blocks each at cfg4) instead of
+  // four per warp with the remainder on the last one: with 37 blocks, four per warp put 12
+  // blocks on SMSP 0 and 8 on SMSPs 2 and 3 (the DMMA pipes are per SMSP); the warps of the
+  // SMSP that also hosts the producer warp (two consumer warps only) get the larger counts
+  __shared__ short w_part[RB_WARPS], w_fb[RB_WARPS], w_cnt[RB_WARPS];
+  __shared__ int nw_active;
   const GemmParams& p = a.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const RbPlan pl = rb_plan(a);
@@ -1317,11 +1324,9 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   const int zr_blocks = a.zero_rows / 8;
   const int mb = p.M / 8;
   auto wplace = [&](int w, int& part, int& fb, int& cnt) {
-    part = w < pl.w0 ? 0 : 1;
-    const int q = part ? w - pl.w0 : w;
-    fb = pl.sb[part] + q * RB_FM;
-    const int left = pl.nb[part] - q * RB_FM;
-    cnt = left < RB_FM ? left : RB_FM;
+    part = w_part[w];
+    fb = w_fb[w];
+    cnt = w_cnt[w];
   };
   auto skips = [&](int fb, int cnt, int g) {
     return g >= zt0 && g < zt1 && fb + cnt <= zr_blocks;
@@ -1329,9 +1334,50 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   const int nparts = pl.nb[1] ? 2 : 1;
 
   if (tid == 0) {
+    const int nb0 = pl.nb[0], nb1 = pl.nb[1], nbt = nb0 + nb1;
+    int wp[2] = {0, 0};
+    if (nbt > 0) {
+      if (nb1 == 0) {
+        wp[0] = min(RB_WARPS, nb0);
+      } else {
+        int w0 = (RB_WARPS * nb0 + nbt / 2) / nbt;  // proportional share of the warps
+        w0 = max(w0, (nb0 + RB_FM - 1) / RB_FM);
+        w0 = min(w0, RB_WARPS - (nb1 + RB_FM - 1) / RB_FM);
+        w0 = max(1, min(w0, nb0));
+        wp[0] = w0;
+        wp[1] = min(RB_WARPS - w0, nb1);
+      }
+    }
+    int w = 0;
+    for (int part = 0; part < 2; ++part) {
+      const int nbp = pl.nb[part], n = wp[part];
+      if (n == 0) continue;
+      const int base = nbp / n;
+      int extra = nbp - base * n;
+      for (int i = 0; i < n; ++i) w_cnt[w + i] = (short)base;
+      for (int pass = 0; pass < 2 && extra > 0; ++pass)  // SMSP 3's warps first
+        for (int i = 0; i < n && extra > 0; ++i)
+          if ((((w + i) & 3) == 3) == (pass == 0)) {
+            ++w_cnt[w + i];
+            --extra;
+          }
+      int fbk = pl.sb[part];
+      for (int i = 0; i < n; ++i) {
+        w_part[w + i] = (short)part;
+        w_fb[w + i] = (short)fbk;
+        fbk += w_cnt[w + i];
+      }
+      w += n;
+    }
+    nw_active = w;
+    for (; w < RB_WARPS; ++w) {
+      w_part[w] = 0;
+      w_fb[w] = (short)pl.sb[0];
+      w_cnt[w] = 0;
+    }
     for (int s = 0; s < RB_STAGES; ++s) {
       mbar_init(bar_full + 8 * s, 1);
-      mbar_init(bar_empty + 8 * s, pl.nw);
+      mbar_init(bar_empty + 8 * s, nw_active);
     }
     done_tickets = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1355,7 +1401,8 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
     }
   }
   __syncthreads();
-  if (pl.nw == 0) return;
+  const int nwa = nw_active;
+  if (nwa == 0) return;
   const int J = a.J;
 
   if (warp == RB_WARPS) {  // producer
@@ -1366,7 +1413,7 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
 #pragma unroll
       for (int w = 0; w < RB_WARPS; ++w) {
         int part = 0, fb = 0, cnt = 0;
-        if (w < pl.nw) wplace(w, part, fb, cnt);
+        wplace(w, part, fb, cnt);
         wrow[w] = pl.e[part] * p.M + fb * 8;
         wcnt[w] = cnt;
         wslot[w] = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);
@@ -1393,12 +1440,7 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
 #pragma unroll
           for (int w = 0; w < RB_WARPS; ++w) {
             if (wcnt[w] == 0 || (zt && wz[w])) continue;
-            if (wcnt[w] == RB_FM) {
-              tma_load_4d(dA + wslot[w] * 1024, &a.ta4[sg], kk, wrow[w], 0, 0, full);
-            } else {
-              for (int x = 0; x < wcnt[w]; ++x)
-                tma_load_4d(dA + (wslot[w] + x) * 1024, &a.ta[sg], kk, wrow[w] + 8 * x, 0, 0, full);
-            }
+            tma_load_4d(dA + wslot[w] * 1024, &a.ta[sg][wcnt[w] - 1], kk, wrow[w], 0, 0, full);
           }
           if (!admitted) {
             // every cover of both members has stored step s - 1 (T tiles above did not wait)
@@ -1422,10 +1464,9 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
     }
     return;
   }
-  if (warp >= pl.nw) return;  // no blocks for this warp
-
   int part, fb, cnt;
   wplace(warp, part, fb, cnt);
+  if (cnt == 0) return;  // no blocks for this warp
   const int slot0 = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);
   const int g = lane >> 2, t4 = lane & 3;
   const unsigned ko0 = swz(g, 4 * t4), ko1 = swz(g, 4 * t4 + 2);
@@ -1527,7 +1568,7 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
         unsigned t;
         asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                      : "=r"(t) : "r"(smem_u32(&done_tickets)) : "memory");
-        if (t + 1 == (unsigned)pl.nw * (unsigned)(s + 1)) {
+        if (t + 1 == (unsigned)nwa * (unsigned)(s + 1)) {
           asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + pl.e[0]) : "memory");
           if (nparts > 1)
             asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + pl.e[1]) : "memory");
@@ -1566,8 +1607,8 @@ void gemm_f64_rowbalanced_chain(const GemmParams& p2, int zero_rows, int zero_k0
   int use[2];
   for (int s = 0; s < 2; ++s) {
     const GemmSeg& g = p2.seg[s];
-    encode_operand(&a.ta[s], use, g.A.p, g.K, p2.M * p2.nb1, g.A.s0, 0, 1, 0, 1, 8);
-    encode_operand(&a.ta4[s], use, g.A.p, g.K, p2.M * p2.nb1, g.A.s0, 0, 1, 0, 1, 8 * RB_FM);
+    for (int f = 1; f <= RB_FM; ++f)
+      encode_operand(&a.ta[s][f - 1], use, g.A.p, g.K, p2.M * p2.nb1, g.A.s0, 0, 1, 0, 1, 8 * f);
   }
   const long long bs1 = p2.seg[0].B.s1;
   const double* bx[3] = {X_in, bufX[0], bufX[1]};
