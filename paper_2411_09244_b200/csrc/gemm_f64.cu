@@ -982,7 +982,10 @@ static void launch_tma_best(const GemmParams& p, cudaStream_t st) {
 // one 8-row 128B-swizzled TMA box per loaded m-block and one box per B tile.  Same
 // canonical k order and epilogue as the other kernels, so a result differs from theirs only
 // by the omitted +0 terms.
-constexpr int RB_WARPS = 11, RB_FM = 4, RB_FN = 4, RB_STAGES = 4;  // 12 warps: 3 per SMSP
+#ifndef RB_WARPS_N
+#define RB_WARPS_N 11
+#endif
+constexpr int RB_WARPS = RB_WARPS_N, RB_FM = 4, RB_FN = 4, RB_STAGES = 4;  // + the producer warp
 constexpr int RB_MAXB = 40;  // m-blocks per CTA range: ceil(a/4) + ceil(b/4) <= 11
 constexpr int RB_A_BYTES = RB_MAXB * 1024, RB_B_BYTES = 8 * RB_FN * 128;
 constexpr int RB_STAGE = RB_A_BYTES + 2 * RB_B_BYTES;
@@ -1291,6 +1294,7 @@ struct alignas(64) RowBalChainArgs {
   int zero_rows, zk0, zk1;
   int wu, ww, zrb;
   int J, has_d0;
+  int wmode, share3;          // block-to-warp split: by work (1) or by count; SMSP 3 share / 2
   const double* X_in;
   double* X_out;
   double* bufX[2];
@@ -1310,10 +1314,9 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   __shared__ unsigned done_tickets;
   __shared__ int ncov_s[2];
   // warp -> (part, first member-local block, block count).  The blocks of a part are spread
-  // evenly over its share of the 11 consumer warps (3 or 4 blocks each at cfg4) instead of
+  // by work over its share of the 11 consumer warps (2-4 blocks each at cfg4) instead of
   // four per warp with the remainder on the last one: with 37 blocks, four per warp put 12
-  // blocks on SMSP 0 and 8 on SMSPs 2 and 3 (the DMMA pipes are per SMSP); the warps of the
-  // SMSP that also hosts the producer warp (two consumer warps only) get the larger counts
+  // blocks on SMSP 0 and 8 on SMSPs 2 and 3 (the DMMA pipes are per SMSP)
   __shared__ short w_part[RB_WARPS], w_fb[RB_WARPS], w_cnt[RB_WARPS];
   __shared__ int nw_active;
   const GemmParams& p = a.p;
@@ -1334,13 +1337,21 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   const int nparts = pl.nb[1] ? 2 : 1;
 
   if (tid == 0) {
-    const int nb0 = pl.nb[0], nb1 = pl.nb[1], nbt = nb0 + nb1;
+    // Work-weighted: a block below the zero-row boundary multiplies wu k-tiles, any other ww;
+    // a warp on the producer's SMSP (two consumer warps instead of three) takes a 3/2 share.
+    auto bw = [&](int part, int b) {
+      return a.wmode ? (pl.sb[part] + b < a.zrb ? a.wu : a.ww) : 1;
+    };
+    long long Wp[2] = {0, 0};
+    for (int part = 0; part < 2; ++part)
+      for (int b = 0; b < pl.nb[part]; ++b) Wp[part] += bw(part, b);
+    const int nb0 = pl.nb[0], nb1 = pl.nb[1];
     int wp[2] = {0, 0};
-    if (nbt > 0) {
+    if (nb0 + nb1 > 0) {
       if (nb1 == 0) {
         wp[0] = min(RB_WARPS, nb0);
       } else {
-        int w0 = (RB_WARPS * nb0 + nbt / 2) / nbt;  // proportional share of the warps
+        int w0 = (int)((RB_WARPS * Wp[0] + (Wp[0] + Wp[1]) / 2) / (Wp[0] + Wp[1]));
         w0 = max(w0, (nb0 + RB_FM - 1) / RB_FM);
         w0 = min(w0, RB_WARPS - (nb1 + RB_FM - 1) / RB_FM);
         w0 = max(1, min(w0, nb0));
@@ -1348,28 +1359,36 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
         wp[1] = min(RB_WARPS - w0, nb1);
       }
     }
-    int w = 0;
+    int w = 0, active = 0;
     for (int part = 0; part < 2; ++part) {
       const int nbp = pl.nb[part], n = wp[part];
       if (n == 0) continue;
-      const int base = nbp / n;
-      int extra = nbp - base * n;
-      for (int i = 0; i < n; ++i) w_cnt[w + i] = (short)base;
-      for (int pass = 0; pass < 2 && extra > 0; ++pass)  // SMSP 3's warps first
-        for (int i = 0; i < n && extra > 0; ++i)
-          if ((((w + i) & 3) == 3) == (pass == 0)) {
-            ++w_cnt[w + i];
-            --extra;
-          }
-      int fbk = pl.sb[part];
+      int S = 0;
+      for (int i = 0; i < n; ++i) S += ((w + i) & 3) == (RB_WARPS & 3) ? a.share3 : 2;
+      int pos = 0, cs = 0;
+      long long cum = 0;
       for (int i = 0; i < n; ++i) {
+        cs += ((w + i) & 3) == (RB_WARPS & 3) ? a.share3 : 2;
+        const long long target = Wp[part] * cs / S;
+        const int lo = max(0, (nbp - pos) - RB_FM * (n - 1 - i)), hi = min(RB_FM, nbp - pos);
+        int c = 0;
+        long long ws = 0;
+        while (c < hi) {
+          const int wb = bw(part, pos + c);
+          if (c >= lo && 2 * (cum + ws) + wb > 2 * target) break;
+          ws += wb;
+          ++c;
+        }
         w_part[w + i] = (short)part;
-        w_fb[w + i] = (short)fbk;
-        fbk += w_cnt[w + i];
+        w_fb[w + i] = (short)(pl.sb[part] + pos);
+        w_cnt[w + i] = (short)c;
+        active += c > 0;
+        pos += c;
+        cum += ws;
       }
       w += n;
     }
-    nw_active = w;
+    nw_active = active;
     for (; w < RB_WARPS; ++w) {
       w_part[w] = 0;
       w_fb[w] = (short)pl.sb[0];
@@ -1624,6 +1643,12 @@ void gemm_f64_rowbalanced_chain(const GemmParams& p2, int zero_rows, int zero_k0
   rb_weights(p2, zero_rows, zero_k0, zero_k1, a.wu, a.ww, a.zrb);
   a.J = J;
   a.has_d0 = D_in != nullptr;
+  // measured at cfg4 (GEMM ms per iteration): by count, producer-SMSP share 3/2: 3.30; share
+  // 1: 3.62; by work, share 3/2: 3.32; share 1: 3.50; share 2: 3.38
+  static const int wmode = getenv("PE_RB_WMODE") ? atoi(getenv("PE_RB_WMODE")) : 0;
+  static const int share3 = getenv("PE_RB_SHARE3") ? atoi(getenv("PE_RB_SHARE3")) : 3;
+  a.wmode = wmode;
+  a.share3 = share3;
   a.X_in = X_in;
   a.X_out = X_out;
   a.bufX[0] = bufX[0];
