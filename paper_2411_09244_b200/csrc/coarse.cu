@@ -40,6 +40,7 @@ __device__ __forceinline__ double warp_sum_c(double v) {
 struct CoarseArgs {
   int d, N, cs;
   int phi_in_smem;
+  int phi_in_reg;      // rows per warp <= 5 and d <= 640: Phi rows in registers (no smem slice)
   const double* Phi;   // (E, d, d) row-major
   const double* gvec;  // (E, d); with a load series (E, N, d): member stride ge, step stride gn
   long long ge, gn;
@@ -94,7 +95,11 @@ __device__ __forceinline__ void cs_fence_proxy() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-template <int RPW, bool PHIS>  // rows per warp (max); Phi slice in shared memory
+// NK > 0: the warp's Phi rows live in REGISTERS for the whole sweep (lane l holds columns
+// l, l + 32, ..., NK per row): the per-step pass over the 180 KB slice in shared memory
+// (1.1 us of a 2.5 us step at d = 600) becomes RPW x NK register FMAs.  Same lane-strided k
+// order and xor tree, so the sums are bitwise those of the shared-memory pass.
+template <int RPW, bool PHIS, int NK = 0>  // rows per warp (max); Phi slice in shared memory
 __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int e, int r0, int nrows,
                                              int ncopy, double* xs2, double* ybuf2,
                                              const double* phis, unsigned bar0, unsigned xs_base,
@@ -117,6 +122,16 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
     rv[j] = rr < nrows;
     rowp[j] = PHIS ? phis + (long long)(rv[j] ? rr : 0) * d
                    : Phi + (long long)(r0 + (rv[j] ? rr : 0)) * d;
+  }
+  double pr[NK > 0 ? RPW : 1][NK > 0 ? NK : 1];
+  if constexpr (NK > 0) {
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+#pragma unroll
+      for (int i = 0; i < NK; ++i) {
+        const int k = lane + 32 * i;
+        pr[j][i] = (rv[j] && k < d) ? __ldg(Phi + (long long)(r0 + warp + COARSE_WARPS * j) * d + k) : 0.0;
+      }
   }
   // Warps without rows neither read x nor send: they leave (with no CTA barrier in the
   // step loop a lagging idle warp could miss a whole phase of the receive barrier).  Warp 0
@@ -179,6 +194,17 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
             for (int j = 0; j < W; ++j) acc[j] = fma(rk[j][u], xk[u], acc[j]);
       }
     };
+    if constexpr (NK > 0) {
+#pragma unroll
+      for (int i = 0; i < NK; ++i) {
+        const int k = lane + 32 * i;
+        if (k < d) {
+          const double xk = xs[k];
+#pragma unroll
+          for (int j = 0; j < RPW; ++j) acc[j] = fma(pr[j][i], xk, acc[j]);
+        }
+      }
+    } else
     switch (wrows) {
       case 0: break;
       case 1: dot(std::integral_constant<int, 1>{}); break;
@@ -191,15 +217,44 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
       default: if constexpr (RPW >= 8) dot(std::integral_constant<int, 8>{}); break;
     }
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[3 * N + 4 + 2 * n] = cs_timer();
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int j = 0; j < RPW; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[3 * N + 5 + 2 * n] = cs_timer();
     double mya = 0.0;  // lane j keeps row j's sum
+    if constexpr (RPW > 2) {
+      // Folded xor tree: at levels 16 / 8 / 4 a lane keeps one row of a pair and hands the
+      // other to its partner, so the RPW (<= 8) trees cost 4 + 2 + 1 + 1 + 1 shuffle-adds
+      // instead of 5 RPW.  Every row is still summed over the pairs (l, l ^ 16), then
+      // (l, l ^ 8), ...: the totals are bitwise those of the plain trees.
+      double v[8];
 #pragma unroll
-    for (int j = 0; j < RPW; ++j)
-      if (lane == j) mya = acc[j];
+      for (int j = 0; j < 8; ++j) v[j] = j < RPW ? acc[j] : 0.0;
+      const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+      double w4[4], w2[2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double keep = b16 ? v[2 * q + 1] : v[2 * q], send = b16 ? v[2 * q] : v[2 * q + 1];
+        w4[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double keep = b8 ? w4[2 * q + 1] : w4[2 * q], send = b8 ? w4[2 * q] : w4[2 * q + 1];
+        w2[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      double t = (b4 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b4 ? w2[0] : w2[1], 4);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      // row j's total sits in the lanes with (bit 4, bit 3, bit 2) = (j & 1, j & 2, j & 4)
+      const int src = ((lane & 1) << 4) | ((lane & 2) << 2) | (lane & 4);
+      mya = __shfl_sync(0xffffffffu, t, src);
+      if (lane >= RPW) mya = 0.0;
+    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+#pragma unroll
+      for (int j = 0; j < RPW; ++j)
+        if (lane == j) mya = acc[j];
+    }
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[3 * N + 5 + 2 * n] = cs_timer();
     const double pf_f = nf_f, pf_g = nf_g, pf_b = nf_b, pf_o = nf_o;
     prefetch(n + 1);
     double sd = 0.0, sn = 0.0;
@@ -218,6 +273,7 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
     // storing to peer q (st.async completing on the peer's mbarrier).  No staging, no CTA
     // barrier: a peer's step n+2 stores into the buffer read here in step n+1 only after it
     // has received this warp's step n+1 rows, i.e. after this warp's dot products.
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[5 * N + 6 + 2 * n] = cs_timer();
     if (n + 1 < N) {
       const unsigned nbar = cs_map_rank(bar0 + 8 * ((n + 1) & 1), lane < a.cs ? lane : 0);
       const unsigned dstb =
@@ -229,9 +285,11 @@ __device__ __forceinline__ void coarse_steps(const CoarseArgs& a, int rank, int 
         if (rr < nrows && lane < a.cs) cs_st_async(dstb + (unsigned)(rr * 8), v, nbar);
       }
     }
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[5 * N + 7 + 2 * n] = cs_timer();
     // per-warp norm partials, summed later in (rank, warp) order
+    // only lanes < RPW (<= 8) hold non-zero squares: the levels 16 and 8 would add +0.0
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 4; o > 0; o >>= 1) {
       sd += __shfl_xor_sync(0xffffffffu, sd, o);
       sn += __shfl_xor_sync(0xffffffffu, sn, o);
     }
@@ -273,7 +331,7 @@ __global__ void __launch_bounds__(COARSE_THREADS, 1) coarse_kernel(const __grid_
   __shared__ __align__(8) unsigned long long mbar[2];
   const double* Phi = a.Phi + (long long)e * d * d;
 
-  if (a.phi_in_smem) {
+  if (a.phi_in_smem && !a.phi_in_reg) {
     // slice -> smem by 16-byte cp.async (no register staging: the staged scalar copy is a
     // latency-bound loop that costs tens of us per cluster, once per member of an ensemble)
     const double* src = Phi + (long long)r0 * d;
@@ -312,7 +370,10 @@ __global__ void __launch_bounds__(COARSE_THREADS, 1) coarse_kernel(const __grid_
   };
   using T1 = std::true_type;
   using F1 = std::false_type;
-  if (rpw <= 1)
+  if (a.phi_in_reg)
+    coarse_steps<5, false, 20>(a, rank, e, r0, nrows, ncopy, xs2, ybuf2, phis, bar0, xs_base, yb_base,
+                               bytes);
+  else if (rpw <= 1)
     a.phi_in_smem ? run(std::integral_constant<int, 1>{}, T1{}) : run(std::integral_constant<int, 1>{}, F1{});
   else if (rpw <= 2)
     a.phi_in_smem ? run(std::integral_constant<int, 2>{}, T1{}) : run(std::integral_constant<int, 2>{}, F1{});
@@ -579,6 +640,8 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   size_t base = sizeof(double) * (2 * (size_t)(2 * half + 2) + 2 * (size_t)rows_max);
   size_t with_phi = base + sizeof(double) * (size_t)rows_max * d;
   a.phi_in_smem = with_phi <= 200 * 1024;
+  static const bool no_reg = getenv("PE_COARSE_NO_REG") != nullptr;
+  a.phi_in_reg = !no_reg && a.phi_in_smem && d <= 640 && rows_max <= 5 * COARSE_WARPS;
   // Large d (Phi not smem-resident): stream Phi from HBM, all SMs per step.  Ensembles with
   // more member clusters than fit at once (~7-9 clusters of 16) also run here: the hardware
   // schedules the member clusters in waves, each keeps its member's Phi in shared memory for
@@ -592,7 +655,7 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
                           active, st);
     return;
   }
-  size_t smem = a.phi_in_smem ? with_phi : base;
+  size_t smem = (a.phi_in_smem && !a.phi_in_reg) ? with_phi : base;
   a.Phi = Phi;
   a.gvec = gvec;
   a.ge = ge;
@@ -607,8 +670,8 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   static const bool trace = getenv("PE_COARSE_TRACE") != nullptr;
   a.trace = nullptr;
   if (trace) {
-    PE_CUDA_CHECK(cudaMalloc(&a.trace, sizeof(unsigned long long) * (5 * N + 8)));
-    PE_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * (5 * N + 8), st));
+    PE_CUDA_CHECK(cudaMalloc(&a.trace, sizeof(unsigned long long) * (7 * N + 10)));
+    PE_CUDA_CHECK(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * (7 * N + 10), st));
   }
   static bool attr_done = false;
   if (!attr_done) {
@@ -633,20 +696,24 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   PE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, coarse_kernel, a));
   ++g_launches;
   if (trace) {
-    std::vector<unsigned long long> h(5 * N + 8);
+    std::vector<unsigned long long> h(7 * N + 10);
     PE_CUDA_CHECK(cudaStreamSynchronize(st));
     PE_CUDA_CHECK(cudaMemcpy(h.data(), a.trace, sizeof(unsigned long long) * h.size(),
                              cudaMemcpyDeviceToHost));
-    double w = 0, cmp = 0, rest = 0, dot = 0, shf = 0;
+    double w = 0, cmp = 0, rest = 0, dot = 0, shf = 0, xc = 0, snd = 0, nrm = 0;
     for (int n = 0; n < N; ++n) {
       dot += (h[3 * N + 4 + 2 * n] - h[2 + 3 * n]) * 1e-3;
       shf += (h[3 * N + 5 + 2 * n] - h[3 * N + 4 + 2 * n]) * 1e-3;
+      xc += (h[5 * N + 6 + 2 * n] - h[3 * N + 5 + 2 * n]) * 1e-3;
+      snd += (h[5 * N + 7 + 2 * n] - h[5 * N + 6 + 2 * n]) * 1e-3;
+      nrm += (h[3 + 3 * n] - h[5 * N + 7 + 2 * n]) * 1e-3;
       w += (h[2 + 3 * n] - h[1 + 3 * n]) * 1e-3;
       cmp += (h[3 + 3 * n] - h[2 + 3 * n]) * 1e-3;
       if (n + 1 < N) rest += (h[1 + 3 * (n + 1)] - h[3 + 3 * n]) * 1e-3;
     }
-    fprintf(stderr, "coarse trace (d=%d cs=%d): per step wait %.3f compute %.3f (dot %.3f shfl %.3f)"
-            " copy %.3f us\n", d, a.cs, w / N, cmp / N, dot / N, shf / N, rest / N);
+    fprintf(stderr, "coarse trace (d=%d cs=%d): per step wait %.3f compute %.3f (dot %.3f shfl %.3f"
+            " x %.3f send %.3f norms %.3f) copy %.3f us\n", d, a.cs, w / N, cmp / N, dot / N, shf / N,
+            xc / N, snd / N, nrm / N, rest / N);
     cudaFree(a.trace);
   }
 }
