@@ -641,7 +641,9 @@ void coarse_correct(int E, int d, int N, const double* Phi, const double* gvec,
   size_t with_phi = base + sizeof(double) * (size_t)rows_max * d;
   a.phi_in_smem = with_phi <= 200 * 1024;
   static const bool no_reg = getenv("PE_COARSE_NO_REG") != nullptr;
-  a.phi_in_reg = !no_reg && a.phi_in_smem && d <= 640 && rows_max <= 5 * COARSE_WARPS;
+  // (3 or more rows per warp: below that the shared-memory pass is short anyway)
+  a.phi_in_reg = !no_reg && a.phi_in_smem && d <= 640 && rows_max <= 5 * COARSE_WARPS &&
+                 rows_max > 2 * COARSE_WARPS;
   // Large d (Phi not smem-resident): stream Phi from HBM, all SMs per step.  Ensembles with
   // more member clusters than fit at once (~7-9 clusters of 16) also run here: the hardware
   // schedules the member clusters in waves, each keeps its member's Phi in shared memory for
