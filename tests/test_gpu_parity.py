@@ -490,25 +490,31 @@ def test_ensemble_members_equal_single_runs():
         assert rel_rows(np.array(run.history), np.array(o["history"])) < REL
 
 
-def test_rowbalanced_ensemble_step_matches_single_members():
-    """The row-balanced ensemble step kernel (gemm_f64.cu, E >= 2, nc <= 32: one contiguous
-    8-row-block range per SM, T's zero u x Du block skipped) against each member run alone
-    (cluster / all-SM chain kernels), config-2 operators (d = 600, d1 = 300: the zero-row
-    boundary falls inside an 8-row block), 3 members, 32 intervals, 16 substeps."""
+@pytest.mark.parametrize("E,nc,J", [(3, 32, 16), (2, 8, 3), (5, 24, 7), (9, 16, 2)])
+def test_rowbalanced_ensemble_step_matches_single_members(E, nc, J):
+    """The row-balanced ensemble kernels (gemm_f64.cu, E >= 2, nc <= 32: one contiguous
+    8-row-block range per SM, T's zero u x Du block skipped; all J steps in one cooperative
+    launch ordered by per-member counters) against each member run alone (cluster / all-SM
+    chain kernels), config-2 operators (d = 600, d1 = 300: the zero-row boundary falls inside
+    an 8-row block).  E = 2 / 3: a member is covered by ~50-74 CTAs; E = 9: by ~16; ragged
+    column counts leave part of the 32-column B box to the next member's columns."""
     P = _pkg()
     s, ld = _system(golden("sys_cfg2.npz"))
     systems, loads = [], []
-    for m, scale in enumerate((1.0, 0.6, 0.3)):
+    for m in range(E):
+        scale = 1.0 / (1.0 + 0.7 * m)
         systems.append(P.CoarseSystem(s.M11, s.A11 * scale, s.M12, s.A12 * scale, s.M22,
                                       s.A22 * scale))
         loads.append(P.ConstantLoads(ld.f1 * (m + 1), ld.f2 * (m + 1)))
-    J, nc, dt = 16, 32, 1.0 / 64 / 64
-    rng = np.random.default_rng(11)
-    X = rng.standard_normal((3, nc, s.d1 + s.d2)) * 0.01
+    dt = 1.0 / 64 / 64
+    rng = np.random.default_rng(11 + E)
+    X = rng.standard_normal((E, nc, s.d1 + s.d2)) * 0.01
     ens = P.PeContext(systems, loads, J)
     ens.prepare_sequential(dt)
     got = ens.fine_sequential(ens.to_dev(X)).cpu().numpy()
-    for m in range(3):
+    again = ens.fine_sequential(ens.to_dev(X)).cpu().numpy()
+    assert np.array_equal(got, again)  # rerun determinism of the counter-ordered chain
+    for m in sorted({0, E // 2, E - 1}):
         one = P.PeContext([systems[m]], [loads[m]], J)
         one.prepare_sequential(dt)
         ref = one.fine_sequential(one.to_dev(X[m:m + 1])).cpu().numpy()[0]
