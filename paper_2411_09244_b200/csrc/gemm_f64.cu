@@ -985,7 +985,13 @@ static void launch_tma_best(const GemmParams& p, cudaStream_t st) {
 #ifndef RB_WARPS_N
 #define RB_WARPS_N 11
 #endif
-constexpr int RB_WARPS = RB_WARPS_N, RB_FM = 4, RB_FN = 4, RB_STAGES = 4;  // + the producer warp
+// ring depth: measured at cfg4 with the chained kernel (GEMM ms per iteration) 4 stages 3.30,
+// 3 stages 3.34, 2 stages 3.38 -- the consumers are not waiting for HBM latency; a stage is
+// released by ALL warps, so the warps of a CTA move through the k-tiles in step
+#ifndef RB_STAGES_N
+#define RB_STAGES_N 4
+#endif
+constexpr int RB_WARPS = RB_WARPS_N, RB_FM = 4, RB_FN = 4, RB_STAGES = RB_STAGES_N;  // + the producer warp
 constexpr int RB_MAXB = 40;  // m-blocks per CTA range: ceil(a/4) + ceil(b/4) <= 11
 constexpr int RB_A_BYTES = RB_MAXB * 1024, RB_B_BYTES = 8 * RB_FN * 128;
 constexpr int RB_STAGE = RB_A_BYTES + 2 * RB_B_BYTES;
