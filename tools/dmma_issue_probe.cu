@@ -57,6 +57,9 @@ int main() {
   double* out;
   cudaMalloc(&out, 1 << 24);
   for (int w : {4, 8, 12}) {
+    run<3, 1>(w, out);  // the all-SM chain kernel's tile (3 row strips x 8 columns)
+    run<2, 1>(w, out);
+    run<1, 1>(w, out);
     run<3, 2>(w, out);
     run<2, 2>(w, out);
     run<4, 4>(w, out);
