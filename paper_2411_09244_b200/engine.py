@@ -93,6 +93,24 @@ class PeContext:
     def empty(self, *shape, dtype=torch.float64):
         return torch.empty(shape, dtype=dtype, device=self.device)
 
+    def reserve_history(self, k_max: int, N: int, pinned: bool = True):
+        """Device buffer (+ pinned host staging) for the (k_max + 1, E, N + 1, d) history of
+        `parareal`.  Called at setup by the ensemble driver: the pinned copy runs at PCIe
+        rate, where a pageable `.cpu()` of the config-4 history (200 MB) took longer than the
+        solve.  `parareal` itself only reserves the device buffer (a pinned allocation inside
+        a run costs more than the pageable copy of a small history)."""
+        shape = (k_max + 1, self.E, N + 1, self.d)
+        if getattr(self, "_hist_shape", None) != shape:
+            self._hist_dev = self.empty(*shape)
+            self._hist_pin = None
+            self._hist_shape = shape
+        if pinned and self._hist_pin is None:
+            try:
+                self._hist_pin = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+            except RuntimeError:  # no pinned memory left: pageable copies
+                self._hist_pin = None
+        return self._hist_dev
+
     # ------------------------------------------------------------------ hot path
     def fine_sequential(self, X: torch.Tensor) -> torch.Tensor:
         """X: (E, nc, d) device -> F(X) over one interval (lags reset)."""
@@ -181,7 +199,7 @@ class PeContext:
                  rule: str = "absolute", record_wr: bool = True):
         """Device-resident parareal loop; returns host numpy results per member."""
         E, d = self.E, self.d
-        hist = self.empty(k_max + 1, E, N + 1, d)
+        hist = self.reserve_history(k_max, N, pinned=False)
         diffs = np.full((max(k_max, 1), E), np.nan)
         iters = np.zeros(E, dtype=np.int32)
         conv = np.zeros(E, dtype=np.int32)
@@ -201,7 +219,15 @@ class PeContext:
             fine_ms.ctypes.data_as(F), coarse_ms.ctypes.data_as(F), C.byref(k_done),
             self.stream()))
         K = k_done.value
-        out = dict(history=hist[: K + 1].cpu().numpy(), diffs=diffs[:K], iterations=iters,
+        if self._hist_pin is not None:
+            # view of the context's staging buffer: valid until the next `parareal` call
+            # (`_runs_from` copies every slab into the ParerealRun it returns)
+            self._hist_pin[: K + 1].copy_(hist[: K + 1], non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()
+            history = self._hist_pin[: K + 1].numpy()
+        else:
+            history = hist[: K + 1].cpu().numpy()
+        out = dict(history=history, diffs=diffs[:K], iterations=iters,
                    converged=conv.astype(bool), fine_ms=fine_ms[:K], coarse_ms=coarse_ms[:K],
                    k_done=K)
         if aao:

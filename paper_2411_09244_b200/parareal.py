@@ -350,6 +350,7 @@ class ParerealEnsemble:
         else:
             self.ctx.prepare_allatonce(tg.dt_sub, config.alpha, config.resolved_fine_tol(),
                                        config.fine_max_iter)
+        self.ctx.reserve_history(config.k_max, tg.n_intervals)
 
     def run(self, initials):
         cfg = self.config
