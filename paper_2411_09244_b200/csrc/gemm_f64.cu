@@ -1015,9 +1015,18 @@ struct RbPlan {
   int e[2], sb[2], nb[2], w0, nw;
 };
 // first block whose cumulative weight reaches w (blocks in member-major order)
+// geometry of a row-balanced split: M rows per member, `blocks` 8-row blocks in all, the
+// first zrb blocks of a member weigh wu k-tiles, the others ww
+struct RbGeom {
+  int M, blocks, zrb, wu, ww;
+};
 template <class Args>
-__device__ __forceinline__ long long rb_block_at(const Args& a, long long w) {
-  const int mb = a.p.M / 8;
+__device__ __forceinline__ RbGeom rb_geom(const Args& a) {
+  return RbGeom{a.p.M, a.blocks, a.zrb, a.wu, a.ww};
+}
+// first block whose cumulative weight reaches w (blocks in member-major order)
+__device__ __forceinline__ long long rb_block_at(const RbGeom& a, long long w) {
+  const int mb = a.M / 8;
   const long long wm = (long long)a.zrb * a.wu + (long long)(mb - a.zrb) * a.ww;
   const long long e = w / wm;
   long long r = w - e * wm;
@@ -1029,17 +1038,15 @@ __device__ __forceinline__ long long rb_block_at(const Args& a, long long w) {
   return e * mb + b;
 }
 // block range [b0, b1) of CTA c
-template <class Args>
-__device__ __forceinline__ void rb_range(const Args& a, int c, long long& b0, long long& b1) {
-  const int mb = a.p.M / 8;
+__device__ __forceinline__ void rb_range(const RbGeom& a, int c, long long& b0, long long& b1) {
+  const int mb = a.M / 8;
   const long long E = a.blocks / mb;
   const long long W = E * ((long long)a.zrb * a.wu + (long long)(mb - a.zrb) * a.ww);
   b0 = c == 0 ? 0 : rb_block_at(a, W * c / gridDim.x);
   b1 = c + 1 == (int)gridDim.x ? a.blocks : rb_block_at(a, W * (c + 1) / gridDim.x);
 }
-template <class Args>
-__device__ __forceinline__ RbPlan rb_plan(const Args& a) {
-  const int mb = a.p.M / 8;
+__device__ __forceinline__ RbPlan rb_plan(const RbGeom& a) {
+  const int mb = a.M / 8;
   long long b0, b1;
   rb_range(a, (int)blockIdx.x, b0, b1);
   RbPlan r;
@@ -1064,7 +1071,7 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   const unsigned bar_empty = bar_full + RB_STAGES * 8;
   const GemmParams& p = a.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const RbPlan pl = rb_plan(a);
+  const RbPlan pl = rb_plan(rb_geom(a));
   const int kt0 = (p.seg[0].K + 15) / 16, kt1 = p.nseg > 1 ? (p.seg[1].K + 15) / 16 : 0;
   const int ktot = kt0 + kt1;
   // k-tiles of the second segment entirely inside its zero k-range, as concatenated indices
@@ -1306,7 +1313,9 @@ struct alignas(64) RowBalChainArgs {
   double* bufX[2];
   double* bufD[2];
   unsigned* cnt;              // per member: covers that finished a step (zeroed before launch)
+  const int* active;          // per member, or null: members with 0 are left out of the split
 };
+constexpr int RB_MAXE = 64;   // members per launch when an active mask is given
 
 constexpr unsigned RB_SPIN_LIMIT = 1u << 26;
 
@@ -1327,7 +1336,27 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
   __shared__ int nw_active;
   const GemmParams& p = a.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const RbPlan pl = rb_plan(a);
+  // Frozen (converged) members take no part: the rows of the ACTIVE members, in member order,
+  // are what the CTAs split, so a sweep costs in proportion to the members still iterating.
+  __shared__ short act_s[RB_MAXE];
+  __shared__ int nact_s;
+  if (tid == 0) {
+    int n = 0;
+    if (a.active) {
+      for (int e = 0; e < p.nb1; ++e)
+        if (a.active[e]) act_s[n++] = (short)e;
+    } else {
+      n = p.nb1;
+    }
+    nact_s = n;
+  }
+  __syncthreads();
+  RbGeom geo = rb_geom(a);
+  geo.blocks = nact_s * (p.M / 8);
+  const RbPlan pl = rb_plan(geo);
+  // plan member index -> member (identity without a mask)
+  auto member = [&](int e) { return a.active ? (int)act_s[e < nact_s ? e : 0] : e; };
+  const int em[2] = {member(pl.e[0]), member(pl.e[1])};
   const int kt0 = (p.seg[0].K + 15) / 16, kt1 = (p.seg[1].K + 15) / 16;
   const int zt0 = kt0 + (a.zk0 + 15) / 16, zt1 = kt0 + a.zk1 / 16;
   const int zr_blocks = a.zero_rows / 8;
@@ -1417,7 +1446,7 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
         bool hit = false;
         if (c < (int)gridDim.x) {
           long long b0, b1;
-          rb_range(a, c, b0, b1);
+          rb_range(geo, c, b0, b1);
           hit = b1 > b0 && b0 < m1 && b1 > m0;
         }
         n += __popc(__ballot_sync(0xffffffffu, hit));
@@ -1439,7 +1468,7 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
       for (int w = 0; w < RB_WARPS; ++w) {
         int part = 0, fb = 0, cnt = 0;
         wplace(w, part, fb, cnt);
-        wrow[w] = pl.e[part] * p.M + fb * 8;
+        wrow[w] = em[part] * p.M + fb * 8;
         wcnt[w] = cnt;
         wslot[w] = (part ? pl.nb[0] : 0) + (fb - pl.sb[part]);
         wz[w] = fb + cnt <= zr_blocks;
@@ -1472,9 +1501,9 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
             unsigned spins = 0;
             for (;;) {
               unsigned c0v, c1v = 0xffffffffu;
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c0v) : "l"(a.cnt + pl.e[0]) : "memory");
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c0v) : "l"(a.cnt + em[0]) : "memory");
               if (nparts > 1)
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c1v) : "l"(a.cnt + pl.e[1]) : "memory");
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c1v) : "l"(a.cnt + em[1]) : "memory");
               if (c0v >= (unsigned)s * need0 && (nparts < 2 || c1v >= (unsigned)s * need1)) break;
               if (++spins > RB_SPIN_LIMIT) __trap();
             }
@@ -1483,7 +1512,7 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
           }
           const CUtensorMap* tb = sg ? &a.tbd[bsel] : &a.tbx[bsel];
           for (int part = 0; part < nparts; ++part)
-            tma_load_4d(dA + RB_A_BYTES + part * RB_B_BYTES, tb, kk, pl.e[part] * p.N, 0, 0, full);
+            tma_load_4d(dA + RB_A_BYTES + part * RB_B_BYTES, tb, kk, em[part] * p.N, 0, 0, full);
         }
       }
     }
@@ -1552,11 +1581,11 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
     // epilogue (gemm_epilogue's arithmetic for alpha = 1, no Cin): C = acc + bias,
     // D = C - X_s; only the three pointers change from step to step
     {
-      const long long cb = (long long)pl.e[part] * p.c_b1;
+      const long long cb = (long long)em[part] * p.c_b1;
       double* C = (last ? a.X_out : a.bufX[s & 1]) + cb;
       double* D = last ? nullptr : a.bufD[s & 1] + cb;
       const double* Xp = last ? nullptr : (s == 0 ? a.X_in : a.bufX[(s - 1) & 1]) + cb;
-      const double* bias = p.bias ? p.bias + (long long)pl.e[part] * p.bias_b1 : nullptr;
+      const double* bias = p.bias ? p.bias + (long long)em[part] * p.bias_b1 : nullptr;
 #pragma unroll
       for (int x = 0; x < RB_FM; ++x) {
         if (x >= cnt) continue;
@@ -1594,9 +1623,9 @@ __global__ void __launch_bounds__((RB_WARPS + 1) * 32, 1)
         asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                      : "=r"(t) : "r"(smem_u32(&done_tickets)) : "memory");
         if (t + 1 == (unsigned)nwa * (unsigned)(s + 1)) {
-          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + pl.e[0]) : "memory");
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + em[0]) : "memory");
           if (nparts > 1)
-            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + pl.e[1]) : "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + em[1]) : "memory");
         }
       }
     }
@@ -1615,7 +1644,7 @@ bool gemm_rowbalanced_chain_eligible(const GemmParams& p2, int zero_rows, int ze
 void gemm_f64_rowbalanced_chain(const GemmParams& p2, int zero_rows, int zero_k0, int zero_k1, int J,
                                 const double* X_in, const double* D_in, double* const bufX[2],
                                 double* const bufD[2], double* X_out, unsigned* cnt,
-                                cudaStream_t st) {
+                                const int* active, cudaStream_t st) {
   if (!gemm_rowbalanced_chain_eligible(p2, zero_rows, zero_k0, zero_k1))
     throw Error{PE_ERR_ARG, "rowbalanced chain: shape not eligible"};
   const long long blocks = (long long)p2.nb1 * (p2.M / 8);
@@ -1662,6 +1691,7 @@ void gemm_f64_rowbalanced_chain(const GemmParams& p2, int zero_rows, int zero_k0
   a.bufD[0] = bufD[0];
   a.bufD[1] = bufD[1];
   a.cnt = cnt;
+  a.active = p2.nb1 <= RB_MAXE ? active : nullptr;
   PE_CUDA_CHECK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * p2.nb1, st));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms());

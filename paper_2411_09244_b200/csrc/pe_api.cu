@@ -190,7 +190,7 @@ static double* coarse_load_terms(pe_ctx* c, int N, const double* Fc, cudaStream_
 
 static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc,
                             cudaStream_t st, const double* X_prev = nullptr, int steps = -1,
-                            const double* Fload = nullptr) {
+                            const double* Fload = nullptr, const int* active = nullptr) {
   const int d = c->d, E = c->E, J = steps < 0 ? c->J : steps;
   // time-dependent loads: per-(step, column) bias terms, per-step GEMMs only
   const double* LB = Fload ? seq_load_terms(c, nc, J, Fload, st) : nullptr;
@@ -282,7 +282,7 @@ static void fine_sequential(pe_ctx* c, const double* X_in, double* X_out, int nc
         const double flops = (Ds ? per2 : per1) + (J - 1) * per2;
         profiled(c, flops, st, [&] {
           gemm_f64_rowbalanced_chain(p2, c->d1, 0, c->d1, J, Xs, Ds, bx, bd, X_out + xo,
-                                     (unsigned*)c->gcnt.p, st);
+                                     (unsigned*)c->gcnt.p, active ? active + e0 : nullptr, st);
         });
         continue;
       }
@@ -998,8 +998,8 @@ static void parareal_iterate(pe_ctx* c, int kind, int N, const double* X_old, do
   PE_CUDA_CHECK(cudaMemcpy2DAsync(c->Xin.d(), sizeof(double) * N * d, X_old,
                                   sizeof(double) * (N + 1) * d, sizeof(double) * N * d, E,
                                   cudaMemcpyDeviceToDevice, st));
-  if (kind == PE_KIND_SEQUENTIAL)
-    fine_sequential(c, c->Xin.d(), c->Xout.d(), N, st);
+  if (kind == PE_KIND_SEQUENTIAL)  // frozen members: skipped by the ensemble chain kernel
+    fine_sequential(c, c->Xin.d(), c->Xout.d(), N, st, nullptr, -1, nullptr, active);
   else
     fine_allatonce(c, c->Xin.d(), c->Xout.d(), N, wr_sweeps, wr_reasons, wr_resid, st);
   if (c->ev_mid) PE_CUDA_CHECK(cudaEventRecord(c->ev_mid, st));

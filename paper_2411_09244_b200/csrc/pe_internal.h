@@ -112,12 +112,13 @@ void gemm_f64_rowbalanced(const GemmParams& p, int zero_rows, int zero_k0, int z
                           cudaStream_t st);
 // J chained steps X_{s+1} = T [X_s ; D_s] + c in one cooperative launch (p2: the two-segment
 // step's parameters; D_in may be null: the first step then has one segment).  bufX / bufD
-// are ping-pong state buffers, cnt holds nb1 counters.
+// are ping-pong state buffers, cnt holds nb1 counters.  active (nb1 ints, device) or null:
+// members with 0 are skipped (their X_out rows are not written).
 bool gemm_rowbalanced_chain_eligible(const GemmParams& p2, int zero_rows, int zero_k0, int zero_k1);
 void gemm_f64_rowbalanced_chain(const GemmParams& p2, int zero_rows, int zero_k0, int zero_k1, int J,
                                 const double* X_in, const double* D_in, double* const bufX[2],
                                 double* const bufD[2], double* X_out, unsigned* cnt,
-                                cudaStream_t st);
+                                const int* active, cudaStream_t st);
 // Flop count of one launch (2*M*N*sumK*batch), for the roofline bookkeeping.
 double gemm_flops(const GemmParams& p);
 
