@@ -521,6 +521,43 @@ def test_rowbalanced_ensemble_step_matches_single_members(E, nc, J):
         assert rel_rows(got[m], ref) < 1e-13, m
 
 
+def test_ensemble_iteration_skips_frozen_members_bitwise():
+    """One parareal iteration of an ensemble with an active mask (pe_parareal_iterate): the
+    chained row-balanced kernel splits only the active members' rows, so the active members'
+    new iterates must equal the unmasked iteration bitwise, and frozen members keep their
+    iterate (parareal.py: a converged run stops; the batch freezes it)."""
+    import torch
+
+    P = _pkg()
+    s, ld = _system(golden("sys_cfg2.npz"))
+    E, N, J = 6, 16, 4
+    systems = [P.CoarseSystem(s.M11, s.A11 / (1 + m), s.M12, s.A12 / (1 + m), s.M22,
+                              s.A22 / (1 + m)) for m in range(E)]
+    loads = [P.ConstantLoads(ld.f1 * (m + 1), ld.f2 * (m + 1)) for m in range(E)]
+    ctx = P.PeContext(systems, loads, J)
+    ctx.prepare_coarse(1.0 / N)
+    ctx.prepare_sequential(1.0 / N / J)
+    d = s.d1 + s.d2
+    rng = np.random.default_rng(5)
+    A = ctx.to_dev(rng.standard_normal((E, N + 1, d)) * 0.01)
+    Gc = ctx.to_dev(rng.standard_normal((E, N, d)) * 0.01)
+    outs = []
+    for mask in (None, [1, 0, 1, 1, 0, 1], [0, 0, 0, 1, 0, 0]):
+        B = torch.zeros_like(A)
+        G = Gc.clone()
+        diff = torch.zeros(E, 2, dtype=torch.float64, device=A.device)
+        act = None if mask is None else torch.tensor(mask, dtype=torch.int32, device=A.device)
+        ctx.iterate("sequential", N, A, B, G, diff, active=act)
+        outs.append((mask, B.cpu().numpy()))
+    full = outs[0][1]
+    for mask, got in outs[1:]:
+        for m in range(E):
+            if mask[m]:
+                assert np.array_equal(got[m], full[m]), (mask, m)
+            else:
+                assert np.array_equal(got[m], A[m].cpu().numpy()), (mask, m)
+
+
 def test_unknown_fine_kind_rejected():
     P = _pkg()
     s, ld = tiny([0.1], [0.2])
